@@ -1,0 +1,190 @@
+"""Seeded synthetic inputs shaped like the paper's workloads.
+
+This module is the ONLY code shared by the oracle tests and the CUDA path. It draws random
+numbers (numpy Philox bit generator, fixed seeds) and builds look-at cameras; it contains none
+of the method's arithmetic (no projection, no compositing, no gradients).
+
+Parameter rows follow DESIGN.md §2: ``[N][80]`` fp32 — 0-2 μ, 3 o, 4-7 q (raw, w,x,y,z),
+8-10 s, 12-27 v (weight SH), 28-75 h (16×3 coefficient-major).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+ROW = 80
+MU, O, Q, S, V, H = 0, 3, 4, 8, 12, 28
+
+
+def rng(seed: int) -> np.random.Generator:
+    return np.random.Generator(np.random.Philox(int(seed)))
+
+
+def look_at(center, target=(0.0, 0.0, 0.0), up=(0.0, 0.0, 1.0), *, width, height, f, cx, cy,
+            znear=0.2) -> dict:
+    """OpenCV-style camera (x right, y down, z forward) at ``center`` looking at ``target``."""
+    c = np.asarray(center, np.float64)
+    fwd = np.asarray(target, np.float64) - c
+    fwd /= np.linalg.norm(fwd)
+    right = np.cross(fwd, np.asarray(up, np.float64))
+    if np.linalg.norm(right) < 1e-9:
+        right = np.cross(fwd, np.array([0.0, 1.0, 0.0]))
+    right /= np.linalg.norm(right)
+    down = np.cross(fwd, right)
+    R = np.stack([right, down, fwd])
+    t = -R @ c
+    return dict(width=int(width), height=int(height), fx=float(f), fy=float(f), cx=float(cx),
+                cy=float(cy), R=R.astype(np.float32).reshape(9), t=t.astype(np.float32),
+                center=c.astype(np.float32), znear=float(znear))
+
+
+def ring_cameras(n, radius, elevation_deg, *, width, height, f, cx, cy, azimuth0=0.0,
+                 height_jitter=0.0, z=None, seed=0) -> list:
+    g = rng(seed + 7001)
+    cams = []
+    el = math.radians(elevation_deg)
+    for k in range(n):
+        az = azimuth0 + 2 * math.pi * k / n
+        zz = radius * math.sin(el) if z is None else z + (g.uniform(-height_jitter, height_jitter) if height_jitter else 0.0)
+        rr = radius * math.cos(el) if z is None else radius
+        cams.append(look_at((rr * math.cos(az), rr * math.sin(az), zz), width=width, height=height,
+                            f=f, cx=cx, cy=cy))
+    return cams
+
+
+def fibonacci_hemisphere_cameras(n, radius, *, width, height, f, cx, cy) -> list:
+    cams = []
+    golden = math.pi * (3.0 - math.sqrt(5.0))
+    for k in range(n):
+        zc = 0.05 + 0.9 * (k + 0.5) / n          # upper hemisphere, avoid the exact pole/horizon
+        r = math.sqrt(1.0 - zc * zc)
+        az = golden * k
+        cams.append(look_at((radius * r * math.cos(az), radius * r * math.sin(az), radius * zc),
+                            width=width, height=height, f=f, cx=cx, cy=cy))
+    return cams
+
+
+def _appearance(g: np.random.Generator, n: int, rows: np.ndarray) -> None:
+    """q ~ 4-normal (raw, unnormalised), o ~ U[0.1,1.0], h DC ~ U[-1.2,1.2], h rest clipped
+    N(0,0.01); v DC ~ U[3,6], v rest clipped N(0,0.02) to ±0.03 (v(r) ≥ 0.3, R4)."""
+    rows[:, Q:Q + 4] = g.standard_normal((n, 4)).astype(np.float32)
+    rows[:, O] = g.uniform(0.1, 1.0, n).astype(np.float32)
+    h = np.clip(g.normal(0.0, 0.01, (n, 16, 3)), -0.01, 0.01)
+    h[:, 0, :] = g.uniform(-1.2, 1.2, (n, 3))
+    rows[:, H:H + 48] = h.reshape(n, 48).astype(np.float32)
+    v = np.clip(g.normal(0.0, 0.02, (n, 16)), -0.03, 0.03)
+    v[:, 0] = g.uniform(3.0, 6.0, n)
+    rows[:, V:V + 16] = v.astype(np.float32)
+
+
+@dataclass
+class Scene:
+    name: str
+    rows: np.ndarray            # [N][80] fp32
+    sigma: float
+    cams: list
+    bg: np.ndarray              # [3]
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def n(self) -> int:
+        return int(self.rows.shape[0])
+
+
+def scene_c1(seed: int = 1, n: int = 1000, n_views: int = 4, res: int = 64) -> Scene:
+    """C1 tiny: μ ~ U[-1,1]³, log s ~ N(ln 0.05, 0.4); 4 views 64×64 on a ring r=4, elev 20°,
+    f=80 (scaled with res), c0=(0.1,0.2,0.3); σ = 4.75 (≈10% of (splat, view) pairs have d ≥ σ)."""
+    g = rng(seed)
+    rows = np.zeros((n, ROW), np.float32)
+    rows[:, MU:MU + 3] = g.uniform(-1.0, 1.0, (n, 3)).astype(np.float32)
+    rows[:, S:S + 3] = np.exp(g.normal(math.log(0.05), 0.4, (n, 3))).astype(np.float32)
+    _appearance(g, n, rows)
+    f = 80.0 * res / 64.0
+    cams = ring_cameras(n_views, 4.0, 20.0, width=res, height=res, f=f, cx=res / 2, cy=res / 2, seed=seed)
+    return Scene("C1", rows, 4.75, cams, np.array([0.1, 0.2, 0.3]), dict(seed=seed))
+
+
+def scene_c2(seed: int = 2, n: int = 300_000, n_views: int = 100, res: int = 800) -> Scene:
+    """C2 NeRF-synthetic-shaped: N on a unit sphere shell (5% radial noise), log s ~ N(ln 0.01, 0.5);
+    views on a Fibonacci upper hemisphere r=4, res×res, f=1111.1·res/800; white background; σ = 4.8."""
+    g = rng(seed)
+    rows = np.zeros((n, ROW), np.float32)
+    d = g.standard_normal((n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    rad = 1.0 + 0.05 * g.standard_normal(n)
+    rows[:, MU:MU + 3] = (d * rad[:, None]).astype(np.float32)
+    rows[:, S:S + 3] = np.exp(g.normal(math.log(0.01), 0.5, (n, 3))).astype(np.float32)
+    _appearance(g, n, rows)
+    f = 1111.1 * res / 800.0
+    cams = fibonacci_hemisphere_cameras(n_views, 4.0, width=res, height=res, f=f, cx=res / 2, cy=res / 2)
+    return Scene("C2", rows, 4.8, cams, np.array([1.0, 1.0, 1.0]), dict(seed=seed))
+
+
+def scene_c3(seed: int = 3, n: int = 3_000_000, n_views: int = 200, width: int = 1600, height: int = 1064) -> Scene:
+    """C3 Mip-NeRF360-shaped: 60% ~U([-2,2]²×[-0.8,0.8]), 40% on an upper-hemisphere shell with
+    radius log-U[8,40]; log s ~ N(ln 0.01, 0.6)·max(1, r/4); views on a ring r=3.5, height
+    0.6±0.1 looking at the origin; f=1150 (scaled), c=(W/2,H/2); black background; σ = 25."""
+    g = rng(seed)
+    rows = np.zeros((n, ROW), np.float32)
+    n_in = int(round(0.6 * n))
+    mu = np.empty((n, 3))
+    mu[:n_in, 0:2] = g.uniform(-2.0, 2.0, (n_in, 2))
+    mu[:n_in, 2] = g.uniform(-0.8, 0.8, n_in)
+    d = g.standard_normal((n - n_in, 3))
+    d[:, 2] = np.abs(d[:, 2])
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    r = np.exp(g.uniform(math.log(8.0), math.log(40.0), n - n_in))
+    mu[n_in:] = d * r[:, None]
+    rows[:, MU:MU + 3] = mu.astype(np.float32)
+    rad = np.linalg.norm(mu, axis=1)
+    logs = g.normal(math.log(0.01), 0.6, (n, 3))
+    rows[:, S:S + 3] = (np.exp(logs) * np.maximum(1.0, rad / 4.0)[:, None]).astype(np.float32)
+    _appearance(g, n, rows)
+    f = 1150.0 * width / 1600.0
+    cams = ring_cameras(n_views, 3.5, 0.0, width=width, height=height, f=f, cx=width / 2, cy=height / 2,
+                        z=0.6, height_jitter=0.1, seed=seed)
+    return Scene("C3", rows, 25.0, cams, np.array([0.0, 0.0, 0.0]), dict(seed=seed))
+
+
+def active_mask(scene: Scene, rho: float, kind: str = "clustered", seed: int = 11) -> np.ndarray:
+    """Forced active set of fraction ρ: 'uniform' (Bernoulli(ρ)) or 'clustered' (μ_x in the top ρ
+    quantile — the paper's "small objects … large number of iterations")."""
+    n = scene.n
+    if rho >= 1.0:
+        return np.ones(n, bool)
+    if kind == "uniform":
+        return rng(seed).random(n) < rho
+    x = scene.rows[:, MU]
+    k = max(1, int(round(rho * n)))
+    thr = np.partition(x, n - k)[n - k]
+    return x >= thr
+
+
+def dl_dimage(cam: dict, seed: int) -> np.ndarray:
+    """Synthetic upstream gradient dL/dC ~ U[-1,1], [3,H,W] fp32."""
+    return rng(seed).uniform(-1.0, 1.0, (3, cam["height"], cam["width"])).astype(np.float32)
+
+
+def target_image(cam: dict, seed: int) -> np.ndarray:
+    """Synthetic training image ~ U[0,1], [3,H,W] fp32."""
+    return rng(seed).uniform(0.0, 1.0, (3, cam["height"], cam["width"])).astype(np.float32)
+
+
+def bits_from_mask(mask: np.ndarray) -> np.ndarray:
+    n = len(mask)
+    padded = np.zeros(((n + 31) // 32) * 32, bool)
+    padded[:n] = mask
+    weights = (np.uint64(1) << np.arange(32, dtype=np.uint64))[None, :]
+    return (padded.reshape(-1, 32).astype(np.uint64) * weights).sum(axis=1).astype(np.uint32)
+
+
+def mask_from_bits(bits: np.ndarray, n: int) -> np.ndarray:
+    b = np.asarray(bits, np.uint32)
+    out = ((b[:, None] >> np.arange(32, dtype=np.uint32)[None, :]) & 1).astype(bool).reshape(-1)
+    return out[:n]
+
+
+def camera_centers(cams) -> np.ndarray:
+    return np.stack([c["center"] for c in cams]).astype(np.float32)
