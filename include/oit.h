@@ -1,0 +1,209 @@
+/*
+ * oit.h — C-ABI of the B200-native SparseOIT hot path (liboit.so).
+ *
+ * SparseOIT (arxiv 2605.13855), PAPER.md cited as P:line. The library implements, as
+ * hand-written sm_100a CUDA kernels, the data-parallel hot path of the paper's active-set
+ * method: project + cull the active splats, bin them to 16x16 tiles with no
+ * depth sort, composite each pixel with the weighted-OIT sum (Eq. 7), back-propagate to every
+ * splat parameter and σ, score the inactive splats with a subsampled gradient, and refresh the
+ * active set (Eq. 8).
+ *
+ * Conventions (all calls):
+ *  - Every array pointer is a DEVICE pointer owned by the caller unless the name ends in _host.
+ *    The library never allocates or frees memory and keeps no global state; scratch memory is
+ *    a caller buffer `ws` of at least the size reported by the matching *_workspace_bytes call.
+ *  - Every call is asynchronous and stream-ordered on `stream` (a cudaStream_t, 0 = legacy
+ *    default stream); calls are reentrant across streams given distinct workspaces.
+ *  - fp32 everywhere; int32 indices (N < 2^31); int64 pair totals.
+ *  - Gradient outputs ACCUMULATE (+=): the caller zeroes them (this lets views accumulate).
+ *  - Synchronous argument errors are returned as oit_status (nothing is launched);
+ *    OIT_ECUDA reports a launch failure (cudaGetLastError). Data-dependent overflow (more
+ *    (splat, tile) pairs than pair_capacity) is reported through the device value *d_n_pairs >
+ *    pair_capacity: nothing past capacity is written and the caller re-calls with more room.
+ *  - Layouts:
+ *      parameter / gradient row [N][80] fp32: 0-2 μ, 3 o ∈ (0,1], 4-7 q (w,x,y,z) raw
+ *        (normalised inside), 8-10 s > 0 (linear), 11 pad, 12-27 v (16 weight-SH coeffs),
+ *        28-75 h (16x3 colour SH, coefficient-major: h[j][ch] at 28+3j+ch), 76-79 pad.
+ *      record rec[n_slots][16] fp32 (64 B): {mx, my, nA, nB}, {nC, thr_lo, thr_hi, log2 o},
+ *        {cR, cG, cB, w}, {rect_x, rect_y (uint32 bits x0|x1<<16), ex, ey}. nA,nB,nC are the
+ *        coefficients of power = nA dx² + nB dx dy + nC dy² = -½ΔᵀΣ'⁻¹Δ; ex, ey the conservative
+ *        pixel half-extents of the α = 1/255 ellipse (DESIGN.md §3 step 12). Culled: all zero.
+ *      pixel state / pre-render cache [5][n_tiles][256] fp32, tile-major (16x16 tiles in
+ *        row-major tile order, row-major pixels inside a tile): planes P_R, P_G, P_B, Q, T.
+ *      images [3][H][W] fp32 (CHW, row-major).
+ *  - Decisions (visibility, tile rectangle, pair contribution, α clamp) follow the fp32 spec of
+ *    DESIGN.md §3 op-by-op, so they are bit-identical to the CPU oracle's.
+ */
+#ifndef OIT_H
+#define OIT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OIT_TILE 16
+#define OIT_ROW 80
+#define OIT_REC 16
+
+typedef void* oit_stream_t; /* cudaStream_t */
+
+typedef enum {
+  OIT_OK = 0,
+  OIT_EINVAL = 1,    /* null required pointer, negative count, non-finite camera, bad enum */
+  OIT_ESHAPE = 2,    /* W/H <= 0 or > 32767, n_slots > N, index arrays too small */
+  OIT_ECAPACITY = 3, /* a statically known capacity (workspace, pair buffer) is too small */
+  OIT_ECUDA = 4      /* a kernel launch failed (cudaGetLastError) */
+} oit_status;
+
+/* Pinhole camera (host struct, read at call time). Pixel (x,y) sits at image coordinates (x,y)
+ * (R12); x_cam = R x_world + t (row-major R); center = camera centre f in world coordinates
+ * (the SH view direction is (μ - f)/‖μ - f‖, Eq. 4 / R2); znear culls tz <= znear. */
+typedef struct {
+  int32_t width, height;
+  float fx, fy, cx, cy;
+  float R[9], t[3];
+  float center[3];
+  float znear;
+} oit_camera;
+
+/* Scene: the Gaussian set G = {μ, q, s, o, h, w} as parameter rows, plus the
+ * global learnable σ of Eq. 1 (R6). Both device pointers, caller-owned. */
+typedef struct {
+  int32_t n;           /* N splats */
+  const float* rows;   /* [N][80] */
+  const float* sigma;  /* [1], σ > 0 */
+} oit_scene;
+
+/* Human-readable text for an oit_status. */
+const char* oit_status_string(int status);
+
+/* Number of 16x16 tiles of a camera (⌈W/16⌉·⌈H/16⌉). */
+int32_t oit_num_tiles(const oit_camera* cam);
+
+/* ---------------------------------------------------------------------------------------
+ * a1  oit_project_cull — Alg. 2 l.1-2 (CullGaussian, ScreenspaceGaussians);
+ *     Eq. 2, Eq. 4, Eq. 5, Eq. 6, Eq. 1.
+ * For each slot k < n_slots, splat i = idx[k] (the compacted active-index list; any order):
+ * normalise q, Σ = R S Sᵀ Rᵀ, Σ' = J W Σ Wᵀ Jᵀ + 0.3 I, conic, μ', colour c = max(0, SH(h, r)+0.5),
+ * weight w = max(0, 1 - tz/σ)·max(0, SH(v, r)), α thresholds, and the opacity-aware
+ * conservative tile rectangle (R9). Writes rec[k][16] and tiles_per_slot[k] (0 if culled).
+ * Errors: OIT_EINVAL (null pointer / n_slots < 0), OIT_ESHAPE (n_slots > scene->n, bad W/H).
+ * idx entries must lie in [0, N) (not checked on the device).
+ * --------------------------------------------------------------------------------------- */
+int oit_project_cull(const oit_scene* scene, const oit_camera* cam, const int32_t* idx,
+                     int32_t n_slots, float* rec, int32_t* tiles_per_slot, oit_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * a2  oit_bin_tiles — Alg. 2 l.3-6 (CreateTiles, DuplicateWithKeys, SortByKeys "only by tile
+ * ID", IdentifyTileRanges). One (tile, slot) pair per tile of each slot's
+ * rectangle, grouped by tile: pair_slot[tile_offsets[t] .. tile_offsets[t+1]) lists the slots
+ * covering tile t. No depth key; the order inside a tile is unspecified (R15).
+ * tile_offsets has n_tiles+1 entries; *d_n_pairs (device int64) receives the total pair count
+ * (if it exceeds pair_capacity, pair_slot holds only a prefix and the caller must re-call).
+ * Scratch: ws of oit_bin_workspace_bytes(cam) bytes.
+ * --------------------------------------------------------------------------------------- */
+size_t oit_bin_workspace_bytes(const oit_camera* cam);
+int oit_bin_tiles(const oit_camera* cam, const float* rec, const int32_t* tiles_per_slot,
+                  int32_t n_slots, int32_t* pair_slot, int64_t pair_capacity,
+                  int32_t* tile_offsets, int64_t* d_n_pairs, void* ws, size_t ws_bytes,
+                  oit_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * a3  oit_composite_fwd — Eq. 7 with Alg. 2 l.7-13 BAN/BAU.
+ * Per pixel: start from base (the per-view pre-rendered accumulators of the frozen set, R16;
+ * NULL = empty: P=Q=0, T=1), add every contributing slot of its tile (P += c α w, Q += α w,
+ * T *= 1-α), resolve F = P/Q (0 if Q = 0, R10) and C = T c0 + (1-T) F.
+ * route (nullable, [n_slots] u8): 0 = ACTIVE, 1 = FOLD — FOLD slots are also accumulated into
+ * base_out (BAU: baking newly frozen splats into the cache, R17). base_out may alias base.
+ * Pairs at positions >= pair_capacity are ignored (memory safety after an overflow).
+ * Outputs: image [3][H][W] (nullable), state [5][n_tiles][256] (nullable; the full pixel state
+ * the backward needs), base_out (required iff route != NULL). bg: host float[3] = c0.
+ * --------------------------------------------------------------------------------------- */
+int oit_composite_fwd(const oit_camera* cam, const float* rec, const int32_t* pair_slot,
+                      const int32_t* tile_offsets, int64_t pair_capacity,
+                      const float bg_host[3], const float* base, const uint8_t* route,
+                      float* image, float* state, float* base_out, oit_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * a4  oit_loss_grad — pixel loss gradient dL/dC of L = mean_{3HW} |C - I| (loss 0, sign(0)=0)
+ * or mean (C - I)² (loss 1): the L1 term of the 3DGS loss (R24).
+ * image, target, dL_dimage: [3][H][W] device; dL_dimage is overwritten.
+ * --------------------------------------------------------------------------------------- */
+int oit_loss_grad(const oit_camera* cam, const float* image, const float* target, int32_t loss,
+                  float* dL_dimage, oit_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * a5+a6  oit_composite_bwd — Eq. B.2, §4.2 per-splat backward, then
+ * the chain rule to every attribute of Eq. 8 and σ.
+ * Given the pixel state of the forward (state, possibly produced over a cache) and dL/dC,
+ * computes per (slot, tile) the 10 moments of the pixel gradients (reduced warp-first, then one
+ * vector atomic per (slot, tile)), then per slot chains to the parameter row:
+ *   grad[k][80] += scale·∂L/∂row(idx[k]), *dL_dsigma += scale·∂L/∂σ,
+ *   dL_dcov[k][6] += scale·∂L/∂Σ (packed xx,xy,xz,yy,yz,zz; off-diagonals = ∂/∂Σij + ∂/∂Σji;
+ *   nullable). rec/pair lists must come from oit_project_cull/oit_bin_tiles of the same idx.
+ * Scratch: ws of oit_bwd_workspace_bytes(cam, n_slots, pair_capacity) bytes.
+ * --------------------------------------------------------------------------------------- */
+size_t oit_bwd_workspace_bytes(const oit_camera* cam, int32_t n_slots, int64_t pair_capacity);
+int oit_composite_bwd(const oit_scene* scene, const oit_camera* cam, const int32_t* idx,
+                      int32_t n_slots, const float* rec, const int32_t* pair_slot,
+                      const int32_t* tile_offsets, int64_t pair_capacity,
+                      const float bg_host[3], const float* state, const float* dL_dimage,
+                      float scale, float* grad, float* dL_dsigma, float* dL_dcov, void* ws,
+                      size_t ws_bytes, oit_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * a7  oit_select_views — farthest point sampling over the camera centres with a Philox4x32-10
+ * random start (§4.1; R22; DESIGN.md §3 FPS spec). Runs as one CUDA block.
+ * centers [n_views][3] fp32 device; views_out [n_sub] int32 device, in pick order.
+ * Errors: OIT_EINVAL unless 0 < n_sub <= n_views <= 8192.
+ * --------------------------------------------------------------------------------------- */
+int oit_select_views(const float* centers, int32_t n_views, int32_t n_sub, uint64_t seed,
+                     uint32_t refresh_index, int32_t* views_out, oit_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * a7  oit_score_subsample — the subsampled gradient score of Alg. 1 l.8-12.
+ * For each subsampled view j = views_host[s]: the full-G pixel state is caches[j] ⊕ the active
+ * set (Rasterize(G, I^pre_j), R16); the L1/L2 loss gradient against targets[j] (R20, R24) is
+ * back-propagated to the scored splats score_idx (normally the inactive set);
+ *   score_grad[n_score][80] += (1/n_sub)·Σ_j ∂L_j/∂row, *dL_dsigma += (1/n_sub)·Σ_j ∂L_j/∂σ.
+ * cams_host [n_views]; targets/caches: HOST arrays of n_views DEVICE pointers ([3][H][W] and
+ * [5][n_tiles][256]; caches[j] may be NULL = nothing frozen). All views share W and H.
+ * *d_max_pairs (device int64) receives the largest pair count met; if > pair_capacity the
+ * result is invalid and the caller re-calls with more room.
+ * Scratch: ws of oit_score_workspace_bytes(...) bytes.
+ * --------------------------------------------------------------------------------------- */
+size_t oit_score_workspace_bytes(const oit_camera* cam, int32_t n_active, int32_t n_score,
+                                 int64_t pair_capacity);
+int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int32_t n_views,
+                        const float* const* targets_host, const float* const* caches_host,
+                        const int32_t* active_idx, int32_t n_active, const int32_t* score_idx,
+                        int32_t n_score, const int32_t* views_host, int32_t n_sub, int32_t loss,
+                        const float bg_host[3], float* score_grad, float* dL_dsigma,
+                        int64_t pair_capacity, int64_t* d_max_pairs, void* ws, size_t ws_bytes,
+                        oit_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * a8  oit_update_active_set — Eq. 8 with the text's ∃ reading (R18), Alg. 1 l.13
+ * (P:172). For each scored splat score_idx[j] (distinct), the per-attribute L2 norms of
+ * score_grad[j] over μ, q, s, o, h, v are compared with eps_host[6] (same order) by the fp32
+ * update spec of DESIGN.md §3; active ⟺ some norm > ε. mode 0 = FRESH (re-evaluated,
+ * reactivation allowed), 1 = MONOTONE (new = old ∧ active) (R21). Bits of unscored splats are
+ * unchanged. active_bits [⌈n_total/32⌉] in/out; active_idx [n_total] receives the ascending
+ * active list (*d_n_active its length); newly_frozen / newly_active [n_total] (nullable, with
+ * their counts) the ascending deltas against the input bitmask.
+ * Scratch: ws of oit_update_workspace_bytes(n_total) bytes.
+ * --------------------------------------------------------------------------------------- */
+size_t oit_update_workspace_bytes(int32_t n_total);
+int oit_update_active_set(const float* score_grad, const int32_t* score_idx, int32_t n_score,
+                          const float eps_host[6], int32_t mode, int32_t n_total,
+                          uint32_t* active_bits, int32_t* active_idx, int32_t* d_n_active,
+                          int32_t* newly_frozen, int32_t* d_n_frozen, int32_t* newly_active,
+                          int32_t* d_n_activated, void* ws, size_t ws_bytes, oit_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OIT_H */

@@ -100,11 +100,11 @@ def sh_basis(r) -> np.ndarray:
 def project_spec(rows32, idx, cam) -> dict:
     """fp32 decision-path projection (DESIGN.md §3 steps 1-12; Eq. 2, 5, 6; Alg. 2 l.1-2)."""
     rows32, idx = _f32(rows32), _i32(idx)
-    out = np.zeros((len(idx), 13), np.float32)
+    out = np.zeros((len(idx), 15), np.float32)
     lib().orc_project_spec(_p(rows32), _p(idx), C.c_int32(len(idx)), C.byref(camera(cam)), _p(out))
     return dict(visible=out[:, 0].astype(bool), rect=out[:, 1:5].astype(np.int32),  # x0,y0,x1,y1
                 mx=out[:, 5], my=out[:, 6], nA=out[:, 7], nB=out[:, 8], nC=out[:, 9],
-                thr_lo=out[:, 10], thr_hi=out[:, 11], tz=out[:, 12])
+                thr_lo=out[:, 10], thr_hi=out[:, 11], tz=out[:, 12], ex=out[:, 13], ey=out[:, 14])
 
 
 def project_value(rows64, sigma, idx, cam) -> dict:

@@ -73,7 +73,7 @@ float orc_speclog(float x) {
 typedef struct {
     int32_t visible;
     int32_t x0, y0, x1, y1;      /* tile rectangle [x0,x1) x [y0,y1) */
-    float mx, my, nA, nB, nC, thr_lo, thr_hi, tz;
+    float mx, my, nA, nB, nC, thr_lo, thr_hi, tz, ex, ey;
 } orc_spec;
 
 static float clampf_spec(float v, float lo, float hi) { return fminf(fmaxf(v, lo), hi); }
@@ -156,13 +156,14 @@ void orc_spec_project(const float* row, const orc_camera* cam, orc_spec* o) {
     const float REL = 1.0009765625f;
     float ex = sqrtf((2.0f * L) * a) * REL + 1.0f;
     float ey = sqrtf((2.0f * L) * c) * REL + 1.0f;
+    o->ex = ex; o->ey = ey;
     float TX = (float)((cam->width + 15) / 16), TY = (float)((cam->height + 15) / 16);
     float fx0 = clampf_spec(floorf((o->mx - ex) * 0.0625f), 0.0f, TX);
     float fx1 = clampf_spec(floorf((o->mx + ex) * 0.0625f) + 1.0f, 0.0f, TX);
     float fy0 = clampf_spec(floorf((o->my - ey) * 0.0625f), 0.0f, TY);
     float fy1 = clampf_spec(floorf((o->my + ey) * 0.0625f) + 1.0f, 0.0f, TY);
     o->x0 = (int32_t)fx0; o->x1 = (int32_t)fx1; o->y0 = (int32_t)fy0; o->y1 = (int32_t)fy1;
-    if (!(o->x1 > o->x0 && o->y1 > o->y0)) { o->x0 = o->x1 = o->y0 = o->y1 = 0; return; }
+    if (!(o->x1 > o->x0 && o->y1 > o->y0)) { o->x0 = o->x1 = o->y0 = o->y1 = 0; o->ex = o->ey = 0.0f; return; }
     o->visible = 1;
 }
 
@@ -348,18 +349,18 @@ static double value_alpha(const orc_val* v, int px, int py, int clamped, double*
  * Public oracle entry points (called from oracle/__init__.py through ctypes)
  * ========================================================================================= */
 
-/* Decision-path projection of n_slots splats rows[idx[k]]. out12[k] =
- * {visible, x0, y0, x1, y1, mx, my, nA, nB, nC, thr_lo, thr_hi, tz} packed as 13 floats
+/* Decision-path projection of n_slots splats rows[idx[k]]. out15[k] =
+ * {visible, x0, y0, x1, y1, mx, my, nA, nB, nC, thr_lo, thr_hi, tz, ex, ey} packed as 15 floats
  * (integers stored exactly as floats). */
 void orc_project_spec(const float* rows, const int32_t* idx, int32_t n_slots, const orc_camera* cam,
-                      float* out13) {
+                      float* out15) {
     for (int32_t k = 0; k < n_slots; k++) {
         orc_spec s;
         orc_spec_project(rows + (size_t)idx[k] * ROW, cam, &s);
-        float* o = out13 + (size_t)k * 13;
+        float* o = out15 + (size_t)k * 15;
         o[0] = (float)s.visible; o[1] = (float)s.x0; o[2] = (float)s.y0; o[3] = (float)s.x1; o[4] = (float)s.y1;
         o[5] = s.mx; o[6] = s.my; o[7] = s.nA; o[8] = s.nB; o[9] = s.nC;
-        o[10] = s.thr_lo; o[11] = s.thr_hi; o[12] = s.tz;
+        o[10] = s.thr_lo; o[11] = s.thr_hi; o[12] = s.tz; o[13] = s.ex; o[14] = s.ey;
     }
 }
 

@@ -1,0 +1,208 @@
+"""ctypes binding of liboit.so (include/oit.h) — argument marshalling only.
+
+Every function here has the name of the C-ABI entry point it calls and forwards torch CUDA
+tensors as raw device pointers; all arithmetic runs in the CUDA kernels of liboit. There is no
+CPU fallback: if the shared library is missing or a call fails, an exception is raised.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "liboit.so")
+
+OIT_TILE = 16
+OIT_ROW = 80
+OIT_REC = 16
+
+
+class OitError(RuntimeError):
+    pass
+
+
+class Camera(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32),
+                ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
+                ("R", C.c_float * 9), ("t", C.c_float * 3), ("center", C.c_float * 3),
+                ("znear", C.c_float)]
+
+
+class Scene(C.Structure):
+    _fields_ = [("n", C.c_int32), ("rows", C.c_void_p), ("sigma", C.c_void_p)]
+
+
+def camera(cam: dict) -> Camera:
+    c = Camera()
+    c.width, c.height = int(cam["width"]), int(cam["height"])
+    c.fx, c.fy, c.cx, c.cy = (float(cam[k]) for k in ("fx", "fy", "cx", "cy"))
+    for i in range(9):
+        c.R[i] = float(cam["R"][i])
+    for i in range(3):
+        c.t[i] = float(cam["t"][i])
+        c.center[i] = float(cam["center"][i])
+    c.znear = float(cam.get("znear", 0.2))
+    return c
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load liboit.so (built in-tree by __graft_entry__.build()); raise if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise OitError(f"liboit.so not built at {LIB_PATH}; run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        sz, i32, i64, vp, f32 = C.c_size_t, C.c_int32, C.c_int64, C.c_void_p, C.c_float
+        cam_p, scene_p = C.POINTER(Camera), C.POINTER(Scene)
+        sig = {
+            "oit_status_string": (C.c_char_p, [C.c_int]),
+            "oit_num_tiles": (i32, [cam_p]),
+            "oit_project_cull": (C.c_int, [scene_p, cam_p, vp, i32, vp, vp, vp]),
+            "oit_bin_workspace_bytes": (sz, [cam_p]),
+            "oit_bin_tiles": (C.c_int, [cam_p, vp, vp, i32, vp, i64, vp, vp, vp, sz, vp]),
+            "oit_composite_fwd": (C.c_int, [cam_p, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp]),
+            "oit_loss_grad": (C.c_int, [cam_p, vp, vp, i32, vp, vp]),
+            "oit_bwd_workspace_bytes": (sz, [cam_p, i32, i64]),
+            "oit_composite_bwd": (C.c_int, [scene_p, cam_p, vp, i32, vp, vp, vp, i64, vp, vp, vp, f32, vp, vp,
+                                            vp, vp, sz, vp]),
+            "oit_select_views": (C.c_int, [vp, i32, i32, C.c_uint64, C.c_uint32, vp, vp]),
+            "oit_score_workspace_bytes": (sz, [cam_p, i32, i32, i64]),
+            "oit_score_subsample": (C.c_int, [scene_p, cam_p, i32, vp, vp, vp, i32, vp, i32, vp, i32, i32, vp, vp,
+                                              vp, i64, vp, vp, sz, vp]),
+            "oit_update_workspace_bytes": (sz, [i32]),
+            "oit_update_active_set": (C.c_int, [vp, vp, i32, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+EXPORTED = ["oit_status_string", "oit_num_tiles", "oit_project_cull", "oit_bin_workspace_bytes", "oit_bin_tiles",
+            "oit_composite_fwd", "oit_loss_grad", "oit_bwd_workspace_bytes", "oit_composite_bwd",
+            "oit_select_views", "oit_score_workspace_bytes", "oit_score_subsample", "oit_update_workspace_bytes",
+            "oit_update_active_set"]
+
+
+# ------------------------------------------------------------------ marshalling helpers ---
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise OitError("liboit takes CUDA tensors (no CPU path)")
+    if not t.is_contiguous():
+        raise OitError("liboit takes contiguous tensors")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def _check(rc: int, name: str):
+    if rc != 0:
+        raise OitError(f"{name}: {lib().oit_status_string(rc).decode()} (status {rc})")
+
+
+def _f3(v):
+    return (C.c_float * 3)(*[float(x) for x in v])
+
+
+def scene(rows: torch.Tensor, sigma: torch.Tensor) -> Scene:
+    assert rows.dtype == torch.float32 and rows.dim() == 2 and rows.shape[1] == OIT_ROW
+    assert sigma.dtype == torch.float32 and sigma.numel() == 1
+    return Scene(int(rows.shape[0]), _ptr(rows), _ptr(sigma))
+
+
+def num_tiles(cam: dict) -> int:
+    return ((int(cam["width"]) + 15) // 16) * ((int(cam["height"]) + 15) // 16)
+
+
+# ------------------------------------------------------------------ the C-ABI, by name ----
+def oit_project_cull(rows, sigma, cam, idx, rec, tiles_per_slot, stream=None):
+    sc, c = scene(rows, sigma), camera(cam)
+    _check(lib().oit_project_cull(C.byref(sc), C.byref(c), _ptr(idx), int(idx.numel()), _ptr(rec),
+                                  _ptr(tiles_per_slot), _stream(stream)), "oit_project_cull")
+
+
+def oit_bin_workspace_bytes(cam) -> int:
+    return int(lib().oit_bin_workspace_bytes(C.byref(camera(cam))))
+
+
+def oit_bin_tiles(cam, rec, tiles_per_slot, n_slots, pair_slot, tile_offsets, n_pairs, ws, stream=None):
+    _check(lib().oit_bin_tiles(C.byref(camera(cam)), _ptr(rec), _ptr(tiles_per_slot), int(n_slots),
+                               _ptr(pair_slot), int(pair_slot.numel()), _ptr(tile_offsets), _ptr(n_pairs),
+                               _ptr(ws), int(ws.numel()), _stream(stream)), "oit_bin_tiles")
+
+
+def oit_composite_fwd(cam, rec, pair_slot, tile_offsets, bg, base=None, route=None, image=None, state=None,
+                      base_out=None, stream=None):
+    _check(lib().oit_composite_fwd(C.byref(camera(cam)), _ptr(rec), _ptr(pair_slot), _ptr(tile_offsets),
+                                   int(pair_slot.numel()), _f3(bg), _ptr(base), _ptr(route), _ptr(image),
+                                   _ptr(state), _ptr(base_out), _stream(stream)), "oit_composite_fwd")
+
+
+def oit_loss_grad(cam, image, target, loss: str, dL_dimage, stream=None):
+    _check(lib().oit_loss_grad(C.byref(camera(cam)), _ptr(image), _ptr(target), 0 if loss == "l1" else 1,
+                               _ptr(dL_dimage), _stream(stream)), "oit_loss_grad")
+
+
+def oit_bwd_workspace_bytes(cam, n_slots: int, pair_capacity: int) -> int:
+    return int(lib().oit_bwd_workspace_bytes(C.byref(camera(cam)), int(n_slots), int(pair_capacity)))
+
+
+def oit_composite_bwd(rows, sigma, cam, idx, rec, pair_slot, tile_offsets, bg, state, dL_dimage, grad, dL_dsigma,
+                      ws, dL_dcov=None, scale: float = 1.0, stream=None):
+    sc, c = scene(rows, sigma), camera(cam)
+    _check(lib().oit_composite_bwd(C.byref(sc), C.byref(c), _ptr(idx), int(idx.numel()), _ptr(rec),
+                                   _ptr(pair_slot), _ptr(tile_offsets), int(pair_slot.numel()), _f3(bg),
+                                   _ptr(state), _ptr(dL_dimage), C.c_float(scale), _ptr(grad), _ptr(dL_dsigma),
+                                   _ptr(dL_dcov), _ptr(ws), int(ws.numel()), _stream(stream)), "oit_composite_bwd")
+
+
+def oit_select_views(centers, n_sub: int, seed: int, refresh: int, views_out, stream=None):
+    _check(lib().oit_select_views(_ptr(centers), int(centers.shape[0]), int(n_sub), C.c_uint64(seed),
+                                  C.c_uint32(refresh), _ptr(views_out), _stream(stream)), "oit_select_views")
+
+
+def oit_score_workspace_bytes(cam, n_active: int, n_score: int, pair_capacity: int) -> int:
+    return int(lib().oit_score_workspace_bytes(C.byref(camera(cam)), int(n_active), int(n_score),
+                                               int(pair_capacity)))
+
+
+def oit_score_subsample(rows, sigma, cams, targets, caches, active_idx, score_idx, views, loss: str, bg,
+                        score_grad, dL_dsigma, pair_capacity: int, max_pairs, ws, stream=None):
+    sc = scene(rows, sigma)
+    V = len(cams)
+    cam_arr = (Camera * V)(*[camera(c) for c in cams])
+    tg = (C.c_void_p * V)(*[t.data_ptr() for t in targets])
+    ch = (C.c_void_p * V)(*[(c.data_ptr() if c is not None else None) for c in caches]) if caches is not None else None
+    vw = (C.c_int32 * len(views))(*[int(v) for v in views])
+    _check(lib().oit_score_subsample(C.byref(sc), cam_arr, V, tg, ch, _ptr(active_idx), int(active_idx.numel()),
+                                     _ptr(score_idx), int(score_idx.numel()), vw, len(views),
+                                     0 if loss == "l1" else 1, _f3(bg), _ptr(score_grad), _ptr(dL_dsigma),
+                                     int(pair_capacity), _ptr(max_pairs), _ptr(ws), int(ws.numel()),
+                                     _stream(stream)), "oit_score_subsample")
+
+
+def oit_update_workspace_bytes(n_total: int) -> int:
+    return int(lib().oit_update_workspace_bytes(int(n_total)))
+
+
+def oit_update_active_set(score_grad, score_idx, eps, mode: str, n_total: int, active_bits, active_idx, n_active,
+                          newly_frozen=None, n_frozen=None, newly_active=None, n_activated=None, ws=None,
+                          stream=None):
+    e = (C.c_float * 6)(*[float(x) for x in eps])
+    _check(lib().oit_update_active_set(_ptr(score_grad), _ptr(score_idx), int(score_idx.numel()), e,
+                                       1 if mode == "monotone" else 0, int(n_total), _ptr(active_bits),
+                                       _ptr(active_idx), _ptr(n_active), _ptr(newly_frozen), _ptr(n_frozen),
+                                       _ptr(newly_active), _ptr(n_activated), _ptr(ws), int(ws.numel()),
+                                       _stream(stream)), "oit_update_active_set")

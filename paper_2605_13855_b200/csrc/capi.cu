@@ -1,0 +1,248 @@
+// capi.cu — the extern "C" boundary of liboit (include/oit.h): argument validation, camera
+// marshalling, workspace carving and launch orchestration. No allocation, no global state.
+#include <cmath>
+#include <cstring>
+
+#include "../../include/oit.h"
+#include "kernels.h"
+
+using namespace oit;
+
+namespace {
+
+bool cam_ok(const oit_camera* c) {
+  if (!c) return false;
+  const float* f[] = {&c->fx, &c->fy, &c->cx, &c->cy, &c->znear};
+  for (const float* p : f)
+    if (!std::isfinite(*p)) return false;
+  for (int i = 0; i < 9; i++)
+    if (!std::isfinite(c->R[i])) return false;
+  for (int i = 0; i < 3; i++)
+    if (!std::isfinite(c->t[i]) || !std::isfinite(c->center[i])) return false;
+  return c->fx > 0.f && c->fy > 0.f;
+}
+
+bool shape_ok(const oit_camera* c) { return c->width > 0 && c->height > 0 && c->width <= 32767 && c->height <= 32767; }
+
+DevCam dev_cam(const oit_camera* c, const float* bg = nullptr) {
+  DevCam d;
+  d.W = c->width;
+  d.H = c->height;
+  d.TX = (c->width + kTile - 1) / kTile;
+  d.TY = (c->height + kTile - 1) / kTile;
+  d.fx = c->fx; d.fy = c->fy; d.cx = c->cx; d.cy = c->cy;
+  std::memcpy(d.R, c->R, sizeof(d.R));
+  std::memcpy(d.t, c->t, sizeof(d.t));
+  std::memcpy(d.center, c->center, sizeof(d.center));
+  d.znear = c->znear;
+  for (int i = 0; i < 3; i++) d.bg[i] = bg ? bg[i] : 0.f;
+  return d;
+}
+
+int launch_status() { return cudaGetLastError() == cudaSuccess ? OIT_OK : OIT_ECUDA; }
+
+inline cudaStream_t S(oit_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// nb of scan blocks supported by the 3-phase scan (4096 blocks of 4096 elements)
+constexpr int64_t kMaxScan = 4096LL * 4096LL;
+
+}  // namespace
+
+extern "C" {
+
+const char* oit_status_string(int status) {
+  switch (status) {
+    case OIT_OK: return "ok";
+    case OIT_EINVAL: return "invalid argument (null pointer, negative count, non-finite camera or bad enum)";
+    case OIT_ESHAPE: return "bad shape (image size, slot count or index range)";
+    case OIT_ECAPACITY: return "capacity too small (workspace or pair buffer)";
+    case OIT_ECUDA: return "CUDA launch failure";
+    default: return "unknown status";
+  }
+}
+
+int32_t oit_num_tiles(const oit_camera* cam) {
+  if (!cam) return 0;
+  return ((cam->width + 15) / 16) * ((cam->height + 15) / 16);
+}
+
+int oit_project_cull(const oit_scene* scene, const oit_camera* cam, const int32_t* idx, int32_t n_slots, float* rec,
+                     int32_t* tiles_per_slot, oit_stream_t stream) {
+  if (!scene || !scene->rows || !scene->sigma || !cam_ok(cam) || n_slots < 0) return OIT_EINVAL;
+  if (n_slots > 0 && (!idx || !rec || !tiles_per_slot)) return OIT_EINVAL;
+  if (!shape_ok(cam) || n_slots > scene->n) return OIT_ESHAPE;
+  launch_project(dev_cam(cam), scene->rows, scene->sigma, idx, n_slots, rec, tiles_per_slot, S(stream));
+  return launch_status();
+}
+
+size_t oit_bin_workspace_bytes(const oit_camera* cam) {
+  if (!cam) return 0;
+  return bin_ws_bytes(oit_num_tiles(cam));
+}
+
+int oit_bin_tiles(const oit_camera* cam, const float* rec, const int32_t* tiles_per_slot, int32_t n_slots,
+                  int32_t* pair_slot, int64_t pair_capacity, int32_t* tile_offsets, int64_t* d_n_pairs, void* ws,
+                  size_t ws_bytes, oit_stream_t stream) {
+  if (!cam_ok(cam) || n_slots < 0 || pair_capacity < 0 || !tile_offsets || !d_n_pairs || !ws) return OIT_EINVAL;
+  if (n_slots > 0 && (!rec || !tiles_per_slot)) return OIT_EINVAL;
+  if (pair_capacity > 0 && !pair_slot) return OIT_EINVAL;
+  if (!shape_ok(cam) || oit_num_tiles(cam) > kMaxScan) return OIT_ESHAPE;
+  if (ws_bytes < oit_bin_workspace_bytes(cam)) return OIT_ECAPACITY;
+  launch_bin(dev_cam(cam), rec, tiles_per_slot, n_slots, pair_slot, pair_capacity, tile_offsets, d_n_pairs, nullptr,
+             ws, S(stream));
+  return launch_status();
+}
+
+int oit_composite_fwd(const oit_camera* cam, const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
+                      int64_t pair_capacity, const float bg_host[3], const float* base, const uint8_t* route,
+                      float* image, float* state, float* base_out, oit_stream_t stream) {
+  if (!cam_ok(cam) || !tile_offsets || !bg_host || pair_capacity < 0) return OIT_EINVAL;
+  if (pair_capacity > 0 && (!rec || !pair_slot)) return OIT_EINVAL;
+  if (route && !base_out) return OIT_EINVAL;
+  if (!shape_ok(cam)) return OIT_ESHAPE;
+  launch_composite_fwd(dev_cam(cam, bg_host), rec, pair_slot, tile_offsets, pair_capacity, base, route, image, state,
+                       base_out, S(stream));
+  return launch_status();
+}
+
+int oit_loss_grad(const oit_camera* cam, const float* image, const float* target, int32_t loss, float* dL_dimage,
+                  oit_stream_t stream) {
+  if (!cam || !image || !target || !dL_dimage || (loss != 0 && loss != 1)) return OIT_EINVAL;
+  if (!shape_ok(cam)) return OIT_ESHAPE;
+  launch_loss_grad(dev_cam(cam), image, target, loss, dL_dimage, S(stream));
+  return launch_status();
+}
+
+static size_t coef_bytes(int32_t n_tiles) {
+  return align_up((size_t)n_tiles * kTilePx * sizeof(float4)) + align_up((size_t)n_tiles * kTilePx * sizeof(float));
+}
+
+size_t oit_bwd_workspace_bytes(const oit_camera* cam, int32_t n_slots, int64_t pair_capacity) {
+  if (!cam || n_slots < 0 || pair_capacity < 0) return 0;
+  int32_t nt = oit_num_tiles(cam);
+  return coef_bytes(nt) + bwd_ws_bytes(nt, n_slots, pair_capacity);
+}
+
+int oit_composite_bwd(const oit_scene* scene, const oit_camera* cam, const int32_t* idx, int32_t n_slots,
+                      const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets, int64_t pair_capacity,
+                      const float bg_host[3], const float* state, const float* dL_dimage, float scale, float* grad,
+                      float* dL_dsigma, float* dL_dcov, void* ws, size_t ws_bytes, oit_stream_t stream) {
+  if (!scene || !scene->rows || !scene->sigma || !cam_ok(cam) || n_slots < 0 || pair_capacity < 0) return OIT_EINVAL;
+  if (!tile_offsets || !bg_host || !state || !dL_dimage || !dL_dsigma || !ws) return OIT_EINVAL;
+  if (n_slots > 0 && (!idx || !rec || !grad)) return OIT_EINVAL;
+  if (pair_capacity > 0 && !pair_slot) return OIT_EINVAL;
+  if (!shape_ok(cam) || n_slots > scene->n || oit_num_tiles(cam) > kMaxScan) return OIT_ESHAPE;
+  if (ws_bytes < oit_bwd_workspace_bytes(cam, n_slots, pair_capacity)) return OIT_ECAPACITY;
+  const int32_t nt = oit_num_tiles(cam);
+  DevCam dc = dev_cam(cam, bg_host);
+  Carve cv(ws);
+  float* coef4 = cv.take<float>((size_t)nt * kTilePx * 4);
+  float* coefa = cv.take<float>((size_t)nt * kTilePx);
+  void* rest = cv.base + cv.off;
+  launch_coef(dc, state, dL_dimage, nullptr, 0, coef4, coefa, S(stream));
+  launch_composite_bwd(dc, scene->rows, scene->sigma, idx, n_slots, rec, pair_slot, tile_offsets, pair_capacity,
+                       coef4, coefa, scale, grad, dL_dsigma, dL_dcov, rest, S(stream));
+  return launch_status();
+}
+
+int oit_select_views(const float* centers, int32_t n_views, int32_t n_sub, uint64_t seed, uint32_t refresh_index,
+                     int32_t* views_out, oit_stream_t stream) {
+  if (!centers || !views_out || n_sub <= 0 || n_sub > n_views || n_views > 8192) return OIT_EINVAL;
+  launch_fps(centers, n_views, n_sub, seed, refresh_index, views_out, S(stream));
+  return launch_status();
+}
+
+// Score workspace: per-view buffers reused across the subsampled views.
+struct ScoreWs {
+  float *rec_a, *rec_s, *state, *coef4, *coefa;
+  int32_t *tps_a, *tps_s, *pairs, *offs;
+  int64_t* npairs;
+  void *bin_ws, *bwd_ws;
+  size_t total;
+};
+
+static ScoreWs score_layout(void* ws, const oit_camera* cam, int32_t n_active, int32_t n_score, int64_t cap) {
+  const int32_t nt = oit_num_tiles(cam);
+  Carve cv(ws);
+  ScoreWs w;
+  w.rec_a = cv.take<float>((size_t)n_active * 16 + 16);
+  w.rec_s = cv.take<float>((size_t)n_score * 16 + 16);
+  w.tps_a = cv.take<int32_t>((size_t)n_active + 1);
+  w.tps_s = cv.take<int32_t>((size_t)n_score + 1);
+  w.pairs = cv.take<int32_t>((size_t)cap + 1);
+  w.offs = cv.take<int32_t>((size_t)nt + 1);
+  w.npairs = cv.take<int64_t>(2);
+  w.state = cv.take<float>((size_t)nt * kTilePx * 5);
+  w.coef4 = cv.take<float>((size_t)nt * kTilePx * 4);
+  w.coefa = cv.take<float>((size_t)nt * kTilePx);
+  w.bin_ws = cv.take<char>(bin_ws_bytes(nt));
+  w.bwd_ws = cv.take<char>(bwd_ws_bytes(nt, n_score, cap));
+  w.total = cv.off;
+  return w;
+}
+
+size_t oit_score_workspace_bytes(const oit_camera* cam, int32_t n_active, int32_t n_score, int64_t pair_capacity) {
+  if (!cam || n_active < 0 || n_score < 0 || pair_capacity < 0) return 0;
+  return score_layout(nullptr, cam, n_active, n_score, pair_capacity).total;
+}
+
+int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int32_t n_views,
+                        const float* const* targets_host, const float* const* caches_host, const int32_t* active_idx,
+                        int32_t n_active, const int32_t* score_idx, int32_t n_score, const int32_t* views_host,
+                        int32_t n_sub, int32_t loss, const float bg_host[3], float* score_grad, float* dL_dsigma,
+                        int64_t pair_capacity, int64_t* d_max_pairs, void* ws, size_t ws_bytes,
+                        oit_stream_t stream) {
+  if (!scene || !scene->rows || !scene->sigma || !cams_host || !targets_host || !views_host || !bg_host ||
+      !dL_dsigma || !d_max_pairs || !ws)
+    return OIT_EINVAL;
+  if (n_views <= 0 || n_sub <= 0 || n_active < 0 || n_score < 0 || pair_capacity < 0 || (loss != 0 && loss != 1))
+    return OIT_EINVAL;
+  if ((n_active > 0 && !active_idx) || (n_score > 0 && (!score_idx || !score_grad))) return OIT_EINVAL;
+  if (n_active > scene->n || n_score > scene->n) return OIT_ESHAPE;
+  for (int s = 0; s < n_sub; s++) {
+    int j = views_host[s];
+    if (j < 0 || j >= n_views || !targets_host[j] || !cam_ok(&cams_host[j])) return OIT_EINVAL;
+    if (cams_host[j].width != cams_host[0].width || cams_host[j].height != cams_host[0].height) return OIT_ESHAPE;
+  }
+  if (!shape_ok(&cams_host[0]) || oit_num_tiles(&cams_host[0]) > kMaxScan) return OIT_ESHAPE;
+  if (ws_bytes < oit_score_workspace_bytes(&cams_host[0], n_active, n_score, pair_capacity)) return OIT_ECAPACITY;
+  ScoreWs w = score_layout(ws, &cams_host[0], n_active, n_score, pair_capacity);
+  cudaStream_t st = S(stream);
+  const float scale = 1.0f / (float)n_sub;
+  for (int s = 0; s < n_sub; s++) {
+    const int j = views_host[s];
+    DevCam dc = dev_cam(&cams_host[j], bg_host);
+    // Rasterize(G, I^pre_j): the active set over the view's cache of the frozen set (R16)
+    launch_project(dc, scene->rows, scene->sigma, active_idx, n_active, w.rec_a, w.tps_a, st);
+    launch_bin(dc, w.rec_a, w.tps_a, n_active, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st);
+    launch_composite_fwd(dc, w.rec_a, w.pairs, w.offs, pair_capacity, caches_host ? caches_host[j] : nullptr, nullptr,
+                         nullptr, w.state, nullptr, st);
+    // L_j and its pixel gradient (fused with the backward coefficients)
+    launch_coef(dc, w.state, nullptr, targets_host[j], loss, w.coef4, w.coefa, st);
+    // back-propagate L_j to the scored splats (R20)
+    launch_project(dc, scene->rows, scene->sigma, score_idx, n_score, w.rec_s, w.tps_s, st);
+    launch_bin(dc, w.rec_s, w.tps_s, n_score, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st);
+    launch_composite_bwd(dc, scene->rows, scene->sigma, score_idx, n_score, w.rec_s, w.pairs, w.offs, pair_capacity,
+                         w.coef4, w.coefa, scale, score_grad, dL_dsigma, nullptr, w.bwd_ws, st);
+  }
+  return launch_status();
+}
+
+size_t oit_update_workspace_bytes(int32_t n_total) { return n_total < 0 ? 0 : update_ws_bytes(n_total); }
+
+int oit_update_active_set(const float* score_grad, const int32_t* score_idx, int32_t n_score, const float eps_host[6],
+                          int32_t mode, int32_t n_total, uint32_t* active_bits, int32_t* active_idx,
+                          int32_t* d_n_active, int32_t* newly_frozen, int32_t* d_n_frozen, int32_t* newly_active,
+                          int32_t* d_n_activated, void* ws, size_t ws_bytes, oit_stream_t stream) {
+  if (!eps_host || (mode != 0 && mode != 1) || n_total < 0 || n_score < 0 || !d_n_active || !ws) return OIT_EINVAL;
+  if (n_total > 0 && (!active_bits || !active_idx)) return OIT_EINVAL;
+  if (n_score > 0 && (!score_grad || !score_idx)) return OIT_EINVAL;
+  if ((newly_frozen && !d_n_frozen) || (newly_active && !d_n_activated)) return OIT_EINVAL;
+  if (n_score > n_total || ((int64_t)n_total + 31) / 32 > kMaxScan) return OIT_ESHAPE;
+  if (ws_bytes < oit_update_workspace_bytes(n_total)) return OIT_ECAPACITY;
+  launch_update(score_grad, score_idx, n_score, eps_host, mode, n_total, active_bits, active_idx, d_n_active,
+                newly_frozen, d_n_frozen, newly_active, d_n_activated, ws, S(stream));
+  return launch_status();
+}
+
+}  // extern "C"

@@ -1,0 +1,474 @@
+// composite_bwd.cu — a4 pixel coefficients, a5 per-(splat, tile) moments, a6 chain to the
+// parameter rows: the analytic backward of Eq. B.2 with the per-splat
+// parallelisation of §4.2.
+//
+// Structure (B200-first; the paper's Fig. 3 design is prior art, not the blueprint):
+//  * k_coef (a4): per pixel, from the forward state (P, Q, T) and dL/dC (or the L1/L2 loss
+//    against a target) — K = (1-T)/Q, u = K g, s = K (g·F), a = T (g·(F - c0)). 20 B/px.
+//  * k_moments (a5): work item = (tile, chunk of 32 slots of the tile's list); one warp per
+//    item, LANE = SPLAT (the paper's "recursive per-splat" idea): each lane keeps its
+//    splat's 10 moments in registers and walks the tile's pixels, whose coefficients are
+//    warp-uniform (broadcast) loads. No shuffle reduction and no per-pixel atomics: every
+//    lane issues exactly 3 × red.global.add.v4.f32 per (splat, tile) — atomic traffic scales
+//    with tiles touched, not pixels. Rows/columns outside the union of the 32 splats'
+//    α = 1/255 extents are skipped warp-uniformly. Items are claimed dynamically (atomic
+//    counter) by a persistent grid sized to the SM count.
+//  * k_epilogue (a6): one thread per slot chains the moments to μ, q, s, o, h, v, σ (and Σ).
+// Moments per (slot, tile): U_RGB = Σ α u, S = Σ α s, Od = Σ d, M1 = Σ d dx, M2 = Σ d dy,
+// XX = Σ d dx², XY = Σ d dx dy, YY = Σ d dy², with dL/dα = a/(1-α) + w (u·c - s) and
+// d = dL/dα · α for unclamped pairs.
+#include "kernels.h"
+
+namespace oit {
+
+constexpr int kMomentsThreads = 256;
+
+// ------------------------------------------------------------------------------ a4 coef ---
+__global__ void __launch_bounds__(256) k_coef(DevCam cam, const float* __restrict__ state,
+                                              const float* __restrict__ dL_dimage, const float* __restrict__ target,
+                                              int32_t loss, float4* __restrict__ coef4, float* __restrict__ coefa) {
+  const int tile = blockIdx.x, tid = threadIdx.x;
+  const int n_tiles = cam.TX * cam.TY;
+  const int x = (tile % cam.TX) * kTile + (tid & 15), y = (tile / cam.TX) * kTile + (tid >> 4);
+  const size_t plane = (size_t)n_tiles * kTilePx, pix = (size_t)tile * kTilePx + tid;
+  if (x >= cam.W || y >= cam.H) {
+    coef4[pix] = make_float4(0.f, 0.f, 0.f, 0.f);
+    coefa[pix] = 0.f;
+    return;
+  }
+  const float P0 = state[pix], P1 = state[plane + pix], P2 = state[2 * plane + pix];
+  const float Q = state[3 * plane + pix], T = state[4 * plane + pix];
+  float F0, F1, F2, C0, C1, C2;
+  resolve_pixel(P0, P1, P2, Q, T, cam.bg, F0, F1, F2, C0, C1, C2);
+  const size_t hw = (size_t)cam.W * cam.H, p = (size_t)y * cam.W + x;
+  float g0, g1, g2;
+  if (target == nullptr) {
+    g0 = dL_dimage[p]; g1 = dL_dimage[hw + p]; g2 = dL_dimage[2 * hw + p];
+  } else {
+    const float inv = 1.0f / (3.0f * (float)hw);
+    const float d0 = C0 - target[p], d1 = C1 - target[hw + p], d2 = C2 - target[2 * hw + p];
+    if (loss == 0) {
+      g0 = (d0 > 0.f ? inv : (d0 < 0.f ? -inv : 0.f));
+      g1 = (d1 > 0.f ? inv : (d1 < 0.f ? -inv : 0.f));
+      g2 = (d2 > 0.f ? inv : (d2 < 0.f ? -inv : 0.f));
+    } else {
+      g0 = 2.f * d0 * inv; g1 = 2.f * d1 * inv; g2 = 2.f * d2 * inv;
+    }
+  }
+  const float K = Q > 0.f ? (1.f - T) / Q : 0.f;
+  const float gF = g0 * F0 + g1 * F1 + g2 * F2;
+  const float a = T * (g0 * (F0 - cam.bg[0]) + g1 * (F1 - cam.bg[1]) + g2 * (F2 - cam.bg[2]));
+  coef4[pix] = make_float4(K * g0, K * g1, K * g2, K * gF);
+  coefa[pix] = a;
+}
+
+// ---------------------------------------------------------------- work items (chunks) ----
+__global__ void k_chunk_counts(const int32_t* __restrict__ offs, int n_tiles, int64_t capacity,
+                               int32_t* __restrict__ counts) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_tiles) return;
+  int64_t s = offs[t], e = offs[t + 1];
+  if (e > capacity) e = capacity;
+  if (s > e) s = e;
+  counts[t] = (int32_t)((e - s + 31) / 32);
+}
+
+__global__ void k_chunk_emit(const int32_t* __restrict__ item_offs, int n_tiles, int32_t* __restrict__ items) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_tiles) return;
+  int o = item_offs[t], n = item_offs[t + 1] - o;
+  for (int c = 0; c < n; c++) items[o + c] = t;
+}
+
+// ------------------------------------------------------------------------- a5 moments ----
+__global__ void __launch_bounds__(kMomentsThreads) k_moments(DevCam cam, const float4* __restrict__ rec,
+                                                             const int32_t* __restrict__ pair_slot,
+                                                             const int32_t* __restrict__ offs, int64_t capacity,
+                                                             const int32_t* __restrict__ items,
+                                                             const int32_t* __restrict__ item_offs,
+                                                             const int32_t* __restrict__ n_items_p,
+                                                             int32_t* __restrict__ counter,
+                                                             const float4* __restrict__ coef4,
+                                                             const float* __restrict__ coefa,
+                                                             float* __restrict__ acc2d) {
+  const int lane = threadIdx.x & 31;
+  const int n_items = *n_items_p;
+  const unsigned FULL = 0xffffffffu;
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(counter, 1);
+    item = __shfl_sync(FULL, item, 0);
+    if (item >= n_items) return;
+    const int tile = items[item];
+    const int chunk = item - item_offs[tile];  // items of one tile are contiguous
+    int64_t e64 = offs[tile + 1];
+    if (e64 > capacity) e64 = capacity;
+    const int end = (int)e64;
+    const int j = offs[tile] + chunk * 32 + lane;
+    const bool valid = j < end;
+    float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0, q2 = q0, q3 = q0;
+    int slot = -1;
+    if (valid) {
+      slot = pair_slot[j];
+      const float4* r = rec + (size_t)slot * 4;
+      q0 = r[0]; q1 = r[1]; q2 = r[2]; q3 = r[3];
+    }
+    const float mx = q0.x, my = q0.y, nA = q0.z, nB = q0.w;
+    const float nC = q1.x, thr_lo = q1.y, thr_hi = q1.z, log2o = q1.w;
+    const float cR = q2.x, cG = q2.y, cB = q2.z, w = q2.w;
+    const float ex = q3.z, ey = q3.w;  // conservative pixel half-extents of the α=1/255 ellipse
+    const int tx0 = (tile % cam.TX) * kTile, ty0 = (tile / cam.TX) * kTile;
+    // warp-uniform pixel window: union of the lanes' extents, clipped to the tile
+    float lo_x = valid ? mx - ex : 1e30f, hi_x = valid ? mx + ex : -1e30f;
+    float lo_y = valid ? my - ey : 1e30f, hi_y = valid ? my + ey : -1e30f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo_x = fminf(lo_x, __shfl_xor_sync(FULL, lo_x, o));
+      hi_x = fmaxf(hi_x, __shfl_xor_sync(FULL, hi_x, o));
+      lo_y = fminf(lo_y, __shfl_xor_sync(FULL, lo_y, o));
+      hi_y = fmaxf(hi_y, __shfl_xor_sync(FULL, hi_y, o));
+    }
+    const int px0 = max(0, (int)floorf(fmaxf(lo_x - (float)tx0, -1.f)));
+    const int px1 = min(kTile - 1, (int)ceilf(fminf(hi_x - (float)tx0, 16.f)));
+    const int py0 = max(0, (int)floorf(fmaxf(lo_y - (float)ty0, -1.f)));
+    const int py1 = min(kTile - 1, (int)ceilf(fminf(hi_y - (float)ty0, 16.f)));
+
+    float U0 = 0.f, U1 = 0.f, U2 = 0.f, S = 0.f, Od = 0.f, M1 = 0.f, M2 = 0.f, XX = 0.f, XY = 0.f, YY = 0.f;
+    const float4* cf4 = coef4 + (size_t)tile * kTilePx;
+    const float* cfa = coefa + (size_t)tile * kTilePx;
+    for (int py = py0; py <= py1; py++) {
+      const float dy = __fsub_rn((float)(ty0 + py), my);
+      const bool ract = valid && fabsf(dy) <= ey;
+      if (!__any_sync(FULL, ract)) continue;
+      const float by = __fmul_rn(nB, dy);
+      const float cyv = __fmul_rn(__fmul_rn(nC, dy), dy);
+      float Rd = 0.f, Rdx = 0.f, Rdxx = 0.f;
+      for (int px = px0; px <= px1; px++) {
+        const float dx = __fsub_rn((float)(tx0 + px), mx);
+        const float power = spec_power_row(nA, dx, by, cyv);
+        const bool contrib = ract && power <= 0.0f && power >= thr_lo;
+        const bool clamp = power >= thr_hi;
+        float alpha = clamp ? 0.99f : ex2_approx(fmaf(power, kLog2e, log2o));
+        alpha = contrib ? alpha : 0.0f;
+        const float4 cu = __ldg(cf4 + py * kTile + px);  // (u_R, u_G, u_B, s): warp-uniform
+        const float ca = __ldg(cfa + py * kTile + px);   // a
+        const float rinv = rcp_approx(1.0f - alpha);
+        const float dot = fmaf(cu.x, cR, fmaf(cu.y, cG, fmaf(cu.z, cB, -cu.w)));
+        const float dLda = fmaf(ca, rinv, w * dot);
+        const float d = (contrib && !clamp) ? dLda * alpha : 0.0f;
+        U0 = fmaf(alpha, cu.x, U0);
+        U1 = fmaf(alpha, cu.y, U1);
+        U2 = fmaf(alpha, cu.z, U2);
+        S = fmaf(alpha, cu.w, S);
+        const float t = d * dx;
+        Rd += d;
+        Rdx += t;
+        Rdxx = fmaf(t, dx, Rdxx);
+      }
+      Od += Rd;
+      M1 += Rdx;
+      M2 = fmaf(dy, Rd, M2);
+      XX += Rdxx;
+      XY = fmaf(dy, Rdx, XY);
+      YY = fmaf(dy * dy, Rd, YY);
+    }
+    if (valid && (U0 != 0.f || U1 != 0.f || U2 != 0.f || S != 0.f || Od != 0.f)) {
+      float* a = acc2d + (size_t)slot * 12;
+      red_add_v4(a, U0, U1, U2, S);
+      red_add_v4(a + 4, Od, M1, M2, XX);
+      red_add_v4(a + 8, XY, YY, 0.f, 0.f);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------ a6 epilogue ----
+__global__ void __launch_bounds__(128) k_epilogue(DevCam cam, const float4* __restrict__ rows,
+                                                  const float* __restrict__ sigma_p, const int32_t* __restrict__ idx,
+                                                  int32_t n_slots, const float4* __restrict__ rec,
+                                                  const float4* __restrict__ acc2d, float scale,
+                                                  float4* __restrict__ grad, float* __restrict__ dL_dsigma,
+                                                  float* __restrict__ dL_dcov) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  float gsig = 0.f;
+  if (k < n_slots) {
+    const float4 q3 = rec[(size_t)k * 4 + 3];
+    const bool vis = __float_as_uint(q3.x) != 0u || __float_as_uint(q3.y) != 0u;
+    const float4 m0 = acc2d[(size_t)k * 3 + 0];  // U0 U1 U2 S
+    const float4 m1 = acc2d[(size_t)k * 3 + 1];  // Od M1 M2 XX
+    const float4 m2 = acc2d[(size_t)k * 3 + 2];  // XY YY
+    if (vis && (m0.x != 0.f || m0.y != 0.f || m0.z != 0.f || m0.w != 0.f || m1.x != 0.f)) {
+      const float4 q0 = rec[(size_t)k * 4 + 0];
+      const float4 q1 = rec[(size_t)k * 4 + 1];
+      const float nA = q0.z, nB = q0.w, nC = q1.x;
+      const float4* r = rows + (size_t)idx[k] * kRow4;
+      const float4 ra = r[0], rb = r[1], rc = r[2];
+      const float mu[3] = {ra.x, ra.y, ra.z};
+      const float op = ra.w;
+      const float W[3][3] = {{cam.R[0], cam.R[1], cam.R[2]}, {cam.R[3], cam.R[4], cam.R[5]}, {cam.R[6], cam.R[7], cam.R[8]}};
+      // ---- recompute the forward quantities (value path, fp32) ----
+      float t[3];
+#pragma unroll
+      for (int i = 0; i < 3; i++) t[i] = W[i][0] * mu[0] + W[i][1] * mu[1] + W[i][2] * mu[2] + cam.t[i];
+      const float tz = t[2], itz = 1.0f / tz, itz2 = itz * itz;
+      const float limx = 1.3f * (0.5f * (float)cam.W / cam.fx), limy = 1.3f * (0.5f * (float)cam.H / cam.fy);
+      const float ux = t[0] * itz, uy = t[1] * itz;
+      const bool clx = ux > limx || ux < -limx, cly = uy > limy || uy < -limy;
+      const float uxc = fminf(limx, fmaxf(-limx, ux)), uyc = fminf(limy, fmaxf(-limy, uy));
+      const float J00 = cam.fx * itz, J02 = -cam.fx * uxc * itz, J11 = cam.fy * itz, J12 = -cam.fy * uyc * itz;
+      float T[2][3];
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        T[0][j] = J00 * W[0][j] + J02 * W[2][j];
+        T[1][j] = J11 * W[1][j] + J12 * W[2][j];
+      }
+      const float qn = sqrtf(rb.x * rb.x + rb.y * rb.y + rb.z * rb.z + rb.w * rb.w), iqn = 1.0f / qn;
+      const float qw = rb.x * iqn, qx = rb.y * iqn, qy = rb.z * iqn, qz = rb.w * iqn;
+      float Rq[3][3];
+      Rq[0][0] = 1.f - 2.f * (qy * qy + qz * qz); Rq[0][1] = 2.f * (qx * qy - qw * qz); Rq[0][2] = 2.f * (qx * qz + qw * qy);
+      Rq[1][0] = 2.f * (qx * qy + qw * qz); Rq[1][1] = 1.f - 2.f * (qx * qx + qz * qz); Rq[1][2] = 2.f * (qy * qz - qw * qx);
+      Rq[2][0] = 2.f * (qx * qz - qw * qy); Rq[2][1] = 2.f * (qy * qz + qw * qx); Rq[2][2] = 1.f - 2.f * (qx * qx + qy * qy);
+      const float s[3] = {rc.x, rc.y, rc.z};
+      float M[3][3], Sg[3][3];
+#pragma unroll
+      for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) M[i][j] = Rq[i][j] * s[j];
+#pragma unroll
+      for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) Sg[i][j] = M[i][0] * M[j][0] + M[i][1] * M[j][1] + M[i][2] * M[j][2];
+      // view direction and SH (Eq. 4), weight (Eq. 1)
+      float dv[3] = {mu[0] - cam.center[0], mu[1] - cam.center[1], mu[2] - cam.center[2]};
+      const float dn = sqrtf(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]), idn = 1.0f / dn;
+      const float rx = dv[0] * idn, ry = dv[1] * idn, rz = dv[2] * idn;
+      float Y[16];
+      sh_basis(rx, ry, rz, Y);
+      float vco[16];
+      float vraw = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const float4 vv = r[3 + q];
+        vco[4 * q] = vv.x; vco[4 * q + 1] = vv.y; vco[4 * q + 2] = vv.z; vco[4 * q + 3] = vv.w;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; j++) vraw += vco[j] * Y[j];
+      float hco[48];
+#pragma unroll
+      for (int q = 0; q < 12; q++) {
+        const float4 hh = r[7 + q];
+        hco[4 * q] = hh.x; hco[4 * q + 1] = hh.y; hco[4 * q + 2] = hh.z; hco[4 * q + 3] = hh.w;
+      }
+      float craw[3] = {0.5f, 0.5f, 0.5f};
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        craw[0] += hco[3 * j] * Y[j];
+        craw[1] += hco[3 * j + 1] * Y[j];
+        craw[2] += hco[3 * j + 2] * Y[j];
+      }
+      const float col[3] = {fmaxf(craw[0], 0.f), fmaxf(craw[1], 0.f), fmaxf(craw[2], 0.f)};
+      const float sigma = *sigma_p;
+      const float ramp_raw = 1.0f - tz / sigma;
+      const float ramp = fmaxf(ramp_raw, 0.f), vplus = fmaxf(vraw, 0.f), w = ramp * vplus;
+
+      // ---- 2D gradients from the moments ----
+      const float U[3] = {m0.x, m0.y, m0.z};
+      const float Ssum = m0.w, Od = m1.x, M1 = m1.y, M2 = m1.z, XX = m1.w, XY = m2.x, YY = m2.y;
+      const float gc[3] = {w * U[0], w * U[1], w * U[2]};
+      const float gw = U[0] * col[0] + U[1] * col[1] + U[2] * col[2] - Ssum;
+      const float go = Od / op;
+      const float gmx = -(2.f * nA * M1 + nB * M2), gmy = -(nB * M1 + 2.f * nC * M2);
+      // conic K = [[-2nA, -nB], [-nB, -2nC]]; dL/dK = -½[[XX, XY], [XY, YY]]; dL/dΣ' = -K dL/dK K
+      const float K00 = -2.f * nA, K01 = -nB, K11 = -2.f * nC;
+      const float A00 = 0.5f * (K00 * XX + K01 * XY), A01 = 0.5f * (K00 * XY + K01 * YY);
+      const float A10 = 0.5f * (K01 * XX + K11 * XY), A11 = 0.5f * (K01 * XY + K11 * YY);
+      const float G00 = A00 * K00 + A01 * K01, G01 = A00 * K01 + A01 * K11, G11 = A10 * K01 + A11 * K11;
+      // Σ' = T Σ Tᵀ + 0.3 I: dL/dΣ = Tᵀ G T, dL/dT = 2 G T Σ
+      const float G[2][2] = {{G00, G01}, {G01, G11}};
+      float gS[3][3], GT[2][3], gT[2][3];
+#pragma unroll
+      for (int p = 0; p < 2; p++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) GT[p][j] = G[p][0] * T[0][j] + G[p][1] * T[1][j];
+#pragma unroll
+      for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) gS[i][j] = T[0][i] * GT[0][j] + T[1][i] * GT[1][j];
+#pragma unroll
+      for (int p = 0; p < 2; p++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) gT[p][j] = 2.f * (GT[p][0] * Sg[0][j] + GT[p][1] * Sg[1][j] + GT[p][2] * Sg[2][j]);
+      // T = J W -> J
+      const float gJ00 = gT[0][0] * W[0][0] + gT[0][1] * W[0][1] + gT[0][2] * W[0][2];
+      const float gJ02 = gT[0][0] * W[2][0] + gT[0][1] * W[2][1] + gT[0][2] * W[2][2];
+      const float gJ11 = gT[1][0] * W[1][0] + gT[1][1] * W[1][1] + gT[1][2] * W[1][2];
+      const float gJ12 = gT[1][0] * W[2][0] + gT[1][1] * W[2][1] + gT[1][2] * W[2][2];
+      float gt[3] = {0.f, 0.f, 0.f};
+      gt[2] += -(cam.fx * gJ00 + cam.fy * gJ11) * itz2 + (gJ02 * cam.fx * uxc + gJ12 * cam.fy * uyc) * itz2;
+      if (!clx) {
+        gt[0] += -gJ02 * cam.fx * itz2;
+        gt[2] += gJ02 * cam.fx * t[0] * itz2 * itz;
+      }
+      if (!cly) {
+        gt[1] += -gJ12 * cam.fy * itz2;
+        gt[2] += gJ12 * cam.fy * t[1] * itz2 * itz;
+      }
+      // μ' -> t
+      gt[0] += gmx * cam.fx * itz;
+      gt[1] += gmy * cam.fy * itz;
+      gt[2] -= (gmx * cam.fx * t[0] + gmy * cam.fy * t[1]) * itz2;
+      // w -> v, σ, tz
+      const float gvplus = gw * ramp, gramp = gw * vplus;
+      if (ramp_raw > 0.f) {
+        gt[2] -= gramp / sigma;
+        gsig = gramp * tz / (sigma * sigma);
+      }
+      // colour / weight SH -> coefficients and direction
+      float gr0 = 0.f, gr1 = 0.f, gr2 = 0.f;
+      float gh[48];
+#pragma unroll
+      for (int ch = 0; ch < 3; ch++) {
+        const bool on = craw[ch] > 0.f;
+        const float g = on ? gc[ch] : 0.f;
+        float cf[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          gh[3 * j + ch] = g * Y[j];
+          cf[j] = g * hco[3 * j + ch];
+        }
+        float ax, ay, az;
+        sh_vjp(rx, ry, rz, cf, ax, ay, az);
+        gr0 += ax; gr1 += ay; gr2 += az;
+      }
+      float gv[16];
+      {
+        const float g = vraw > 0.f ? gvplus : 0.f;
+        float cf[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          gv[j] = g * Y[j];
+          cf[j] = g * vco[j];
+        }
+        float ax, ay, az;
+        sh_vjp(rx, ry, rz, cf, ax, ay, az);
+        gr0 += ax; gr1 += ay; gr2 += az;
+      }
+      const float rdot = rx * gr0 + ry * gr1 + rz * gr2;
+      float gmu[3];
+      gmu[0] = (gr0 - rx * rdot) * idn + W[0][0] * gt[0] + W[1][0] * gt[1] + W[2][0] * gt[2];
+      gmu[1] = (gr1 - ry * rdot) * idn + W[0][1] * gt[0] + W[1][1] * gt[1] + W[2][1] * gt[2];
+      gmu[2] = (gr2 - rz * rdot) * idn + W[0][2] * gt[0] + W[1][2] * gt[1] + W[2][2] * gt[2];
+      // Σ = M Mᵀ -> M -> (s, R)
+      float gM[3][3];
+#pragma unroll
+      for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++)
+          gM[i][j] = 2.f * (gS[i][0] * M[0][j] + gS[i][1] * M[1][j] + gS[i][2] * M[2][j]);
+      float gs[3];
+#pragma unroll
+      for (int j = 0; j < 3; j++) gs[j] = gM[0][j] * Rq[0][j] + gM[1][j] * Rq[1][j] + gM[2][j] * Rq[2][j];
+      float gR[3][3];
+#pragma unroll
+      for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) gR[i][j] = gM[i][j] * s[j];
+      float gq[4];
+      gq[0] = 2.f * (-qz * gR[0][1] + qy * gR[0][2] + qz * gR[1][0] - qx * gR[1][2] - qy * gR[2][0] + qx * gR[2][1]);
+      gq[1] = 2.f * (qy * gR[0][1] + qz * gR[0][2] + qy * gR[1][0] - 2.f * qx * gR[1][1] - qw * gR[1][2] +
+                     qz * gR[2][0] + qw * gR[2][1] - 2.f * qx * gR[2][2]);
+      gq[2] = 2.f * (-2.f * qy * gR[0][0] + qx * gR[0][1] + qw * gR[0][2] + qx * gR[1][0] + qz * gR[1][2] -
+                     qw * gR[2][0] + qz * gR[2][1] - 2.f * qy * gR[2][2]);
+      gq[3] = 2.f * (-2.f * qz * gR[0][0] - qw * gR[0][1] + qx * gR[0][2] + qw * gR[1][0] - 2.f * qz * gR[1][1] +
+                     qy * gR[1][2] + qx * gR[2][0] + qy * gR[2][1]);
+      const float qdot = qw * gq[0] + qx * gq[1] + qy * gq[2] + qz * gq[3];
+      const float gqr[4] = {(gq[0] - qw * qdot) * iqn, (gq[1] - qx * qdot) * iqn, (gq[2] - qy * qdot) * iqn,
+                            (gq[3] - qz * qdot) * iqn};
+      // ---- accumulate into the gradient row (+=, scaled) ----
+      float4* gr = grad + (size_t)k * kRow4;
+      float4 v;
+      v = gr[0]; v.x += scale * gmu[0]; v.y += scale * gmu[1]; v.z += scale * gmu[2]; v.w += scale * go; gr[0] = v;
+      v = gr[1]; v.x += scale * gqr[0]; v.y += scale * gqr[1]; v.z += scale * gqr[2]; v.w += scale * gqr[3]; gr[1] = v;
+      v = gr[2]; v.x += scale * gs[0]; v.y += scale * gs[1]; v.z += scale * gs[2]; gr[2] = v;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        v = gr[3 + q];
+        v.x += scale * gv[4 * q]; v.y += scale * gv[4 * q + 1]; v.z += scale * gv[4 * q + 2]; v.w += scale * gv[4 * q + 3];
+        gr[3 + q] = v;
+      }
+#pragma unroll
+      for (int q = 0; q < 12; q++) {
+        v = gr[7 + q];
+        v.x += scale * gh[4 * q]; v.y += scale * gh[4 * q + 1]; v.z += scale * gh[4 * q + 2]; v.w += scale * gh[4 * q + 3];
+        gr[7 + q] = v;
+      }
+      if (dL_dcov) {
+        float* dc = dL_dcov + (size_t)k * 6;
+        dc[0] += scale * gS[0][0];
+        dc[1] += scale * (gS[0][1] + gS[1][0]);
+        dc[2] += scale * (gS[0][2] + gS[2][0]);
+        dc[3] += scale * gS[1][1];
+        dc[4] += scale * (gS[1][2] + gS[2][1]);
+        dc[5] += scale * gS[2][2];
+      }
+    }
+  }
+  // σ: warp reduce, one atomic per warp
+  gsig = warp_sum(gsig * scale);
+  if ((threadIdx.x & 31) == 0 && gsig != 0.f) atomicAdd(dL_dsigma, gsig);
+}
+
+// --------------------------------------------------------------------------- launchers ----
+size_t bwd_ws_bytes(int32_t n_tiles, int32_t n_slots, int64_t capacity) {
+  int64_t max_items = capacity / 32 + n_tiles + 1;
+  return align_up((size_t)n_slots * 12 * sizeof(float)) + align_up((size_t)(n_tiles + 1) * 4) * 2 +
+         align_up((size_t)max_items * 4) + align_up(16) + scan_tmp_bytes(n_tiles);
+}
+
+void launch_coef(const DevCam& cam, const float* state, const float* dL_dimage, const float* target, int32_t loss,
+                 float* coef4, float* coefa, cudaStream_t st) {
+  int n_tiles = cam.TX * cam.TY;
+  k_coef<<<n_tiles, 256, 0, st>>>(cam, state, dL_dimage, target, loss, reinterpret_cast<float4*>(coef4), coefa);
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sigma, const int32_t* idx,
+                          int32_t n_slots, const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
+                          int64_t capacity, const float* coef4, const float* coefa, float scale, float* grad,
+                          float* dL_dsigma, float* dL_dcov, void* ws, cudaStream_t st) {
+  if (n_slots <= 0) return;
+  const int n_tiles = cam.TX * cam.TY;
+  const int64_t max_items = capacity / 32 + n_tiles + 1;
+  Carve cv(ws);
+  float* acc2d = cv.take<float>((size_t)n_slots * 12);
+  int32_t* counts = cv.take<int32_t>(n_tiles + 1);
+  int32_t* item_offs = cv.take<int32_t>(n_tiles + 1);
+  int32_t* items = cv.take<int32_t>(max_items);
+  int32_t* counter = cv.take<int32_t>(4);
+  void* tmp = cv.take<char>(scan_tmp_bytes(n_tiles));
+  cudaMemsetAsync(acc2d, 0, sizeof(float) * 12 * (size_t)n_slots, st);
+  cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
+  const int tb = (n_tiles + 255) / 256;
+  k_chunk_counts<<<tb, 256, 0, st>>>(tile_offsets, n_tiles, capacity, counts);
+  launch_exclusive_scan(counts, item_offs, n_tiles, tmp, st);
+  k_chunk_emit<<<tb, 256, 0, st>>>(item_offs, n_tiles, items);
+  const int blocks = sm_count() * 6;  // persistent: 6 × 8 warps per SM, dynamic item claiming
+  k_moments<<<blocks, kMomentsThreads, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), pair_slot, tile_offsets,
+                                                capacity, items, item_offs, item_offs + n_tiles, counter,
+                                                reinterpret_cast<const float4*>(coef4), coefa, acc2d);
+  k_epilogue<<<(n_slots + 127) / 128, 128, 0, st>>>(cam, reinterpret_cast<const float4*>(rows), sigma, idx, n_slots,
+                                                    reinterpret_cast<const float4*>(rec),
+                                                    reinterpret_cast<const float4*>(acc2d), scale,
+                                                    reinterpret_cast<float4*>(grad), dL_dsigma, dL_dcov);
+}
+
+}  // namespace oit

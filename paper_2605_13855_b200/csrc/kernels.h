@@ -1,0 +1,66 @@
+// kernels.h — internal launchers of liboit (host side). The C-ABI in capi.cu validates
+// arguments, carves workspaces and calls these; every launcher is asynchronous on `st`.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace oit {
+
+// project.cu — a1
+void launch_project(const DevCam& cam, const float* rows, const float* sigma, const int32_t* idx, int32_t n_slots,
+                    float* rec, int32_t* tiles_per_slot, cudaStream_t st);
+
+// scan.cu — exclusive scan of n int32 counts; out[n] = total. tmp: scan_tmp_bytes(n).
+size_t scan_tmp_bytes(int64_t n);
+void launch_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, void* tmp, cudaStream_t st);
+
+// bin.cu — a2
+size_t bin_ws_bytes(int32_t n_tiles);
+void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_slot, int32_t n_slots,
+                int32_t* pair_slot, int64_t capacity, int32_t* tile_offsets, int64_t* d_n_pairs,
+                int64_t* d_max_pairs, void* ws, cudaStream_t st);
+
+// composite_fwd.cu — a3
+void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pair_slot,
+                          const int32_t* tile_offsets, int64_t capacity, const float* base, const uint8_t* route,
+                          float* image, float* state, float* base_out, cudaStream_t st);
+
+// composite_bwd.cu — a4 coefficients, a5 moments, a6 epilogue
+size_t bwd_ws_bytes(int32_t n_tiles, int32_t n_slots, int64_t capacity);
+void launch_coef(const DevCam& cam, const float* state, const float* dL_dimage, const float* target, int32_t loss,
+                 float* coef4, float* coefa, cudaStream_t st);
+void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sigma, const int32_t* idx,
+                          int32_t n_slots, const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
+                          int64_t capacity, const float* coef4, const float* coefa, float scale, float* grad,
+                          float* dL_dsigma, float* dL_dcov, void* ws, cudaStream_t st);
+
+// loss / select / update — a4, a7, a8
+void launch_loss_grad(const DevCam& cam, const float* image, const float* target, int32_t loss, float* g,
+                      cudaStream_t st);
+void launch_fps(const float* centers, int32_t V, int32_t S, uint64_t seed, uint32_t refresh, int32_t* out,
+                cudaStream_t st);
+size_t update_ws_bytes(int32_t n_total);
+void launch_update(const float* score_grad, const int32_t* score_idx, int32_t n_score, const float eps[6],
+                   int32_t mode, int32_t n_total, uint32_t* bits, int32_t* active_idx, int32_t* d_n_active,
+                   int32_t* frozen, int32_t* d_n_frozen, int32_t* activated, int32_t* d_n_activated, void* ws,
+                   cudaStream_t st);
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// Bump allocator over a caller workspace.
+struct Carve {
+  char* base;
+  size_t off = 0;
+  explicit Carve(void* p) : base(static_cast<char*>(p)) {}
+  template <class T>
+  T* take(size_t count) {
+    T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    off += align_up(count * sizeof(T));
+    return p;
+  }
+};
+
+}  // namespace oit

@@ -1,0 +1,67 @@
+"""Buffer management around the C-ABI for one camera shape (PyTorch = device memory + streams).
+
+``ViewPipeline`` owns the per-view scratch of the hot path (records, pair lists, pixel state,
+workspaces) and runs a1 → a2 → a3 (forward) and a4 → a5 → a6 (backward) for one view by
+calling the ``oit_*`` entry points. It performs no arithmetic of its own.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib as L
+
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+class ViewPipeline:
+    def __init__(self, cam: dict, max_slots: int, pair_capacity: int, device="cuda"):
+        self.cam = cam
+        self.device = device
+        self.W, self.H = int(cam["width"]), int(cam["height"])
+        self.n_tiles = L.num_tiles(cam)
+        self.max_slots = int(max_slots)
+        self.capacity = int(pair_capacity)
+        dev = device
+        self.rec = torch.empty((max(self.max_slots, 1), L.OIT_REC), dtype=torch.float32, device=dev)
+        self.tps = torch.empty(max(self.max_slots, 1), dtype=torch.int32, device=dev)
+        self.pairs = torch.empty(max(self.capacity, 1), dtype=torch.int32, device=dev)
+        self.offs = torch.empty(self.n_tiles + 1, dtype=torch.int32, device=dev)
+        self.n_pairs = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.bin_ws = _ws(L.oit_bin_workspace_bytes(cam), dev)
+        self.bwd_ws = _ws(L.oit_bwd_workspace_bytes(cam, self.max_slots, self.capacity), dev)
+        self.state = torch.empty((5, self.n_tiles, 256), dtype=torch.float32, device=dev)
+        self.image = torch.empty((3, self.H, self.W), dtype=torch.float32, device=dev)
+
+    def set_camera(self, cam: dict):
+        assert int(cam["width"]) == self.W and int(cam["height"]) == self.H
+        self.cam = cam
+
+    def project_bin(self, rows, sigma, idx, stream=None):
+        n = int(idx.numel())
+        assert n <= self.max_slots
+        rec, tps = self.rec[:n], self.tps[:n]
+        L.oit_project_cull(rows, sigma, self.cam, idx, rec, tps, stream)
+        L.oit_bin_tiles(self.cam, rec, tps, n, self.pairs, self.offs, self.n_pairs, self.bin_ws, stream)
+        return rec
+
+    def forward(self, rows, sigma, idx, bg, base=None, route=None, base_out=None, image=True, stream=None):
+        """a1-a3: returns (image or None, state). ``state`` is this pipeline's buffer."""
+        rec = self.project_bin(rows, sigma, idx, stream)
+        L.oit_composite_fwd(self.cam, rec, self.pairs, self.offs, bg, base=base, route=route,
+                            image=self.image if image else None, state=self.state, base_out=base_out,
+                            stream=stream)
+        return (self.image if image else None), self.state
+
+    def backward(self, rows, sigma, idx, bg, state, dL_dimage, grad, dL_dsigma, dL_dcov=None, scale=1.0,
+                 reuse_bins=True, stream=None):
+        """a4-a6 for the splats idx (grad rows += ...). With reuse_bins the records/pairs of the
+        preceding forward over the same idx are reused."""
+        n = int(idx.numel())
+        rec = self.rec[:n] if reuse_bins else self.project_bin(rows, sigma, idx, stream)
+        L.oit_composite_bwd(rows, sigma, self.cam, idx, rec, self.pairs, self.offs, bg, state, dL_dimage, grad,
+                            dL_dsigma, self.bwd_ws, dL_dcov=dL_dcov, scale=scale, stream=stream)
+
+    def pairs_used(self) -> int:
+        return int(self.n_pairs.item())

@@ -1,0 +1,326 @@
+"""GPU ↔ oracle parity through the C-ABI (liboit.so) on seeded synthetic scenes.
+
+Bars (north star / DESIGN.md): decision fields, rectangles, tile lists, membership and FPS
+indices bit-exact; images within 1e-5 absolute; gradients within 1e-4 relative with a 1e-6
+absolute floor (elementwise).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2605_13855_b200 import synth
+from tests.helpers import decode_rect, grad_close, plain_to_tile_major, tile_major_to_plain
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+
+
+def _L():
+    from paper_2605_13855_b200 import _lib
+    return _lib
+
+
+def _pipe(cam, n, cap=1 << 20):
+    from paper_2605_13855_b200.pipeline import ViewPipeline
+    return ViewPipeline(cam, max(n, 1), cap, device=DEV)
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def _scenes():
+    out = [synth.scene_c1()]
+    out.append(synth.scene_c2(n=20000, n_views=3, res=200))     # 13×13 tiles: ragged tail (200 = 12.5·16)
+    sc = synth.scene_c1(seed=9, n=2000, n_views=2, res=64)
+    for c in sc.cams:                                            # non-square, ragged both ways
+        c["width"], c["height"], c["cx"], c["cy"] = 100, 75, 50.0, 37.5
+    out.append(sc)
+    return out
+
+
+SCENES = _scenes()
+
+
+@pytest.fixture(scope="module", params=range(len(SCENES)), ids=["C1", "C2s-200", "ragged-100x75"])
+def scene(request):
+    return SCENES[request.param]
+
+
+# ------------------------------------------------------------------ a1 project_cull ------
+def test_project_cull_bitexact(scene):
+    L = _L()
+    rows, sigma = _t(scene.rows), _t(np.array([scene.sigma], np.float32))
+    g = np.random.default_rng(0)
+    idx = g.permutation(scene.n).astype(np.int32)           # any order (compacted active list)
+    for cam in scene.cams:
+        rec = torch.empty((scene.n, 16), dtype=torch.float32, device=DEV)
+        tps = torch.empty(scene.n, dtype=torch.int32, device=DEV)
+        L.oit_project_cull(rows, sigma, cam, _t(idx), rec, tps)
+        r = rec.cpu().numpy()
+        sp = O.project_spec(scene.rows, idx, cam)
+        pv = O.project_value(scene.rows, scene.sigma, idx, cam)
+        vis = sp["visible"]
+        x0, y0, x1, y1 = decode_rect(r)
+        assert np.array_equal(np.stack([x0, y0, x1, y1], 1)[vis], sp["rect"][vis])
+        assert np.all((x0 == x1)[~vis]) and np.all(tps.cpu().numpy()[~vis] == 0)
+        assert np.array_equal(tps.cpu().numpy()[vis], ((x1 - x0) * (y1 - y0))[vis])
+        for col, key in [(0, "mx"), (1, "my"), (2, "nA"), (3, "nB"), (4, "nC"), (5, "thr_lo"), (6, "thr_hi"),
+                         (14, "ex"), (15, "ey")]:
+            assert np.array_equal(r[vis, col].view(np.uint32), sp[key][vis].view(np.uint32)), key
+        assert np.allclose(r[vis, 8:11], pv["color"][vis], atol=2e-6, rtol=0)
+        assert np.allclose(r[vis, 11], pv["w"][vis], atol=2e-6, rtol=2e-6)
+        assert np.allclose(r[vis, 7], np.log2(pv["o"][vis]), atol=1e-6)
+        assert vis.sum() > 0.5 * scene.n
+
+
+def test_project_cull_empty_and_errors():
+    L = _L()
+    sc = SCENES[0]
+    rows, sigma = _t(sc.rows), _t(np.array([sc.sigma], np.float32))
+    rec = torch.empty((1, 16), dtype=torch.float32, device=DEV)
+    tps = torch.empty(1, dtype=torch.int32, device=DEV)
+    L.oit_project_cull(rows, sigma, sc.cams[0], torch.empty(0, dtype=torch.int32, device=DEV), rec, tps)
+    bad = dict(sc.cams[0])
+    bad["width"] = 0
+    with pytest.raises(L.OitError):
+        L.oit_project_cull(rows, sigma, bad, _t(np.arange(10, dtype=np.int32)), rec, tps)
+
+
+# ------------------------------------------------------------------ a2 bin_tiles ---------
+def test_bin_tiles_bitexact(scene):
+    idx = np.arange(scene.n, dtype=np.int32)
+    for cam in scene.cams:
+        p = _pipe(cam, scene.n)
+        p.project_bin(_t(scene.rows), _t(np.array([scene.sigma], np.float32)), _t(idx))
+        n = p.pairs_used()
+        pairs = p.pairs[:n].cpu().numpy()
+        offs = p.offs.cpu().numpy()
+        ref_pairs, ref_offs = O.bin_tiles(scene.rows, idx, cam)
+        assert n == len(ref_pairs)
+        assert np.array_equal(offs, ref_offs)
+        for t in range(len(offs) - 1):       # the per-tile SET is unique (order unspecified, R15)
+            assert np.array_equal(np.sort(pairs[offs[t]:offs[t + 1]]), ref_pairs[ref_offs[t]:ref_offs[t + 1]])
+
+
+def test_bin_tiles_overflow_is_reported_and_safe():
+    sc = SCENES[0]
+    cam = sc.cams[0]
+    idx = np.arange(sc.n, dtype=np.int32)
+    ref_pairs, _ = O.bin_tiles(sc.rows, idx, cam)
+    p = _pipe(cam, sc.n, cap=100)
+    p.forward(_t(sc.rows), _t(np.array([sc.sigma], np.float32)), _t(idx), sc.bg)
+    torch.cuda.synchronize()
+    assert p.pairs_used() == len(ref_pairs) > 100
+
+
+# ------------------------------------------------------------------ a3 composite_fwd -----
+def test_composite_fwd_parity(scene):
+    idx = np.arange(scene.n, dtype=np.int32)
+    for cam in scene.cams:
+        p = _pipe(cam, scene.n)
+        img, state = p.forward(_t(scene.rows), _t(np.array([scene.sigma], np.float32)), _t(idx), scene.bg)
+        ref = O.render(scene.rows, scene.sigma, idx, cam, scene.bg, mode="brute")
+        W, H = cam["width"], cam["height"]
+        assert np.abs(img.cpu().numpy() - ref["image"]).max() < 1e-5
+        st = tile_major_to_plain(state.cpu().numpy(), W, H)
+        assert np.allclose(st, ref["state"], rtol=1e-5, atol=1e-6)
+
+
+def test_composite_fwd_cache_decomposition_and_fold():
+    """render(𝒜 over cache(𝒜̄)) = render(𝒜 ∪ 𝒜̄) (§4.1); FOLD routing bakes into base_out."""
+    sc = SCENES[1]
+    mask = synth.active_mask(sc, 0.2, "clustered")
+    act, ina = np.flatnonzero(mask).astype(np.int32), np.flatnonzero(~mask).astype(np.int32)
+    cam = sc.cams[0]
+    W, H = cam["width"], cam["height"]
+    rows, sigma = _t(sc.rows), _t(np.array([sc.sigma], np.float32))
+    p = _pipe(cam, sc.n)
+    _, st_in = p.forward(rows, sigma, _t(ina), sc.bg, image=False)
+    cache = st_in.clone()
+    img, st = p.forward(rows, sigma, _t(act), sc.bg, base=cache)
+    ref = O.render(sc.rows, sc.sigma, np.arange(sc.n), cam, sc.bg)
+    assert np.abs(img.cpu().numpy() - ref["image"]).max() < 1e-5
+    # FOLD half the active slots into a copy of the cache
+    route = (np.arange(len(act)) % 2).astype(np.uint8)
+    base_out = torch.empty_like(cache)
+    img2, _ = p.forward(rows, sigma, _t(act), sc.bg, base=cache, route=_t(route), base_out=base_out)
+    assert np.abs(img2.cpu().numpy() - ref["image"]).max() < 1e-5
+    ref_bo = O.render(sc.rows, sc.sigma, np.concatenate([ina, act[route == 1]]), cam, sc.bg)["state"]
+    assert np.allclose(tile_major_to_plain(base_out.cpu().numpy(), W, H), ref_bo, rtol=1e-5, atol=1e-6)
+    # also with an oracle-built cache as input (no GPU value on the oracle side)
+    oc = O.render(sc.rows, sc.sigma, ina, cam, sc.bg)["state"]
+    img3, _ = p.forward(rows, sigma, _t(act), sc.bg, base=_t(plain_to_tile_major(oc, W, H).astype(np.float32)))
+    assert np.abs(img3.cpu().numpy() - ref["image"]).max() < 1e-5
+
+
+def test_composite_fwd_empty_and_permutation():
+    sc = SCENES[0]
+    cam = sc.cams[1]
+    rows, sigma = _t(sc.rows), _t(np.array([sc.sigma], np.float32))
+    p = _pipe(cam, sc.n)
+    img, _ = p.forward(rows, sigma, torch.empty(0, dtype=torch.int32, device=DEV), sc.bg)
+    assert np.array_equal(img.cpu().numpy(), np.broadcast_to(sc.bg[:, None, None], img.shape).astype(np.float32))
+    idx = np.arange(sc.n, dtype=np.int32)
+    a, _ = p.forward(rows, sigma, _t(idx), sc.bg)
+    a = a.cpu().numpy().copy()
+    b, _ = p.forward(rows, sigma, _t(np.random.default_rng(1).permutation(idx).astype(np.int32)), sc.bg)
+    assert np.abs(a - b.cpu().numpy()).max() < 1e-5
+
+
+# ------------------------------------------------------------------ a4-a6 backward -------
+def _bwd_case(sc, cam, idx, seed=5, base=None):
+    rows, sigma = _t(sc.rows), _t(np.array([sc.sigma], np.float32))
+    p = _pipe(cam, len(idx))
+    _, state = p.forward(rows, sigma, _t(idx), sc.bg, base=base)
+    g = synth.dl_dimage(cam, seed)
+    grad = torch.zeros((len(idx), 80), dtype=torch.float32, device=DEV)
+    dsig = torch.zeros(1, dtype=torch.float32, device=DEV)
+    dcov = torch.zeros((len(idx), 6), dtype=torch.float32, device=DEV)
+    p.backward(rows, sigma, _t(idx), sc.bg, state, _t(g), grad, dsig, dL_dcov=dcov)
+    return grad.cpu().numpy(), float(dsig.item()), dcov.cpu().numpy(), g
+
+
+def test_composite_bwd_parity(scene):
+    idx = np.arange(scene.n, dtype=np.int32)
+    for cam in scene.cams:
+        grad, dsig, dcov, g = _bwd_case(scene, cam, idx)
+        ref = O.render(scene.rows, scene.sigma, idx, cam, scene.bg)
+        gref, dsref, cref = O.backward(scene.rows, scene.sigma, idx, cam, scene.bg, ref["state"], g)
+        ok, bad = grad_close(grad, gref)
+        assert ok, f"{bad.sum()} mismatches; worst rows {np.unique(np.nonzero(bad)[0])[:5]} fields {np.unique(np.nonzero(bad)[1])}"
+        assert abs(dsig - dsref) <= 1e-4 * abs(dsref) + 1e-6
+        ok, _ = grad_close(dcov, cref)
+        assert ok
+        assert np.abs(gref).max() > 0
+
+
+def test_composite_bwd_through_cache_matches_full():
+    """Gradients of 𝒜 computed over a cache equal the 𝒜-rows of the full backward (frozen-exactness)."""
+    sc = SCENES[1]
+    cam = sc.cams[1]
+    mask = synth.active_mask(sc, 0.3, "uniform")
+    act, ina = np.flatnonzero(mask).astype(np.int32), np.flatnonzero(~mask).astype(np.int32)
+    W, H = cam["width"], cam["height"]
+    oc = O.render(sc.rows, sc.sigma, ina, cam, sc.bg)["state"]
+    grad, dsig, _, g = _bwd_case(sc, cam, act, base=_t(plain_to_tile_major(oc, W, H).astype(np.float32)))
+    full = O.render(sc.rows, sc.sigma, np.arange(sc.n), cam, sc.bg)
+    gref, dsref, _ = O.backward(sc.rows, sc.sigma, act, cam, sc.bg, full["state"], g)
+    ok, bad = grad_close(grad, gref)
+    assert ok, bad.sum()
+
+
+def test_loss_grad_kernel():
+    L = _L()
+    cam = SCENES[0].cams[0]
+    g = np.random.default_rng(2)
+    img = g.random((3, 64, 64)).astype(np.float32)
+    tgt = g.random((3, 64, 64)).astype(np.float32)
+    tgt[0, 0, :8] = img[0, 0, :8]
+    out = torch.empty((3, 64, 64), dtype=torch.float32, device=DEV)
+    for loss in ("l1", "l2"):
+        L.oit_loss_grad(cam, _t(img), _t(tgt), loss, out)
+        ref = O.loss_grad(img.astype(np.float64), tgt.astype(np.float64), loss)
+        assert np.allclose(out.cpu().numpy(), ref, rtol=1e-6, atol=1e-12)
+        if loss == "l1":
+            assert np.array_equal(np.sign(out.cpu().numpy()), np.sign(ref))
+
+
+# ------------------------------------------------------------------ a7 select / score ----
+@pytest.mark.parametrize("V,S,seed,refresh", [(4, 2, 7, 0), (100, 5, 1, 3), (300, 30, 123, 9), (300, 300, 5, 1),
+                                              (1, 1, 0, 0), (2000, 64, 99, 17)])
+def test_select_views_bitexact(V, S, seed, refresh):
+    L = _L()
+    if V <= 300:
+        cams = synth.scene_c3(n=10, n_views=V).cams
+        centers = synth.camera_centers(cams)
+    else:
+        centers = synth.rng(seed).normal(size=(V, 3)).astype(np.float32)
+    out = torch.empty(S, dtype=torch.int32, device=DEV)
+    L.oit_select_views(_t(centers), S, seed, refresh, out)
+    assert np.array_equal(out.cpu().numpy(), O.fps(centers, S, seed, refresh))
+
+
+@pytest.mark.parametrize("loss", ["l1", "l2"])
+def test_score_subsample_parity(loss):
+    L = _L()
+    sc = synth.scene_c2(n=8000, n_views=6, res=96)
+    mask = synth.active_mask(sc, 0.25, "clustered")
+    act, ina = np.flatnonzero(mask).astype(np.int32), np.flatnonzero(~mask).astype(np.int32)
+    caches_o = [O.render(sc.rows, sc.sigma, ina, c, sc.bg)["state"] for c in sc.cams]
+    # targets = oracle image ± an offset bounded away from 0 (so the L1 sign is unambiguous)
+    targets = []
+    for k, c in enumerate(sc.cams):
+        img = O.render(sc.rows, sc.sigma, np.arange(sc.n), c, sc.bg)["image"]
+        off = synth.rng(300 + k).uniform(0.01, 0.1, img.shape) * np.where(synth.rng(400 + k).random(img.shape) < 0.5, -1, 1)
+        targets.append((img + off).astype(np.float32))
+    views = [0, 3, 5]
+    ref, dsref = O.score_subsample(sc.rows, sc.sigma, sc.cams, targets, caches_o, act, ina, views, sc.bg, loss)
+    W, H = sc.cams[0]["width"], sc.cams[0]["height"]
+    caches = [_t(plain_to_tile_major(c, W, H).astype(np.float32)) for c in caches_o]
+    cap = 1 << 20
+    ws = torch.empty(L.oit_score_workspace_bytes(sc.cams[0], len(act), len(ina), cap), dtype=torch.uint8, device=DEV)
+    sg = torch.zeros((len(ina), 80), dtype=torch.float32, device=DEV)
+    dsig = torch.zeros(1, dtype=torch.float32, device=DEV)
+    mp = torch.zeros(1, dtype=torch.int64, device=DEV)
+    L.oit_score_subsample(_t(sc.rows), _t(np.array([sc.sigma], np.float32)), sc.cams, [_t(t) for t in targets],
+                          caches, _t(act), _t(ina), views, loss, sc.bg, sg, dsig, cap, mp, ws)
+    torch.cuda.synchronize()
+    assert 0 < mp.item() <= cap
+    ok, bad = grad_close(sg.cpu().numpy(), ref, rtol=1e-4, atol=1e-9 if loss == "l1" else 1e-8)
+    assert ok, bad.sum()
+
+
+# ------------------------------------------------------------------ a8 update ------------
+@pytest.mark.parametrize("mode", ["fresh", "monotone"])
+def test_update_active_set_bitexact(mode):
+    L = _L()
+    n = 100_003
+    g = synth.rng(77)
+    old_mask = g.random(n) < 0.3
+    score_idx = np.sort(g.choice(n, 40_000, replace=False)).astype(np.int32)
+    sgrad = (g.normal(size=(len(score_idx), 80)) * g.choice([1e-4, 1e-2, 1.0], size=(len(score_idx), 1))).astype(np.float32)
+    eps = np.array([0.05, 0.02, 0.03, 0.01, 0.2, 0.1], np.float32)
+    bits0 = synth.bits_from_mask(old_mask)
+    ref_bits, ref_act, ref_fro, ref_new = O.update_active(sgrad, score_idx, eps, mode, n, bits0)
+    bits = _t(bits0.view(np.int32))
+    act = torch.empty(n, dtype=torch.int32, device=DEV)
+    fro = torch.empty(n, dtype=torch.int32, device=DEV)
+    new = torch.empty(n, dtype=torch.int32, device=DEV)
+    cnt = torch.zeros(3, dtype=torch.int32, device=DEV)
+    ws = torch.empty(L.oit_update_workspace_bytes(n), dtype=torch.uint8, device=DEV)
+    L.oit_update_active_set(_t(sgrad), _t(score_idx), eps, mode, n, bits, act, cnt[0:1], fro, cnt[1:2], new,
+                            cnt[2:3], ws)
+    c = cnt.cpu().numpy()
+    assert np.array_equal(bits.cpu().numpy().view(np.uint32), ref_bits)
+    assert np.array_equal(act[:c[0]].cpu().numpy(), ref_act)
+    assert np.array_equal(fro[:c[1]].cpu().numpy(), ref_fro)
+    assert np.array_equal(new[:c[2]].cpu().numpy(), ref_new)
+    assert 0 < len(ref_act) < n
+
+
+# ------------------------------------------------------------------ full-size sampled ----
+@pytest.mark.slow
+def test_c2_full_size_parity_sampled():
+    """configs[1] (300k splats, 800×800) at ρ = 0.2, the launch configuration bench.py times:
+    rectangles/tile sets exact; image within 1e-5; sampled gradient rows within the bar."""
+    sc = synth.scene_c2(n_views=2)
+    mask = synth.active_mask(sc, 0.2, "clustered")
+    act = np.flatnonzero(mask).astype(np.int32)
+    cam = sc.cams[1]
+    rows, sigma = _t(sc.rows), _t(np.array([sc.sigma], np.float32))
+    p = _pipe(cam, len(act), cap=1 << 23)
+    img, state = p.forward(rows, sigma, _t(act), sc.bg)
+    ref = O.render(sc.rows, sc.sigma, act, cam, sc.bg)
+    assert np.abs(img.cpu().numpy() - ref["image"]).max() < 1e-5
+    assert p.pairs_used() == ref["tile_pairs"]
+    g = synth.dl_dimage(cam, 11)
+    grad = torch.zeros((len(act), 80), dtype=torch.float32, device=DEV)
+    dsig = torch.zeros(1, dtype=torch.float32, device=DEV)
+    p.backward(rows, sigma, _t(act), sc.bg, state, _t(g), grad, dsig)
+    sample = np.sort(synth.rng(5).choice(len(act), 2000, replace=False))
+    gref, _, _ = O.backward(sc.rows, sc.sigma, act[sample], cam, sc.bg, ref["state"], g)
+    ok, bad = grad_close(grad.cpu().numpy()[sample], gref)
+    assert ok, bad.sum()
