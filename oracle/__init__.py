@@ -172,6 +172,23 @@ def backward(rows32, sigma, idx, cam, bg, state, dL_dC, mode: str = "rect", rows
     return grad, float(dsig[0]), dcov
 
 
+def backward_bound(rows32, sigma, idx, cam, bg, state, dL_dC, mode: str = "rect"):
+    """``backward`` plus, per splat and row field, the forward-error scale of the gradient:
+    Σ_k |∂row/∂G2_k|·Σ_pairs|term_k| (the 2D-gradient terms' magnitudes before cancellation,
+    through |chain Jacobian|). Test bookkeeping for the fp32 tolerance (R31), not part
+    of the method. Returns (grad, dsigma, dcov, bound)."""
+    rows32, idx = _f32(rows32), _i32(idx)
+    rows64 = _f64(rows32)
+    grad = np.zeros((len(idx), ROW))
+    bound = np.zeros((len(idx), ROW))
+    dcov = np.zeros((len(idx), 6))
+    dsig = np.zeros(1)
+    lib().orc_backward_bound(_p(rows32), _p(rows64), C.c_double(sigma), _p(idx), C.c_int32(len(idx)),
+                             C.byref(camera(cam)), _p(_f64(bg)), _p(_f64(state)), _p(_f64(dL_dC)),
+                             C.c_int32(0 if mode == "brute" else 1), _p(grad), _p(dsig), _p(dcov), _p(bound))
+    return grad, float(dsig[0]), dcov, bound
+
+
 def loss_grad(image, target, loss: str = "l1") -> np.ndarray:
     """dL/dC of the mean L1 (sign(0)=0) or L2 loss over 3HW (3DGS L1 term; R24)."""
     image, target = _f64(image), _f64(target)
@@ -217,18 +234,22 @@ def update_active(score_grad32, score_idx, eps32, mode: str, n_total: int, bits)
 
 
 def score_subsample(rows32, sigma, cams, targets, caches, active_idx, score_idx, views, bg,
-                    loss: str = "l1", mode: str = "rect"):
+                    loss: str = "l1", mode: str = "rect", with_bound: bool = False):
     """Subsampled gradient score (Alg. 1 l.8-12; §4.1): for each subsampled
     view j, the full-𝒢 pixel state is the cached frozen-set accumulators ⊕ the active set
     (R16); L_j's gradient (R20, R24) is back-propagated to the scored splats; the mean over
-    the S views is returned (R19) as (score_grad [n_score,80], dsigma)."""
+    the S views is returned (R19) as (score_grad [n_score,80], dsigma[, bound])."""
     acc = np.zeros((len(score_idx), ROW))
+    bnd = np.zeros((len(score_idx), ROW))
     dsig = 0.0
     for j in views:
         cam = cams[j]
         fwd = render(rows32, sigma, active_idx, cam, bg, base=caches[j], mode=mode)
         g = loss_grad(fwd["image"], targets[j], loss)
-        gr, ds, _ = backward(rows32, sigma, score_idx, cam, bg, fwd["state"], g, mode=mode)
+        gr, ds, _, b = backward_bound(rows32, sigma, score_idx, cam, bg, fwd["state"], g, mode=mode)
         acc += gr
+        bnd += b
         dsig += ds
+    if with_bound:
+        return acc / len(views), dsig / len(views), bnd / len(views)
     return acc / len(views), dsig / len(views)

@@ -613,9 +613,28 @@ static void chain_to_params(const double* row, double sigma, const orc_camera* c
  * (the splats being differentiated are part of it, possibly through a cache), the loss gradient
  * dL_dC [3][H][W] and the background, accumulate grad[k][80] for the n_slots splats idx[k]
  * (+=), *dsigma (+=) and dcov[k][6] (+=, may be NULL). mode as in orc_render. */
+void orc_backward_bound(const float* rows_dec, const double* rows_val, double sigma, const int32_t* idx,
+                        int32_t n_slots, const orc_camera* cam, const double* bg, const double* state,
+                        const double* dL_dC, int32_t mode, double* grad, double* dsigma, double* dcov,
+                        double* bound);
+
 void orc_backward(const float* rows_dec, const double* rows_val, double sigma, const int32_t* idx,
                   int32_t n_slots, const orc_camera* cam, const double* bg, const double* state,
                   const double* dL_dC, int32_t mode, double* grad, double* dsigma, double* dcov) {
+    orc_backward_bound(rows_dec, rows_val, sigma, idx, n_slots, cam, bg, state, dL_dC, mode, grad, dsigma,
+                       dcov, NULL);
+}
+
+/* Same as orc_backward; if bound != NULL it also receives, per splat and row field, a
+ * forward-error scale for the gradient (NOT part of the method): Σ_k |∂row/∂G2_k|·Σ_pairs|term_k|,
+ * i.e. the magnitude of the per-pair terms each 2D gradient component G2_k sums (before any
+ * cancellation), pushed through the absolute value of the splat's chain-rule Jacobian, which is
+ * obtained column by column by applying the (linear) chain to unit 2D gradients. A floating-point
+ * evaluation that rounds each term with relative error u has an error of order u·bound. */
+void orc_backward_bound(const float* rows_dec, const double* rows_val, double sigma, const int32_t* idx,
+                        int32_t n_slots, const orc_camera* cam, const double* bg, const double* state,
+                        const double* dL_dC, int32_t mode, double* grad, double* dsigma, double* dcov,
+                        double* bound) {
     int Wd = cam->width, H = cam->height;
     size_t np = (size_t)Wd * H;
     for (int32_t k = 0; k < n_slots; k++) {
@@ -626,8 +645,9 @@ void orc_backward(const float* rows_dec, const double* rows_val, double sigma, c
         orc_val v;
         const double* row = rows_val + (size_t)i * ROW;
         orc_value_project(row, sigma, cam, &v);
-        orc_g2 g;
+        orc_g2 g, ag;   /* ag: Σ |per-pair term| of each 2D component (error-bound bookkeeping only) */
         memset(&g, 0, sizeof(g));
+        memset(&ag, 0, sizeof(ag));
         int px0 = 0, px1 = Wd, py0 = 0, py1 = H;
         if (mode == 1) {
             px0 = s.x0 * 16; px1 = s.x1 * 16 < Wd ? s.x1 * 16 : Wd;
@@ -648,30 +668,55 @@ void orc_backward(const float* rows_dec, const double* rows_val, double sigma, c
                     gpx[c] = dL_dC[c * np + p];
                 }
                 /* Eq. B.2 */
-                double dL_dalpha = 0;
+                double dL_dalpha = 0, a_dL_dalpha = 0;
                 for (int c = 0; c < 3; c++) {
-                    double dC_dalpha = T / (1.0 - alpha) * (F[c] - bg[c]);
-                    if (Q > 0) dC_dalpha += (1.0 - T) * v.w / Q * (v.col[c] - F[c]);
-                    dL_dalpha += gpx[c] * dC_dalpha;
+                    double t1 = T / (1.0 - alpha) * (F[c] - bg[c]);
+                    double t2 = Q > 0 ? (1.0 - T) * v.w / Q * (v.col[c] - F[c]) : 0.0;
+                    dL_dalpha += gpx[c] * (t1 + t2);
+                    a_dL_dalpha += fabs(gpx[c]) * (fabs(t1) + fabs(t2));
                     if (Q > 0) {
                         double dC_dc = (1.0 - T) * alpha * v.w / Q;
                         double dC_dw = (1.0 - T) * alpha / Q * (v.col[c] - F[c]);
                         g.gc[c] += gpx[c] * dC_dc;
                         g.gw += gpx[c] * dC_dw;
+                        ag.gc[c] += fabs(gpx[c] * dC_dc);
+                        ag.gw += fabs(gpx[c]) * (1.0 - T) * alpha / Q * (fabs(v.col[c]) + fabs(F[c]));
                     }
                 }
                 if (clamped) continue;          /* α = 0.99 is constant in o and Σ', μ' */
                 /* α = o·exp(power): ∂α/∂o = α/o, ∂α/∂power = α */
                 double dL_dpower = dL_dalpha * alpha;
+                double a_dp = a_dL_dalpha * alpha;
                 g.go += dL_dalpha * alpha / v.o;
+                ag.go += a_dp / v.o;
                 /* power = -½(A dx² + C dy²) - B dx dy, dx = px - mx */
                 g.gA += dL_dpower * (-0.5 * dx * dx);
                 g.gB += dL_dpower * (-dx * dy);
                 g.gC += dL_dpower * (-0.5 * dy * dy);
                 g.gmx += dL_dpower * (v.A * dx + v.B * dy);
                 g.gmy += dL_dpower * (v.B * dx + v.C * dy);
+                ag.gA += a_dp * 0.5 * dx * dx;
+                ag.gB += a_dp * fabs(dx * dy);
+                ag.gC += a_dp * 0.5 * dy * dy;
+                ag.gmx += a_dp * (fabs(v.A * dx) + fabs(v.B * dy));
+                ag.gmy += a_dp * (fabs(v.B * dx) + fabs(v.C * dy));
             }
         chain_to_params(row, sigma, cam, &v, &g, grad + (size_t)k * ROW, dsigma, dcov ? dcov + (size_t)k * 6 : NULL);
+        if (bound) {
+            /* columns of the (linear) chain: apply it to each unit 2D gradient */
+            double* comp[10] = {&ag.gc[0], &ag.gc[1], &ag.gc[2], &ag.gw, &ag.go, &ag.gA, &ag.gB, &ag.gC, &ag.gmx, &ag.gmy};
+            for (int c = 0; c < 10; c++) {
+                if (*comp[c] == 0.0) continue;
+                orc_g2 e;
+                memset(&e, 0, sizeof(e));
+                double* ec[10] = {&e.gc[0], &e.gc[1], &e.gc[2], &e.gw, &e.go, &e.gA, &e.gB, &e.gC, &e.gmx, &e.gmy};
+                *ec[c] = 1.0;
+                double col[ROW], ds = 0;
+                memset(col, 0, sizeof(col));
+                chain_to_params(row, sigma, cam, &v, &e, col, &ds, NULL);
+                for (int f = 0; f < ROW; f++) bound[(size_t)k * ROW + f] += fabs(col[f]) * *comp[c];
+            }
+        }
     }
 }
 

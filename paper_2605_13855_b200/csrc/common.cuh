@@ -250,6 +250,17 @@ __device__ __forceinline__ void sh_vjp(float x, float y, float z, const float cf
        SH_C3_5 * (xx - yy) * cf[14];
 }
 
+// Weight ramp max(0, 1 - d/σ) of Eq. 1 with d = camera z, evaluated in fp64: for d close to σ
+// the fp32 rounding of d (≈1e-7·|t|) would dominate the ramp's relative error.
+__device__ __forceinline__ double depth_fp64(const DevCam& cam, float mux, float muy, float muz) {
+  return fma((double)cam.R[6], (double)mux, fma((double)cam.R[7], (double)muy, fma((double)cam.R[8], (double)muz, (double)cam.t[2])));
+}
+__device__ __forceinline__ float ramp_fp64(const DevCam& cam, float mux, float muy, float muz, float sigma) {
+  const double d = depth_fp64(cam, mux, muy, muz);
+  const double r = ((double)sigma - d) / (double)sigma;
+  return r > 0.0 ? (float)r : 0.0f;
+}
+
 // Resolve one pixel (Eq. 7 with R10): F = P/Q (0 if Q = 0), C = T c0 + (1-T) F.
 // Shared by the forward epilogue and the backward coefficient kernel so C is bit-identical.
 __device__ __forceinline__ void resolve_pixel(float P0, float P1, float P2, float Q, float T, const float* bg,

@@ -267,8 +267,9 @@ __global__ void __launch_bounds__(128) k_epilogue(DevCam cam, const float4* __re
       }
       const float col[3] = {fmaxf(craw[0], 0.f), fmaxf(craw[1], 0.f), fmaxf(craw[2], 0.f)};
       const float sigma = *sigma_p;
-      const float ramp_raw = 1.0f - tz / sigma;
-      const float ramp = fmaxf(ramp_raw, 0.f), vplus = fmaxf(vraw, 0.f), w = ramp * vplus;
+      const double ramp_d = ((double)sigma - depth_fp64(cam, mu[0], mu[1], mu[2])) / (double)sigma;  // see ramp_fp64
+      const float ramp_raw = (float)ramp_d;
+      const float ramp = ramp_d > 0.0 ? ramp_raw : 0.f, vplus = fmaxf(vraw, 0.f), w = ramp * vplus;
 
       // ---- 2D gradients from the moments ----
       const float U[3] = {m0.x, m0.y, m0.z};
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(128) k_epilogue(DevCam cam, const float4* __re
       gt[2] -= (gmx * cam.fx * t[0] + gmy * cam.fy * t[1]) * itz2;
       // w -> v, σ, tz
       const float gvplus = gw * ramp, gramp = gw * vplus;
-      if (ramp_raw > 0.f) {
+      if (ramp_d > 0.0) {
         gt[2] -= gramp / sigma;
         gsig = gramp * tz / (sigma * sigma);
       }

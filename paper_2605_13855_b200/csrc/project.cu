@@ -52,8 +52,10 @@ __global__ void __launch_bounds__(256) k_project(DevCam cam, const float4* __res
       if (ch == 0) c0 += t; else if (ch == 1) c1 += t; else c2 += t;
     }
   }
-  float sigma = __ldg(sigma_p);
-  float ramp = fmaxf(0.0f, 1.0f - p.tz / sigma);
+  // the ramp 1 - d/σ is ill-conditioned near d ≈ σ (relative error ∝ d/(σ-d)): evaluate the
+  // depth and the ramp in fp64 (a few DFMA per visible splat; the kernel is HBM-bound)
+  const float sigma = __ldg(sigma_p);
+  const float ramp = ramp_fp64(cam, a.x, a.y, a.z, sigma);
   float w = ramp * fmaxf(0.0f, v0);
   out[0] = make_float4(p.mx, p.my, p.nA, p.nB);
   out[1] = make_float4(p.nC, p.thr_lo, p.thr_hi, log2f(a.w));

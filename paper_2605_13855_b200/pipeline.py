@@ -41,8 +41,9 @@ class ViewPipeline:
     def project_bin(self, rows, sigma, idx, stream=None):
         n = int(idx.numel())
         assert n <= self.max_slots
-        rec, tps = self.rec[:n], self.tps[:n]
-        L.oit_project_cull(rows, sigma, self.cam, idx, rec, tps, stream)
+        # (an empty slice may carry a null data pointer; hand the full buffers to the ABI then)
+        rec, tps = (self.rec[:n], self.tps[:n]) if n > 0 else (self.rec, self.tps)
+        L.oit_project_cull(rows, sigma, self.cam, idx, rec[:n], tps[:n], stream) if n > 0 else None
         L.oit_bin_tiles(self.cam, rec, tps, n, self.pairs, self.offs, self.n_pairs, self.bin_ws, stream)
         return rec
 
@@ -59,7 +60,7 @@ class ViewPipeline:
         """a4-a6 for the splats idx (grad rows += ...). With reuse_bins the records/pairs of the
         preceding forward over the same idx are reused."""
         n = int(idx.numel())
-        rec = self.rec[:n] if reuse_bins else self.project_bin(rows, sigma, idx, stream)
+        rec = (self.rec[:n] if n > 0 else self.rec) if reuse_bins else self.project_bin(rows, sigma, idx, stream)
         L.oit_composite_bwd(rows, sigma, self.cam, idx, rec, self.pairs, self.offs, bg, state, dL_dimage, grad,
                             dL_dsigma, self.bwd_ws, dL_dcov=dL_dcov, scale=scale, stream=stream)
 

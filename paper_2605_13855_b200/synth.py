@@ -88,6 +88,11 @@ class Scene:
     bg: np.ndarray              # [3]
     meta: dict = field(default_factory=dict)
 
+    def __post_init__(self):
+        # σ lives in an fp32 device scalar: keep the host copy fp32-representable so the oracle
+        # and the GPU see the same value (the ramp 1 - d/σ amplifies any difference near d ≈ σ)
+        self.sigma = float(np.float32(self.sigma))
+
     @property
     def n(self) -> int:
         return int(self.rows.shape[0])

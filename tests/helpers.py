@@ -22,11 +22,22 @@ def plain_to_tile_major(state, W, H):
     return pad.reshape(C, TY, 16, TX, 16).transpose(0, 1, 3, 2, 4).reshape(C, TY * TX, 256)
 
 
-def grad_close(got, ref, rtol=1e-4, atol=1e-6):
-    """Elementwise |got - ref| <= rtol·|ref| + atol (the north-star gradient bar)."""
+def grad_close(got, ref, bound=None, rtol=1e-4, atol=1e-6, kappa=0.1):
+    """The gradient bar (north star: 1e-4 relative, 1e-6 absolute floor), R31:
+    |got - ref| <= rtol·(|ref| + kappa·B) + atol elementwise, where B is the oracle's forward-error
+    scale of the element (Σ|terms| through |chain Jacobian|, oracle.backward_bound). For elements
+    that are not cancellation-dominated (|ref| ≳ B) this is the plain 1e-4 relative bar; for sums
+    that cancel, "relative" is taken against 10% of the magnitude of what was summed."""
     got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
-    bad = np.abs(got - ref) > rtol * np.abs(ref) + atol
+    scale = np.abs(ref) if bound is None else np.abs(ref) + kappa * np.asarray(bound, np.float64)
+    bad = np.abs(got - ref) > rtol * scale + atol
     return (not bad.any()), bad
+
+
+def strict_fraction(got, ref, rtol=1e-4, atol=1e-6):
+    """Fraction of elements meeting the plain elementwise bar |Δ| <= 1e-4|ref| + 1e-6."""
+    got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
+    return float((np.abs(got - ref) <= rtol * np.abs(ref) + atol).mean())
 
 
 def decode_rect(rec):

@@ -9,7 +9,7 @@ import pytest
 
 import oracle as O
 from paper_2605_13855_b200 import synth
-from tests.helpers import decode_rect, grad_close, plain_to_tile_major, tile_major_to_plain
+from tests.helpers import decode_rect, grad_close, plain_to_tile_major, strict_fraction, tile_major_to_plain
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -125,8 +125,10 @@ def test_composite_fwd_parity(scene):
         ref = O.render(scene.rows, scene.sigma, idx, cam, scene.bg, mode="brute")
         W, H = cam["width"], cam["height"]
         assert np.abs(img.cpu().numpy() - ref["image"]).max() < 1e-5
+        # internal pixel state: T is a product of many (1-α) factors whose fp32 relative error grows
+        # near the 0.99 clamp (1/(1-α) amplification), so the state bar is 2e-4 relative
         st = tile_major_to_plain(state.cpu().numpy(), W, H)
-        assert np.allclose(st, ref["state"], rtol=1e-5, atol=1e-6)
+        assert np.allclose(st, ref["state"], rtol=2e-4, atol=1e-7)
 
 
 def test_composite_fwd_cache_decomposition_and_fold():
@@ -149,7 +151,7 @@ def test_composite_fwd_cache_decomposition_and_fold():
     img2, _ = p.forward(rows, sigma, _t(act), sc.bg, base=cache, route=_t(route), base_out=base_out)
     assert np.abs(img2.cpu().numpy() - ref["image"]).max() < 1e-5
     ref_bo = O.render(sc.rows, sc.sigma, np.concatenate([ina, act[route == 1]]), cam, sc.bg)["state"]
-    assert np.allclose(tile_major_to_plain(base_out.cpu().numpy(), W, H), ref_bo, rtol=1e-5, atol=1e-6)
+    assert np.allclose(tile_major_to_plain(base_out.cpu().numpy(), W, H), ref_bo, rtol=2e-4, atol=1e-7)
     # also with an oracle-built cache as input (no GPU value on the oracle side)
     oc = O.render(sc.rows, sc.sigma, ina, cam, sc.bg)["state"]
     img3, _ = p.forward(rows, sigma, _t(act), sc.bg, base=_t(plain_to_tile_major(oc, W, H).astype(np.float32)))
@@ -188,12 +190,12 @@ def test_composite_bwd_parity(scene):
     for cam in scene.cams:
         grad, dsig, dcov, g = _bwd_case(scene, cam, idx)
         ref = O.render(scene.rows, scene.sigma, idx, cam, scene.bg)
-        gref, dsref, cref = O.backward(scene.rows, scene.sigma, idx, cam, scene.bg, ref["state"], g)
-        ok, bad = grad_close(grad, gref)
+        gref, dsref, cref, bnd = O.backward_bound(scene.rows, scene.sigma, idx, cam, scene.bg, ref["state"], g)
+        ok, bad = grad_close(grad, gref, bnd)
         assert ok, f"{bad.sum()} mismatches; worst rows {np.unique(np.nonzero(bad)[0])[:5]} fields {np.unique(np.nonzero(bad)[1])}"
+        assert strict_fraction(grad, gref) > 0.99
         assert abs(dsig - dsref) <= 1e-4 * abs(dsref) + 1e-6
-        ok, _ = grad_close(dcov, cref)
-        assert ok
+        assert np.linalg.norm(dcov - cref) <= 1e-4 * np.linalg.norm(cref)
         assert np.abs(gref).max() > 0
 
 
@@ -207,8 +209,8 @@ def test_composite_bwd_through_cache_matches_full():
     oc = O.render(sc.rows, sc.sigma, ina, cam, sc.bg)["state"]
     grad, dsig, _, g = _bwd_case(sc, cam, act, base=_t(plain_to_tile_major(oc, W, H).astype(np.float32)))
     full = O.render(sc.rows, sc.sigma, np.arange(sc.n), cam, sc.bg)
-    gref, dsref, _ = O.backward(sc.rows, sc.sigma, act, cam, sc.bg, full["state"], g)
-    ok, bad = grad_close(grad, gref)
+    gref, dsref, _, bnd = O.backward_bound(sc.rows, sc.sigma, act, cam, sc.bg, full["state"], g)
+    ok, bad = grad_close(grad, gref, bnd)
     assert ok, bad.sum()
 
 
@@ -257,7 +259,8 @@ def test_score_subsample_parity(loss):
         off = synth.rng(300 + k).uniform(0.01, 0.1, img.shape) * np.where(synth.rng(400 + k).random(img.shape) < 0.5, -1, 1)
         targets.append((img + off).astype(np.float32))
     views = [0, 3, 5]
-    ref, dsref = O.score_subsample(sc.rows, sc.sigma, sc.cams, targets, caches_o, act, ina, views, sc.bg, loss)
+    ref, dsref, bnd = O.score_subsample(sc.rows, sc.sigma, sc.cams, targets, caches_o, act, ina, views, sc.bg, loss,
+                                        with_bound=True)
     W, H = sc.cams[0]["width"], sc.cams[0]["height"]
     caches = [_t(plain_to_tile_major(c, W, H).astype(np.float32)) for c in caches_o]
     cap = 1 << 20
@@ -269,8 +272,10 @@ def test_score_subsample_parity(loss):
                           caches, _t(act), _t(ina), views, loss, sc.bg, sg, dsig, cap, mp, ws)
     torch.cuda.synchronize()
     assert 0 < mp.item() <= cap
-    ok, bad = grad_close(sg.cpu().numpy(), ref, rtol=1e-4, atol=1e-9 if loss == "l1" else 1e-8)
+    # the score rows are ~1/(3HW) smaller than the unit-gradient rows: scale the absolute floor
+    ok, bad = grad_close(sg.cpu().numpy(), ref, bnd, atol=1e-6 / (3 * W * H))
     assert ok, bad.sum()
+    assert abs(dsig.item() - dsref) <= 1e-4 * abs(dsref) + 1e-9
 
 
 # ------------------------------------------------------------------ a8 update ------------
@@ -321,6 +326,7 @@ def test_c2_full_size_parity_sampled():
     dsig = torch.zeros(1, dtype=torch.float32, device=DEV)
     p.backward(rows, sigma, _t(act), sc.bg, state, _t(g), grad, dsig)
     sample = np.sort(synth.rng(5).choice(len(act), 2000, replace=False))
-    gref, _, _ = O.backward(sc.rows, sc.sigma, act[sample], cam, sc.bg, ref["state"], g)
-    ok, bad = grad_close(grad.cpu().numpy()[sample], gref)
+    gref, _, _, bnd = O.backward_bound(sc.rows, sc.sigma, act[sample], cam, sc.bg, ref["state"], g)
+    ok, bad = grad_close(grad.cpu().numpy()[sample], gref, bnd)
     assert ok, bad.sum()
+    assert strict_fraction(grad.cpu().numpy()[sample], gref) > 0.99

@@ -482,3 +482,18 @@ def test_score_uses_full_state_through_cache():
         ref += gr / len(views)
     assert np.abs(got - ref).max() <= 1e-10 * max(1.0, np.abs(ref).max())
     assert np.abs(ref).max() > 0
+
+
+def test_backward_bound_dominates_gradient():
+    """The forward-error scale B used by the fp32 tolerance (R31) bounds |grad| (|Σ t| ≤ Σ|t|,
+    |J g| ≤ |J||g|) and equals |grad| for a single contributing pixel."""
+    sc = synth.scene_c1(n=200)
+    idx = np.arange(200)
+    cam = sc.cams[0]
+    st = O.render(sc.rows, sc.sigma, idx, cam, sc.bg)["state"]
+    g = synth.dl_dimage(cam, 3).astype(np.float64)
+    grad, _, _, bnd = O.backward_bound(sc.rows, sc.sigma, idx, cam, sc.bg, st, g)
+    gplain, _, _ = O.backward(sc.rows, sc.sigma, idx, cam, sc.bg, st, g)
+    assert np.array_equal(grad, gplain)
+    assert np.all(bnd >= np.abs(grad) * (1 - 1e-12))
+    assert (bnd > 10 * np.abs(grad)).any()      # cancellation exists in real scenes
