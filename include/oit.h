@@ -24,10 +24,13 @@
  *      parameter / gradient row [N][80] fp32: 0-2 μ, 3 o ∈ (0,1], 4-7 q (w,x,y,z) raw
  *        (normalised inside), 8-10 s > 0 (linear), 11 pad, 12-27 v (16 weight-SH coeffs),
  *        28-75 h (16x3 colour SH, coefficient-major: h[j][ch] at 28+3j+ch), 76-79 pad.
- *      record rec[n_slots][16] fp32 (64 B): {mx, my, nA, nB}, {nC, thr_lo, thr_hi, log2 o},
- *        {cR, cG, cB, w}, {rect_x, rect_y (uint32 bits x0|x1<<16), ex, ey}. nA,nB,nC are the
- *        coefficients of power = nA dx² + nB dx dy + nC dy² = -½ΔᵀΣ'⁻¹Δ; ex, ey the conservative
- *        pixel half-extents of the α = 1/255 ellipse (DESIGN.md §3 step 12). Culled: all zero.
+ *      record rec[n_slots][20] fp32 (80 B): {mx, my, nA, nB}, {nC, thr_lo, thr_hi, log2 o},
+ *        {cR, cG, cB, w}, {rect_x, rect_y (uint32 bits x0|x1<<16), kx, ky}, {ex, ey, δx, δy}.
+ *        nA,nB,nC: power = nA dx² + nB dx dy + nC dy² = -½ΔᵀΣ'⁻¹Δ (decision spec);
+ *        ex, ey: conservative pixel half-extents of the α = 1/255 ellipse (step 12);
+ *        δx, δy: fp64 μ' minus the spec's fp32 μ'; kx, ky: log2(e)·(2nA δx + nB δy, nB δx + 2nC δy),
+ *        the first-order correction of the exponent the value path applies (α = 2^(power·log2e +
+ *        log2 o − kx dx − ky dy)). Culled slots: all zero.
  *      pixel state / pre-render cache [5][n_tiles][256] fp32, tile-major (16x16 tiles in
  *        row-major tile order, row-major pixels inside a tile): planes P_R, P_G, P_B, Q, T.
  *      images [3][H][W] fp32 (CHW, row-major).
@@ -46,7 +49,7 @@ extern "C" {
 
 #define OIT_TILE 16
 #define OIT_ROW 80
-#define OIT_REC 16
+#define OIT_REC 20
 
 typedef void* oit_stream_t; /* cudaStream_t */
 
@@ -89,7 +92,7 @@ int32_t oit_num_tiles(const oit_camera* cam);
  * For each slot k < n_slots, splat i = idx[k] (the compacted active-index list; any order):
  * normalise q, Σ = R S Sᵀ Rᵀ, Σ' = J W Σ Wᵀ Jᵀ + 0.3 I, conic, μ', colour c = max(0, SH(h, r)+0.5),
  * weight w = max(0, 1 - tz/σ)·max(0, SH(v, r)), α thresholds, and the opacity-aware
- * conservative tile rectangle (R9). Writes rec[k][16] and tiles_per_slot[k] (0 if culled).
+ * conservative tile rectangle (R9). Writes rec[k][20] and tiles_per_slot[k] (0 if culled).
  * Errors: OIT_EINVAL (null pointer / n_slots < 0), OIT_ESHAPE (n_slots > scene->n, bad W/H).
  * idx entries must lie in [0, N) (not checked on the device).
  * --------------------------------------------------------------------------------------- */

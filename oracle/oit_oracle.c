@@ -673,7 +673,8 @@ void orc_backward_bound(const float* rows_dec, const double* rows_val, double si
                     double t1 = T / (1.0 - alpha) * (F[c] - bg[c]);
                     double t2 = Q > 0 ? (1.0 - T) * v.w / Q * (v.col[c] - F[c]) : 0.0;
                     dL_dalpha += gpx[c] * (t1 + t2);
-                    a_dL_dalpha += fabs(gpx[c]) * (fabs(t1) + fabs(t2));
+                    /* t1's sensitivity to a relative error of α is α/(1-α): count |t1|/(1-α) */
+                    a_dL_dalpha += fabs(gpx[c]) * (fabs(t1) / (1.0 - alpha) + fabs(t2));
                     if (Q > 0) {
                         double dC_dc = (1.0 - T) * alpha * v.w / Q;
                         double dC_dw = (1.0 - T) * alpha / Q * (v.col[c] - F[c]);

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "liboit.so")
 
 OIT_TILE = 16
 OIT_ROW = 80
-OIT_REC = 16
+OIT_REC = 20
 
 
 class OitError(RuntimeError):

@@ -13,7 +13,7 @@
 namespace oit {
 
 __device__ __forceinline__ void rect_of(const float4* rec, int k, int& x0, int& y0, int& x1, int& y1) {
-  float4 q3 = rec[(size_t)k * 4 + 3];
+  float4 q3 = rec[(size_t)k * kRec4 + 3];
   uint32_t rx = __float_as_uint(q3.x), ry = __float_as_uint(q3.y);
   x0 = rx & 0xffff; x1 = rx >> 16; y0 = ry & 0xffff; y1 = ry >> 16;
 }

@@ -165,8 +165,8 @@ static ScoreWs score_layout(void* ws, const oit_camera* cam, int32_t n_active, i
   const int32_t nt = oit_num_tiles(cam);
   Carve cv(ws);
   ScoreWs w;
-  w.rec_a = cv.take<float>((size_t)n_active * 16 + 16);
-  w.rec_s = cv.take<float>((size_t)n_score * 16 + 16);
+  w.rec_a = cv.take<float>(((size_t)n_active + 1) * kRec4 * 4);
+  w.rec_s = cv.take<float>(((size_t)n_score + 1) * kRec4 * 4);
   w.tps_a = cv.take<int32_t>((size_t)n_active + 1);
   w.tps_s = cv.take<int32_t>((size_t)n_score + 1);
   w.pairs = cv.take<int32_t>((size_t)cap + 1);

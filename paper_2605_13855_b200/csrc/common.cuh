@@ -16,6 +16,7 @@ constexpr int kTile = 16;
 constexpr int kTilePx = 256;
 constexpr int kRow = 80;        // parameter row (floats)
 constexpr int kRow4 = 20;       // parameter row (float4)
+constexpr int kRec4 = 5;        // projected record (float4): 80 B, include/oit.h
 // parameter row fields
 constexpr int kMu = 0, kO = 3, kQ = 4, kS = 8, kV = 12, kH = 28;
 
@@ -254,6 +255,13 @@ __device__ __forceinline__ void sh_vjp(float x, float y, float z, const float cf
 // the fp32 rounding of d (≈1e-7·|t|) would dominate the ramp's relative error.
 __device__ __forceinline__ double depth_fp64(const DevCam& cam, float mux, float muy, float muz) {
   return fma((double)cam.R[6], (double)mux, fma((double)cam.R[7], (double)muy, fma((double)cam.R[8], (double)muz, (double)cam.t[2])));
+}
+// Camera-space position in fp64 (value-path refinement of the spec's fp32 transform).
+__device__ __forceinline__ void cam_point_fp64(const DevCam& cam, float mux, float muy, float muz, double t[3]) {
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+    t[i] = fma((double)cam.R[3 * i], (double)mux,
+               fma((double)cam.R[3 * i + 1], (double)muy, fma((double)cam.R[3 * i + 2], (double)muz, (double)cam.t[i])));
 }
 __device__ __forceinline__ float ramp_fp64(const DevCam& cam, float mux, float muy, float muz, float sigma) {
   const double d = depth_fp64(cam, mux, muy, muz);

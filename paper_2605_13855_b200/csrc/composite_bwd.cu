@@ -106,17 +106,18 @@ __global__ void __launch_bounds__(kMomentsThreads) k_moments(DevCam cam, const f
     const int end = (int)e64;
     const int j = offs[tile] + chunk * 32 + lane;
     const bool valid = j < end;
-    float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0, q2 = q0, q3 = q0;
+    float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0, q2 = q0, q3 = q0, q4 = q0;
     int slot = -1;
     if (valid) {
       slot = pair_slot[j];
-      const float4* r = rec + (size_t)slot * 4;
-      q0 = r[0]; q1 = r[1]; q2 = r[2]; q3 = r[3];
+      const float4* r = rec + (size_t)slot * kRec4;
+      q0 = r[0]; q1 = r[1]; q2 = r[2]; q3 = r[3]; q4 = r[4];
     }
     const float mx = q0.x, my = q0.y, nA = q0.z, nB = q0.w;
     const float nC = q1.x, thr_lo = q1.y, thr_hi = q1.z, log2o = q1.w;
     const float cR = q2.x, cG = q2.y, cB = q2.z, w = q2.w;
-    const float ex = q3.z, ey = q3.w;  // conservative pixel half-extents of the α=1/255 ellipse
+    const float kx = q3.z, ky = q3.w;  // sub-ulp μ' correction of the exponent (value path)
+    const float ex = q4.x, ey = q4.y;  // conservative pixel half-extents of the α=1/255 ellipse
     const int tx0 = (tile % cam.TX) * kTile, ty0 = (tile / cam.TX) * kTile;
     // warp-uniform pixel window: union of the lanes' extents, clipped to the tile
     float lo_x = valid ? mx - ex : 1e30f, hi_x = valid ? mx + ex : -1e30f;
@@ -148,7 +149,8 @@ __global__ void __launch_bounds__(kMomentsThreads) k_moments(DevCam cam, const f
         const float power = spec_power_row(nA, dx, by, cyv);
         const bool contrib = ract && power <= 0.0f && power >= thr_lo;
         const bool clamp = power >= thr_hi;
-        float alpha = clamp ? 0.99f : ex2_approx(fmaf(power, kLog2e, log2o));
+        const float arg = fmaf(-kx, dx, fmaf(-ky, dy, fmaf(power, kLog2e, log2o)));
+        float alpha = clamp ? 0.99f : ex2_approx(arg);
         alpha = contrib ? alpha : 0.0f;
         const float4 cu = __ldg(cf4 + py * kTile + px);  // (u_R, u_G, u_B, s): warp-uniform
         const float ca = __ldg(cfa + py * kTile + px);   // a
@@ -191,14 +193,15 @@ __global__ void __launch_bounds__(128) k_epilogue(DevCam cam, const float4* __re
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   float gsig = 0.f;
   if (k < n_slots) {
-    const float4 q3 = rec[(size_t)k * 4 + 3];
+    const float4 q3 = rec[(size_t)k * kRec4 + 3];
     const bool vis = __float_as_uint(q3.x) != 0u || __float_as_uint(q3.y) != 0u;
     const float4 m0 = acc2d[(size_t)k * 3 + 0];  // U0 U1 U2 S
     const float4 m1 = acc2d[(size_t)k * 3 + 1];  // Od M1 M2 XX
     const float4 m2 = acc2d[(size_t)k * 3 + 2];  // XY YY
     if (vis && (m0.x != 0.f || m0.y != 0.f || m0.z != 0.f || m0.w != 0.f || m1.x != 0.f)) {
-      const float4 q0 = rec[(size_t)k * 4 + 0];
-      const float4 q1 = rec[(size_t)k * 4 + 1];
+      const float4 q0 = rec[(size_t)k * kRec4 + 0];
+      const float4 q1 = rec[(size_t)k * kRec4 + 1];
+      const float4 q4 = rec[(size_t)k * kRec4 + 4];
       const float nA = q0.z, nB = q0.w, nC = q1.x;
       const float4* r = rows + (size_t)idx[k] * kRow4;
       const float4 ra = r[0], rb = r[1], rc = r[2];
@@ -273,7 +276,14 @@ __global__ void __launch_bounds__(128) k_epilogue(DevCam cam, const float4* __re
 
       // ---- 2D gradients from the moments ----
       const float U[3] = {m0.x, m0.y, m0.z};
-      const float Ssum = m0.w, Od = m1.x, M1 = m1.y, M2 = m1.z, XX = m1.w, XY = m2.x, YY = m2.y;
+      // the moments were accumulated with the spec offsets dx = x - μ'_spec; the true offsets are
+      // dx - δx (δ = μ'_fp64 - μ'_spec, rec q4.zw): re-centre the moments exactly
+      const float dmx = q4.z, dmy = q4.w;
+      const float Ssum = m0.w, Od = m1.x, M1s = m1.y, M2s = m1.z;
+      const float M1 = M1s - dmx * Od, M2 = M2s - dmy * Od;
+      const float XX = m1.w - 2.f * dmx * M1s + dmx * dmx * Od;
+      const float XY = m2.x - dmy * M1s - dmx * M2s + dmx * dmy * Od;
+      const float YY = m2.y - 2.f * dmy * M2s + dmy * dmy * Od;
       const float gc[3] = {w * U[0], w * U[1], w * U[2]};
       const float gw = U[0] * col[0] + U[1] * col[1] + U[2] * col[2] - Ssum;
       const float go = Od / op;

@@ -20,6 +20,7 @@ __global__ void __launch_bounds__(256) k_fwd(DevCam cam, const float4* __restric
                                              float* __restrict__ image, float* __restrict__ state,
                                              float* base_out) {
   __shared__ float4 s_q0[256], s_q1[256], s_q2[256];
+  __shared__ float2 s_k[256];
   __shared__ uint8_t s_route[kRoute ? 256 : 1];
   const int tile = blockIdx.x, tid = threadIdx.x;
   const int n_tiles = cam.TX * cam.TY;
@@ -44,10 +45,11 @@ __global__ void __launch_bounds__(256) k_fwd(DevCam cam, const float4* __restric
     __syncthreads();
     if (tid < n) {
       const int slot = pair_slot[b + tid];
-      const float4* r = rec + (size_t)slot * 4;
+      const float4* r = rec + (size_t)slot * kRec4;
       s_q0[tid] = r[0];
       s_q1[tid] = r[1];
       s_q2[tid] = r[2];
+      s_k[tid] = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(r + 3) + 2);
       if (kRoute) s_route[tid] = route[slot];
     }
     __syncthreads();
@@ -57,7 +59,9 @@ __global__ void __launch_bounds__(256) k_fwd(DevCam cam, const float4* __restric
       const float dx = __fsub_rn(fx, q0.x), dy = __fsub_rn(fy, q0.y);
       const float power = spec_power(q0.z, q0.w, q1.x, dx, dy);
       if (power <= 0.0f && power >= q1.y) {
-        const float alpha = power >= q1.z ? 0.99f : ex2_approx(fmaf(power, kLog2e, q1.w));
+        const float2 kk = s_k[i];  // sub-ulp μ' correction of the exponent (value path only)
+        const float arg = fmaf(-kk.x, dx, fmaf(-kk.y, dy, fmaf(power, kLog2e, q1.w)));
+        const float alpha = power >= q1.z ? 0.99f : ex2_approx(arg);
         const float4 q2 = s_q2[i];  // cR cG cB w
         const float aw = alpha * q2.w;
         P0 = fmaf(q2.x, aw, P0);

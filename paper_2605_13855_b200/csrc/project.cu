@@ -3,7 +3,7 @@
 //
 // One thread per active slot. The 320-B parameter row is read with float4 loads (the row is
 // 64-B aligned); culled splats stop after the first three float4s, so the 256 B of SH
-// coefficients are only fetched for visible splats. Output: a 64-B record (4 × float4 stores)
+// coefficients are only fetched for visible splats. Output: an 80-B record (5 × float4 stores)
 // and the slot's tile count. HBM-bound: ≈ 320 B in + 68 B out per visible slot.
 #include "kernels.h"
 
@@ -20,15 +20,22 @@ __global__ void __launch_bounds__(256) k_project(DevCam cam, const float4* __res
   float4 b = __ldg(r + 1);  // qw qx qy qz
   float4 c = __ldg(r + 2);  // s0 s1 s2 pad
   SpecProj p = spec_project(cam, a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z);
-  float4* out = rec + (size_t)k * 4;
+  float4* out = rec + (size_t)k * kRec4;
   if (!p.visible) {
-    out[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-    out[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-    out[2] = make_float4(0.f, 0.f, 0.f, 0.f);
-    out[3] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < kRec4; q++) out[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     tps[k] = 0;
     return;
   }
+  // ---- value-path refinement of μ' (the spec's fp32 μ' is off by up to ½ ulp(|μ'|), 3e-5 px at
+  // 400 px, which would dominate α's error): residual δ = μ'_fp64 - μ'_spec and the matching
+  // first-order correction of the Gaussian exponent, power_true ≈ power_spec - kx·dx - ky·dy ----
+  double t64[3];
+  cam_point_fp64(cam, a.x, a.y, a.z, t64);
+  const float dmx = (float)(fma((double)cam.fx, t64[0] / t64[2], (double)cam.cx) - (double)p.mx);
+  const float dmy = (float)(fma((double)cam.fy, t64[1] / t64[2], (double)cam.cy) - (double)p.my);
+  const float kx = (2.0f * p.nA * dmx + p.nB * dmy) * kLog2e;
+  const float ky = (p.nB * dmx + 2.0f * p.nC * dmy) * kLog2e;
   // ---- value path: view direction, colour SH (Eq. 4, R2, R7), weight (Eq. 1, R4-R6) ----
   float dxw = a.x - cam.center[0], dyw = a.y - cam.center[1], dzw = a.z - cam.center[2];
   float inv = rsqrtf(dxw * dxw + dyw * dyw + dzw * dzw);
@@ -61,7 +68,8 @@ __global__ void __launch_bounds__(256) k_project(DevCam cam, const float4* __res
   out[1] = make_float4(p.nC, p.thr_lo, p.thr_hi, log2f(a.w));
   out[2] = make_float4(fmaxf(c0, 0.0f), fmaxf(c1, 0.0f), fmaxf(c2, 0.0f), w);
   out[3] = make_float4(__uint_as_float((uint32_t)p.x0 | ((uint32_t)p.x1 << 16)),
-                       __uint_as_float((uint32_t)p.y0 | ((uint32_t)p.y1 << 16)), p.ex, p.ey);
+                       __uint_as_float((uint32_t)p.y0 | ((uint32_t)p.y1 << 16)), kx, ky);
+  out[4] = make_float4(p.ex, p.ey, dmx, dmy);
   tps[k] = (p.x1 - p.x0) * (p.y1 - p.y0);
 }
 

@@ -34,6 +34,16 @@ def grad_close(got, ref, bound=None, rtol=1e-4, atol=1e-6, kappa=0.1):
     return (not bad.any()), bad
 
 
+def describe_bad(got, ref, bad, bound=None, k=5):
+    r, c = np.nonzero(np.atleast_2d(bad))
+    out = []
+    for i in range(min(k, len(r))):
+        g, f = np.atleast_2d(got)[r[i], c[i]], np.atleast_2d(ref)[r[i], c[i]]
+        b = np.atleast_2d(bound)[r[i], c[i]] if bound is not None else float("nan")
+        out.append(f"[{r[i]},{c[i]}] got {g:.7g} ref {f:.7g} bound {b:.3g}")
+    return f"{len(r)} mismatches: " + "; ".join(out)
+
+
 def strict_fraction(got, ref, rtol=1e-4, atol=1e-6):
     """Fraction of elements meeting the plain elementwise bar |Δ| <= 1e-4|ref| + 1e-6."""
     got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)

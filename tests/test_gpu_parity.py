@@ -9,7 +9,7 @@ import pytest
 
 import oracle as O
 from paper_2605_13855_b200 import synth
-from tests.helpers import decode_rect, grad_close, plain_to_tile_major, strict_fraction, tile_major_to_plain
+from tests.helpers import decode_rect, describe_bad, grad_close, plain_to_tile_major, strict_fraction, tile_major_to_plain
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -56,7 +56,7 @@ def test_project_cull_bitexact(scene):
     g = np.random.default_rng(0)
     idx = g.permutation(scene.n).astype(np.int32)           # any order (compacted active list)
     for cam in scene.cams:
-        rec = torch.empty((scene.n, 16), dtype=torch.float32, device=DEV)
+        rec = torch.empty((scene.n, 20), dtype=torch.float32, device=DEV)
         tps = torch.empty(scene.n, dtype=torch.int32, device=DEV)
         L.oit_project_cull(rows, sigma, cam, _t(idx), rec, tps)
         r = rec.cpu().numpy()
@@ -68,11 +68,14 @@ def test_project_cull_bitexact(scene):
         assert np.all((x0 == x1)[~vis]) and np.all(tps.cpu().numpy()[~vis] == 0)
         assert np.array_equal(tps.cpu().numpy()[vis], ((x1 - x0) * (y1 - y0))[vis])
         for col, key in [(0, "mx"), (1, "my"), (2, "nA"), (3, "nB"), (4, "nC"), (5, "thr_lo"), (6, "thr_hi"),
-                         (14, "ex"), (15, "ey")]:
+                         (16, "ex"), (17, "ey")]:
             assert np.array_equal(r[vis, col].view(np.uint32), sp[key][vis].view(np.uint32)), key
         assert np.allclose(r[vis, 8:11], pv["color"][vis], atol=2e-6, rtol=0)
         assert np.allclose(r[vis, 11], pv["w"][vis], atol=2e-6, rtol=2e-6)
         assert np.allclose(r[vis, 7], np.log2(pv["o"][vis]), atol=1e-6)
+        # the value-path residual of μ' brings it to fp64 accuracy
+        assert np.abs((r[vis, 0].astype(np.float64) + r[vis, 18]) - pv["mx"][vis]).max() < 1e-9 * np.abs(pv["mx"][vis]).max() + 1e-12
+        assert np.abs((r[vis, 1].astype(np.float64) + r[vis, 19]) - pv["my"][vis]).max() < 1e-9 * np.abs(pv["my"][vis]).max() + 1e-12
         assert vis.sum() > 0.5 * scene.n
 
 
@@ -80,7 +83,7 @@ def test_project_cull_empty_and_errors():
     L = _L()
     sc = SCENES[0]
     rows, sigma = _t(sc.rows), _t(np.array([sc.sigma], np.float32))
-    rec = torch.empty((1, 16), dtype=torch.float32, device=DEV)
+    rec = torch.empty((1, 20), dtype=torch.float32, device=DEV)
     tps = torch.empty(1, dtype=torch.int32, device=DEV)
     L.oit_project_cull(rows, sigma, sc.cams[0], torch.empty(0, dtype=torch.int32, device=DEV), rec, tps)
     bad = dict(sc.cams[0])
@@ -192,7 +195,7 @@ def test_composite_bwd_parity(scene):
         ref = O.render(scene.rows, scene.sigma, idx, cam, scene.bg)
         gref, dsref, cref, bnd = O.backward_bound(scene.rows, scene.sigma, idx, cam, scene.bg, ref["state"], g)
         ok, bad = grad_close(grad, gref, bnd)
-        assert ok, f"{bad.sum()} mismatches; worst rows {np.unique(np.nonzero(bad)[0])[:5]} fields {np.unique(np.nonzero(bad)[1])}"
+        assert ok, describe_bad(grad, gref, bad, bnd)
         assert strict_fraction(grad, gref) > 0.99
         assert abs(dsig - dsref) <= 1e-4 * abs(dsref) + 1e-6
         assert np.linalg.norm(dcov - cref) <= 1e-4 * np.linalg.norm(cref)
