@@ -130,6 +130,15 @@ int oit_composite_fwd(const oit_camera* cam, const float* rec, const int32_t* pa
                       const float bg_host[3], const float* base, const uint8_t* route,
                       float* image, float* state, float* base_out, oit_stream_t stream);
 
+/* Same as oit_composite_fwd; d_counters (nullable, device int64[2], accumulated +=) receives
+ * [0] the number of contributing (splat, pixel) pairs (α ≥ 1/255, inside the image) and [1] the
+ * tile-granular splat-pixel evaluations (256 per (splat, tile) pair) — the work counters of the
+ * metric. Counting adds one reduction per tile; the plain call skips it. */
+int oit_composite_fwd_ex(const oit_camera* cam, const float* rec, const int32_t* pair_slot,
+                         const int32_t* tile_offsets, int64_t pair_capacity, const float bg_host[3],
+                         const float* base, const uint8_t* route, float* image, float* state,
+                         float* base_out, int64_t* d_counters, oit_stream_t stream);
+
 /* ---------------------------------------------------------------------------------------
  * a4  oit_loss_grad — pixel loss gradient dL/dC of L = mean_{3HW} |C - I| (loss 0, sign(0)=0)
  * or mean (C - I)² (loss 1): the L1 term of the 3DGS loss (R24).
@@ -156,6 +165,20 @@ int oit_composite_bwd(const oit_scene* scene, const oit_camera* cam, const int32
                       const float bg_host[3], const float* state, const float* dL_dimage,
                       float scale, float* grad, float* dL_dsigma, float* dL_dcov, void* ws,
                       size_t ws_bytes, oit_stream_t stream);
+
+/* Same as oit_composite_bwd; ev (nullable) holds two cudaEvent_t recorded on `stream` right
+ * before and after the a5 moment kernel (the hot loop), so callers can time it with events
+ * (also inside CUDA-graph capture, where they are recorded as external event nodes). */
+typedef struct {
+  void* moments_begin; /* cudaEvent_t or NULL */
+  void* moments_end;   /* cudaEvent_t or NULL */
+} oit_bwd_events;
+int oit_composite_bwd_ex(const oit_scene* scene, const oit_camera* cam, const int32_t* idx,
+                         int32_t n_slots, const float* rec, const int32_t* pair_slot,
+                         const int32_t* tile_offsets, int64_t pair_capacity, const float bg_host[3],
+                         const float* state, const float* dL_dimage, float scale, float* grad,
+                         float* dL_dsigma, float* dL_dcov, void* ws, size_t ws_bytes,
+                         const oit_bwd_events* ev, oit_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------
  * a7  oit_select_views — farthest point sampling over the camera centres with a Philox4x32-10

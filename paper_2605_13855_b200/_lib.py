@@ -30,6 +30,10 @@ class Camera(C.Structure):
                 ("znear", C.c_float)]
 
 
+class BwdEvents(C.Structure):
+    _fields_ = [("moments_begin", C.c_void_p), ("moments_end", C.c_void_p)]
+
+
 class Scene(C.Structure):
     _fields_ = [("n", C.c_int32), ("rows", C.c_void_p), ("sigma", C.c_void_p)]
 
@@ -66,10 +70,13 @@ def lib() -> C.CDLL:
             "oit_bin_workspace_bytes": (sz, [cam_p]),
             "oit_bin_tiles": (C.c_int, [cam_p, vp, vp, i32, vp, i64, vp, vp, vp, sz, vp]),
             "oit_composite_fwd": (C.c_int, [cam_p, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp]),
+            "oit_composite_fwd_ex": (C.c_int, [cam_p, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp]),
             "oit_loss_grad": (C.c_int, [cam_p, vp, vp, i32, vp, vp]),
             "oit_bwd_workspace_bytes": (sz, [cam_p, i32, i64]),
             "oit_composite_bwd": (C.c_int, [scene_p, cam_p, vp, i32, vp, vp, vp, i64, vp, vp, vp, f32, vp, vp,
                                             vp, vp, sz, vp]),
+            "oit_composite_bwd_ex": (C.c_int, [scene_p, cam_p, vp, i32, vp, vp, vp, i64, vp, vp, vp, f32, vp, vp,
+                                               vp, vp, sz, C.POINTER(BwdEvents), vp]),
             "oit_select_views": (C.c_int, [vp, i32, i32, C.c_uint64, C.c_uint32, vp, vp]),
             "oit_score_workspace_bytes": (sz, [cam_p, i32, i32, i64]),
             "oit_score_subsample": (C.c_int, [scene_p, cam_p, i32, vp, vp, vp, i32, vp, i32, vp, i32, i32, vp, vp,
@@ -86,7 +93,7 @@ def lib() -> C.CDLL:
 
 
 EXPORTED = ["oit_status_string", "oit_num_tiles", "oit_project_cull", "oit_bin_workspace_bytes", "oit_bin_tiles",
-            "oit_composite_fwd", "oit_loss_grad", "oit_bwd_workspace_bytes", "oit_composite_bwd",
+            "oit_composite_fwd", "oit_composite_fwd_ex", "oit_loss_grad", "oit_bwd_workspace_bytes", "oit_composite_bwd", "oit_composite_bwd_ex",
             "oit_select_views", "oit_score_workspace_bytes", "oit_score_subsample", "oit_update_workspace_bytes",
             "oit_update_active_set"]
 
@@ -144,10 +151,15 @@ def oit_bin_tiles(cam, rec, tiles_per_slot, n_slots, pair_slot, tile_offsets, n_
 
 
 def oit_composite_fwd(cam, rec, pair_slot, tile_offsets, bg, base=None, route=None, image=None, state=None,
-                      base_out=None, stream=None):
-    _check(lib().oit_composite_fwd(C.byref(camera(cam)), _ptr(rec), _ptr(pair_slot), _ptr(tile_offsets),
-                                   int(pair_slot.numel()), _f3(bg), _ptr(base), _ptr(route), _ptr(image),
-                                   _ptr(state), _ptr(base_out), _stream(stream)), "oit_composite_fwd")
+                      base_out=None, stream=None, counters=None):
+    """counters: optional int64[2] device tensor (+=): contributing pairs, tile-granular evals
+    (oit_composite_fwd_ex)."""
+    args = (C.byref(camera(cam)), _ptr(rec), _ptr(pair_slot), _ptr(tile_offsets), int(pair_slot.numel()), _f3(bg),
+            _ptr(base), _ptr(route), _ptr(image), _ptr(state), _ptr(base_out))
+    if counters is None:
+        _check(lib().oit_composite_fwd(*args, _stream(stream)), "oit_composite_fwd")
+    else:
+        _check(lib().oit_composite_fwd_ex(*args, _ptr(counters), _stream(stream)), "oit_composite_fwd_ex")
 
 
 def oit_loss_grad(cam, image, target, loss: str, dL_dimage, stream=None):
@@ -160,12 +172,18 @@ def oit_bwd_workspace_bytes(cam, n_slots: int, pair_capacity: int) -> int:
 
 
 def oit_composite_bwd(rows, sigma, cam, idx, rec, pair_slot, tile_offsets, bg, state, dL_dimage, grad, dL_dsigma,
-                      ws, dL_dcov=None, scale: float = 1.0, stream=None):
+                      ws, dL_dcov=None, scale: float = 1.0, stream=None, events=None):
+    """events: optional (begin, end) torch.cuda.Event pair recorded around the a5 moment kernel
+    (oit_composite_bwd_ex)."""
     sc, c = scene(rows, sigma), camera(cam)
-    _check(lib().oit_composite_bwd(C.byref(sc), C.byref(c), _ptr(idx), int(idx.numel()), _ptr(rec),
-                                   _ptr(pair_slot), _ptr(tile_offsets), int(pair_slot.numel()), _f3(bg),
-                                   _ptr(state), _ptr(dL_dimage), C.c_float(scale), _ptr(grad), _ptr(dL_dsigma),
-                                   _ptr(dL_dcov), _ptr(ws), int(ws.numel()), _stream(stream)), "oit_composite_bwd")
+    args = (C.byref(sc), C.byref(c), _ptr(idx), int(idx.numel()), _ptr(rec), _ptr(pair_slot), _ptr(tile_offsets),
+            int(pair_slot.numel()), _f3(bg), _ptr(state), _ptr(dL_dimage), C.c_float(scale), _ptr(grad),
+            _ptr(dL_dsigma), _ptr(dL_dcov), _ptr(ws), int(ws.numel()))
+    if events is None:
+        _check(lib().oit_composite_bwd(*args, _stream(stream)), "oit_composite_bwd")
+    else:
+        ev = BwdEvents(C.c_void_p(events[0].cuda_event), C.c_void_p(events[1].cuda_event))
+        _check(lib().oit_composite_bwd_ex(*args, C.byref(ev), _stream(stream)), "oit_composite_bwd_ex")
 
 
 def oit_select_views(centers, n_sub: int, seed: int, refresh: int, views_out, stream=None):

@@ -455,8 +455,13 @@ static int sm_count() {
 void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sigma, const int32_t* idx,
                           int32_t n_slots, const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
                           int64_t capacity, const float* coef4, const float* coefa, float scale, float* grad,
-                          float* dL_dsigma, float* dL_dcov, void* ws, cudaStream_t st) {
-  if (n_slots <= 0) return;
+                          float* dL_dsigma, float* dL_dcov, void* ws, cudaStream_t st, cudaEvent_t ev_begin,
+                          cudaEvent_t ev_end) {
+  if (n_slots <= 0) {
+    record_event(ev_begin, st);
+    record_event(ev_end, st);
+    return;
+  }
   const int n_tiles = cam.TX * cam.TY;
   const int64_t max_items = capacity / 32 + n_tiles + 1;
   Carve cv(ws);
@@ -473,9 +478,11 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
   launch_exclusive_scan(counts, item_offs, n_tiles, tmp, st);
   k_chunk_emit<<<tb, 256, 0, st>>>(item_offs, n_tiles, items);
   const int blocks = sm_count() * 6;  // persistent: 6 × 8 warps per SM, dynamic item claiming
+  record_event(ev_begin, st);
   k_moments<<<blocks, kMomentsThreads, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), pair_slot, tile_offsets,
                                                 capacity, items, item_offs, item_offs + n_tiles, counter,
                                                 reinterpret_cast<const float4*>(coef4), coefa, acc2d);
+  record_event(ev_end, st);
   k_epilogue<<<(n_slots + 127) / 128, 128, 0, st>>>(cam, reinterpret_cast<const float4*>(rows), sigma, idx, n_slots,
                                                     reinterpret_cast<const float4*>(rec),
                                                     reinterpret_cast<const float4*>(acc2d), scale,

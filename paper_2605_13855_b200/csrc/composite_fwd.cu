@@ -12,13 +12,14 @@
 
 namespace oit {
 
-template <bool kRoute, bool kBase>
+template <bool kRoute, bool kBase, bool kCount>
 __global__ void __launch_bounds__(256) k_fwd(DevCam cam, const float4* __restrict__ rec,
                                              const int32_t* __restrict__ pair_slot,
                                              const int32_t* __restrict__ offs, int64_t capacity,
                                              const float* __restrict__ base, const uint8_t* __restrict__ route,
                                              float* __restrict__ image, float* __restrict__ state,
-                                             float* base_out) {
+                                             float* base_out, unsigned long long* __restrict__ counters) {
+  int n_contrib = 0;
   __shared__ float4 s_q0[256], s_q1[256], s_q2[256];
   __shared__ float2 s_k[256];
   __shared__ uint8_t s_route[kRoute ? 256 : 1];
@@ -59,6 +60,7 @@ __global__ void __launch_bounds__(256) k_fwd(DevCam cam, const float4* __restric
       const float dx = __fsub_rn(fx, q0.x), dy = __fsub_rn(fy, q0.y);
       const float power = spec_power(q0.z, q0.w, q1.x, dx, dy);
       if (power <= 0.0f && power >= q1.y) {
+        if (kCount) n_contrib += (x < cam.W && y < cam.H);
         const float2 kk = s_k[i];  // sub-ulp μ' correction of the exponent (value path only)
         const float arg = fmaf(-kk.x, dx, fmaf(-kk.y, dy, fmaf(power, kLog2e, q1.w)));
         const float alpha = power >= q1.z ? 0.99f : ex2_approx(arg);
@@ -79,6 +81,13 @@ __global__ void __launch_bounds__(256) k_fwd(DevCam cam, const float4* __restric
       }
     }
   }
+  if (kCount) {  // contributing (splat, pixel) pairs and tile-granular evaluations of this tile
+    unsigned long long c = (unsigned long long)n_contrib;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((tid & 31) == 0) atomicAdd(counters, c);
+    if (tid == 0) atomicAdd(counters + 1, (unsigned long long)(end - start) * kTilePx);
+  }
   if (state) {
     state[pix] = P0; state[plane + pix] = P1; state[2 * plane + pix] = P2;
     state[3 * plane + pix] = Q; state[4 * plane + pix] = T;
@@ -97,16 +106,20 @@ __global__ void __launch_bounds__(256) k_fwd(DevCam cam, const float4* __restric
 
 void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pair_slot,
                           const int32_t* tile_offsets, int64_t capacity, const float* base, const uint8_t* route,
-                          float* image, float* state, float* base_out, cudaStream_t st) {
-  int n_tiles = cam.TX * cam.TY;
+                          float* image, float* state, float* base_out, cudaStream_t st, int64_t* counters) {
+  const int n_tiles = cam.TX * cam.TY;
   const float4* r4 = reinterpret_cast<const float4*>(rec);
-  if (route) {
-    if (base) k_fwd<true, true><<<n_tiles, 256, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, base, route, image, state, base_out);
-    else k_fwd<true, false><<<n_tiles, 256, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, base, route, image, state, base_out);
+  auto* cnt = reinterpret_cast<unsigned long long*>(counters);
+#define OIT_FWD(R, B, K) \
+  k_fwd<R, B, K><<<n_tiles, 256, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, base, route, image, state, base_out, cnt)
+  if (counters) {
+    if (route) { if (base) OIT_FWD(true, true, true); else OIT_FWD(true, false, true); }
+    else { if (base) OIT_FWD(false, true, true); else OIT_FWD(false, false, true); }
   } else {
-    if (base) k_fwd<false, true><<<n_tiles, 256, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, base, route, image, state, base_out);
-    else k_fwd<false, false><<<n_tiles, 256, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, base, route, image, state, base_out);
+    if (route) { if (base) OIT_FWD(true, true, false); else OIT_FWD(true, false, false); }
+    else { if (base) OIT_FWD(false, true, false); else OIT_FWD(false, false, false); }
   }
+#undef OIT_FWD
 }
 
 }  // namespace oit

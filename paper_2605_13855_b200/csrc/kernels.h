@@ -26,7 +26,7 @@ void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_sl
 // composite_fwd.cu — a3
 void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pair_slot,
                           const int32_t* tile_offsets, int64_t capacity, const float* base, const uint8_t* route,
-                          float* image, float* state, float* base_out, cudaStream_t st);
+                          float* image, float* state, float* base_out, cudaStream_t st, int64_t* counters = nullptr);
 
 // composite_bwd.cu — a4 coefficients, a5 moments, a6 epilogue
 size_t bwd_ws_bytes(int32_t n_tiles, int32_t n_slots, int64_t capacity);
@@ -35,7 +35,17 @@ void launch_coef(const DevCam& cam, const float* state, const float* dL_dimage, 
 void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sigma, const int32_t* idx,
                           int32_t n_slots, const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
                           int64_t capacity, const float* coef4, const float* coefa, float scale, float* grad,
-                          float* dL_dsigma, float* dL_dcov, void* ws, cudaStream_t st);
+                          float* dL_dsigma, float* dL_dcov, void* ws, cudaStream_t st,
+                          cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr);
+
+// Record an event on a stream, as an external event node when the stream is being captured.
+inline void record_event(cudaEvent_t ev, cudaStream_t st) {
+  if (!ev) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
+  else cudaEventRecord(ev, st);
+}
 
 // loss / select / update — a4, a7, a8
 void launch_loss_grad(const DevCam& cam, const float* image, const float* target, int32_t loss, float* g,
