@@ -212,6 +212,23 @@ class ClockSampler:
                 "n_samples": len(self.samples)}
 
 
+_CUDART = None
+
+
+def event_ms(a, b):
+    """cudaEventElapsedTime on raw event handles (the moment-kernel events are recorded inside
+    liboit, which torch's own bookkeeping does not see)."""
+    global _CUDART
+    import ctypes
+    if _CUDART is None:
+        _CUDART = ctypes.CDLL("libcudart.so.12")
+    ms = ctypes.c_float(0.0)
+    rc = _CUDART.cudaEventElapsedTime(ctypes.byref(ms), ctypes.c_void_p(a.cuda_event), ctypes.c_void_p(b.cuda_event))
+    if rc != 0:
+        raise RuntimeError(f"cudaEventElapsedTime failed ({rc})")
+    return ms.value
+
+
 def scan_kernels(n):
     if n <= 0:
         return 0
@@ -305,6 +322,10 @@ class Workload:
         self.ev_fwd = [(mk(), mk()) for _ in range(self.V)]
         self.ev_bwd = [(mk(), mk()) for _ in range(self.V)]
         self.ev_seg = [mk() for _ in range(3)]
+        for pair in self.ev_fwd + self.ev_bwd:    # torch creates the CUDA event lazily on first record
+            pair[0].record()
+            pair[1].record()
+        torch.cuda.synchronize()
 
     # ---------------------------------------------------------------------------------------
     def train_views(self):
@@ -457,8 +478,8 @@ def time_workload(args, torch, dist, wl, world, headline_run):
             if allred:
                 dist.barrier()
             times.append(t_start.elapsed_time(t_end))
-            fwd_ms.append(sum(a.elapsed_time(b) for a, b in wl.ev_fwd))
-            bwd_ms.append(sum(a.elapsed_time(b) for a, b in wl.ev_bwd))
+            fwd_ms.append(sum(event_ms(a, b) for a, b in wl.ev_fwd))
+            bwd_ms.append(sum(event_ms(a, b) for a, b in wl.ev_bwd))
     ms = float(np.mean(times))
     if allred:
         t = torch.tensor([ms], dtype=torch.float64, device=wl.dev)
