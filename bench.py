@@ -261,7 +261,7 @@ class Workload:
         self.bg = sc.bg
         H = W = args.res
         self.H, self.W = H, W
-        cap = 1 << 24
+        cap = 1 << 22   # ≥ 2× the largest per-view pair count of C2 (checked below)
         self.pipe = ViewPipeline(cams[0], max(self.n_act, self.n_ina, 1), cap, device=dev)
         nt = self.pipe.n_tiles
         self.n_tiles = nt

@@ -124,11 +124,15 @@ int oit_bin_tiles(const oit_camera* cam, const float* rec, const int32_t* tiles_
  * Pairs at positions >= pair_capacity are ignored (memory safety after an overflow).
  * Outputs: image [3][H][W] (nullable), state [5][n_tiles][256] (nullable; the full pixel state
  * the backward needs), base_out (required iff route != NULL). bg: host float[3] = c0.
+ * Scratch: ws of oit_fwd_workspace_bytes(cam, pair_capacity) bytes (work items and the partial
+ * accumulators of tiles split across CTAs; ≈ 20 B per pair of capacity).
  * --------------------------------------------------------------------------------------- */
+size_t oit_fwd_workspace_bytes(const oit_camera* cam, int64_t pair_capacity);
 int oit_composite_fwd(const oit_camera* cam, const float* rec, const int32_t* pair_slot,
                       const int32_t* tile_offsets, int64_t pair_capacity,
                       const float bg_host[3], const float* base, const uint8_t* route,
-                      float* image, float* state, float* base_out, oit_stream_t stream);
+                      float* image, float* state, float* base_out, void* ws, size_t ws_bytes,
+                      oit_stream_t stream);
 
 /* Same as oit_composite_fwd; d_counters (nullable, device int64[2], accumulated +=) receives
  * [0] the number of contributing (splat, pixel) pairs (α ≥ 1/255, inside the image) and [1] the
@@ -137,7 +141,8 @@ int oit_composite_fwd(const oit_camera* cam, const float* rec, const int32_t* pa
 int oit_composite_fwd_ex(const oit_camera* cam, const float* rec, const int32_t* pair_slot,
                          const int32_t* tile_offsets, int64_t pair_capacity, const float bg_host[3],
                          const float* base, const uint8_t* route, float* image, float* state,
-                         float* base_out, int64_t* d_counters, oit_stream_t stream);
+                         float* base_out, int64_t* d_counters, void* ws, size_t ws_bytes,
+                         oit_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------
  * a4  oit_loss_grad — pixel loss gradient dL/dC of L = mean_{3HW} |C - I| (loss 0, sign(0)=0)

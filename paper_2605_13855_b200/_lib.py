@@ -69,8 +69,9 @@ def lib() -> C.CDLL:
             "oit_project_cull": (C.c_int, [scene_p, cam_p, vp, i32, vp, vp, vp]),
             "oit_bin_workspace_bytes": (sz, [cam_p]),
             "oit_bin_tiles": (C.c_int, [cam_p, vp, vp, i32, vp, i64, vp, vp, vp, sz, vp]),
-            "oit_composite_fwd": (C.c_int, [cam_p, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp]),
-            "oit_composite_fwd_ex": (C.c_int, [cam_p, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp]),
+            "oit_fwd_workspace_bytes": (sz, [cam_p, i64]),
+            "oit_composite_fwd": (C.c_int, [cam_p, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+            "oit_composite_fwd_ex": (C.c_int, [cam_p, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
             "oit_loss_grad": (C.c_int, [cam_p, vp, vp, i32, vp, vp]),
             "oit_bwd_workspace_bytes": (sz, [cam_p, i32, i64]),
             "oit_composite_bwd": (C.c_int, [scene_p, cam_p, vp, i32, vp, vp, vp, i64, vp, vp, vp, f32, vp, vp,
@@ -93,7 +94,7 @@ def lib() -> C.CDLL:
 
 
 EXPORTED = ["oit_status_string", "oit_num_tiles", "oit_project_cull", "oit_bin_workspace_bytes", "oit_bin_tiles",
-            "oit_composite_fwd", "oit_composite_fwd_ex", "oit_loss_grad", "oit_bwd_workspace_bytes", "oit_composite_bwd", "oit_composite_bwd_ex",
+            "oit_fwd_workspace_bytes", "oit_composite_fwd", "oit_composite_fwd_ex", "oit_loss_grad", "oit_bwd_workspace_bytes", "oit_composite_bwd", "oit_composite_bwd_ex",
             "oit_select_views", "oit_score_workspace_bytes", "oit_score_subsample", "oit_update_workspace_bytes",
             "oit_update_active_set"]
 
@@ -150,16 +151,21 @@ def oit_bin_tiles(cam, rec, tiles_per_slot, n_slots, pair_slot, tile_offsets, n_
                                _ptr(ws), int(ws.numel()), _stream(stream)), "oit_bin_tiles")
 
 
-def oit_composite_fwd(cam, rec, pair_slot, tile_offsets, bg, base=None, route=None, image=None, state=None,
+def oit_fwd_workspace_bytes(cam, pair_capacity: int) -> int:
+    return int(lib().oit_fwd_workspace_bytes(C.byref(camera(cam)), int(pair_capacity)))
+
+
+def oit_composite_fwd(cam, rec, pair_slot, tile_offsets, bg, ws, base=None, route=None, image=None, state=None,
                       base_out=None, stream=None, counters=None):
     """counters: optional int64[2] device tensor (+=): contributing pairs, tile-granular evals
     (oit_composite_fwd_ex)."""
     args = (C.byref(camera(cam)), _ptr(rec), _ptr(pair_slot), _ptr(tile_offsets), int(pair_slot.numel()), _f3(bg),
             _ptr(base), _ptr(route), _ptr(image), _ptr(state), _ptr(base_out))
     if counters is None:
-        _check(lib().oit_composite_fwd(*args, _stream(stream)), "oit_composite_fwd")
+        _check(lib().oit_composite_fwd(*args, _ptr(ws), int(ws.numel()), _stream(stream)), "oit_composite_fwd")
     else:
-        _check(lib().oit_composite_fwd_ex(*args, _ptr(counters), _stream(stream)), "oit_composite_fwd_ex")
+        _check(lib().oit_composite_fwd_ex(*args, _ptr(counters), _ptr(ws), int(ws.numel()), _stream(stream)),
+               "oit_composite_fwd_ex")
 
 
 def oit_loss_grad(cam, image, target, loss: str, dL_dimage, stream=None):

@@ -93,23 +93,30 @@ int oit_bin_tiles(const oit_camera* cam, const float* rec, const int32_t* tiles_
   return launch_status();
 }
 
+size_t oit_fwd_workspace_bytes(const oit_camera* cam, int64_t pair_capacity) {
+  if (!cam || pair_capacity < 0) return 0;
+  return fwd_ws_bytes(oit_num_tiles(cam), pair_capacity);
+}
+
 int oit_composite_fwd(const oit_camera* cam, const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
                       int64_t pair_capacity, const float bg_host[3], const float* base, const uint8_t* route,
-                      float* image, float* state, float* base_out, oit_stream_t stream) {
+                      float* image, float* state, float* base_out, void* ws, size_t ws_bytes, oit_stream_t stream) {
   return oit_composite_fwd_ex(cam, rec, pair_slot, tile_offsets, pair_capacity, bg_host, base, route, image, state,
-                              base_out, nullptr, stream);
+                              base_out, nullptr, ws, ws_bytes, stream);
 }
 
 int oit_composite_fwd_ex(const oit_camera* cam, const float* rec, const int32_t* pair_slot,
                          const int32_t* tile_offsets, int64_t pair_capacity, const float bg_host[3], const float* base,
                          const uint8_t* route, float* image, float* state, float* base_out, int64_t* d_counters,
-                         oit_stream_t stream) {
+                         void* ws, size_t ws_bytes, oit_stream_t stream) {
   if (!cam_ok(cam) || !tile_offsets || !bg_host || pair_capacity < 0) return OIT_EINVAL;
   if (pair_capacity > 0 && (!rec || !pair_slot)) return OIT_EINVAL;
   if (route && !base_out) return OIT_EINVAL;
+  if (!route && !ws) return OIT_EINVAL;
   if (!shape_ok(cam)) return OIT_ESHAPE;
+  if (!route && ws_bytes < oit_fwd_workspace_bytes(cam, pair_capacity)) return OIT_ECAPACITY;
   launch_composite_fwd(dev_cam(cam, bg_host), rec, pair_slot, tile_offsets, pair_capacity, base, route, image, state,
-                       base_out, S(stream), d_counters);
+                       base_out, S(stream), d_counters, ws);
   return launch_status();
 }
 
@@ -176,7 +183,7 @@ struct ScoreWs {
   float *rec_a, *rec_s, *state, *coef4, *coefa;
   int32_t *tps_a, *tps_s, *pairs, *offs;
   int64_t* npairs;
-  void *bin_ws, *bwd_ws;
+  void *bin_ws, *bwd_ws, *fwd_ws;
   size_t total;
 };
 
@@ -195,6 +202,7 @@ static ScoreWs score_layout(void* ws, const oit_camera* cam, int32_t n_active, i
   w.coef4 = cv.take<float>((size_t)nt * kTilePx * 4);
   w.coefa = cv.take<float>((size_t)nt * kTilePx);
   w.bin_ws = cv.take<char>(bin_ws_bytes(nt));
+  w.fwd_ws = cv.take<char>(fwd_ws_bytes(nt, cap));
   w.bwd_ws = cv.take<char>(bwd_ws_bytes(nt, n_score, cap));
   w.total = cv.off;
   return w;
@@ -235,7 +243,7 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
     launch_project(dc, scene->rows, scene->sigma, active_idx, n_active, w.rec_a, w.tps_a, st);
     launch_bin(dc, w.rec_a, w.tps_a, n_active, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st);
     launch_composite_fwd(dc, w.rec_a, w.pairs, w.offs, pair_capacity, caches_host ? caches_host[j] : nullptr, nullptr,
-                         nullptr, w.state, nullptr, st);
+                         nullptr, w.state, nullptr, st, nullptr, w.fwd_ws);
     // L_j and its pixel gradient (fused with the backward coefficients)
     launch_coef(dc, w.state, nullptr, targets_host[j], loss, w.coef4, w.coefa, st);
     // back-propagate L_j to the scored splats (R20)

@@ -62,30 +62,11 @@ __global__ void __launch_bounds__(256) k_coef(DevCam cam, const float* __restric
   coefa[pix] = a;
 }
 
-// ---------------------------------------------------------------- work items (chunks) ----
-__global__ void k_chunk_counts(const int32_t* __restrict__ offs, int n_tiles, int64_t capacity,
-                               int32_t* __restrict__ counts) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_tiles) return;
-  int64_t s = offs[t], e = offs[t + 1];
-  if (e > capacity) e = capacity;
-  if (s > e) s = e;
-  counts[t] = (int32_t)((e - s + 31) / 32);
-}
-
-__global__ void k_chunk_emit(const int32_t* __restrict__ item_offs, int n_tiles, int32_t* __restrict__ items) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_tiles) return;
-  int o = item_offs[t], n = item_offs[t + 1] - o;
-  for (int c = 0; c < n; c++) items[o + c] = t;
-}
-
 // ------------------------------------------------------------------------- a5 moments ----
 __global__ void __launch_bounds__(kMomentsThreads) k_moments(DevCam cam, const float4* __restrict__ rec,
                                                              const int32_t* __restrict__ pair_slot,
                                                              const int32_t* __restrict__ offs, int64_t capacity,
-                                                             const int32_t* __restrict__ items,
-                                                             const int32_t* __restrict__ item_offs,
+                                                             const int2* __restrict__ items,
                                                              const int32_t* __restrict__ n_items_p,
                                                              int32_t* __restrict__ counter,
                                                              const float4* __restrict__ coef4,
@@ -99,8 +80,8 @@ __global__ void __launch_bounds__(kMomentsThreads) k_moments(DevCam cam, const f
     if (lane == 0) item = atomicAdd(counter, 1);
     item = __shfl_sync(FULL, item, 0);
     if (item >= n_items) return;
-    const int tile = items[item];
-    const int chunk = item - item_offs[tile];  // items of one tile are contiguous
+    const int2 it = items[item];
+    const int tile = it.x, chunk = it.y;
     int64_t e64 = offs[tile + 1];
     if (e64 > capacity) e64 = capacity;
     const int end = (int)e64;
@@ -430,26 +411,13 @@ __global__ void __launch_bounds__(128) k_epilogue(DevCam cam, const float4* __re
 
 // --------------------------------------------------------------------------- launchers ----
 size_t bwd_ws_bytes(int32_t n_tiles, int32_t n_slots, int64_t capacity) {
-  int64_t max_items = capacity / 32 + n_tiles + 1;
-  return align_up((size_t)n_slots * 12 * sizeof(float)) + align_up((size_t)(n_tiles + 1) * 4) * 2 +
-         align_up((size_t)max_items * 4) + align_up(16) + scan_tmp_bytes(n_tiles);
+  return align_up((size_t)n_slots * 12 * sizeof(float)) + items_bytes(n_tiles, capacity, 32) + align_up(16);
 }
 
 void launch_coef(const DevCam& cam, const float* state, const float* dL_dimage, const float* target, int32_t loss,
                  float* coef4, float* coefa, cudaStream_t st) {
   int n_tiles = cam.TX * cam.TY;
   k_coef<<<n_tiles, 256, 0, st>>>(cam, state, dL_dimage, target, loss, reinterpret_cast<float4*>(coef4), coefa);
-}
-
-static int sm_count() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
 }
 
 void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sigma, const int32_t* idx,
@@ -466,21 +434,17 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
   const int64_t max_items = capacity / 32 + n_tiles + 1;
   Carve cv(ws);
   float* acc2d = cv.take<float>((size_t)n_slots * 12);
-  int32_t* counts = cv.take<int32_t>(n_tiles + 1);
-  int32_t* item_offs = cv.take<int32_t>(n_tiles + 1);
-  int32_t* items = cv.take<int32_t>(max_items);
+  int2* items = cv.take<int2>(max_items);
+  int32_t* n_items = cv.take<int32_t>(4);
+  int32_t* tile_nch = cv.take<int32_t>(n_tiles + 1);
   int32_t* counter = cv.take<int32_t>(4);
-  void* tmp = cv.take<char>(scan_tmp_bytes(n_tiles));
   cudaMemsetAsync(acc2d, 0, sizeof(float) * 12 * (size_t)n_slots, st);
   cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
-  const int tb = (n_tiles + 255) / 256;
-  k_chunk_counts<<<tb, 256, 0, st>>>(tile_offsets, n_tiles, capacity, counts);
-  launch_exclusive_scan(counts, item_offs, n_tiles, tmp, st);
-  k_chunk_emit<<<tb, 256, 0, st>>>(item_offs, n_tiles, items);
+  launch_build_items(tile_offsets, n_tiles, capacity, 32, 0, items, n_items, tile_nch, st);
   const int blocks = sm_count() * 6;  // persistent: 6 × 8 warps per SM, dynamic item claiming
   record_event(ev_begin, st);
   k_moments<<<blocks, kMomentsThreads, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), pair_slot, tile_offsets,
-                                                capacity, items, item_offs, item_offs + n_tiles, counter,
+                                                capacity, items, n_items, counter,
                                                 reinterpret_cast<const float4*>(coef4), coefa, acc2d);
   record_event(ev_end, st);
   k_epilogue<<<(n_slots + 127) / 128, 128, 0, st>>>(cam, reinterpret_cast<const float4*>(rows), sigma, idx, n_slots,

@@ -1,16 +1,168 @@
 // composite_fwd.cu — a3 oit_composite_fwd: weighted-OIT compositing (Eq. 7) with
 // BAN (blend & normalise) and BAU (blend & update the pre-render) of Alg. 2 l.7-13.
 //
-// One CTA per 16×16 tile, one thread per pixel (lane = pixel): the pixel's accumulators
-// (P_RGB, Q, T — and the FOLD copy for BAU) live in registers for the whole tile list, so the
-// forward needs no reduction at all. The tile's slot list is staged through shared memory in
-// batches of 256 records (48 B each: the three float4 the composite needs, gathered from L2);
-// every thread then reads each record as a broadcast. There is no early termination (OIT has
-// no front-to-back order), and no depth sort. A warp skips the value work of a splat
-// when none of its 32 pixels passes the fp32 spec test (DESIGN.md §3 step 13).
+// Lane = pixel: a pixel's accumulators (P_RGB, Q, T) live in registers for its whole splat list,
+// so the forward needs no reduction. Splat records are staged through shared memory and read as
+// broadcasts. There is no early termination (OIT has no front-to-back order) and no depth sort
+// (P:339).
+//
+// k_fwd_items (the default path): work items are (tile, chunk of ≤ kFwdChunk slots), longest
+// tiles first, claimed by a persistent grid — OIT's order independence makes splitting a tile
+// legal: partial (P, Q, T) of the chunks combine as P = ΣP_k, Q = ΣQ_k, T = ΠT_k, done in chunk
+// order by the last CTA to finish the tile (deterministic). Each thread owns 2 pixels of one row
+// (x and x+8), which shares the record loads and the row terms of the spec test and gives two
+// independent dependency chains. k_fwd (one CTA per tile) serves the BAU route path.
 #include "kernels.h"
 
 namespace oit {
+
+constexpr int kFwdThreads = 128;   // 2 pixels per thread
+constexpr int kFwdChunk = 256;     // slots per work item
+
+__device__ __forceinline__ void accum_px(float power, float thr_hi, float arg, const float4& q2, float& P0, float& P1,
+                                         float& P2, float& Q, float& T) {
+  const float alpha = power >= thr_hi ? 0.99f : ex2_approx(arg);
+  const float aw = alpha * q2.w;
+  P0 = fmaf(q2.x, aw, P0);
+  P1 = fmaf(q2.y, aw, P1);
+  P2 = fmaf(q2.z, aw, P2);
+  Q += aw;
+  T = fmaf(-alpha, T, T);
+}
+
+template <bool kBase, bool kCount>
+__global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
+    DevCam cam, const float4* __restrict__ rec, const int32_t* __restrict__ pair_slot,
+    const int32_t* __restrict__ offs, int64_t capacity, const int2* __restrict__ items,
+    const int32_t* __restrict__ n_items_p, int32_t* __restrict__ counter, const int32_t* __restrict__ tile_nch,
+    int32_t* __restrict__ done, float* __restrict__ partial, const float* __restrict__ base,
+    float* __restrict__ image, float* __restrict__ state, unsigned long long* __restrict__ counters) {
+  __shared__ float4 s_q0[kFwdThreads], s_q1[kFwdThreads], s_q2[kFwdThreads];
+  __shared__ float2 s_k[kFwdThreads];
+  __shared__ int s_item, s_last;
+  const int tid = threadIdx.x;
+  const int n_tiles = cam.TX * cam.TY;
+  const size_t plane = (size_t)n_tiles * kTilePx;
+  const int n_items = *n_items_p;
+  const int ly = tid >> 3, lx = tid & 7;     // pixels (lx, ly) and (lx + 8, ly) of the tile
+  const int p0 = ly * kTile + lx, p1 = p0 + 8;
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(counter, 1);
+    __syncthreads();
+    const int item = s_item;
+    __syncthreads();
+    if (item >= n_items) return;
+    const int2 it = items[item];
+    const int tile = it.x, chunk = it.y;
+    const int nch = tile_nch[tile];
+    const int tx0 = (tile % cam.TX) * kTile, ty0 = (tile / cam.TX) * kTile;
+    const float fy = (float)(ty0 + ly), fx0 = (float)(tx0 + lx), fx1 = (float)(tx0 + lx + 8);
+    const size_t px0 = (size_t)tile * kTilePx + p0, px1 = px0 + 8;
+    float A0 = 0.f, A1 = 0.f, A2 = 0.f, AQ = 0.f, AT = 1.f;   // pixel 0
+    float B0 = 0.f, B1 = 0.f, B2 = 0.f, BQ = 0.f, BT = 1.f;   // pixel 1
+    if (kBase && nch == 1) {
+      A0 = base[px0]; A1 = base[plane + px0]; A2 = base[2 * plane + px0]; AQ = base[3 * plane + px0]; AT = base[4 * plane + px0];
+      B0 = base[px1]; B1 = base[plane + px1]; B2 = base[2 * plane + px1]; BQ = base[3 * plane + px1]; BT = base[4 * plane + px1];
+    }
+    int64_t e64 = offs[tile + 1];
+    if (e64 > capacity) e64 = capacity;
+    const int begin = offs[tile] + chunk * kFwdChunk;
+    const int end = (int)min((int64_t)begin + kFwdChunk, e64);
+    int n_contrib = 0;
+    for (int b = begin; b < end; b += kFwdThreads) {
+      const int n = min(kFwdThreads, end - b);
+      if (tid < n) {
+        const float4* r = rec + (size_t)pair_slot[b + tid] * kRec4;
+        s_q0[tid] = r[0];
+        s_q1[tid] = r[1];
+        s_q2[tid] = r[2];
+        s_k[tid] = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(r + 3) + 2);
+      }
+      __syncthreads();
+#pragma unroll 2
+      for (int i = 0; i < n; i++) {
+        const float4 q0 = s_q0[i];  // mx my nA nB
+        const float4 q1 = s_q1[i];  // nC thr_lo thr_hi log2o
+        const float dy = __fsub_rn(fy, q0.y);
+        const float by = __fmul_rn(q0.w, dy);
+        const float cy = __fmul_rn(__fmul_rn(q1.x, dy), dy);
+        const float dx0 = __fsub_rn(fx0, q0.x), dx1 = __fsub_rn(fx1, q0.x);
+        const float pw0 = spec_power_row(q0.z, dx0, by, cy);
+        const float pw1 = spec_power_row(q0.z, dx1, by, cy);
+        const bool c0 = pw0 <= 0.0f && pw0 >= q1.y;
+        const bool c1 = pw1 <= 0.0f && pw1 >= q1.y;
+        if (c0 || c1) {
+          const float4 q2 = s_q2[i];  // cR cG cB w
+          const float2 kk = s_k[i];   // sub-ulp μ' correction of the exponent (value path)
+          const float base_arg = fmaf(-kk.y, dy, q1.w);
+          if (c0) accum_px(pw0, q1.z, fmaf(-kk.x, dx0, fmaf(pw0, kLog2e, base_arg)), q2, A0, A1, A2, AQ, AT);
+          if (c1) accum_px(pw1, q1.z, fmaf(-kk.x, dx1, fmaf(pw1, kLog2e, base_arg)), q2, B0, B1, B2, BQ, BT);
+          if (kCount) n_contrib += (c0 && tx0 + lx < cam.W && ty0 + ly < cam.H) + (c1 && tx0 + lx + 8 < cam.W && ty0 + ly < cam.H);
+        }
+      }
+      __syncthreads();
+    }
+    if (kCount) {
+      unsigned long long c = (unsigned long long)n_contrib;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if ((tid & 31) == 0 && c) atomicAdd(counters, c);
+      if (tid == 0) atomicAdd(counters + 1, (unsigned long long)(end - begin) * kTilePx);
+    }
+    bool write_final = true;
+    if (nch > 1) {
+      // multi-chunk tile: publish this chunk's partial; the last chunk to finish combines them
+      float* pa = partial + (size_t)item * 5 * kTilePx;
+      pa[p0] = A0; pa[kTilePx + p0] = A1; pa[2 * kTilePx + p0] = A2; pa[3 * kTilePx + p0] = AQ; pa[4 * kTilePx + p0] = AT;
+      pa[p1] = B0; pa[kTilePx + p1] = B1; pa[2 * kTilePx + p1] = B2; pa[3 * kTilePx + p1] = BQ; pa[4 * kTilePx + p1] = BT;
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) s_last = (atomicAdd(done + tile, 1) == nch - 1);
+      __syncthreads();
+      write_final = s_last;
+      if (write_final) {
+        __threadfence();
+        const int first = item - chunk;
+        if (kBase) {
+          A0 = base[px0]; A1 = base[plane + px0]; A2 = base[2 * plane + px0]; AQ = base[3 * plane + px0]; AT = base[4 * plane + px0];
+          B0 = base[px1]; B1 = base[plane + px1]; B2 = base[2 * plane + px1]; BQ = base[3 * plane + px1]; BT = base[4 * plane + px1];
+        } else {
+          A0 = A1 = A2 = AQ = 0.f; AT = 1.f;
+          B0 = B1 = B2 = BQ = 0.f; BT = 1.f;
+        }
+        for (int k = 0; k < nch; k++) {  // fixed chunk order: deterministic combination
+          const float* pk = partial + (size_t)(first + k) * 5 * kTilePx;
+          A0 += __ldcg(pk + p0); A1 += __ldcg(pk + kTilePx + p0); A2 += __ldcg(pk + 2 * kTilePx + p0);
+          AQ += __ldcg(pk + 3 * kTilePx + p0); AT *= __ldcg(pk + 4 * kTilePx + p0);
+          B0 += __ldcg(pk + p1); B1 += __ldcg(pk + kTilePx + p1); B2 += __ldcg(pk + 2 * kTilePx + p1);
+          BQ += __ldcg(pk + 3 * kTilePx + p1); BT *= __ldcg(pk + 4 * kTilePx + p1);
+        }
+        if (tid == 0) done[tile] = 0;  // re-arm for the next call
+      }
+    }
+    if (write_final) {
+      if (state) {
+        state[px0] = A0; state[plane + px0] = A1; state[2 * plane + px0] = A2; state[3 * plane + px0] = AQ; state[4 * plane + px0] = AT;
+        state[px1] = B0; state[plane + px1] = B1; state[2 * plane + px1] = B2; state[3 * plane + px1] = BQ; state[4 * plane + px1] = BT;
+      }
+      if (image) {
+        const size_t hw = (size_t)cam.W * cam.H;
+        const int y = ty0 + ly;
+        float F0, F1, F2, C0, C1, C2;
+        if (y < cam.H && tx0 + lx < cam.W) {
+          resolve_pixel(A0, A1, A2, AQ, AT, cam.bg, F0, F1, F2, C0, C1, C2);
+          const size_t p = (size_t)y * cam.W + tx0 + lx;
+          image[p] = C0; image[hw + p] = C1; image[2 * hw + p] = C2;
+        }
+        if (y < cam.H && tx0 + lx + 8 < cam.W) {
+          resolve_pixel(B0, B1, B2, BQ, BT, cam.bg, F0, F1, F2, C0, C1, C2);
+          const size_t p = (size_t)y * cam.W + tx0 + lx + 8;
+          image[p] = C0; image[hw + p] = C1; image[2 * hw + p] = C2;
+        }
+      }
+    }
+  }
+}
 
 template <bool kRoute, bool kBase, bool kCount>
 __global__ void __launch_bounds__(256) k_fwd(DevCam cam, const float4* __restrict__ rec,
@@ -104,12 +256,39 @@ __global__ void __launch_bounds__(256) k_fwd(DevCam cam, const float4* __restric
   }
 }
 
+size_t fwd_ws_bytes(int32_t n_tiles, int64_t capacity) {
+  const int64_t max_items = capacity / kFwdChunk + n_tiles + 1;
+  return items_bytes(n_tiles, capacity, kFwdChunk) + align_up((size_t)n_tiles * 4) + align_up(16) +
+         align_up((size_t)max_items * 5 * kTilePx * sizeof(float));
+}
+
 void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pair_slot,
                           const int32_t* tile_offsets, int64_t capacity, const float* base, const uint8_t* route,
-                          float* image, float* state, float* base_out, cudaStream_t st, int64_t* counters) {
+                          float* image, float* state, float* base_out, cudaStream_t st, int64_t* counters, void* ws) {
   const int n_tiles = cam.TX * cam.TY;
   const float4* r4 = reinterpret_cast<const float4*>(rec);
   auto* cnt = reinterpret_cast<unsigned long long*>(counters);
+  if (!route) {
+    const int64_t max_items = capacity / kFwdChunk + n_tiles + 1;
+    Carve cv(ws);
+    int2* items = cv.take<int2>(max_items);
+    int32_t* n_items = cv.take<int32_t>(4);
+    int32_t* tile_nch = cv.take<int32_t>(n_tiles + 1);
+    int32_t* done = cv.take<int32_t>(n_tiles);
+    int32_t* counter = cv.take<int32_t>(4);
+    float* partial = cv.take<float>((size_t)max_items * 5 * kTilePx);
+    cudaMemsetAsync(done, 0, sizeof(int32_t) * n_tiles, st);
+    cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
+    launch_build_items(tile_offsets, n_tiles, capacity, kFwdChunk, 1, items, n_items, tile_nch, st);
+    const int grid = sm_count() * 12;  // persistent; items are claimed dynamically
+#define OIT_FWD2(B, K)                                                                                         \
+  k_fwd_items<B, K><<<grid, kFwdThreads, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, items, n_items, \
+                                                  counter, tile_nch, done, partial, base, image, state, cnt)
+    if (counters) { if (base) OIT_FWD2(true, true); else OIT_FWD2(false, true); }
+    else { if (base) OIT_FWD2(true, false); else OIT_FWD2(false, false); }
+#undef OIT_FWD2
+    return;
+  }
 #define OIT_FWD(R, B, K) \
   k_fwd<R, B, K><<<n_tiles, 256, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, base, route, image, state, base_out, cnt)
   if (counters) {

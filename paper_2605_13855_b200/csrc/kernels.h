@@ -26,7 +26,24 @@ void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_sl
 // composite_fwd.cu — a3
 void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pair_slot,
                           const int32_t* tile_offsets, int64_t capacity, const float* base, const uint8_t* route,
-                          float* image, float* state, float* base_out, cudaStream_t st, int64_t* counters = nullptr);
+                          float* image, float* state, float* base_out, cudaStream_t st, int64_t* counters, void* ws);
+size_t fwd_ws_bytes(int32_t n_tiles, int64_t capacity);
+
+// items.cu — (tile, chunk) work lists, longest tiles first
+size_t items_bytes(int32_t n_tiles, int64_t capacity, int chunk);
+void launch_build_items(const int32_t* tile_offsets, int n_tiles, int64_t capacity, int chunk, int empty_items,
+                        int2* items, int32_t* n_items, int32_t* tile_nch, cudaStream_t st);
+
+inline int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
 
 // composite_bwd.cu — a4 coefficients, a5 moments, a6 epilogue
 size_t bwd_ws_bytes(int32_t n_tiles, int32_t n_slots, int64_t capacity);

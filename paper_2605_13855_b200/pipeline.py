@@ -30,6 +30,7 @@ class ViewPipeline:
         self.offs = torch.empty(self.n_tiles + 1, dtype=torch.int32, device=dev)
         self.n_pairs = torch.zeros(1, dtype=torch.int64, device=dev)
         self.bin_ws = _ws(L.oit_bin_workspace_bytes(cam), dev)
+        self.fwd_ws = _ws(L.oit_fwd_workspace_bytes(cam, self.capacity), dev)
         self.bwd_ws = _ws(L.oit_bwd_workspace_bytes(cam, self.max_slots, self.capacity), dev)
         self.state = torch.empty((5, self.n_tiles, 256), dtype=torch.float32, device=dev)
         self.image = torch.empty((3, self.H, self.W), dtype=torch.float32, device=dev)
@@ -54,7 +55,7 @@ class ViewPipeline:
         rec = self.project_bin(rows, sigma, idx, stream)
         if events is not None:
             events[0].record()
-        L.oit_composite_fwd(self.cam, rec, self.pairs, self.offs, bg, base=base, route=route,
+        L.oit_composite_fwd(self.cam, rec, self.pairs, self.offs, bg, self.fwd_ws, base=base, route=route,
                             image=self.image if image else None, state=self.state, base_out=base_out,
                             stream=stream, counters=counters)
         if events is not None:

@@ -38,7 +38,7 @@ def run(sc, cam, idx, tag):
     r2[vis, 8:11] = pv["color"][vis]
     r2[vis, 11] = pv["w"][vis]
     rec.copy_(t(r2))
-    L.oit_composite_fwd(cam, rec, p.pairs, p.offs, sc.bg, image=p.image, state=p.state)
+    L.oit_composite_fwd(cam, rec, p.pairs, p.offs, sc.bg, p.fwd_ws, image=p.image, state=p.state)
     e1 = np.abs(p.image.cpu().numpy() - ref["image"])
     print(f"    E1 (oracle c,w) max {e1.max():.3e}, n>1e-5 {(e1 > 1e-5).sum()}")
     # backward: GPU state vs oracle state as input, oracle c,w in rec
