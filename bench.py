@@ -366,11 +366,12 @@ class Workload:
         a, s = self.n_act, self.n_ina
         proj = lambda n: 1 if n > 0 else 0  # noqa: E731
         binn = lambda n: (1 if n > 0 else 0) + scan_kernels(nt) + 1  # noqa: E731
-        bwd = lambda n: 1 + ((4 + scan_kernels(nt)) if n > 0 else 0)  # noqa: E731  coef | chunks, scan, emit, moments, epilogue
-        train = self.V * (proj(a) + binn(a) + 1 + 1 + bwd(a))
+        fwd = 2                                            # build_items, k_fwd_items
+        bwd = lambda n: 1 + (3 if n > 0 else 0)  # noqa: E731  coef | build_items, moments, epilogue
+        train = self.V * (proj(a) + binn(a) + fwd + 1 + bwd(a))
         refresh = 1
         if s > 0:
-            refresh += self.S * (proj(a) + binn(a) + 1 + 1 + proj(s) + binn(s) + (bwd(s) - 1))
+            refresh += self.S * (proj(a) + binn(a) + fwd + 1 + proj(s) + binn(s) + (bwd(s) - 1))
             refresh += 1 + 1 + 3 * scan_kernels(nw) + 1
         return train + refresh
 

@@ -21,7 +21,7 @@
 
 namespace oit {
 
-constexpr int kMomentsThreads = 256;
+constexpr int kMomentsThreads = 128;
 
 // ------------------------------------------------------------------------------ a4 coef ---
 __global__ void __launch_bounds__(256) k_coef(DevCam cam, const float* __restrict__ state,
@@ -63,7 +63,68 @@ __global__ void __launch_bounds__(256) k_coef(DevCam cam, const float* __restric
 }
 
 // ------------------------------------------------------------------------- a5 moments ----
-__global__ void __launch_bounds__(kMomentsThreads) k_moments(DevCam cam, const float4* __restrict__ rec,
+struct Moments {
+  float U0, U1, U2, S, Od, M1, M2, XX, XY, YY;
+};
+
+// One lane = one splat; walks the pixel window [py0,py1]×[px0,px1] of its tile. The tile's
+// coefficients sit in this warp's shared-memory slice (broadcast reads). kClamp: some lane of the
+// warp may hit the 0.99 clamp (only splats with o ≥ 0.99 can: thr_hi ≤ 0).
+template <bool kClamp>
+__device__ __forceinline__ void moments_window(Moments& m, const float4* __restrict__ s_cu,
+                                               const float* __restrict__ s_ca, int tx0, int ty0, int px0, int px1,
+                                               int py0, int py1, bool valid, float mx, float my, float nA, float nB,
+                                               float nC, float thr_lo, float thr_hi, float log2o, float cR, float cG,
+                                               float cB, float w, float kx, float ky, float ey) {
+  const unsigned FULL = 0xffffffffu;
+  for (int py = py0; py <= py1; py++) {
+    const float dy = __fsub_rn((float)(ty0 + py), my);
+    const bool ract = valid && fabsf(dy) <= ey;
+    if (!__any_sync(FULL, ract)) continue;
+    const float by = __fmul_rn(nB, dy);
+    const float cyv = __fmul_rn(__fmul_rn(nC, dy), dy);
+    const float row_arg = fmaf(-ky, dy, log2o);
+    const float lo = ract ? thr_lo : 1.0f;  // folds the row test into the pixel test
+    float Rd = 0.f, Rdx = 0.f, Rdxx = 0.f;
+    const float4* cu_row = s_cu + py * kTile;
+    const float* ca_row = s_ca + py * kTile;
+#pragma unroll 4
+    for (int px = px0; px <= px1; px++) {
+      const float dx = __fsub_rn((float)(tx0 + px), mx);
+      const float power = spec_power_row(nA, dx, by, cyv);
+      const bool contrib = power <= 0.0f && power >= lo;
+      float alpha = ex2_approx(fmaf(-kx, dx, fmaf(power, kLog2e, row_arg)));
+      bool clamp = false;
+      if (kClamp) {
+        clamp = power >= thr_hi;
+        alpha = clamp ? 0.99f : alpha;
+      }
+      alpha = contrib ? alpha : 0.0f;
+      const float4 cu = cu_row[px];  // (u_R, u_G, u_B, s): broadcast
+      const float ca = ca_row[px];   // a
+      const float rinv = rcp_approx(1.0f - alpha);
+      const float dot = fmaf(cu.x, cR, fmaf(cu.y, cG, fmaf(cu.z, cB, -cu.w)));
+      float d = fmaf(ca, rinv, w * dot) * alpha;  // dL/dα · α (0 where α = 0)
+      if (kClamp) d = clamp ? 0.0f : d;
+      m.U0 = fmaf(alpha, cu.x, m.U0);
+      m.U1 = fmaf(alpha, cu.y, m.U1);
+      m.U2 = fmaf(alpha, cu.z, m.U2);
+      m.S = fmaf(alpha, cu.w, m.S);
+      const float t = d * dx;
+      Rd += d;
+      Rdx += t;
+      Rdxx = fmaf(t, dx, Rdxx);
+    }
+    m.Od += Rd;
+    m.M1 += Rdx;
+    m.M2 = fmaf(dy, Rd, m.M2);
+    m.XX += Rdxx;
+    m.XY = fmaf(dy, Rdx, m.XY);
+    m.YY = fmaf(dy * dy, Rd, m.YY);
+  }
+}
+
+__global__ void __launch_bounds__(kMomentsThreads, 8) k_moments(DevCam cam, const float4* __restrict__ rec,
                                                              const int32_t* __restrict__ pair_slot,
                                                              const int32_t* __restrict__ offs, int64_t capacity,
                                                              const int2* __restrict__ items,
@@ -72,9 +133,14 @@ __global__ void __launch_bounds__(kMomentsThreads) k_moments(DevCam cam, const f
                                                              const float4* __restrict__ coef4,
                                                              const float* __restrict__ coefa,
                                                              float* __restrict__ acc2d) {
-  const int lane = threadIdx.x & 31;
+  __shared__ float4 s_cu_all[kMomentsThreads / 32][kTilePx];
+  __shared__ float s_ca_all[kMomentsThreads / 32][kTilePx];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float4* s_cu = s_cu_all[wid];
+  float* s_ca = s_ca_all[wid];
   const int n_items = *n_items_p;
   const unsigned FULL = 0xffffffffu;
+  int staged_tile = -1;
   for (;;) {
     int item = 0;
     if (lane == 0) item = atomicAdd(counter, 1);
@@ -82,6 +148,23 @@ __global__ void __launch_bounds__(kMomentsThreads) k_moments(DevCam cam, const f
     if (item >= n_items) return;
     const int2 it = items[item];
     const int tile = it.x, chunk = it.y;
+    if (tile != staged_tile) {  // stage the tile's pixel coefficients (5 KB) with coalesced 16-B loads
+      const float4* g4 = coef4 + (size_t)tile * kTilePx;
+      const float4* ga = reinterpret_cast<const float4*>(coefa + (size_t)tile * kTilePx);
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; h++) {  // two waves of 5 independent 16-B loads per lane
+        float4 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) v[k] = __ldcg(g4 + lane + 32 * (4 * h + k));
+        const float4 va = __ldcg(ga + lane + 32 * h);
+#pragma unroll
+        for (int k = 0; k < 4; k++) s_cu[lane + 32 * (4 * h + k)] = v[k];
+        reinterpret_cast<float4*>(s_ca)[lane + 32 * h] = va;
+      }
+      __syncwarp();
+      staged_tile = tile;
+    }
     int64_t e64 = offs[tile + 1];
     if (e64 > capacity) e64 = capacity;
     const int end = (int)e64;
@@ -94,11 +177,7 @@ __global__ void __launch_bounds__(kMomentsThreads) k_moments(DevCam cam, const f
       const float4* r = rec + (size_t)slot * kRec4;
       q0 = r[0]; q1 = r[1]; q2 = r[2]; q3 = r[3]; q4 = r[4];
     }
-    const float mx = q0.x, my = q0.y, nA = q0.z, nB = q0.w;
-    const float nC = q1.x, thr_lo = q1.y, thr_hi = q1.z, log2o = q1.w;
-    const float cR = q2.x, cG = q2.y, cB = q2.z, w = q2.w;
-    const float kx = q3.z, ky = q3.w;  // sub-ulp μ' correction of the exponent (value path)
-    const float ex = q4.x, ey = q4.y;  // conservative pixel half-extents of the α=1/255 ellipse
+    const float mx = q0.x, my = q0.y, ex = q4.x, ey = q4.y;
     const int tx0 = (tile % cam.TX) * kTile, ty0 = (tile / cam.TX) * kTile;
     // warp-uniform pixel window: union of the lanes' extents, clipped to the tile
     float lo_x = valid ? mx - ex : 1e30f, hi_x = valid ? mx + ex : -1e30f;
@@ -114,52 +193,18 @@ __global__ void __launch_bounds__(kMomentsThreads) k_moments(DevCam cam, const f
     const int px1 = min(kTile - 1, (int)ceilf(fminf(hi_x - (float)tx0, 16.f)));
     const int py0 = max(0, (int)floorf(fmaxf(lo_y - (float)ty0, -1.f)));
     const int py1 = min(kTile - 1, (int)ceilf(fminf(hi_y - (float)ty0, 16.f)));
-
-    float U0 = 0.f, U1 = 0.f, U2 = 0.f, S = 0.f, Od = 0.f, M1 = 0.f, M2 = 0.f, XX = 0.f, XY = 0.f, YY = 0.f;
-    const float4* cf4 = coef4 + (size_t)tile * kTilePx;
-    const float* cfa = coefa + (size_t)tile * kTilePx;
-    for (int py = py0; py <= py1; py++) {
-      const float dy = __fsub_rn((float)(ty0 + py), my);
-      const bool ract = valid && fabsf(dy) <= ey;
-      if (!__any_sync(FULL, ract)) continue;
-      const float by = __fmul_rn(nB, dy);
-      const float cyv = __fmul_rn(__fmul_rn(nC, dy), dy);
-      float Rd = 0.f, Rdx = 0.f, Rdxx = 0.f;
-      for (int px = px0; px <= px1; px++) {
-        const float dx = __fsub_rn((float)(tx0 + px), mx);
-        const float power = spec_power_row(nA, dx, by, cyv);
-        const bool contrib = ract && power <= 0.0f && power >= thr_lo;
-        const bool clamp = power >= thr_hi;
-        const float arg = fmaf(-kx, dx, fmaf(-ky, dy, fmaf(power, kLog2e, log2o)));
-        float alpha = clamp ? 0.99f : ex2_approx(arg);
-        alpha = contrib ? alpha : 0.0f;
-        const float4 cu = __ldg(cf4 + py * kTile + px);  // (u_R, u_G, u_B, s): warp-uniform
-        const float ca = __ldg(cfa + py * kTile + px);   // a
-        const float rinv = rcp_approx(1.0f - alpha);
-        const float dot = fmaf(cu.x, cR, fmaf(cu.y, cG, fmaf(cu.z, cB, -cu.w)));
-        const float dLda = fmaf(ca, rinv, w * dot);
-        const float d = (contrib && !clamp) ? dLda * alpha : 0.0f;
-        U0 = fmaf(alpha, cu.x, U0);
-        U1 = fmaf(alpha, cu.y, U1);
-        U2 = fmaf(alpha, cu.z, U2);
-        S = fmaf(alpha, cu.w, S);
-        const float t = d * dx;
-        Rd += d;
-        Rdx += t;
-        Rdxx = fmaf(t, dx, Rdxx);
-      }
-      Od += Rd;
-      M1 += Rdx;
-      M2 = fmaf(dy, Rd, M2);
-      XX += Rdxx;
-      XY = fmaf(dy, Rdx, XY);
-      YY = fmaf(dy * dy, Rd, YY);
-    }
-    if (valid && (U0 != 0.f || U1 != 0.f || U2 != 0.f || S != 0.f || Od != 0.f)) {
+    Moments m = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (__any_sync(FULL, valid && q1.z <= 0.0f))
+      moments_window<true>(m, s_cu, s_ca, tx0, ty0, px0, px1, py0, py1, valid, mx, my, q0.z, q0.w, q1.x, q1.y, q1.z,
+                           q1.w, q2.x, q2.y, q2.z, q2.w, q3.z, q3.w, ey);
+    else
+      moments_window<false>(m, s_cu, s_ca, tx0, ty0, px0, px1, py0, py1, valid, mx, my, q0.z, q0.w, q1.x, q1.y, q1.z,
+                            q1.w, q2.x, q2.y, q2.z, q2.w, q3.z, q3.w, ey);
+    if (valid && (m.U0 != 0.f || m.U1 != 0.f || m.U2 != 0.f || m.S != 0.f || m.Od != 0.f)) {
       float* a = acc2d + (size_t)slot * 12;
-      red_add_v4(a, U0, U1, U2, S);
-      red_add_v4(a + 4, Od, M1, M2, XX);
-      red_add_v4(a + 8, XY, YY, 0.f, 0.f);
+      red_add_v4(a, m.U0, m.U1, m.U2, m.S);
+      red_add_v4(a + 4, m.Od, m.M1, m.M2, m.XX);
+      red_add_v4(a + 8, m.XY, m.YY, 0.f, 0.f);
     }
   }
 }
@@ -441,7 +486,7 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
   cudaMemsetAsync(acc2d, 0, sizeof(float) * 12 * (size_t)n_slots, st);
   cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
   launch_build_items(tile_offsets, n_tiles, capacity, 32, 0, items, n_items, tile_nch, st);
-  const int blocks = sm_count() * 6;  // persistent: 6 × 8 warps per SM, dynamic item claiming
+  const int blocks = sm_count() * 8;  // persistent: 8 × 4 warps per SM, dynamic item claiming
   record_event(ev_begin, st);
   k_moments<<<blocks, kMomentsThreads, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), pair_slot, tile_offsets,
                                                 capacity, items, n_items, counter,
