@@ -18,11 +18,14 @@ __device__ __forceinline__ void rect_of(const float4* rec, int k, int& x0, int& 
   x0 = rx & 0xffff; x1 = rx >> 16; y0 = ry & 0xffff; y1 = ry >> 16;
 }
 
-// A warp takes 32 consecutive slots and enumerates their (slot, tile) pairs 32-wide: the owner of
+// A warp takes kSlotsPerWarp consecutive slots and enumerates their (slot, tile) pairs 32-wide
+// (8 slots ≈ 50 pairs per warp keeps enough warps in flight to hide the atomics' latency): the owner of
 // pair j is found by a binary search over the warp's exclusive scan of the slots' tile counts
 // (shuffles only), so one huge splat does not serialise its warp. Pairs of the same tile inside a
 // warp step are combined into one atomic (__match_any_sync): hot tiles see far fewer atomics.
 // kScatter = false: histogram (counts[tile] += n); true: cursor claims and pair_slot writes.
+constexpr int kSlotsPerWarp = 8;
+
 template <bool kScatter>
 __global__ void __launch_bounds__(128) k_bin_expand(const float4* __restrict__ rec, const int32_t* __restrict__ tps,
                                                     int32_t n_slots, int TX, int32_t* __restrict__ cnt,
@@ -38,10 +41,10 @@ __global__ void __launch_bounds__(128) k_bin_expand(const float4* __restrict__ r
     *d_n_pairs = n;
     if (d_max) atomicMax(reinterpret_cast<unsigned long long*>(d_max), (unsigned long long)n);
   }
-  for (int base = gw * 32; base < n_slots; base += nw * 32) {
+  for (int base = gw * kSlotsPerWarp; base < n_slots; base += nw * kSlotsPerWarp) {
     const int k = base + lane;
     int c = 0, x0 = 0, y0 = 0, w = 1;
-    if (k < n_slots) {
+    if (lane < kSlotsPerWarp && k < n_slots) {
       c = tps[k];
       if (c) {
         int x1, y1;
@@ -100,7 +103,7 @@ void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_sl
   void* tmp = cv.take<char>(scan_tmp_bytes(n_tiles));
   cudaMemsetAsync(counts, 0, sizeof(int32_t) * n_tiles, st);
   const float4* r4 = reinterpret_cast<const float4*>(rec);
-  const int warps = n_slots > 0 ? (n_slots + 31) / 32 : 1;
+  const int warps = n_slots > 0 ? (n_slots + kSlotsPerWarp - 1) / kSlotsPerWarp : 1;
   const int blocks = (warps + 3) / 4;
   if (n_slots > 0)
     k_bin_expand<false><<<blocks, 128, 0, st>>>(r4, tiles_per_slot, n_slots, cam.TX, counts, pair_slot, capacity,

@@ -210,7 +210,11 @@ __global__ void __launch_bounds__(kMomentsThreads, 8) k_moments(DevCam cam, cons
 }
 
 // ------------------------------------------------------------------------ a6 epilogue ----
-__global__ void __launch_bounds__(128) k_epilogue(DevCam cam, const float4* __restrict__ rows,
+// One thread per slot. Phase 1 (appearance): view direction, SH colour/weight and their
+// gradients, the h/v rows are updated while streaming the coefficients, and the direction's
+// gradient is reduced to 3 floats. Phase 2 (geometry): μ', conic → Σ' → (Σ, J) → (q, s, μ).
+// Ordering the phases keeps the SH and the 3×3 geometry state from being live together.
+__global__ void __launch_bounds__(128, 3) k_epilogue(DevCam cam, const float4* __restrict__ rows,
                                                   const float* __restrict__ sigma_p, const int32_t* __restrict__ idx,
                                                   int32_t n_slots, const float4* __restrict__ rec,
                                                   const float4* __restrict__ acc2d, float scale,
@@ -225,19 +229,89 @@ __global__ void __launch_bounds__(128) k_epilogue(DevCam cam, const float4* __re
     const float4 m1 = acc2d[(size_t)k * 3 + 1];  // Od M1 M2 XX
     const float4 m2 = acc2d[(size_t)k * 3 + 2];  // XY YY
     if (vis && (m0.x != 0.f || m0.y != 0.f || m0.z != 0.f || m0.w != 0.f || m1.x != 0.f)) {
+      const float4* r = rows + (size_t)idx[k] * kRow4;
+      float4* gr = grad + (size_t)k * kRow4;
+      const float4 ra = r[0];
+      const float mu0 = ra.x, mu1 = ra.y, mu2 = ra.z, op = ra.w;
+      float gmu0, gmu1, gmu2, gtz_w = 0.f;
+      // =============================== phase 1: appearance (Eq. 4 colour, Eq. 1 weight) ====
+      {
+        const float dvx = mu0 - cam.center[0], dvy = mu1 - cam.center[1], dvz = mu2 - cam.center[2];
+        const float dn = sqrtf(dvx * dvx + dvy * dvy + dvz * dvz), idn = 1.0f / dn;
+        const float rx = dvx * idn, ry = dvy * idn, rz = dvz * idn;
+        float Y[16];
+        sh_basis(rx, ry, rz, Y);
+        float vraw = 0.f;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const float4 vv = r[3 + q];
+          vraw += vv.x * Y[4 * q] + vv.y * Y[4 * q + 1] + vv.z * Y[4 * q + 2] + vv.w * Y[4 * q + 3];
+        }
+        float craw[3] = {0.5f, 0.5f, 0.5f};
+#pragma unroll
+        for (int q = 0; q < 12; q++) {
+          const float4 hh = r[7 + q];
+          const float e[4] = {hh.x, hh.y, hh.z, hh.w};
+#pragma unroll
+          for (int u = 0; u < 4; u++) craw[(4 * q + u) % 3] += e[u] * Y[(4 * q + u) / 3];
+        }
+        const float sigma = *sigma_p;
+        const double ramp_d = ((double)sigma - depth_fp64(cam, mu0, mu1, mu2)) / (double)sigma;  // see ramp_fp64
+        const float ramp = ramp_d > 0.0 ? (float)ramp_d : 0.f, vplus = fmaxf(vraw, 0.f), w = ramp * vplus;
+        const float col0 = fmaxf(craw[0], 0.f), col1 = fmaxf(craw[1], 0.f), col2 = fmaxf(craw[2], 0.f);
+        // dL/dc = w U, dL/dw = U·c − S
+        const float gw = m0.x * col0 + m0.y * col1 + m0.z * col2 - m0.w;
+        const float gch[3] = {craw[0] > 0.f ? w * m0.x : 0.f, craw[1] > 0.f ? w * m0.y : 0.f,
+                              craw[2] > 0.f ? w * m0.z : 0.f};
+        const float gvp = vraw > 0.f ? gw * ramp : 0.f;  // dL/dv⁺ through the max(0, ·) of R4
+        if (ramp_d > 0.0) {
+          const float gramp = gw * vplus;
+          gtz_w = -gramp / sigma;                                   // ∂w/∂d = −v⁺/σ
+          gsig = gramp * (float)((double)sigma - ramp_d * (double)sigma) / (sigma * sigma);  // ∂w/∂σ = v⁺ d/σ²
+        }
+        // h, v rows: dL/dh_j,ch = gc_ch Y_j, dL/dv_j = gv⁺ Y_j; direction: Σ_j cf_j ∇Y_j
+        float cf[16];
+        const float sv = scale * gvp;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const float4 vv = r[3 + q];
+          cf[4 * q] = gvp * vv.x; cf[4 * q + 1] = gvp * vv.y; cf[4 * q + 2] = gvp * vv.z; cf[4 * q + 3] = gvp * vv.w;
+          float4 g = gr[3 + q];
+          g.x = fmaf(sv, Y[4 * q], g.x); g.y = fmaf(sv, Y[4 * q + 1], g.y);
+          g.z = fmaf(sv, Y[4 * q + 2], g.z); g.w = fmaf(sv, Y[4 * q + 3], g.w);
+          gr[3 + q] = g;
+        }
+        const float sh3[3] = {scale * gch[0], scale * gch[1], scale * gch[2]};
+#pragma unroll
+        for (int q = 0; q < 12; q++) {
+          const float4 hh = r[7 + q];
+          const float e[4] = {hh.x, hh.y, hh.z, hh.w};
+#pragma unroll
+          for (int u = 0; u < 4; u++) cf[(4 * q + u) / 3] = fmaf(gch[(4 * q + u) % 3], e[u], cf[(4 * q + u) / 3]);
+          float4 g = gr[7 + q];
+          g.x = fmaf(sh3[(4 * q) % 3], Y[(4 * q) / 3], g.x);
+          g.y = fmaf(sh3[(4 * q + 1) % 3], Y[(4 * q + 1) / 3], g.y);
+          g.z = fmaf(sh3[(4 * q + 2) % 3], Y[(4 * q + 2) / 3], g.z);
+          g.w = fmaf(sh3[(4 * q + 3) % 3], Y[(4 * q + 3) / 3], g.w);
+          gr[7 + q] = g;
+        }
+        float gr0, gr1, gr2;
+        sh_vjp(rx, ry, rz, cf, gr0, gr1, gr2);
+        const float rdot = rx * gr0 + ry * gr1 + rz * gr2;  // r = (μ − f)/‖μ − f‖ → μ
+        gmu0 = (gr0 - rx * rdot) * idn;
+        gmu1 = (gr1 - ry * rdot) * idn;
+        gmu2 = (gr2 - rz * rdot) * idn;
+      }
+      // =============================== phase 2: geometry (Eq. 2, 5, 6) =====================
       const float4 q0 = rec[(size_t)k * kRec4 + 0];
       const float4 q1 = rec[(size_t)k * kRec4 + 1];
       const float4 q4 = rec[(size_t)k * kRec4 + 4];
       const float nA = q0.z, nB = q0.w, nC = q1.x;
-      const float4* r = rows + (size_t)idx[k] * kRow4;
-      const float4 ra = r[0], rb = r[1], rc = r[2];
-      const float mu[3] = {ra.x, ra.y, ra.z};
-      const float op = ra.w;
+      const float4 rb = r[1], rc = r[2];
       const float W[3][3] = {{cam.R[0], cam.R[1], cam.R[2]}, {cam.R[3], cam.R[4], cam.R[5]}, {cam.R[6], cam.R[7], cam.R[8]}};
-      // ---- recompute the forward quantities (value path, fp32) ----
       float t[3];
 #pragma unroll
-      for (int i = 0; i < 3; i++) t[i] = W[i][0] * mu[0] + W[i][1] * mu[1] + W[i][2] * mu[2] + cam.t[i];
+      for (int i = 0; i < 3; i++) t[i] = W[i][0] * mu0 + W[i][1] * mu1 + W[i][2] * mu2 + cam.t[i];
       const float tz = t[2], itz = 1.0f / tz, itz2 = itz * itz;
       const float limx = 1.3f * (0.5f * (float)cam.W / cam.fx), limy = 1.3f * (0.5f * (float)cam.H / cam.fy);
       const float ux = t[0] * itz, uy = t[1] * itz;
@@ -266,52 +340,14 @@ __global__ void __launch_bounds__(128) k_epilogue(DevCam cam, const float4* __re
       for (int i = 0; i < 3; i++)
 #pragma unroll
         for (int j = 0; j < 3; j++) Sg[i][j] = M[i][0] * M[j][0] + M[i][1] * M[j][1] + M[i][2] * M[j][2];
-      // view direction and SH (Eq. 4), weight (Eq. 1)
-      float dv[3] = {mu[0] - cam.center[0], mu[1] - cam.center[1], mu[2] - cam.center[2]};
-      const float dn = sqrtf(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]), idn = 1.0f / dn;
-      const float rx = dv[0] * idn, ry = dv[1] * idn, rz = dv[2] * idn;
-      float Y[16];
-      sh_basis(rx, ry, rz, Y);
-      float vco[16];
-      float vraw = 0.f;
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        const float4 vv = r[3 + q];
-        vco[4 * q] = vv.x; vco[4 * q + 1] = vv.y; vco[4 * q + 2] = vv.z; vco[4 * q + 3] = vv.w;
-      }
-#pragma unroll
-      for (int j = 0; j < 16; j++) vraw += vco[j] * Y[j];
-      float hco[48];
-#pragma unroll
-      for (int q = 0; q < 12; q++) {
-        const float4 hh = r[7 + q];
-        hco[4 * q] = hh.x; hco[4 * q + 1] = hh.y; hco[4 * q + 2] = hh.z; hco[4 * q + 3] = hh.w;
-      }
-      float craw[3] = {0.5f, 0.5f, 0.5f};
-#pragma unroll
-      for (int j = 0; j < 16; j++) {
-        craw[0] += hco[3 * j] * Y[j];
-        craw[1] += hco[3 * j + 1] * Y[j];
-        craw[2] += hco[3 * j + 2] * Y[j];
-      }
-      const float col[3] = {fmaxf(craw[0], 0.f), fmaxf(craw[1], 0.f), fmaxf(craw[2], 0.f)};
-      const float sigma = *sigma_p;
-      const double ramp_d = ((double)sigma - depth_fp64(cam, mu[0], mu[1], mu[2])) / (double)sigma;  // see ramp_fp64
-      const float ramp_raw = (float)ramp_d;
-      const float ramp = ramp_d > 0.0 ? ramp_raw : 0.f, vplus = fmaxf(vraw, 0.f), w = ramp * vplus;
-
-      // ---- 2D gradients from the moments ----
-      const float U[3] = {m0.x, m0.y, m0.z};
       // the moments were accumulated with the spec offsets dx = x - μ'_spec; the true offsets are
       // dx - δx (δ = μ'_fp64 - μ'_spec, rec q4.zw): re-centre the moments exactly
       const float dmx = q4.z, dmy = q4.w;
-      const float Ssum = m0.w, Od = m1.x, M1s = m1.y, M2s = m1.z;
+      const float Od = m1.x, M1s = m1.y, M2s = m1.z;
       const float M1 = M1s - dmx * Od, M2 = M2s - dmy * Od;
       const float XX = m1.w - 2.f * dmx * M1s + dmx * dmx * Od;
       const float XY = m2.x - dmy * M1s - dmx * M2s + dmx * dmy * Od;
       const float YY = m2.y - 2.f * dmy * M2s + dmy * dmy * Od;
-      const float gc[3] = {w * U[0], w * U[1], w * U[2]};
-      const float gw = U[0] * col[0] + U[1] * col[1] + U[2] * col[2] - Ssum;
       const float go = Od / op;
       const float gmx = -(2.f * nA * M1 + nB * M2), gmy = -(nB * M1 + 2.f * nC * M2);
       // conic K = [[-2nA, -nB], [-nB, -2nC]]; dL/dK = -½[[XX, XY], [XY, YY]]; dL/dΣ' = -K dL/dK K
@@ -339,7 +375,7 @@ __global__ void __launch_bounds__(128) k_epilogue(DevCam cam, const float4* __re
       const float gJ02 = gT[0][0] * W[2][0] + gT[0][1] * W[2][1] + gT[0][2] * W[2][2];
       const float gJ11 = gT[1][0] * W[1][0] + gT[1][1] * W[1][1] + gT[1][2] * W[1][2];
       const float gJ12 = gT[1][0] * W[2][0] + gT[1][1] * W[2][1] + gT[1][2] * W[2][2];
-      float gt[3] = {0.f, 0.f, 0.f};
+      float gt[3] = {0.f, 0.f, gtz_w};
       gt[2] += -(cam.fx * gJ00 + cam.fy * gJ11) * itz2 + (gJ02 * cam.fx * uxc + gJ12 * cam.fy * uyc) * itz2;
       if (!clx) {
         gt[0] += -gJ02 * cam.fx * itz2;
@@ -353,47 +389,9 @@ __global__ void __launch_bounds__(128) k_epilogue(DevCam cam, const float4* __re
       gt[0] += gmx * cam.fx * itz;
       gt[1] += gmy * cam.fy * itz;
       gt[2] -= (gmx * cam.fx * t[0] + gmy * cam.fy * t[1]) * itz2;
-      // w -> v, σ, tz
-      const float gvplus = gw * ramp, gramp = gw * vplus;
-      if (ramp_d > 0.0) {
-        gt[2] -= gramp / sigma;
-        gsig = gramp * tz / (sigma * sigma);
-      }
-      // colour / weight SH -> coefficients and direction
-      float gr0 = 0.f, gr1 = 0.f, gr2 = 0.f;
-      float gh[48];
-#pragma unroll
-      for (int ch = 0; ch < 3; ch++) {
-        const bool on = craw[ch] > 0.f;
-        const float g = on ? gc[ch] : 0.f;
-        float cf[16];
-#pragma unroll
-        for (int j = 0; j < 16; j++) {
-          gh[3 * j + ch] = g * Y[j];
-          cf[j] = g * hco[3 * j + ch];
-        }
-        float ax, ay, az;
-        sh_vjp(rx, ry, rz, cf, ax, ay, az);
-        gr0 += ax; gr1 += ay; gr2 += az;
-      }
-      float gv[16];
-      {
-        const float g = vraw > 0.f ? gvplus : 0.f;
-        float cf[16];
-#pragma unroll
-        for (int j = 0; j < 16; j++) {
-          gv[j] = g * Y[j];
-          cf[j] = g * vco[j];
-        }
-        float ax, ay, az;
-        sh_vjp(rx, ry, rz, cf, ax, ay, az);
-        gr0 += ax; gr1 += ay; gr2 += az;
-      }
-      const float rdot = rx * gr0 + ry * gr1 + rz * gr2;
-      float gmu[3];
-      gmu[0] = (gr0 - rx * rdot) * idn + W[0][0] * gt[0] + W[1][0] * gt[1] + W[2][0] * gt[2];
-      gmu[1] = (gr1 - ry * rdot) * idn + W[0][1] * gt[0] + W[1][1] * gt[1] + W[2][1] * gt[2];
-      gmu[2] = (gr2 - rz * rdot) * idn + W[0][2] * gt[0] + W[1][2] * gt[1] + W[2][2] * gt[2];
+      gmu0 += W[0][0] * gt[0] + W[1][0] * gt[1] + W[2][0] * gt[2];
+      gmu1 += W[0][1] * gt[0] + W[1][1] * gt[1] + W[2][1] * gt[2];
+      gmu2 += W[0][2] * gt[0] + W[1][2] * gt[1] + W[2][2] * gt[2];
       // Σ = M Mᵀ -> M -> (s, R)
       float gM[3][3];
 #pragma unroll
@@ -418,26 +416,14 @@ __global__ void __launch_bounds__(128) k_epilogue(DevCam cam, const float4* __re
       gq[3] = 2.f * (-2.f * qz * gR[0][0] - qw * gR[0][1] + qx * gR[0][2] + qw * gR[1][0] - 2.f * qz * gR[1][1] +
                      qy * gR[1][2] + qx * gR[2][0] + qy * gR[2][1]);
       const float qdot = qw * gq[0] + qx * gq[1] + qy * gq[2] + qz * gq[3];
-      const float gqr[4] = {(gq[0] - qw * qdot) * iqn, (gq[1] - qx * qdot) * iqn, (gq[2] - qy * qdot) * iqn,
-                            (gq[3] - qz * qdot) * iqn};
       // ---- accumulate into the gradient row (+=, scaled) ----
-      float4* gr = grad + (size_t)k * kRow4;
       float4 v;
-      v = gr[0]; v.x += scale * gmu[0]; v.y += scale * gmu[1]; v.z += scale * gmu[2]; v.w += scale * go; gr[0] = v;
-      v = gr[1]; v.x += scale * gqr[0]; v.y += scale * gqr[1]; v.z += scale * gqr[2]; v.w += scale * gqr[3]; gr[1] = v;
+      v = gr[0]; v.x += scale * gmu0; v.y += scale * gmu1; v.z += scale * gmu2; v.w += scale * go; gr[0] = v;
+      v = gr[1];
+      v.x += scale * (gq[0] - qw * qdot) * iqn; v.y += scale * (gq[1] - qx * qdot) * iqn;
+      v.z += scale * (gq[2] - qy * qdot) * iqn; v.w += scale * (gq[3] - qz * qdot) * iqn;
+      gr[1] = v;
       v = gr[2]; v.x += scale * gs[0]; v.y += scale * gs[1]; v.z += scale * gs[2]; gr[2] = v;
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        v = gr[3 + q];
-        v.x += scale * gv[4 * q]; v.y += scale * gv[4 * q + 1]; v.z += scale * gv[4 * q + 2]; v.w += scale * gv[4 * q + 3];
-        gr[3 + q] = v;
-      }
-#pragma unroll
-      for (int q = 0; q < 12; q++) {
-        v = gr[7 + q];
-        v.x += scale * gh[4 * q]; v.y += scale * gh[4 * q + 1]; v.z += scale * gh[4 * q + 2]; v.w += scale * gh[4 * q + 3];
-        gr[7 + q] = v;
-      }
       if (dL_dcov) {
         float* dc = dL_dcov + (size_t)k * 6;
         dc[0] += scale * gS[0][0];
@@ -482,10 +468,11 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
   int2* items = cv.take<int2>(max_items);
   int32_t* n_items = cv.take<int32_t>(4);
   int32_t* tile_nch = cv.take<int32_t>(n_tiles + 1);
+  int32_t* scratch = cv.take<int32_t>(66);
   int32_t* counter = cv.take<int32_t>(4);
   cudaMemsetAsync(acc2d, 0, sizeof(float) * 12 * (size_t)n_slots, st);
   cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
-  launch_build_items(tile_offsets, n_tiles, capacity, 32, 0, items, n_items, tile_nch, st);
+  launch_build_items(tile_offsets, n_tiles, capacity, 32, 0, items, n_items, tile_nch, scratch, st);
   const int blocks = sm_count() * 8;  // persistent: 8 × 4 warps per SM, dynamic item claiming
   record_event(ev_begin, st);
   k_moments<<<blocks, kMomentsThreads, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), pair_slot, tile_offsets,

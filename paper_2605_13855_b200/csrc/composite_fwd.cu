@@ -274,12 +274,13 @@ void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pa
     int2* items = cv.take<int2>(max_items);
     int32_t* n_items = cv.take<int32_t>(4);
     int32_t* tile_nch = cv.take<int32_t>(n_tiles + 1);
+    int32_t* scratch = cv.take<int32_t>(66);
     int32_t* done = cv.take<int32_t>(n_tiles);
     int32_t* counter = cv.take<int32_t>(4);
     float* partial = cv.take<float>((size_t)max_items * 5 * kTilePx);
     cudaMemsetAsync(done, 0, sizeof(int32_t) * n_tiles, st);
     cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
-    launch_build_items(tile_offsets, n_tiles, capacity, kFwdChunk, 1, items, n_items, tile_nch, st);
+    launch_build_items(tile_offsets, n_tiles, capacity, kFwdChunk, 1, items, n_items, tile_nch, scratch, st);
     const int grid = sm_count() * 12;  // persistent; items are claimed dynamically
 #define OIT_FWD2(B, K)                                                                                         \
   k_fwd_items<B, K><<<grid, kFwdThreads, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, items, n_items, \
