@@ -390,8 +390,9 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     L.lib()  # fail loudly if liboit.so is missing
+    from paper_2605_13855_b200 import dist as D
     all_cams = synth.scene_c2(n=10, n_views=args.views * world, res=args.res).cams
-    cams = all_cams[rank * args.views:(rank + 1) * args.views]
+    cams = [all_cams[v] for v in D.views_of_rank(args.views, rank)]   # weak scaling: V views per rank
 
     rhos = [args.rho] + ([] if args.no_sweep else [r for r in (1.0, 0.05) if r != args.rho])
     results = {}
@@ -423,14 +424,15 @@ def time_workload(args, torch, dist, wl, world, headline_run):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=wl.dev)   # 256 MB > 126 MB L2
     allred = world > 1
 
-    def comm():
-        if allred:
-            dist.all_reduce(wl.grad)
-            dist.all_reduce(wl.dsig)
+    from paper_2605_13855_b200 import dist as D
 
-    def comm2():
+    def comm():   # a9: NCCL all-reduce of the compacted gradient rows + dσ
+        if allred:
+            D.combine_gradients(wl.grad, wl.dsig)
+
+    def comm2():  # refresh: global mean of the per-rank score rows
         if allred and wl.n_ina > 0:
-            dist.all_reduce(wl.score_grad)
+            D.combine_scores(wl.score_grad, wl.S * world, wl.S)
 
     use_graph = not args.no_graph
     # warm-up eagerly once (also initialises lazy state inside the library)
