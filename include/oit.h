@@ -92,7 +92,8 @@ int32_t oit_num_tiles(const oit_camera* cam);
  * For each slot k < n_slots, splat i = idx[k] (the compacted active-index list; any order):
  * normalise q, Σ = R S Sᵀ Rᵀ, Σ' = J W Σ Wᵀ Jᵀ + 0.3 I, conic, μ', colour c = max(0, SH(h, r)+0.5),
  * weight w = max(0, 1 - tz/σ)·max(0, SH(v, r)), α thresholds, and the opacity-aware
- * conservative tile rectangle (R9). Writes rec[k][20] and tiles_per_slot[k] (0 if culled).
+ * conservative tile rectangle (R9). Writes rec[k][20] and tiles_per_slot[k] = the rectangle's
+ * tile count (the bin's candidates; 0 if culled).
  * Errors: OIT_EINVAL (null pointer / n_slots < 0), OIT_ESHAPE (n_slots > scene->n, bad W/H).
  * idx entries must lie in [0, N) (not checked on the device).
  * --------------------------------------------------------------------------------------- */
@@ -102,7 +103,7 @@ int oit_project_cull(const oit_scene* scene, const oit_camera* cam, const int32_
 /* ---------------------------------------------------------------------------------------
  * a2  oit_bin_tiles — Alg. 2 l.3-6 (CreateTiles, DuplicateWithKeys, SortByKeys "only by tile
  * ID", IdentifyTileRanges). One (tile, slot) pair per tile of each slot's
- * rectangle, grouped by tile: pair_slot[tile_offsets[t] .. tile_offsets[t+1]) lists the slots
+ * rectangle that passes the exact tile–ellipse test (DESIGN.md §3 step 12b), grouped by tile: pair_slot[tile_offsets[t] .. tile_offsets[t+1]) lists the slots
  * covering tile t. No depth key; the order inside a tile is unspecified (R15).
  * tile_offsets has n_tiles+1 entries; *d_n_pairs (device int64) receives the total pair count
  * (if it exceeds pair_capacity, pair_slot holds only a prefix and the caller must re-call).

@@ -121,8 +121,19 @@ def n_tiles(cam) -> tuple:
     return (int(cam["width"]) + 15) // 16, (int(cam["height"]) + 15) // 16
 
 
+def tile_contrib(rows32, idx, cam) -> np.ndarray:
+    """Brute force: [n_slots, n_tiles] bool, True iff some pixel of the tile passes the spec
+    contribution test for the slot (used to pin the tile culling as conservative)."""
+    rows32, idx = _f32(rows32), _i32(idx)
+    tx, ty = n_tiles(cam)
+    out = np.zeros((len(idx), tx * ty), np.uint8)
+    lib().orc_tile_contrib(_p(rows32), _p(idx), C.c_int32(len(idx)), C.byref(camera(cam)), _p(out))
+    return out.astype(bool)
+
+
 def bin_tiles(rows32, idx, cam):
-    """Brute-force (splat, tile) binning keyed by tile only (Alg. 2 l.3-6).
+    """Brute-force (splat, tile) binning keyed by tile only (Alg. 2 l.3-6), over the
+    tiles of each slot's rectangle that pass the exact tile test (DESIGN.md §3 step 12b).
     Returns (pair_slot ascending within each tile, tile_offsets[n_tiles+1])."""
     rows32, idx = _f32(rows32), _i32(idx)
     tx, ty = n_tiles(cam)

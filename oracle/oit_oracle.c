@@ -167,6 +167,29 @@ void orc_spec_project(const float* row, const orc_camera* cam, orc_spec* o) {
     o->visible = 1;
 }
 
+/* DESIGN.md §3 step 12b: exact tile test. Max of the (concave) power over one edge of the tile's
+ * pixel-centre rectangle: t ranges over [b0, b1] along the edge, the other offset is fixed to a. */
+static float edge_max(float a, float b0, float b1, float P, float Qc, float R) {
+    float q = Qc * a;
+    float t = fminf(fmaxf((-q) / (2.0f * R), b0), b1);
+    return fmaf(t, fmaf(R, t, q), (P * a) * a);
+}
+
+/* Keep tile (tx, ty) of a visible splat iff the continuous max of power over the tile's pixel-centre
+ * rectangle reaches thr_lo·(1 + 2^-10) (conservative: no contributing pixel is ever dropped). */
+int orc_spec_tile_keep(const orc_spec* s, int tx, int ty, int W, int H) {
+    int xe = 16 * tx + 15 < W - 1 ? 16 * tx + 15 : W - 1;
+    int ye = 16 * ty + 15 < H - 1 ? 16 * ty + 15 : H - 1;
+    float ax0 = (float)(16 * tx) - s->mx, ax1 = (float)xe - s->mx;
+    float ay0 = (float)(16 * ty) - s->my, ay1 = (float)ye - s->my;
+    if (ax0 <= 0.0f && 0.0f <= ax1 && ay0 <= 0.0f && 0.0f <= ay1) return 1;
+    float m = edge_max(ax0, ay0, ay1, s->nA, s->nB, s->nC);
+    m = fmaxf(m, edge_max(ax1, ay0, ay1, s->nA, s->nB, s->nC));
+    m = fmaxf(m, edge_max(ay0, ax0, ax1, s->nC, s->nB, s->nA));
+    m = fmaxf(m, edge_max(ay1, ax0, ax1, s->nC, s->nB, s->nA));
+    return m >= s->thr_lo * 1.0009765625f;
+}
+
 /* DESIGN.md §3 step 13: contribution / clamp decision for pixel (px, py). */
 static void spec_pixel(const orc_spec* s, int px, int py, int* contrib, int* clamped) {
     float dx = (float)px - s->mx;
@@ -376,6 +399,24 @@ void orc_project_value(const double* rows, double sigma, const int32_t* idx, int
     }
 }
 
+/* Brute force, for the binning pins: out[k][t] = 1 iff some pixel of tile t passes the step-13
+ * contribution test for slot k (independent of the rectangle and of the tile test). */
+void orc_tile_contrib(const float* rows, const int32_t* idx, int32_t n_slots, const orc_camera* cam, uint8_t* out) {
+    int TX = (cam->width + 15) / 16, TY = (cam->height + 15) / 16;
+    for (int32_t k = 0; k < n_slots; k++) {
+        orc_spec s;
+        orc_spec_project(rows + (size_t)idx[k] * ROW, cam, &s);
+        for (int t = 0; t < TX * TY; t++) out[(size_t)k * TX * TY + t] = 0;
+        if (!s.visible) continue;
+        for (int py = 0; py < cam->height; py++)
+            for (int px = 0; px < cam->width; px++) {
+                int c, cl;
+                spec_pixel(&s, px, py, &c, &cl);
+                if (c) out[(size_t)k * TX * TY + (py / 16) * TX + px / 16] = 1;
+            }
+    }
+}
+
 /* Brute-force tile binning (Alg. 2 l.3-6): for every tile in row-major order, the slots whose
  * spec rectangle covers it, in ascending slot order. Returns n_pairs (writes at most capacity). */
 int64_t orc_bin(const float* rows, const int32_t* idx, int32_t n_slots, const orc_camera* cam,
@@ -389,7 +430,8 @@ int64_t orc_bin(const float* rows, const int32_t* idx, int32_t n_slots, const or
             tile_offsets[ty * TX + tx] = (int32_t)n;
             for (int32_t k = 0; k < n_slots; k++) {
                 const orc_spec* s = &sp[k];
-                if (s->visible && tx >= s->x0 && tx < s->x1 && ty >= s->y0 && ty < s->y1) {
+                if (s->visible && tx >= s->x0 && tx < s->x1 && ty >= s->y0 && ty < s->y1 &&
+                    orc_spec_tile_keep(s, tx, ty, cam->width, cam->height)) {
                     if (n < capacity) pair_slot[n] = k;
                     n++;
                 }
@@ -425,7 +467,8 @@ void orc_render(const float* rows_dec, const double* rows_val, double sigma, con
         orc_spec s;
         orc_spec_project(rows_dec + (size_t)i * ROW, cam, &s);
         if (!s.visible) continue;
-        tile_pairs += (int64_t)(s.x1 - s.x0) * (s.y1 - s.y0);
+        for (int ty = s.y0; ty < s.y1; ty++)
+            for (int tx = s.x0; tx < s.x1; tx++) tile_pairs += orc_spec_tile_keep(&s, tx, ty, Wd, H);
         orc_val v;
         orc_value_project(rows_val + (size_t)i * ROW, sigma, cam, &v);
         int px0 = 0, px1 = Wd, py0 = 0, py1 = H;
@@ -436,6 +479,7 @@ void orc_render(const float* rows_dec, const double* rows_val, double sigma, con
         int fold = route ? (route[k] == 1) : 0;
         for (int py = py0; py < py1; py++)
             for (int px = px0; px < px1; px++) {
+                if (mode == 1 && !orc_spec_tile_keep(&s, px / 16, py / 16, Wd, H)) continue;  /* culled tile */
                 int contrib, clamped;
                 spec_pixel(&s, px, py, &contrib, &clamped);
                 if (!contrib) continue;
@@ -655,6 +699,7 @@ void orc_backward_bound(const float* rows_dec, const double* rows_val, double si
         }
         for (int py = py0; py < py1; py++)
             for (int px = px0; px < px1; px++) {
+                if (mode == 1 && !orc_spec_tile_keep(&s, px / 16, py / 16, Wd, H)) continue;  /* culled tile */
                 int contrib, clamped;
                 spec_pixel(&s, px, py, &contrib, &clamped);
                 if (!contrib) continue;

@@ -28,7 +28,7 @@ constexpr int kSlotsPerWarp = 8;
 
 template <bool kScatter>
 __global__ void __launch_bounds__(128) k_bin_expand(const float4* __restrict__ rec, const int32_t* __restrict__ tps,
-                                                    int32_t n_slots, int TX, int32_t* __restrict__ cnt,
+                                                    int32_t n_slots, int TX, int W, int H, int32_t* __restrict__ cnt,
                                                     int32_t* __restrict__ pair_slot, int64_t capacity,
                                                     const int32_t* __restrict__ offsets, int n_tiles,
                                                     int64_t* __restrict__ d_n_pairs, int64_t* __restrict__ d_max) {
@@ -44,12 +44,18 @@ __global__ void __launch_bounds__(128) k_bin_expand(const float4* __restrict__ r
   for (int base = gw * kSlotsPerWarp; base < n_slots; base += nw * kSlotsPerWarp) {
     const int k = base + lane;
     int c = 0, x0 = 0, y0 = 0, w = 1;
+    float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float thr_lo = 0.f, nC = 0.f;
     if (lane < kSlotsPerWarp && k < n_slots) {
       c = tps[k];
       if (c) {
         int x1, y1;
         rect_of(rec, k, x0, y0, x1, y1);
         w = x1 - x0;
+        q0 = rec[(size_t)k * kRec4];
+        const float4 q1 = rec[(size_t)k * kRec4 + 1];
+        nC = q1.x;
+        thr_lo = q1.y;
       }
     }
     int inc = c;
@@ -72,8 +78,13 @@ __global__ void __launch_bounds__(128) k_bin_expand(const float4* __restrict__ r
       const int local = j - __shfl_sync(FULL, exc, owner);
       const int ox0 = __shfl_sync(FULL, x0, owner), oy0 = __shfl_sync(FULL, y0, owner);
       const int ow = __shfl_sync(FULL, w, owner);
-      if (j < total) {
-        const int tile = (oy0 + local / ow) * TX + ox0 + local % ow;
+      const float omx = __shfl_sync(FULL, q0.x, owner), omy = __shfl_sync(FULL, q0.y, owner);
+      const float onA = __shfl_sync(FULL, q0.z, owner), onB = __shfl_sync(FULL, q0.w, owner);
+      const float onC = __shfl_sync(FULL, nC, owner), olo = __shfl_sync(FULL, thr_lo, owner);
+      const int ty = oy0 + local / ow, tx = ox0 + local % ow;
+      // candidate tiles of the rectangle are kept by the exact tile test (DESIGN.md §3 step 12b)
+      if (j < total && spec_tile_keep(tx, ty, W, H, omx, omy, onA, onB, onC, olo)) {
+        const int tile = ty * TX + tx;
         const unsigned peers = __match_any_sync(__activemask(), tile);
         const int leader = __ffs(peers) - 1;
         const int n = __popc(peers);
@@ -106,11 +117,11 @@ void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_sl
   const int warps = n_slots > 0 ? (n_slots + kSlotsPerWarp - 1) / kSlotsPerWarp : 1;
   const int blocks = (warps + 3) / 4;
   if (n_slots > 0)
-    k_bin_expand<false><<<blocks, 128, 0, st>>>(r4, tiles_per_slot, n_slots, cam.TX, counts, pair_slot, capacity,
+    k_bin_expand<false><<<blocks, 128, 0, st>>>(r4, tiles_per_slot, n_slots, cam.TX, cam.W, cam.H, counts, pair_slot, capacity,
                                                 tile_offsets, n_tiles, d_n_pairs, d_max_pairs);
   launch_exclusive_scan(counts, tile_offsets, n_tiles, tmp, st);
   cudaMemcpyAsync(counts, tile_offsets, sizeof(int32_t) * n_tiles, cudaMemcpyDeviceToDevice, st);
-  k_bin_expand<true><<<blocks, 128, 0, st>>>(r4, tiles_per_slot, n_slots, cam.TX, counts, pair_slot, capacity,
+  k_bin_expand<true><<<blocks, 128, 0, st>>>(r4, tiles_per_slot, n_slots, cam.TX, cam.W, cam.H, counts, pair_slot, capacity,
                                              tile_offsets, n_tiles, d_n_pairs, d_max_pairs);
 }
 

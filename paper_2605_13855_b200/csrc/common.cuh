@@ -173,6 +173,28 @@ __device__ __forceinline__ SpecProj spec_project(const DevCam& cam, float mux, f
   return o;
 }
 
+// DESIGN.md §3 step 12b: exact tile test — max of the concave power over one edge of the tile's
+// pixel-centre rectangle (offset a fixed, t ∈ [b0, b1] along the edge).
+__device__ __forceinline__ float spec_edge_max(float a, float b0, float b1, float P, float Qc, float R) {
+  const float q = __fmul_rn(Qc, a);
+  const float t = fminf(fmaxf(__fdiv_rn(-q, __fmul_rn(2.0f, R)), b0), b1);
+  return __fmaf_rn(t, __fmaf_rn(R, t, q), __fmul_rn(__fmul_rn(P, a), a));
+}
+// Keep tile (tx, ty) of a visible splat iff the continuous max of its power over the tile's
+// pixel-centre rectangle reaches thr_lo·(1 + 2^-10): conservative, and bit-identical to the spec.
+__device__ __forceinline__ bool spec_tile_keep(int tx, int ty, int W, int H, float mx, float my, float nA, float nB,
+                                               float nC, float thr_lo) {
+  const int xe = min(16 * tx + 15, W - 1), ye = min(16 * ty + 15, H - 1);
+  const float ax0 = __fsub_rn((float)(16 * tx), mx), ax1 = __fsub_rn((float)xe, mx);
+  const float ay0 = __fsub_rn((float)(16 * ty), my), ay1 = __fsub_rn((float)ye, my);
+  if (ax0 <= 0.0f && 0.0f <= ax1 && ay0 <= 0.0f && 0.0f <= ay1) return true;
+  float m = spec_edge_max(ax0, ay0, ay1, nA, nB, nC);
+  m = fmaxf(m, spec_edge_max(ax1, ay0, ay1, nA, nB, nC));
+  m = fmaxf(m, spec_edge_max(ay0, ax0, ax1, nC, nB, nA));
+  m = fmaxf(m, spec_edge_max(ay1, ax0, ax1, nC, nB, nA));
+  return m >= __fmul_rn(thr_lo, 1.0009765625f);
+}
+
 // DESIGN.md §3 step 13 (the per-pixel power; exact op order, no contraction beyond the two fmas).
 __device__ __forceinline__ float spec_power(float nA, float nB, float nC, float dx, float dy) {
   float by = __fmul_rn(nB, dy);
