@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--splats", type=int, default=300_000)
     ap.add_argument("--res", type=int, default=800)
     ap.add_argument("--sub-rate", type=float, default=0.05, help="refresh subsample rate S/V")
+    ap.add_argument("--streams", type=int, default=4, help="training views processed concurrently (one stream each)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -263,6 +264,12 @@ class Workload:
         self.H, self.W = H, W
         cap = 1 << 22   # ≥ 2× the largest per-view pair count of C2 (checked below)
         self.pipe = ViewPipeline(cams[0], max(self.n_act, self.n_ina, 1), cap, device=dev)
+        # independent views run concurrently: one pipeline (buffers + workspaces) per stream; the
+        # gradient rows are accumulated with vector atomics, so all streams share grad / dσ
+        self.n_streams = max(1, args.streams)
+        self.pipes = [self.pipe] + [ViewPipeline(cams[0], max(self.n_act, 1), cap, device=dev)
+                                    for _ in range(self.n_streams - 1)]
+        self.streams = [torch.cuda.Stream() for _ in range(self.n_streams)]
         nt = self.pipe.n_tiles
         self.n_tiles = nt
         # ---- untimed setup: per-view pre-render caches of the frozen set (Alg. 1 I^pre), targets ----
@@ -292,7 +299,7 @@ class Workload:
         assert max_pairs <= cap, "pair capacity overflow"
         self.max_pairs_train = max_pairs
         # ---- buffers of the step ----
-        self.dLdC = torch.empty((3, H, W), dtype=torch.float32, device=dev)
+        self.dLdC = [torch.empty((3, H, W), dtype=torch.float32, device=dev) for _ in range(self.n_streams)]
         self.grad = torch.zeros((max(self.n_act, 1), 80), dtype=torch.float32, device=dev)
         self.dsig = torch.zeros(1, dtype=torch.float32, device=dev)
         # refresh: FPS over this rank's view centres, S = 5% of the views, scored set = inactive set
@@ -329,16 +336,26 @@ class Workload:
 
     # ---------------------------------------------------------------------------------------
     def train_views(self):
-        """a1-a6 over every training view (Alg. 1 l.3-6, one view per iteration)."""
-        L, p = self.L, self.pipe
+        """a1-a6 over every training view (Alg. 1 l.3-6, one view per iteration); views are dealt
+        round-robin to n_streams streams (fork/join on the current stream)."""
+        torch, L = self.torch, self.L
+        main = torch.cuda.current_stream()
         self.grad.zero_()
         self.dsig.zero_()
+        for st_ in self.streams:
+            st_.wait_stream(main)
         for v, cam in enumerate(self.cams):
-            p.set_camera(cam)
-            img, st = p.forward(self.rows, self.sigma, self.act, self.bg, base=self.caches[v], events=self.ev_fwd[v])
-            L.oit_loss_grad(cam, img, self.targets[v], "l1", self.dLdC)
-            p.backward(self.rows, self.sigma, self.act, self.bg, st, self.dLdC, self.grad, self.dsig,
-                       events=self.ev_bwd[v])
+            k = v % self.n_streams
+            p = self.pipes[k]
+            with torch.cuda.stream(self.streams[k]):
+                p.set_camera(cam)
+                img, st = p.forward(self.rows, self.sigma, self.act, self.bg, base=self.caches[v],
+                                    events=self.ev_fwd[v])
+                L.oit_loss_grad(cam, img, self.targets[v], "l1", self.dLdC[k])
+                p.backward(self.rows, self.sigma, self.act, self.bg, st, self.dLdC[k], self.grad, self.dsig,
+                           events=self.ev_bwd[v])
+        for st_ in self.streams:
+            main.wait_stream(st_)
 
     def refresh(self):
         """a7 (FPS + subsampled score of the inactive splats) and a8 (Eq. 8 update)."""
@@ -565,7 +582,8 @@ def build_line(args, world, res, results):
                    "rho": res["rho"], "mask": args.kind, "n_active": res["n_act"], "refresh_views_S": res["S"],
                    "step": "I=100 iterations (one view each, fwd+bwd) + one refresh (a7 score over the inactive "
                            "set on S views, a8 update)",
-                   "l2": "flushed between timed steps (256 MB write)", "graph": not args.no_graph},
+                   "l2": "flushed between timed steps (256 MB write)", "graph": not args.no_graph,
+                   "streams": args.streams},
         "splat_pixel_evals_per_s": evals / (res["ms"] * 1e-3),
         "contributing_fraction_f_c": f_c,
         "kernel_ms_per_step": {"fwd_composite": res["fwd_ms"], "bwd_moments": res["bwd_ms"]},

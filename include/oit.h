@@ -162,6 +162,8 @@ int oit_loss_grad(const oit_camera* cam, const float* image, const float* target
  *   grad[k][80] += scale·∂L/∂row(idx[k]), *dL_dsigma += scale·∂L/∂σ,
  *   dL_dcov[k][6] += scale·∂L/∂Σ (packed xx,xy,xz,yy,yz,zz; off-diagonals = ∂/∂Σij + ∂/∂Σji;
  *   nullable). rec/pair lists must come from oit_project_cull/oit_bin_tiles of the same idx.
+ * The += into grad / dL_dsigma / dL_dcov uses atomics, so calls on several streams (one view
+ * each, distinct workspaces) may accumulate into the same output buffers concurrently.
  * Scratch: ws of oit_bwd_workspace_bytes(cam, n_slots, pair_capacity) bytes.
  * --------------------------------------------------------------------------------------- */
 size_t oit_bwd_workspace_bytes(const oit_camera* cam, int32_t n_slots, int64_t pair_capacity);

@@ -276,10 +276,8 @@ __global__ void __launch_bounds__(128, 3) k_epilogue(DevCam cam, const float4* _
         for (int q = 0; q < 4; q++) {
           const float4 vv = r[3 + q];
           cf[4 * q] = gvp * vv.x; cf[4 * q + 1] = gvp * vv.y; cf[4 * q + 2] = gvp * vv.z; cf[4 * q + 3] = gvp * vv.w;
-          float4 g = gr[3 + q];
-          g.x = fmaf(sv, Y[4 * q], g.x); g.y = fmaf(sv, Y[4 * q + 1], g.y);
-          g.z = fmaf(sv, Y[4 * q + 2], g.z); g.w = fmaf(sv, Y[4 * q + 3], g.w);
-          gr[3 + q] = g;
+          red_add_v4(reinterpret_cast<float*>(gr + 3 + q), sv * Y[4 * q], sv * Y[4 * q + 1], sv * Y[4 * q + 2],
+                     sv * Y[4 * q + 3]);
         }
         const float sh3[3] = {scale * gch[0], scale * gch[1], scale * gch[2]};
 #pragma unroll
@@ -288,12 +286,9 @@ __global__ void __launch_bounds__(128, 3) k_epilogue(DevCam cam, const float4* _
           const float e[4] = {hh.x, hh.y, hh.z, hh.w};
 #pragma unroll
           for (int u = 0; u < 4; u++) cf[(4 * q + u) / 3] = fmaf(gch[(4 * q + u) % 3], e[u], cf[(4 * q + u) / 3]);
-          float4 g = gr[7 + q];
-          g.x = fmaf(sh3[(4 * q) % 3], Y[(4 * q) / 3], g.x);
-          g.y = fmaf(sh3[(4 * q + 1) % 3], Y[(4 * q + 1) / 3], g.y);
-          g.z = fmaf(sh3[(4 * q + 2) % 3], Y[(4 * q + 2) / 3], g.z);
-          g.w = fmaf(sh3[(4 * q + 3) % 3], Y[(4 * q + 3) / 3], g.w);
-          gr[7 + q] = g;
+          red_add_v4(reinterpret_cast<float*>(gr + 7 + q), sh3[(4 * q) % 3] * Y[(4 * q) / 3],
+                     sh3[(4 * q + 1) % 3] * Y[(4 * q + 1) / 3], sh3[(4 * q + 2) % 3] * Y[(4 * q + 2) / 3],
+                     sh3[(4 * q + 3) % 3] * Y[(4 * q + 3) / 3]);
         }
         float gr0, gr1, gr2;
         sh_vjp(rx, ry, rz, cf, gr0, gr1, gr2);
@@ -416,22 +411,21 @@ __global__ void __launch_bounds__(128, 3) k_epilogue(DevCam cam, const float4* _
       gq[3] = 2.f * (-2.f * qz * gR[0][0] - qw * gR[0][1] + qx * gR[0][2] + qw * gR[1][0] - 2.f * qz * gR[1][1] +
                      qy * gR[1][2] + qx * gR[2][0] + qy * gR[2][1]);
       const float qdot = qw * gq[0] + qx * gq[1] + qy * gq[2] + qz * gq[3];
-      // ---- accumulate into the gradient row (+=, scaled) ----
-      float4 v;
-      v = gr[0]; v.x += scale * gmu0; v.y += scale * gmu1; v.z += scale * gmu2; v.w += scale * go; gr[0] = v;
-      v = gr[1];
-      v.x += scale * (gq[0] - qw * qdot) * iqn; v.y += scale * (gq[1] - qx * qdot) * iqn;
-      v.z += scale * (gq[2] - qy * qdot) * iqn; v.w += scale * (gq[3] - qz * qdot) * iqn;
-      gr[1] = v;
-      v = gr[2]; v.x += scale * gs[0]; v.y += scale * gs[1]; v.z += scale * gs[2]; gr[2] = v;
+      // ---- accumulate into the gradient row (+=, scaled) with vector atomics: concurrent views
+      // (one stream each) may accumulate into the same rows ----
+      float* g = reinterpret_cast<float*>(gr);
+      red_add_v4(g, scale * gmu0, scale * gmu1, scale * gmu2, scale * go);
+      red_add_v4(g + 4, scale * (gq[0] - qw * qdot) * iqn, scale * (gq[1] - qx * qdot) * iqn,
+                 scale * (gq[2] - qy * qdot) * iqn, scale * (gq[3] - qz * qdot) * iqn);
+      red_add_v4(g + 8, scale * gs[0], scale * gs[1], scale * gs[2], 0.f);
       if (dL_dcov) {
         float* dc = dL_dcov + (size_t)k * 6;
-        dc[0] += scale * gS[0][0];
-        dc[1] += scale * (gS[0][1] + gS[1][0]);
-        dc[2] += scale * (gS[0][2] + gS[2][0]);
-        dc[3] += scale * gS[1][1];
-        dc[4] += scale * (gS[1][2] + gS[2][1]);
-        dc[5] += scale * gS[2][2];
+        atomicAdd(dc + 0, scale * gS[0][0]);
+        atomicAdd(dc + 1, scale * (gS[0][1] + gS[1][0]));
+        atomicAdd(dc + 2, scale * (gS[0][2] + gS[2][0]));
+        atomicAdd(dc + 3, scale * gS[1][1]);
+        atomicAdd(dc + 4, scale * (gS[1][2] + gS[2][1]));
+        atomicAdd(dc + 5, scale * gS[2][2]);
       }
     }
   }
