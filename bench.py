@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--splats", type=int, default=300_000)
     ap.add_argument("--res", type=int, default=800)
     ap.add_argument("--sub-rate", type=float, default=0.05, help="refresh subsample rate S/V")
-    ap.add_argument("--streams", type=int, default=4, help="training views processed concurrently (one stream each)")
+    ap.add_argument("--streams", type=int, default=8, help="training views processed concurrently (one stream each)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -309,8 +309,9 @@ class Workload:
         L.oit_select_views(self.centers, self.S, 2605, 0, self.views_dev)
         self.views_host = [int(x) for x in self.views_dev.cpu().numpy()]   # same refresh index each step
         self.score_cap = cap
-        self.score_ws = torch.empty(max(L.oit_score_workspace_bytes(cams[0], self.n_act, self.n_ina, cap), 256),
-                                    dtype=torch.uint8, device=dev)
+        nsc = max(1, min(self.S, self.n_streams))
+        self.score_ws = [torch.empty(max(L.oit_score_workspace_bytes(cams[0], self.n_act, self.n_ina, cap), 256),
+                                     dtype=torch.uint8, device=dev) for _ in range(nsc)]
         self.score_grad = torch.zeros((max(self.n_ina, 1), 80), dtype=torch.float32, device=dev)
         self.score_dsig = torch.zeros(1, dtype=torch.float32, device=dev)
         self.max_pairs = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -329,23 +330,24 @@ class Workload:
         self.ev_fwd = [(mk(), mk()) for _ in range(self.V)]
         self.ev_bwd = [(mk(), mk()) for _ in range(self.V)]
         self.ev_seg = [mk() for _ in range(3)]
-        for pair in self.ev_fwd + self.ev_bwd:    # torch creates the CUDA event lazily on first record
-            pair[0].record()
+        for pair in self.ev_fwd + self.ev_bwd + [tuple(self.ev_seg[:2]), tuple(self.ev_seg[1:])]:
+            pair[0].record()                      # torch creates the CUDA event lazily on first record
             pair[1].record()
         torch.cuda.synchronize()
 
     # ---------------------------------------------------------------------------------------
-    def train_views(self):
+    def train_views(self, n_streams=None):
         """a1-a6 over every training view (Alg. 1 l.3-6, one view per iteration); views are dealt
         round-robin to n_streams streams (fork/join on the current stream)."""
         torch, L = self.torch, self.L
+        ns = self.n_streams if n_streams is None else n_streams
         main = torch.cuda.current_stream()
         self.grad.zero_()
         self.dsig.zero_()
-        for st_ in self.streams:
+        for st_ in self.streams[:ns]:
             st_.wait_stream(main)
         for v, cam in enumerate(self.cams):
-            k = v % self.n_streams
+            k = v % ns
             p = self.pipes[k]
             with torch.cuda.stream(self.streams[k]):
                 p.set_camera(cam)
@@ -354,19 +356,31 @@ class Workload:
                 L.oit_loss_grad(cam, img, self.targets[v], "l1", self.dLdC[k])
                 p.backward(self.rows, self.sigma, self.act, self.bg, st, self.dLdC[k], self.grad, self.dsig,
                            events=self.ev_bwd[v])
-        for st_ in self.streams:
+        for st_ in self.streams[:ns]:
             main.wait_stream(st_)
 
     def refresh(self):
         """a7 (FPS + subsampled score of the inactive splats) and a8 (Eq. 8 update)."""
         L = self.L
+        torch = self.torch
         L.oit_select_views(self.centers, self.S, 2605, 0, self.views_dev)
         self.score_grad.zero_()
         self.score_dsig.zero_()
         if self.n_ina > 0:
-            L.oit_score_subsample(self.rows, self.sigma, self.cams, self.targets_list, self.caches_list, self.act,
-                                  self.ina, self.views_host, "l1", self.bg, self.score_grad, self.score_dsig,
-                                  self.score_cap, self.max_pairs, self.score_ws)
+            # the S subsampled views are scored concurrently (disjoint subsets, scale 1/S each)
+            main = torch.cuda.current_stream()
+            parts = [self.views_host[k::len(self.score_ws)] for k in range(len(self.score_ws))]
+            for k, part in enumerate(parts):
+                if not part:
+                    continue
+                self.streams[k].wait_stream(main)
+                with torch.cuda.stream(self.streams[k]):
+                    L.oit_score_subsample(self.rows, self.sigma, self.cams, self.targets_list, self.caches_list,
+                                          self.act, self.ina, part, "l1", self.bg, self.score_grad, self.score_dsig,
+                                          self.score_cap, self.max_pairs, self.score_ws[k], scale=1.0 / self.S)
+            for k, part in enumerate(parts):
+                if part:
+                    main.wait_stream(self.streams[k])
 
     def update(self):
         L = self.L
@@ -460,7 +474,15 @@ def time_workload(args, torch, dist, wl, world, headline_run):
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
-            for fn in ([wl.train_views, wl.refresh, wl.update] if allred else [lambda: (wl.train_views(), wl.refresh(), wl.update())]):
+            def whole():
+                wl.ev_seg[0].record()
+                wl.train_views()
+                wl.ev_seg[1].record()
+                wl.refresh()
+                wl.update()
+                wl.ev_seg[2].record()
+
+            for fn in ([wl.train_views, wl.refresh, wl.update] if allred else [whole]):
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=s):
                     fn()
@@ -482,7 +504,7 @@ def time_workload(args, torch, dist, wl, world, headline_run):
     torch.cuda.synchronize()
     if allred:
         dist.barrier()
-    times, fwd_ms, bwd_ms = [], [], []
+    times, fwd_ms, bwd_ms, seg_ms = [], [], [], []
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(torch.cuda.current_device())
     with sampler:
@@ -500,17 +522,44 @@ def time_workload(args, torch, dist, wl, world, headline_run):
             times.append(t_start.elapsed_time(t_end))
             fwd_ms.append(sum(event_ms(a, b) for a, b in wl.ev_fwd))
             bwd_ms.append(sum(event_ms(a, b) for a, b in wl.ev_bwd))
+            if use_graph and not allred:
+                seg_ms.append((event_ms(wl.ev_seg[0], wl.ev_seg[1]), event_ms(wl.ev_seg[1], wl.ev_seg[2])))
     ms = float(np.mean(times))
     if allred:
         t = torch.tensor([ms], dtype=torch.float64, device=wl.dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    # roofline pass: the same training views on ONE stream (no concurrency), so each hot kernel's
+    # event-timed duration is its own; timed steps between L2 flushes as above
+    ser_fwd, ser_bwd = fwd_ms, bwd_ms
+    if headline_run and wl.n_streams > 1:
+        ser = None
+        if use_graph:
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                ser = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(ser, stream=s):
+                    wl.train_views(1)
+            torch.cuda.current_stream().wait_stream(s)
+        ser_fwd, ser_bwd = [], []
+        for i in range(args.warmup + args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            ser.replay() if ser is not None else wl.train_views(1)
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                ser_fwd.append(sum(event_ms(a, b) for a, b in wl.ev_fwd))
+                ser_bwd.append(sum(event_ms(a, b) for a, b in wl.ev_bwd))
     # the FPS kernel's device output must equal the host list the score used
     assert [int(x) for x in wl.views_dev.cpu().numpy()] == wl.views_host
     res = dict(ms=ms, fwd_ms=float(np.mean(fwd_ms)), bwd_ms=float(np.mean(bwd_ms)), clocks=sampler.summary(),
+               ser_fwd_ms=float(np.mean(ser_fwd)), ser_bwd_ms=float(np.mean(ser_bwd)),
                pairs=int(sum(wl.pairs_act)), contrib=wl.contrib, tile_evals=wl.tile_evals, V=wl.V, H=wl.H, W=wl.W,
                n_act=wl.n_act, n_ina=wl.n_ina, S=wl.S, launches=wl.kernel_launches(), rho=wl.rho,
-               max_score_pairs=int(wl.max_pairs.item()))
+               max_score_pairs=int(wl.max_pairs.item()),
+               train_ms=float(np.mean([a for a, _ in seg_ms])) if seg_ms else None,
+               refresh_ms=float(np.mean([b for _, b in seg_ms])) if seg_ms else None)
     if headline_run and not args.no_e2e:
         res["e2e"] = time_e2e(args, torch, dist, wl, step, flush, allred)
     return res
@@ -562,16 +611,17 @@ def build_line(args, world, res, results):
     # roofline of the dominant kernel (fwd composite or bwd moments, both FP32-ALU bound)
     fwd_flops = res["tile_evals"] * FWD_F_TEST + res["contrib"] * FWD_F_CONTRIB
     bwd_flops = res["tile_evals"] * BWD_F_TEST + res["contrib"] * BWD_F_CONTRIB
-    if res["bwd_ms"] >= res["fwd_ms"]:
-        kern, flops, kms = "k_moments (oit_composite_bwd a5)", bwd_flops, res["bwd_ms"]
+    if res["ser_bwd_ms"] >= res["ser_fwd_ms"]:
+        kern, flops, kms = "k_moments (oit_composite_bwd a5)", bwd_flops, res["ser_bwd_ms"]
     else:
-        kern, flops, kms = "k_fwd (oit_composite_fwd a3)", fwd_flops, res["fwd_ms"]
+        kern, flops, kms = "k_fwd_items (oit_composite_fwd a3)", fwd_flops, res["ser_fwd_ms"]
     achieved = flops / (kms * 1e-3) / 1e12
     sweep = {}
     for rho, r in sorted(results.items(), reverse=True):
         sweep[str(rho)] = {"mpix_per_s": mpix_per_s(r, world), "ms_per_step": r["ms"],
                            "evals_per_s": world * 256 * r["pairs"] / (r["ms"] * 1e-3),
                            "fwd_kernel_ms": r["fwd_ms"], "bwd_moments_ms": r["bwd_ms"], "n_active": r["n_act"],
+                           "train_ms": r["train_ms"], "refresh_ms": r["refresh_ms"],
                            "pairs_per_view": r["pairs"] / r["V"],
                            "f_c": r["contrib"] / max(r["tile_evals"], 1)}
     line = {
@@ -586,8 +636,13 @@ def build_line(args, world, res, results):
                    "streams": args.streams},
         "splat_pixel_evals_per_s": evals / (res["ms"] * 1e-3),
         "contributing_fraction_f_c": f_c,
-        "kernel_ms_per_step": {"fwd_composite": res["fwd_ms"], "bwd_moments": res["bwd_ms"]},
+        "kernel_ms_per_step": {"fwd_composite": res["ser_fwd_ms"], "bwd_moments": res["ser_bwd_ms"],
+                               "note": "sum over the step's training views, single-stream roofline pass; the timed "
+                                       "step runs views on several streams concurrently",
+                               "concurrent_fwd_composite": res["fwd_ms"], "concurrent_bwd_moments": res["bwd_ms"]},
+        "segments_ms": {"train_views": res["train_ms"], "refresh": res["refresh_ms"]},
         "roofline": {"kernel": kern, "bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
+                     "algorithmic_flops_per_step": flops, "kernel_ms_per_step": kms,
                      "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS, "traffic": None,
                      "peak_source": "148 SMs x 128 FP32 lanes x 2 (FMA) x 1965 MHz (B200_PROFILING.md unit counts)"},
         "clocks": res["clocks"], "gpu_launches": res["launches"] * args.steps,

@@ -202,7 +202,9 @@ int oit_select_views(const float* centers, int32_t n_views, int32_t n_sub, uint6
  * For each subsampled view j = views_host[s]: the full-G pixel state is caches[j] ⊕ the active
  * set (Rasterize(G, I^pre_j), R16); the L1/L2 loss gradient against targets[j] (R20, R24) is
  * back-propagated to the scored splats score_idx (normally the inactive set);
- *   score_grad[n_score][80] += (1/n_sub)·Σ_j ∂L_j/∂row, *dL_dsigma += (1/n_sub)·Σ_j ∂L_j/∂σ.
+ *   score_grad[n_score][80] += scale·Σ_j ∂L_j/∂row, *dL_dsigma += scale·Σ_j ∂L_j/∂σ
+ * (scale = 1/S gives the mean over the S subsampled views of R19; disjoint subsets of the S views
+ * may be scored by concurrent calls on different streams, each with scale = 1/S).
  * cams_host [n_views]; targets/caches: HOST arrays of n_views DEVICE pointers ([3][H][W] and
  * [5][n_tiles][256]; caches[j] may be NULL = nothing frozen). All views share W and H.
  * *d_max_pairs (device int64) receives the largest pair count met; if > pair_capacity the
@@ -215,7 +217,7 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
                         const float* const* targets_host, const float* const* caches_host,
                         const int32_t* active_idx, int32_t n_active, const int32_t* score_idx,
                         int32_t n_score, const int32_t* views_host, int32_t n_sub, int32_t loss,
-                        const float bg_host[3], float* score_grad, float* dL_dsigma,
+                        const float bg_host[3], float scale, float* score_grad, float* dL_dsigma,
                         int64_t pair_capacity, int64_t* d_max_pairs, void* ws, size_t ws_bytes,
                         oit_stream_t stream);
 

@@ -80,8 +80,8 @@ def lib() -> C.CDLL:
                                                vp, vp, sz, C.POINTER(BwdEvents), vp]),
             "oit_select_views": (C.c_int, [vp, i32, i32, C.c_uint64, C.c_uint32, vp, vp]),
             "oit_score_workspace_bytes": (sz, [cam_p, i32, i32, i64]),
-            "oit_score_subsample": (C.c_int, [scene_p, cam_p, i32, vp, vp, vp, i32, vp, i32, vp, i32, i32, vp, vp,
-                                              vp, i64, vp, vp, sz, vp]),
+            "oit_score_subsample": (C.c_int, [scene_p, cam_p, i32, vp, vp, vp, i32, vp, i32, vp, i32, i32, vp, f32,
+                                              vp, vp, i64, vp, vp, sz, vp]),
             "oit_update_workspace_bytes": (sz, [i32]),
             "oit_update_active_set": (C.c_int, [vp, vp, i32, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         }
@@ -203,7 +203,8 @@ def oit_score_workspace_bytes(cam, n_active: int, n_score: int, pair_capacity: i
 
 
 def oit_score_subsample(rows, sigma, cams, targets, caches, active_idx, score_idx, views, loss: str, bg,
-                        score_grad, dL_dsigma, pair_capacity: int, max_pairs, ws, stream=None):
+                        score_grad, dL_dsigma, pair_capacity: int, max_pairs, ws, stream=None, scale=None):
+    """scale: weight of each view's gradient (default 1/len(views): the mean over these views)."""
     sc = scene(rows, sigma)
     V = len(cams)
     cam_arr = (Camera * V)(*[camera(c) for c in cams])
@@ -212,7 +213,9 @@ def oit_score_subsample(rows, sigma, cams, targets, caches, active_idx, score_id
     vw = (C.c_int32 * len(views))(*[int(v) for v in views])
     _check(lib().oit_score_subsample(C.byref(sc), cam_arr, V, tg, ch, _ptr(active_idx), int(active_idx.numel()),
                                      _ptr(score_idx), int(score_idx.numel()), vw, len(views),
-                                     0 if loss == "l1" else 1, _f3(bg), _ptr(score_grad), _ptr(dL_dsigma),
+                                     0 if loss == "l1" else 1, _f3(bg),
+                                     C.c_float(1.0 / len(views) if scale is None else scale), _ptr(score_grad),
+                                     _ptr(dL_dsigma),
                                      int(pair_capacity), _ptr(max_pairs), _ptr(ws), int(ws.numel()),
                                      _stream(stream)), "oit_score_subsample")
 

@@ -216,7 +216,7 @@ size_t oit_score_workspace_bytes(const oit_camera* cam, int32_t n_active, int32_
 int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int32_t n_views,
                         const float* const* targets_host, const float* const* caches_host, const int32_t* active_idx,
                         int32_t n_active, const int32_t* score_idx, int32_t n_score, const int32_t* views_host,
-                        int32_t n_sub, int32_t loss, const float bg_host[3], float* score_grad, float* dL_dsigma,
+                        int32_t n_sub, int32_t loss, const float bg_host[3], float scale, float* score_grad, float* dL_dsigma,
                         int64_t pair_capacity, int64_t* d_max_pairs, void* ws, size_t ws_bytes,
                         oit_stream_t stream) {
   if (!scene || !scene->rows || !scene->sigma || !cams_host || !targets_host || !views_host || !bg_host ||
@@ -235,7 +235,6 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
   if (ws_bytes < oit_score_workspace_bytes(&cams_host[0], n_active, n_score, pair_capacity)) return OIT_ECAPACITY;
   ScoreWs w = score_layout(ws, &cams_host[0], n_active, n_score, pair_capacity);
   cudaStream_t st = S(stream);
-  const float scale = 1.0f / (float)n_sub;
   for (int s = 0; s < n_sub; s++) {
     const int j = views_host[s];
     DevCam dc = dev_cam(&cams_host[j], bg_host);
