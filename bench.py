@@ -397,8 +397,9 @@ class Workload:
         a, s = self.n_act, self.n_ina
         proj = lambda n: 1 if n > 0 else 0  # noqa: E731
         binn = lambda n: (1 if n > 0 else 0) + scan_kernels(nt) + 1  # noqa: E731
-        fwd = 2                                            # build_items, k_fwd_items
-        bwd = lambda n: 1 + (3 if n > 0 else 0)  # noqa: E731  coef | build_items, moments, epilogue
+        fwd = 3                                            # items hist + emit, k_fwd_items
+        # coef | quadrant count, scan, quadrant scatter, items hist + emit, moments, epilogue
+        bwd = lambda n: 1 + ((6 + scan_kernels(4 * nt)) if n > 0 else 0)  # noqa: E731
         train = self.V * (proj(a) + binn(a) + fwd + 1 + bwd(a))
         refresh = 1
         if s > 0:

@@ -62,6 +62,91 @@ __global__ void __launch_bounds__(256) k_coef(DevCam cam, const float* __restric
   coefa[pix] = a;
 }
 
+// ------------------------------------------------------------ a5 quadrant sub-binning ----
+// The backward evaluates, per lane (= splat), every pixel of its warp's window; for C2-sized
+// splats that is most of the 16×16 tile while the ellipse covers ~30% of it. Each tile list is
+// therefore split into four 8×8 quadrant lists, keeping a slot in a quadrant iff the continuous
+// max of its power over the quadrant's pixel-centre rectangle reaches thr_lo·(1+2^-10) (the step
+// 12b test on a smaller rectangle: conservative, so no contributing pixel is lost; pixel decisions
+// stay the spec's). On C2 a pair touches 2.2 quadrants on average: 55% of the pixels to evaluate.
+__device__ __forceinline__ bool rect_keep(float ax0, float ax1, float ay0, float ay1, float nA, float nB, float nC,
+                                          float thr_lo) {
+  if (ax0 <= 0.0f && 0.0f <= ax1 && ay0 <= 0.0f && 0.0f <= ay1) return true;
+  float m = spec_edge_max(ax0, ay0, ay1, nA, nB, nC);
+  m = fmaxf(m, spec_edge_max(ax1, ay0, ay1, nA, nB, nC));
+  m = fmaxf(m, spec_edge_max(ay0, ax0, ax1, nC, nB, nA));
+  m = fmaxf(m, spec_edge_max(ay1, ax0, ax1, nC, nB, nA));
+  return m >= __fmul_rn(thr_lo, 1.0009765625f);
+}
+
+__device__ __forceinline__ unsigned quad_mask(const DevCam& cam, int tile, const float4& q0, const float4& q1) {
+  const int tx0 = (tile % cam.TX) * kTile, ty0 = (tile / cam.TX) * kTile;
+  unsigned m = 0;
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const int X0 = tx0 + 8 * (q & 1), Y0 = ty0 + 8 * (q >> 1);
+    if (X0 >= cam.W || Y0 >= cam.H) continue;
+    const int X1 = min(X0 + 7, cam.W - 1), Y1 = min(Y0 + 7, cam.H - 1);
+    if (rect_keep(__fsub_rn((float)X0, q0.x), __fsub_rn((float)X1, q0.x), __fsub_rn((float)Y0, q0.y),
+                  __fsub_rn((float)Y1, q0.y), q0.z, q0.w, q1.x, q1.y))
+      m |= 1u << q;
+  }
+  return m;
+}
+
+// One warp per tile (grid-stride). Pass 0 counts the quadrant lists (and keeps each pair's 4-bit
+// mask); pass 1 scatters the slots in list order (ballot prefix sums: deterministic).
+template <bool kScatter>
+__global__ void __launch_bounds__(128) k_quad_bin(DevCam cam, const float4* __restrict__ rec,
+                                                  const int32_t* __restrict__ pair_slot,
+                                                  const int32_t* __restrict__ offs, int64_t capacity,
+                                                  uint8_t* __restrict__ qmask, int32_t* __restrict__ qcount,
+                                                  const int32_t* __restrict__ qoffs, int32_t* __restrict__ qslot) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const int n_tiles = cam.TX * cam.TY;
+  for (int t = gw; t < n_tiles; t += nw) {
+    int64_t s64 = offs[t], e64 = offs[t + 1];
+    if (e64 > capacity) e64 = capacity;
+    if (s64 > e64) s64 = e64;
+    const int s = (int)s64, e = (int)e64;
+    int c0 = 0, c1 = 0, c2 = 0, c3 = 0;  // running counts (warp-uniform)
+    int b0s = 0, b1s = 0, b2s = 0, b3s = 0;
+    if (kScatter) {
+      b0s = qoffs[4 * t]; b1s = qoffs[4 * t + 1]; b2s = qoffs[4 * t + 2]; b3s = qoffs[4 * t + 3];
+    }
+    for (int j0 = s; j0 < e; j0 += 32) {
+      const int j = j0 + lane;
+      unsigned m = 0;
+      int slot = 0;
+      if (j < e) {
+        slot = pair_slot[j];
+        if (!kScatter) {
+          const float4* r = rec + (size_t)slot * kRec4;
+          m = quad_mask(cam, t, r[0], r[1]);
+          qmask[j] = (uint8_t)m;
+        } else {
+          m = qmask[j];
+        }
+      }
+      const unsigned lt = (1u << lane) - 1u;
+      const unsigned b0 = __ballot_sync(FULL, m & 1u), b1 = __ballot_sync(FULL, m & 2u);
+      const unsigned b2 = __ballot_sync(FULL, m & 4u), b3 = __ballot_sync(FULL, m & 8u);
+      if (kScatter) {
+        if (m & 1u) qslot[b0s + c0 + __popc(b0 & lt)] = slot;
+        if (m & 2u) qslot[b1s + c1 + __popc(b1 & lt)] = slot;
+        if (m & 4u) qslot[b2s + c2 + __popc(b2 & lt)] = slot;
+        if (m & 8u) qslot[b3s + c3 + __popc(b3 & lt)] = slot;
+      }
+      c0 += __popc(b0); c1 += __popc(b1); c2 += __popc(b2); c3 += __popc(b3);
+    }
+    if (!kScatter && lane == 0) {
+      qcount[4 * t + 0] = c0; qcount[4 * t + 1] = c1; qcount[4 * t + 2] = c2; qcount[4 * t + 3] = c3;
+    }
+  }
+}
+
 // ------------------------------------------------------------------------- a5 moments ----
 struct Moments {
   float U0, U1, U2, S, Od, M1, M2, XX, XY, YY;
@@ -72,7 +157,8 @@ struct Moments {
 // warp may hit the 0.99 clamp (only splats with o ≥ 0.99 can: thr_hi ≤ 0).
 template <bool kClamp>
 __device__ __forceinline__ void moments_window(Moments& m, const float4* __restrict__ s_cu,
-                                               const float* __restrict__ s_ca, int tx0, int ty0, int px0, int px1,
+                                               const float* __restrict__ s_ca, int qx0, int qy0, int tx0, int ty0,
+                                               int px0, int px1,
                                                int py0, int py1, bool valid, float mx, float my, float nA, float nB,
                                                float nC, float thr_lo, float thr_hi, float log2o, float cR, float cG,
                                                float cB, float w, float kx, float ky, float ey) {
@@ -86,8 +172,8 @@ __device__ __forceinline__ void moments_window(Moments& m, const float4* __restr
     const float row_arg = fmaf(-ky, dy, log2o);
     const float lo = ract ? thr_lo : 1.0f;  // folds the row test into the pixel test
     float Rd = 0.f, Rdx = 0.f, Rdxx = 0.f;
-    const float4* cu_row = s_cu + py * kTile;
-    const float* ca_row = s_ca + py * kTile;
+    const float4* cu_row = s_cu + (py - qy0) * 8 - qx0;  // the staged 8×8 quadrant
+    const float* ca_row = s_ca + (py - qy0) * 8 - qx0;
 #pragma unroll 4
     for (int px = px0; px <= px1; px++) {
       const float dx = __fsub_rn((float)(tx0 + px), mx);
@@ -133,42 +219,42 @@ __global__ void __launch_bounds__(kMomentsThreads, 8) k_moments(DevCam cam, cons
                                                              const float4* __restrict__ coef4,
                                                              const float* __restrict__ coefa,
                                                              float* __restrict__ acc2d) {
-  __shared__ float4 s_cu_all[kMomentsThreads / 32][kTilePx];
-  __shared__ float s_ca_all[kMomentsThreads / 32][kTilePx];
+  __shared__ float4 s_cu_all[kMomentsThreads / 32][64];
+  __shared__ float s_ca_all[kMomentsThreads / 32][64];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   float4* s_cu = s_cu_all[wid];
   float* s_ca = s_ca_all[wid];
   const int n_items = *n_items_p;
   const unsigned FULL = 0xffffffffu;
-  int staged_tile = -1;
+  int staged = -1;
   for (;;) {
     int item = 0;
     if (lane == 0) item = atomicAdd(counter, 1);
     item = __shfl_sync(FULL, item, 0);
     if (item >= n_items) return;
     const int2 it = items[item];
-    const int tile = it.x, chunk = it.y;
-    if (tile != staged_tile) {  // stage the tile's pixel coefficients (5 KB) with coalesced 16-B loads
+    const int vt = it.x, chunk = it.y;  // vt = 4·tile + quadrant
+    const int tile = vt >> 2, quad = vt & 3;
+    const int qx0 = 8 * (quad & 1), qy0 = 8 * (quad >> 1);
+    if (vt != staged) {  // stage the quadrant's 64 pixel coefficients (1.25 KB), coalesced
       const float4* g4 = coef4 + (size_t)tile * kTilePx;
-      const float4* ga = reinterpret_cast<const float4*>(coefa + (size_t)tile * kTilePx);
+      const float* ga = coefa + (size_t)tile * kTilePx;
       __syncwarp();
-#pragma unroll
-      for (int h = 0; h < 2; h++) {  // two waves of 5 independent 16-B loads per lane
-        float4 v[4];
-#pragma unroll
-        for (int k = 0; k < 4; k++) v[k] = __ldcg(g4 + lane + 32 * (4 * h + k));
-        const float4 va = __ldcg(ga + lane + 32 * h);
-#pragma unroll
-        for (int k = 0; k < 4; k++) s_cu[lane + 32 * (4 * h + k)] = v[k];
-        reinterpret_cast<float4*>(s_ca)[lane + 32 * h] = va;
-      }
+      const int r0 = lane >> 3, c0 = lane & 7;  // lanes cover rows r0 and r0 + 4 of the quadrant
+      const float4 v0 = __ldcg(g4 + (qy0 + r0) * kTile + qx0 + c0);
+      const float4 v1 = __ldcg(g4 + (qy0 + r0 + 4) * kTile + qx0 + c0);
+      const float a0 = __ldcg(ga + (qy0 + r0) * kTile + qx0 + c0);
+      const float a1 = __ldcg(ga + (qy0 + r0 + 4) * kTile + qx0 + c0);
+      s_cu[r0 * 8 + c0] = v0;
+      s_cu[(r0 + 4) * 8 + c0] = v1;
+      s_ca[r0 * 8 + c0] = a0;
+      s_ca[(r0 + 4) * 8 + c0] = a1;
       __syncwarp();
-      staged_tile = tile;
+      staged = vt;
     }
-    int64_t e64 = offs[tile + 1];
-    if (e64 > capacity) e64 = capacity;
-    const int end = (int)e64;
-    const int j = offs[tile] + chunk * 32 + lane;
+
+    const int end = offs[vt + 1];   // quadrant lists (built within capacity)
+    const int j = offs[vt] + chunk * 32 + lane;
     const bool valid = j < end;
     float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0, q2 = q0, q3 = q0, q4 = q0;
     int slot = -1;
@@ -189,16 +275,16 @@ __global__ void __launch_bounds__(kMomentsThreads, 8) k_moments(DevCam cam, cons
       lo_y = fminf(lo_y, __shfl_xor_sync(FULL, lo_y, o));
       hi_y = fmaxf(hi_y, __shfl_xor_sync(FULL, hi_y, o));
     }
-    const int px0 = max(0, (int)floorf(fmaxf(lo_x - (float)tx0, -1.f)));
-    const int px1 = min(kTile - 1, (int)ceilf(fminf(hi_x - (float)tx0, 16.f)));
-    const int py0 = max(0, (int)floorf(fmaxf(lo_y - (float)ty0, -1.f)));
-    const int py1 = min(kTile - 1, (int)ceilf(fminf(hi_y - (float)ty0, 16.f)));
+    const int px0 = max(qx0, (int)floorf(fmaxf(lo_x - (float)tx0, -1.f)));
+    const int px1 = min(qx0 + 7, (int)ceilf(fminf(hi_x - (float)tx0, 16.f)));
+    const int py0 = max(qy0, (int)floorf(fmaxf(lo_y - (float)ty0, -1.f)));
+    const int py1 = min(qy0 + 7, (int)ceilf(fminf(hi_y - (float)ty0, 16.f)));
     Moments m = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (__any_sync(FULL, valid && q1.z <= 0.0f))
-      moments_window<true>(m, s_cu, s_ca, tx0, ty0, px0, px1, py0, py1, valid, mx, my, q0.z, q0.w, q1.x, q1.y, q1.z,
+      moments_window<true>(m, s_cu, s_ca, qx0, qy0, tx0, ty0, px0, px1, py0, py1, valid, mx, my, q0.z, q0.w, q1.x, q1.y, q1.z,
                            q1.w, q2.x, q2.y, q2.z, q2.w, q3.z, q3.w, ey);
     else
-      moments_window<false>(m, s_cu, s_ca, tx0, ty0, px0, px1, py0, py1, valid, mx, my, q0.z, q0.w, q1.x, q1.y, q1.z,
+      moments_window<false>(m, s_cu, s_ca, qx0, qy0, tx0, ty0, px0, px1, py0, py1, valid, mx, my, q0.z, q0.w, q1.x, q1.y, q1.z,
                             q1.w, q2.x, q2.y, q2.z, q2.w, q3.z, q3.w, ey);
     if (valid && (m.U0 != 0.f || m.U1 != 0.f || m.U2 != 0.f || m.S != 0.f || m.Od != 0.f)) {
       float* a = acc2d + (size_t)slot * 12;
@@ -436,7 +522,10 @@ __global__ void __launch_bounds__(128, 3) k_epilogue(DevCam cam, const float4* _
 
 // --------------------------------------------------------------------------- launchers ----
 size_t bwd_ws_bytes(int32_t n_tiles, int32_t n_slots, int64_t capacity) {
-  return align_up((size_t)n_slots * 12 * sizeof(float)) + items_bytes(n_tiles, capacity, 32) + align_up(16);
+  const int64_t qcap = 4 * capacity;
+  return align_up((size_t)n_slots * 12 * sizeof(float)) + items_bytes(4 * n_tiles, qcap, 32) + align_up(16) +
+         2 * align_up((size_t)(4 * n_tiles + 1) * 4) + align_up((size_t)qcap * 4) + align_up((size_t)capacity) +
+         scan_tmp_bytes(4 * (int64_t)n_tiles);
 }
 
 void launch_coef(const DevCam& cam, const float* state, const float* dL_dimage, const float* target, int32_t loss,
@@ -456,21 +545,34 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
     return;
   }
   const int n_tiles = cam.TX * cam.TY;
-  const int64_t max_items = capacity / 32 + n_tiles + 1;
+  const int64_t qcap = 4 * capacity;
+  const int64_t max_items = qcap / 32 + 4 * n_tiles + 1;
   Carve cv(ws);
   float* acc2d = cv.take<float>((size_t)n_slots * 12);
   int2* items = cv.take<int2>(max_items);
   int32_t* n_items = cv.take<int32_t>(4);
-  int32_t* tile_nch = cv.take<int32_t>(n_tiles + 1);
+  int32_t* tile_nch = cv.take<int32_t>(4 * n_tiles + 1);
   int32_t* scratch = cv.take<int32_t>(66);
   int32_t* counter = cv.take<int32_t>(4);
+  int32_t* qcount = cv.take<int32_t>(4 * n_tiles + 1);
+  int32_t* qoffs = cv.take<int32_t>(4 * n_tiles + 1);
+  int32_t* qslot = cv.take<int32_t>(qcap);
+  uint8_t* qmask = cv.take<uint8_t>(capacity);
+  void* tmp = cv.take<char>(scan_tmp_bytes(4 * (int64_t)n_tiles));
   cudaMemsetAsync(acc2d, 0, sizeof(float) * 12 * (size_t)n_slots, st);
   cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
-  launch_build_items(tile_offsets, n_tiles, capacity, 32, 0, items, n_items, tile_nch, scratch, st);
+  // quadrant sub-binning of the tile lists, then (quadrant, 32-slot chunk) items
+  const int qblocks = (n_tiles + 3) / 4;  // one warp per tile
+  k_quad_bin<false><<<qblocks, 128, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), pair_slot, tile_offsets,
+                                             capacity, qmask, qcount, qoffs, qslot);
+  launch_exclusive_scan(qcount, qoffs, 4 * (int64_t)n_tiles, tmp, st);
+  k_quad_bin<true><<<qblocks, 128, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), pair_slot, tile_offsets,
+                                            capacity, qmask, qcount, qoffs, qslot);
+  launch_build_items(qoffs, 4 * n_tiles, qcap, 32, 0, items, n_items, tile_nch, scratch, st);
   const int blocks = sm_count() * 8;  // persistent: 8 × 4 warps per SM, dynamic item claiming
   record_event(ev_begin, st);
-  k_moments<<<blocks, kMomentsThreads, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), pair_slot, tile_offsets,
-                                                capacity, items, n_items, counter,
+  k_moments<<<blocks, kMomentsThreads, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), qslot, qoffs,
+                                                qcap, items, n_items, counter,
                                                 reinterpret_cast<const float4*>(coef4), coefa, acc2d);
   record_event(ev_end, st);
   k_epilogue<<<(n_slots + 127) / 128, 128, 0, st>>>(cam, reinterpret_cast<const float4*>(rows), sigma, idx, n_slots,
