@@ -624,7 +624,8 @@ def build_line(args, world, res, results):
                            "fwd_kernel_ms": r["fwd_ms"], "bwd_moments_ms": r["bwd_ms"], "n_active": r["n_act"],
                            "train_ms": r["train_ms"], "refresh_ms": r["refresh_ms"],
                            "pairs_per_view": r["pairs"] / r["V"],
-                           "f_c": r["contrib"] / max(r["tile_evals"], 1)}
+                           "f_c": r["contrib"] / max(r["tile_evals"], 1),
+                           "f_c_tile_granular": r["contrib"] / max(256 * r["pairs"], 1)}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": res["ms"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
@@ -637,6 +638,7 @@ def build_line(args, world, res, results):
                    "streams": args.streams},
         "splat_pixel_evals_per_s": evals / (res["ms"] * 1e-3),
         "contributing_fraction_f_c": f_c,
+        "evaluated_splat_pixels_per_view": res["tile_evals"] / res["V"],
         "kernel_ms_per_step": {"fwd_composite": res["ser_fwd_ms"], "bwd_moments": res["ser_bwd_ms"],
                                "note": "sum over the step's training views, single-stream roofline pass; the timed "
                                        "step runs views on several streams concurrently",

@@ -137,8 +137,9 @@ int oit_composite_fwd(const oit_camera* cam, const float* rec, const int32_t* pa
 
 /* Same as oit_composite_fwd; d_counters (nullable, device int64[2], accumulated +=) receives
  * [0] the number of contributing (splat, pixel) pairs (α ≥ 1/255, inside the image) and [1] the
- * tile-granular splat-pixel evaluations (256 per (splat, tile) pair) — the work counters of the
- * metric. Counting adds one reduction per tile; the plain call skips it. */
+ * splat-pixel evaluations the kernel performs (64 per (splat, 8×8 quadrant) pair after the
+ * quadrant sub-binning; the metric's tile-granular count is 256 × *d_n_pairs of the bin).
+ * Counting adds one reduction per work item; the plain call skips it. */
 int oit_composite_fwd_ex(const oit_camera* cam, const float* rec, const int32_t* pair_slot,
                          const int32_t* tile_offsets, int64_t pair_capacity, const float bg_host[3],
                          const float* base, const uint8_t* route, float* image, float* state,
