@@ -195,6 +195,33 @@ __device__ __forceinline__ bool spec_tile_keep(int tx, int ty, int W, int H, flo
   return m >= __fmul_rn(thr_lo, 1.0009765625f);
 }
 
+// Work partitioning below the tile (not a spec decision): the step-12b test on an 8×8 quadrant's
+// pixel-centre rectangle; conservative, so a quadrant holding a contributing pixel is never dropped.
+__device__ __forceinline__ bool rect_keep(float ax0, float ax1, float ay0, float ay1, float nA, float nB, float nC,
+                                          float thr_lo) {
+  if (ax0 <= 0.0f && 0.0f <= ax1 && ay0 <= 0.0f && 0.0f <= ay1) return true;
+  float m = spec_edge_max(ax0, ay0, ay1, nA, nB, nC);
+  m = fmaxf(m, spec_edge_max(ax1, ay0, ay1, nA, nB, nC));
+  m = fmaxf(m, spec_edge_max(ay0, ax0, ax1, nC, nB, nA));
+  m = fmaxf(m, spec_edge_max(ay1, ax0, ax1, nC, nB, nA));
+  return m >= __fmul_rn(thr_lo, 1.0009765625f);
+}
+
+__device__ __forceinline__ unsigned quadrant_mask(const DevCam& cam, int tile, const float4& q0, const float4& q1) {
+  const int tx0 = (tile % cam.TX) * kTile, ty0 = (tile / cam.TX) * kTile;
+  unsigned m = 0;
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const int X0 = tx0 + 8 * (q & 1), Y0 = ty0 + 8 * (q >> 1);
+    if (X0 >= cam.W || Y0 >= cam.H) continue;
+    const int X1 = min(X0 + 7, cam.W - 1), Y1 = min(Y0 + 7, cam.H - 1);
+    if (rect_keep(__fsub_rn((float)X0, q0.x), __fsub_rn((float)X1, q0.x), __fsub_rn((float)Y0, q0.y),
+                  __fsub_rn((float)Y1, q0.y), q0.z, q0.w, q1.x, q1.y))
+      m |= 1u << q;
+  }
+  return m;
+}
+
 // DESIGN.md §3 step 13 (the per-pixel power; exact op order, no contraction beyond the two fmas).
 __device__ __forceinline__ float spec_power(float nA, float nB, float nC, float dx, float dy) {
   float by = __fmul_rn(nB, dy);

@@ -6,13 +6,15 @@
 // broadcasts. There is no early termination (OIT has no front-to-back order) and no depth sort
 // (P:339).
 //
-// k_fwd_quad (the default path): each tile list is sub-binned into its four 8×8 quadrants
-// (conservative rectangle test, items.cu), and work items are (quadrant, chunk of ≤ kFwdChunk
-// slots), longest lists first, claimed by persistent warps — OIT's order independence makes
-// splitting a list legal: partial (P, Q, T) of the chunks combine as P = ΣP_k, Q = ΣQ_k,
-// T = ΠT_k, in chunk order, by the last warp to finish the quadrant (deterministic). Each lane
-// owns 2 pixels of one row (x and x+4), sharing the record loads and the row terms of the spec
-// test. k_fwd (one CTA per tile) serves the BAU route path.
+// k_fwd_items (the default path): work items are (tile, chunk of ≤ kFwdChunk slots), longest
+// tiles first, claimed by a persistent grid — OIT's order independence makes splitting a tile
+// legal: partial (P, Q, T) of the chunks combine as P = ΣP_k, Q = ΣQ_k, T = ΠT_k, done in chunk
+// order by the last CTA to finish the tile (deterministic). Warp w of the CTA owns the 8×8
+// quadrant w of the tile (2 pixels per lane: columns c and c+4 of row r); each staged record
+// carries a 4-bit mask of the quadrants its α = 1/255 ellipse can reach (conservative rectangle
+// test, quadrant_mask), and a warp skips — warp-uniformly — the records outside its quadrant:
+// on C2 a (splat, tile) pair reaches 2.2 of the 4 quadrants. k_fwd (one CTA per tile) serves
+// the BAU route path.
 #include "kernels.h"
 
 namespace oit {
@@ -31,38 +33,37 @@ __device__ __forceinline__ void accum_px(float power, float thr_hi, float arg, c
   T = fmaf(-alpha, T, T);
 }
 
-// Quadrant work items: (tile, 8×8 quadrant, chunk of ≤ kFwdChunk slots of the quadrant list).
-// One warp per item, 2 pixels per lane (rows r = lane/4, columns c and c + 4 of the quadrant);
-// records staged in the warp's shared slice 32 at a time and read as broadcasts.
 template <bool kBase, bool kCount>
-__global__ void __launch_bounds__(kFwdThreads) k_fwd_quad(
-    DevCam cam, const float4* __restrict__ rec, const int32_t* __restrict__ qslot,
-    const int32_t* __restrict__ qoffs, const int2* __restrict__ items, const int32_t* __restrict__ n_items_p,
-    int32_t* __restrict__ counter, const int32_t* __restrict__ vt_nch, int32_t* __restrict__ done,
-    float* __restrict__ partial, const float* __restrict__ base, float* __restrict__ image,
-    float* __restrict__ state, unsigned long long* __restrict__ counters) {
-  constexpr int kW = kFwdThreads / 32;
-  __shared__ float4 s_q0[kW][32], s_q1[kW][32], s_q2[kW][32];
-  __shared__ float2 s_k[kW][32];
-  const unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+__global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
+    DevCam cam, const float4* __restrict__ rec, const int32_t* __restrict__ pair_slot,
+    const int32_t* __restrict__ offs, int64_t capacity, const int2* __restrict__ items,
+    const int32_t* __restrict__ n_items_p, int32_t* __restrict__ counter, const int32_t* __restrict__ tile_nch,
+    int32_t* __restrict__ done, float* __restrict__ partial, const float* __restrict__ base,
+    float* __restrict__ image, float* __restrict__ state, unsigned long long* __restrict__ counters) {
+  __shared__ float4 s_q0[kFwdThreads], s_q1[kFwdThreads], s_q2[kFwdThreads];
+  __shared__ float2 s_k[kFwdThreads];
+  __shared__ uint8_t s_m[kFwdThreads];
+  __shared__ int s_item, s_last;
+  const int tid = threadIdx.x;
   const int n_tiles = cam.TX * cam.TY;
   const size_t plane = (size_t)n_tiles * kTilePx;
   const int n_items = *n_items_p;
-  const int r = lane >> 2, c = lane & 3;
+  const int wq = tid >> 5, lane = tid & 31;                  // warp = quadrant wq
+  const int qx0 = 8 * (wq & 1), qy0 = 8 * (wq >> 1);
+  const unsigned qbit = 1u << wq;
+  const int ly = qy0 + (lane >> 2), lx = qx0 + (lane & 3);   // pixels (lx, ly) and (lx + 4, ly)
+  const int p0 = ly * kTile + lx, p1 = p0 + 4;
   for (;;) {
-    int item = 0;
-    if (lane == 0) item = atomicAdd(counter, 1);
-    item = __shfl_sync(FULL, item, 0);
+    if (tid == 0) s_item = atomicAdd(counter, 1);
+    __syncthreads();
+    const int item = s_item;
+    __syncthreads();
     if (item >= n_items) return;
     const int2 it = items[item];
-    const int vt = it.x, chunk = it.y;
-    const int tile = vt >> 2, quad = vt & 3;
-    const int qx0 = 8 * (quad & 1), qy0 = 8 * (quad >> 1);
-    const int nch = vt_nch[vt];
+    const int tile = it.x, chunk = it.y;
+    const int nch = tile_nch[tile];
     const int tx0 = (tile % cam.TX) * kTile, ty0 = (tile / cam.TX) * kTile;
-    const int p0 = (qy0 + r) * kTile + qx0 + c, p1 = p0 + 4;  // pixel indices inside the tile
-    const float fy = (float)(ty0 + qy0 + r), fx0 = (float)(tx0 + qx0 + c), fx1 = fx0 + 4.0f;
+    const float fy = (float)(ty0 + ly), fx0 = (float)(tx0 + lx), fx1 = (float)(tx0 + lx + 4);
     const size_t px0 = (size_t)tile * kTilePx + p0, px1 = px0 + 4;
     float A0 = 0.f, A1 = 0.f, A2 = 0.f, AQ = 0.f, AT = 1.f;   // pixel 0
     float B0 = 0.f, B1 = 0.f, B2 = 0.f, BQ = 0.f, BT = 1.f;   // pixel 1
@@ -70,24 +71,27 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_quad(
       A0 = base[px0]; A1 = base[plane + px0]; A2 = base[2 * plane + px0]; AQ = base[3 * plane + px0]; AT = base[4 * plane + px0];
       B0 = base[px1]; B1 = base[plane + px1]; B2 = base[2 * plane + px1]; BQ = base[3 * plane + px1]; BT = base[4 * plane + px1];
     }
-    const int begin = qoffs[vt] + chunk * kFwdChunk;
-    const int end = min(begin + kFwdChunk, qoffs[vt + 1]);
-    int n_contrib = 0;
-    for (int b = begin; b < end; b += 32) {
-      const int n = min(32, end - b);
-      __syncwarp();
-      if (lane < n) {
-        const float4* rp = rec + (size_t)qslot[b + lane] * kRec4;
-        s_q0[wid][lane] = rp[0];
-        s_q1[wid][lane] = rp[1];
-        s_q2[wid][lane] = rp[2];
-        s_k[wid][lane] = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(rp + 3) + 2);
+    int64_t e64 = offs[tile + 1];
+    if (e64 > capacity) e64 = capacity;
+    const int begin = offs[tile] + chunk * kFwdChunk;
+    const int end = (int)min((int64_t)begin + kFwdChunk, e64);
+    int n_contrib = 0, n_quad_evals = 0;
+    for (int b = begin; b < end; b += kFwdThreads) {
+      const int n = min(kFwdThreads, end - b);
+      if (tid < n) {
+        const float4* r = rec + (size_t)pair_slot[b + tid] * kRec4;
+        s_q0[tid] = r[0];
+        s_q1[tid] = r[1];
+        s_q2[tid] = r[2];
+        s_k[tid] = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(r + 3) + 2);
+        s_m[tid] = (uint8_t)quadrant_mask(cam, tile, r[0], r[1]);
       }
-      __syncwarp();
+      __syncthreads();
 #pragma unroll 2
       for (int i = 0; i < n; i++) {
-        const float4 q0 = s_q0[wid][i];  // mx my nA nB
-        const float4 q1 = s_q1[wid][i];  // nC thr_lo thr_hi log2o
+        if (!(s_m[i] & qbit)) continue;  // warp-uniform: the splat cannot reach this quadrant
+        const float4 q0 = s_q0[i];  // mx my nA nB
+        const float4 q1 = s_q1[i];  // nC thr_lo thr_hi log2o
         const float dy = __fsub_rn(fy, q0.y);
         const float by = __fmul_rn(q0.w, dy);
         const float cy = __fmul_rn(__fmul_rn(q1.x, dy), dy);
@@ -97,39 +101,36 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_quad(
         const bool c0 = pw0 <= 0.0f && pw0 >= q1.y;
         const bool c1 = pw1 <= 0.0f && pw1 >= q1.y;
         if (c0 || c1) {
-          const float4 q2 = s_q2[wid][i];  // cR cG cB w
-          const float2 kk = s_k[wid][i];   // sub-ulp μ' correction of the exponent (value path)
+          const float4 q2 = s_q2[i];  // cR cG cB w
+          const float2 kk = s_k[i];   // sub-ulp μ' correction of the exponent (value path)
           const float base_arg = fmaf(-kk.y, dy, q1.w);
           if (c0) accum_px(pw0, q1.z, fmaf(-kk.x, dx0, fmaf(pw0, kLog2e, base_arg)), q2, A0, A1, A2, AQ, AT);
           if (c1) accum_px(pw1, q1.z, fmaf(-kk.x, dx1, fmaf(pw1, kLog2e, base_arg)), q2, B0, B1, B2, BQ, BT);
-          if (kCount) {
-            const bool in_y = ty0 + qy0 + r < cam.H;
-            n_contrib += (c0 && in_y && tx0 + qx0 + c < cam.W) + (c1 && in_y && tx0 + qx0 + c + 4 < cam.W);
-          }
+          if (kCount) n_contrib += (c0 && tx0 + lx < cam.W && ty0 + ly < cam.H) + (c1 && tx0 + lx + 4 < cam.W && ty0 + ly < cam.H);
         }
       }
+      if (kCount && tid == 0)
+        for (int i = 0; i < n; i++) n_quad_evals += __popc((unsigned)s_m[i]);
+      __syncthreads();
     }
     if (kCount) {
-      unsigned long long cc = (unsigned long long)n_contrib;
+      unsigned long long c = (unsigned long long)n_contrib;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) cc += __shfl_xor_sync(FULL, cc, o);
-      if (lane == 0) {
-        if (cc) atomicAdd(counters, cc);
-        atomicAdd(counters + 1, (unsigned long long)(end - begin) * 64ull);  // quadrant-granular evaluations
-      }
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if ((tid & 31) == 0 && c) atomicAdd(counters, c);
+      if (tid == 0) atomicAdd(counters + 1, (unsigned long long)n_quad_evals * 64ull);
     }
     bool write_final = true;
     if (nch > 1) {
-      // multi-chunk quadrant: publish this chunk's partial; the last chunk to finish combines them
-      float* pa = partial + (size_t)item * 5 * 64;
-      const int q0i = r * 8 + c, q1i = q0i + 4;
-      pa[q0i] = A0; pa[64 + q0i] = A1; pa[128 + q0i] = A2; pa[192 + q0i] = AQ; pa[256 + q0i] = AT;
-      pa[q1i] = B0; pa[64 + q1i] = B1; pa[128 + q1i] = B2; pa[192 + q1i] = BQ; pa[256 + q1i] = BT;
+      // multi-chunk tile: publish this chunk's partial; the last chunk to finish combines them
+      float* pa = partial + (size_t)item * 5 * kTilePx;
+      pa[p0] = A0; pa[kTilePx + p0] = A1; pa[2 * kTilePx + p0] = A2; pa[3 * kTilePx + p0] = AQ; pa[4 * kTilePx + p0] = AT;
+      pa[p1] = B0; pa[kTilePx + p1] = B1; pa[2 * kTilePx + p1] = B2; pa[3 * kTilePx + p1] = BQ; pa[4 * kTilePx + p1] = BT;
       __threadfence();
-      __syncwarp();
-      int last = 0;
-      if (lane == 0) last = (atomicAdd(done + vt, 1) == nch - 1);
-      write_final = __shfl_sync(FULL, last, 0);
+      __syncthreads();
+      if (tid == 0) s_last = (atomicAdd(done + tile, 1) == nch - 1);
+      __syncthreads();
+      write_final = s_last;
       if (write_final) {
         __threadfence();
         const int first = item - chunk;
@@ -141,13 +142,13 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_quad(
           B0 = B1 = B2 = BQ = 0.f; BT = 1.f;
         }
         for (int k = 0; k < nch; k++) {  // fixed chunk order: deterministic combination
-          const float* pk = partial + (size_t)(first + k) * 5 * 64;
-          A0 += __ldcg(pk + q0i); A1 += __ldcg(pk + 64 + q0i); A2 += __ldcg(pk + 128 + q0i);
-          AQ += __ldcg(pk + 192 + q0i); AT *= __ldcg(pk + 256 + q0i);
-          B0 += __ldcg(pk + q1i); B1 += __ldcg(pk + 64 + q1i); B2 += __ldcg(pk + 128 + q1i);
-          BQ += __ldcg(pk + 192 + q1i); BT *= __ldcg(pk + 256 + q1i);
+          const float* pk = partial + (size_t)(first + k) * 5 * kTilePx;
+          A0 += __ldcg(pk + p0); A1 += __ldcg(pk + kTilePx + p0); A2 += __ldcg(pk + 2 * kTilePx + p0);
+          AQ += __ldcg(pk + 3 * kTilePx + p0); AT *= __ldcg(pk + 4 * kTilePx + p0);
+          B0 += __ldcg(pk + p1); B1 += __ldcg(pk + kTilePx + p1); B2 += __ldcg(pk + 2 * kTilePx + p1);
+          BQ += __ldcg(pk + 3 * kTilePx + p1); BT *= __ldcg(pk + 4 * kTilePx + p1);
         }
-        if (lane == 0) done[vt] = 0;  // re-arm for the next call
+        if (tid == 0) done[tile] = 0;  // re-arm for the next call
       }
     }
     if (write_final) {
@@ -157,17 +158,17 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_quad(
       }
       if (image) {
         const size_t hw = (size_t)cam.W * cam.H;
-        const int y = ty0 + qy0 + r, x = tx0 + qx0 + c;
+        const int y = ty0 + ly;
         float F0, F1, F2, C0, C1, C2;
-        if (y < cam.H && x < cam.W) {
+        if (y < cam.H && tx0 + lx < cam.W) {
           resolve_pixel(A0, A1, A2, AQ, AT, cam.bg, F0, F1, F2, C0, C1, C2);
-          const size_t pp = (size_t)y * cam.W + x;
-          image[pp] = C0; image[hw + pp] = C1; image[2 * hw + pp] = C2;
+          const size_t p = (size_t)y * cam.W + tx0 + lx;
+          image[p] = C0; image[hw + p] = C1; image[2 * hw + p] = C2;
         }
-        if (y < cam.H && x + 4 < cam.W) {
+        if (y < cam.H && tx0 + lx + 4 < cam.W) {
           resolve_pixel(B0, B1, B2, BQ, BT, cam.bg, F0, F1, F2, C0, C1, C2);
-          const size_t pp = (size_t)y * cam.W + x + 4;
-          image[pp] = C0; image[hw + pp] = C1; image[2 * hw + pp] = C2;
+          const size_t p = (size_t)y * cam.W + tx0 + lx + 4;
+          image[p] = C0; image[hw + p] = C1; image[2 * hw + p] = C2;
         }
       }
     }
@@ -267,10 +268,9 @@ __global__ void __launch_bounds__(256) k_fwd(DevCam cam, const float4* __restric
 }
 
 size_t fwd_ws_bytes(int32_t n_tiles, int64_t capacity) {
-  const int64_t qcap = 4 * capacity;
-  const int64_t max_items = qcap / kFwdChunk + 4 * n_tiles + 1;
-  return quad_bytes(n_tiles, capacity) + items_bytes(4 * n_tiles, qcap, kFwdChunk) +
-         align_up((size_t)4 * n_tiles * 4) + align_up(16) + align_up((size_t)max_items * 5 * 64 * sizeof(float));
+  const int64_t max_items = capacity / kFwdChunk + n_tiles + 1;
+  return items_bytes(n_tiles, capacity, kFwdChunk) + align_up((size_t)n_tiles * 4) + align_up(16) +
+         align_up((size_t)max_items * 5 * kTilePx * sizeof(float));
 }
 
 void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pair_slot,
@@ -280,32 +280,25 @@ void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pa
   const float4* r4 = reinterpret_cast<const float4*>(rec);
   auto* cnt = reinterpret_cast<unsigned long long*>(counters);
   if (!route) {
-    const int64_t qcap = 4 * capacity;
-    const int64_t max_items = qcap / kFwdChunk + 4 * n_tiles + 1;
+    const int64_t max_items = capacity / kFwdChunk + n_tiles + 1;
     Carve cv(ws);
-    int32_t* qcount = cv.take<int32_t>(4 * n_tiles + 1);
-    int32_t* qoffs = cv.take<int32_t>(4 * n_tiles + 1);
-    int32_t* qslot = cv.take<int32_t>(qcap);
-    uint8_t* qmask = cv.take<uint8_t>(capacity);
-    void* tmp = cv.take<char>(scan_tmp_bytes(4 * (int64_t)n_tiles));
     int2* items = cv.take<int2>(max_items);
     int32_t* n_items = cv.take<int32_t>(4);
-    int32_t* vt_nch = cv.take<int32_t>(4 * n_tiles + 1);
+    int32_t* tile_nch = cv.take<int32_t>(n_tiles + 1);
     int32_t* scratch = cv.take<int32_t>(66);
-    int32_t* done = cv.take<int32_t>(4 * n_tiles);
+    int32_t* done = cv.take<int32_t>(n_tiles);
     int32_t* counter = cv.take<int32_t>(4);
-    float* partial = cv.take<float>((size_t)max_items * 5 * 64);
-    cudaMemsetAsync(done, 0, sizeof(int32_t) * 4 * n_tiles, st);
+    float* partial = cv.take<float>((size_t)max_items * 5 * kTilePx);
+    cudaMemsetAsync(done, 0, sizeof(int32_t) * n_tiles, st);
     cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
-    launch_quad_bin(cam, rec, pair_slot, tile_offsets, capacity, qmask, qcount, qoffs, qslot, tmp, st);
-    launch_build_items(qoffs, 4 * n_tiles, qcap, kFwdChunk, 1, items, n_items, vt_nch, scratch, st);
-    const int grid = sm_count() * 12;  // persistent; warps claim items dynamically
-#define OIT_FWDQ(B, K)                                                                                          \
-  k_fwd_quad<B, K><<<grid, kFwdThreads, 0, st>>>(cam, r4, qslot, qoffs, items, n_items, counter, vt_nch, done, \
-                                                 partial, base, image, state, cnt)
-    if (counters) { if (base) OIT_FWDQ(true, true); else OIT_FWDQ(false, true); }
-    else { if (base) OIT_FWDQ(true, false); else OIT_FWDQ(false, false); }
-#undef OIT_FWDQ
+    launch_build_items(tile_offsets, n_tiles, capacity, kFwdChunk, 1, items, n_items, tile_nch, scratch, st);
+    const int grid = sm_count() * 12;  // persistent; items are claimed dynamically
+#define OIT_FWD2(B, K)                                                                                         \
+  k_fwd_items<B, K><<<grid, kFwdThreads, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, items, n_items, \
+                                                  counter, tile_nch, done, partial, base, image, state, cnt)
+    if (counters) { if (base) OIT_FWD2(true, true); else OIT_FWD2(false, true); }
+    else { if (base) OIT_FWD2(true, false); else OIT_FWD2(false, false); }
+#undef OIT_FWD2
     return;
   }
 #define OIT_FWD(R, B, K) \

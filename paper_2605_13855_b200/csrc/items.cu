@@ -84,31 +84,6 @@ __global__ void __launch_bounds__(256) k_items_emit(const int32_t* __restrict__ 
 // max of its power over the quadrant's pixel-centre rectangle reaches thr_lo·(1+2^-10) (the step
 // 12b test on a smaller rectangle: conservative, so no contributing pixel is lost; pixel decisions
 // stay the spec's). On C2 a pair touches 2.2 quadrants on average: 55% of the pixels to evaluate.
-__device__ __forceinline__ bool rect_keep(float ax0, float ax1, float ay0, float ay1, float nA, float nB, float nC,
-                                          float thr_lo) {
-  if (ax0 <= 0.0f && 0.0f <= ax1 && ay0 <= 0.0f && 0.0f <= ay1) return true;
-  float m = spec_edge_max(ax0, ay0, ay1, nA, nB, nC);
-  m = fmaxf(m, spec_edge_max(ax1, ay0, ay1, nA, nB, nC));
-  m = fmaxf(m, spec_edge_max(ay0, ax0, ax1, nC, nB, nA));
-  m = fmaxf(m, spec_edge_max(ay1, ax0, ax1, nC, nB, nA));
-  return m >= __fmul_rn(thr_lo, 1.0009765625f);
-}
-
-__device__ __forceinline__ unsigned quad_mask(const DevCam& cam, int tile, const float4& q0, const float4& q1) {
-  const int tx0 = (tile % cam.TX) * kTile, ty0 = (tile / cam.TX) * kTile;
-  unsigned m = 0;
-#pragma unroll
-  for (int q = 0; q < 4; q++) {
-    const int X0 = tx0 + 8 * (q & 1), Y0 = ty0 + 8 * (q >> 1);
-    if (X0 >= cam.W || Y0 >= cam.H) continue;
-    const int X1 = min(X0 + 7, cam.W - 1), Y1 = min(Y0 + 7, cam.H - 1);
-    if (rect_keep(__fsub_rn((float)X0, q0.x), __fsub_rn((float)X1, q0.x), __fsub_rn((float)Y0, q0.y),
-                  __fsub_rn((float)Y1, q0.y), q0.z, q0.w, q1.x, q1.y))
-      m |= 1u << q;
-  }
-  return m;
-}
-
 // One warp per tile (grid-stride). Pass 0 counts the quadrant lists (and keeps each pair's 4-bit
 // mask); pass 1 scatters the slots in list order (ballot prefix sums: deterministic).
 template <bool kScatter>
@@ -139,7 +114,7 @@ __global__ void __launch_bounds__(128) k_quad_bin(DevCam cam, const float4* __re
         slot = pair_slot[j];
         if (!kScatter) {
           const float4* r = rec + (size_t)slot * kRec4;
-          m = quad_mask(cam, t, r[0], r[1]);
+          m = quadrant_mask(cam, t, r[0], r[1]);
           qmask[j] = (uint8_t)m;
         } else {
           m = qmask[j];
