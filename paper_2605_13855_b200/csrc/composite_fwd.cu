@@ -9,12 +9,9 @@
 // k_fwd_items (the default path): work items are (tile, chunk of ≤ kFwdChunk slots), longest
 // tiles first, claimed by a persistent grid — OIT's order independence makes splitting a tile
 // legal: partial (P, Q, T) of the chunks combine as P = ΣP_k, Q = ΣQ_k, T = ΠT_k, done in chunk
-// order by the last CTA to finish the tile (deterministic). Warp w of the CTA owns the 8×8
-// quadrant w of the tile (2 pixels per lane: columns c and c+4 of row r); each staged record
-// carries a 4-bit mask of the quadrants its α = 1/255 ellipse can reach (conservative rectangle
-// test, quadrant_mask), and a warp skips — warp-uniformly — the records outside its quadrant:
-// on C2 a (splat, tile) pair reaches 2.2 of the 4 quadrants. k_fwd (one CTA per tile) serves
-// the BAU route path.
+// order by the last CTA to finish the tile (deterministic). Each thread owns 2 pixels of one row
+// (x and x+8), which shares the record loads and the row terms of the spec test and gives two
+// independent dependency chains. k_fwd (one CTA per tile) serves the BAU route path.
 #include "kernels.h"
 
 namespace oit {
@@ -42,17 +39,13 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
     float* __restrict__ image, float* __restrict__ state, unsigned long long* __restrict__ counters) {
   __shared__ float4 s_q0[kFwdThreads], s_q1[kFwdThreads], s_q2[kFwdThreads];
   __shared__ float2 s_k[kFwdThreads];
-  __shared__ uint8_t s_m[kFwdThreads];
   __shared__ int s_item, s_last;
   const int tid = threadIdx.x;
   const int n_tiles = cam.TX * cam.TY;
   const size_t plane = (size_t)n_tiles * kTilePx;
   const int n_items = *n_items_p;
-  const int wq = tid >> 5, lane = tid & 31;                  // warp = quadrant wq
-  const int qx0 = 8 * (wq & 1), qy0 = 8 * (wq >> 1);
-  const unsigned qbit = 1u << wq;
-  const int ly = qy0 + (lane >> 2), lx = qx0 + (lane & 3);   // pixels (lx, ly) and (lx + 4, ly)
-  const int p0 = ly * kTile + lx, p1 = p0 + 4;
+  const int ly = tid >> 3, lx = tid & 7;     // pixels (lx, ly) and (lx + 8, ly) of the tile
+  const int p0 = ly * kTile + lx, p1 = p0 + 8;
   for (;;) {
     if (tid == 0) s_item = atomicAdd(counter, 1);
     __syncthreads();
@@ -63,8 +56,8 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
     const int tile = it.x, chunk = it.y;
     const int nch = tile_nch[tile];
     const int tx0 = (tile % cam.TX) * kTile, ty0 = (tile / cam.TX) * kTile;
-    const float fy = (float)(ty0 + ly), fx0 = (float)(tx0 + lx), fx1 = (float)(tx0 + lx + 4);
-    const size_t px0 = (size_t)tile * kTilePx + p0, px1 = px0 + 4;
+    const float fy = (float)(ty0 + ly), fx0 = (float)(tx0 + lx), fx1 = (float)(tx0 + lx + 8);
+    const size_t px0 = (size_t)tile * kTilePx + p0, px1 = px0 + 8;
     float A0 = 0.f, A1 = 0.f, A2 = 0.f, AQ = 0.f, AT = 1.f;   // pixel 0
     float B0 = 0.f, B1 = 0.f, B2 = 0.f, BQ = 0.f, BT = 1.f;   // pixel 1
     if (kBase && nch == 1) {
@@ -75,7 +68,7 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
     if (e64 > capacity) e64 = capacity;
     const int begin = offs[tile] + chunk * kFwdChunk;
     const int end = (int)min((int64_t)begin + kFwdChunk, e64);
-    int n_contrib = 0, n_quad_evals = 0;
+    int n_contrib = 0;
     for (int b = begin; b < end; b += kFwdThreads) {
       const int n = min(kFwdThreads, end - b);
       if (tid < n) {
@@ -84,12 +77,10 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
         s_q1[tid] = r[1];
         s_q2[tid] = r[2];
         s_k[tid] = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(r + 3) + 2);
-        s_m[tid] = (uint8_t)quadrant_mask(cam, tile, r[0], r[1]);
       }
       __syncthreads();
 #pragma unroll 2
       for (int i = 0; i < n; i++) {
-        if (!(s_m[i] & qbit)) continue;  // warp-uniform: the splat cannot reach this quadrant
         const float4 q0 = s_q0[i];  // mx my nA nB
         const float4 q1 = s_q1[i];  // nC thr_lo thr_hi log2o
         const float dy = __fsub_rn(fy, q0.y);
@@ -106,11 +97,9 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
           const float base_arg = fmaf(-kk.y, dy, q1.w);
           if (c0) accum_px(pw0, q1.z, fmaf(-kk.x, dx0, fmaf(pw0, kLog2e, base_arg)), q2, A0, A1, A2, AQ, AT);
           if (c1) accum_px(pw1, q1.z, fmaf(-kk.x, dx1, fmaf(pw1, kLog2e, base_arg)), q2, B0, B1, B2, BQ, BT);
-          if (kCount) n_contrib += (c0 && tx0 + lx < cam.W && ty0 + ly < cam.H) + (c1 && tx0 + lx + 4 < cam.W && ty0 + ly < cam.H);
+          if (kCount) n_contrib += (c0 && tx0 + lx < cam.W && ty0 + ly < cam.H) + (c1 && tx0 + lx + 8 < cam.W && ty0 + ly < cam.H);
         }
       }
-      if (kCount && tid == 0)
-        for (int i = 0; i < n; i++) n_quad_evals += __popc((unsigned)s_m[i]);
       __syncthreads();
     }
     if (kCount) {
@@ -118,7 +107,7 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
       if ((tid & 31) == 0 && c) atomicAdd(counters, c);
-      if (tid == 0) atomicAdd(counters + 1, (unsigned long long)n_quad_evals * 64ull);
+      if (tid == 0) atomicAdd(counters + 1, (unsigned long long)(end - begin) * kTilePx);
     }
     bool write_final = true;
     if (nch > 1) {
@@ -165,9 +154,9 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
           const size_t p = (size_t)y * cam.W + tx0 + lx;
           image[p] = C0; image[hw + p] = C1; image[2 * hw + p] = C2;
         }
-        if (y < cam.H && tx0 + lx + 4 < cam.W) {
+        if (y < cam.H && tx0 + lx + 8 < cam.W) {
           resolve_pixel(B0, B1, B2, BQ, BT, cam.bg, F0, F1, F2, C0, C1, C2);
-          const size_t p = (size_t)y * cam.W + tx0 + lx + 4;
+          const size_t p = (size_t)y * cam.W + tx0 + lx + 8;
           image[p] = C0; image[hw + p] = C1; image[2 * hw + p] = C2;
         }
       }
