@@ -270,6 +270,8 @@ class Workload:
         self.pipes = [self.pipe] + [ViewPipeline(cams[0], max(self.n_act, 1), cap, device=dev)
                                     for _ in range(self.n_streams - 1)]
         self.streams = [torch.cuda.Stream() for _ in range(self.n_streams)]
+        self.copy_stream = torch.cuda.Stream()
+        self.ev_copy = [torch.cuda.Event() for _ in range(len(cams))]
         nt = self.pipe.n_tiles
         self.n_tiles = nt
         # ---- untimed setup: per-view pre-render caches of the frozen set (Alg. 1 I^pre), targets ----
@@ -336,14 +338,22 @@ class Workload:
         torch.cuda.synchronize()
 
     # ---------------------------------------------------------------------------------------
-    def train_views(self, n_streams=None):
+    def train_views(self, n_streams=None, host_targets=None):
         """a1-a6 over every training view (Alg. 1 l.3-6, one view per iteration); views are dealt
-        round-robin to n_streams streams (fork/join on the current stream)."""
+        round-robin to n_streams streams (fork/join on the current stream). host_targets (e2e):
+        pinned-host training images, copied in view order on a copy stream; each view's loss
+        waits only for its own image (copies overlap the compute of earlier views)."""
         torch, L = self.torch, self.L
         ns = self.n_streams if n_streams is None else n_streams
         main = torch.cuda.current_stream()
         self.grad.zero_()
         self.dsig.zero_()
+        if host_targets is not None:
+            self.copy_stream.wait_stream(main)
+            with torch.cuda.stream(self.copy_stream):
+                for v in range(self.V):
+                    self.targets[v].copy_(host_targets[v], non_blocking=True)
+                    self.ev_copy[v].record(self.copy_stream)
         for st_ in self.streams[:ns]:
             st_.wait_stream(main)
         for v, cam in enumerate(self.cams):
@@ -353,11 +363,15 @@ class Workload:
                 p.set_camera(cam)
                 img, st = p.forward(self.rows, self.sigma, self.act, self.bg, base=self.caches[v],
                                     events=self.ev_fwd[v])
+                if host_targets is not None:
+                    self.streams[k].wait_event(self.ev_copy[v])
                 L.oit_loss_grad(cam, img, self.targets[v], "l1", self.dLdC[k])
                 p.backward(self.rows, self.sigma, self.act, self.bg, st, self.dLdC[k], self.grad, self.dsig,
                            events=self.ev_bwd[v])
         for st_ in self.streams[:ns]:
             main.wait_stream(st_)
+        if host_targets is not None:
+            main.wait_stream(self.copy_stream)
 
     def refresh(self):
         """a7 (FPS + subsampled score of the inactive splats) and a8 (Eq. 8 update)."""
@@ -568,14 +582,40 @@ def time_workload(args, torch, dist, wl, world, headline_run):
 
 def time_e2e(args, torch, dist, wl, step, flush, allred):
     """Same step through the public API with HOST inputs: per step, pinned-host → device copies of
-    the parameter rows and the training images, and device → host reads of the gradient rows and
-    the refreshed active-set bitmask, all inside the timed region."""
+    the parameter rows (before anything else) and of every training image (on a copy stream, in
+    view order; each view waits only for its own image, so the copies overlap the compute of the
+    earlier views), and device → host reads of the gradient rows and the refreshed bitmask — all
+    inside the timed region (one CUDA graph per step, copies included)."""
     rows_h = wl.rows.cpu().pin_memory()
     targets_h = wl.targets.cpu().pin_memory()
     grad_h = torch.empty_like(wl.grad, device="cpu").pin_memory()
     bits_h = torch.empty_like(wl.bits, device="cpu").pin_memory()
     h2d = rows_h.numel() * 4 + targets_h.numel() * 4
     d2h = grad_h.numel() * 4 + bits_h.numel() * 4
+    host_views = [targets_h[v] for v in range(wl.V)]
+
+    def e2e_step():
+        wl.rows.copy_(rows_h, non_blocking=True)
+        wl.train_views(host_targets=host_views)
+        if allred:
+            return
+        wl.refresh()
+        wl.update()
+        grad_h.copy_(wl.grad, non_blocking=True)
+        bits_h.copy_(wl.bits, non_blocking=True)
+
+    graph = None
+    if not args.no_graph and not allred:
+        e2e_step()
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=s):
+                e2e_step()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     times = []
     for i in range(args.warmup + args.steps):
@@ -584,11 +624,16 @@ def time_e2e(args, torch, dist, wl, step, flush, allred):
         if allred:
             dist.barrier()
         t0.record()
-        wl.rows.copy_(rows_h, non_blocking=True)
-        wl.targets.copy_(targets_h, non_blocking=True)
-        step()
-        grad_h.copy_(wl.grad, non_blocking=True)
-        bits_h.copy_(wl.bits, non_blocking=True)
+        if graph is not None:
+            graph.replay()
+        elif allred:
+            wl.rows.copy_(rows_h, non_blocking=True)
+            wl.targets.copy_(targets_h, non_blocking=True)
+            step()
+            grad_h.copy_(wl.grad, non_blocking=True)
+            bits_h.copy_(wl.bits, non_blocking=True)
+        else:
+            e2e_step()
         t1.record()
         torch.cuda.synchronize()
         if i >= args.warmup:
