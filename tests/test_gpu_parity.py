@@ -333,3 +333,86 @@ def test_c2_full_size_parity_sampled():
     ok, bad = grad_close(grad.cpu().numpy()[sample], gref, bnd)
     assert ok, bad.sum()
     assert strict_fraction(grad.cpu().numpy()[sample], gref) > 0.99
+
+
+# ------------------------------------------------------------------ concurrency ----------
+def test_concurrent_views_accumulate_like_sequential():
+    """Views on several streams accumulate into the same gradient rows (vector atomics) and give
+    the sequential result within fp32 reordering; equal to the oracle's sum over the views."""
+    from paper_2605_13855_b200.pipeline import ViewPipeline
+    sc = SCENES[1]
+    idx = np.arange(sc.n, dtype=np.int32)
+    rows, sigma, idx_t = _t(sc.rows), _t(np.array([sc.sigma], np.float32)), _t(idx)
+    gs = [_t(synth.dl_dimage(c, 40 + k)) for k, c in enumerate(sc.cams)]
+
+    def run(n_streams):
+        pipes = [ViewPipeline(sc.cams[0], sc.n, 1 << 20, device=DEV) for _ in range(n_streams)]
+        streams = [torch.cuda.Stream() for _ in range(n_streams)]
+        grad = torch.zeros((sc.n, 80), dtype=torch.float32, device=DEV)
+        dsig = torch.zeros(1, dtype=torch.float32, device=DEV)
+        main = torch.cuda.current_stream()
+        for s_ in streams:
+            s_.wait_stream(main)
+        for v, cam in enumerate(sc.cams):
+            k = v % n_streams
+            with torch.cuda.stream(streams[k]):
+                pipes[k].set_camera(cam)
+                _, st = pipes[k].forward(rows, sigma, idx_t, sc.bg)
+                pipes[k].backward(rows, sigma, idx_t, sc.bg, st, gs[v], grad, dsig)
+        for s_ in streams:
+            main.wait_stream(s_)
+        torch.cuda.synchronize()
+        return grad.cpu().numpy(), float(dsig.item())
+
+    g1, d1 = run(1)
+    g3, d3 = run(3)
+    assert np.abs(g3 - g1).max() <= 1e-5 * np.abs(g1).max()
+    assert abs(d3 - d1) <= 1e-5 * abs(d1)
+    ref = np.zeros_like(g1)
+    bnd = np.zeros_like(g1)
+    for v, cam in enumerate(sc.cams):
+        st = O.render(sc.rows, sc.sigma, idx, cam, sc.bg)["state"]
+        gr, _, _, b = O.backward_bound(sc.rows, sc.sigma, idx, cam, sc.bg, st, gs[v].cpu().numpy().astype(np.float64))
+        ref += gr
+        bnd += b
+    ok, bad = grad_close(g3, ref, bnd)
+    assert ok, describe_bad(g3, ref, bad, bnd)
+
+
+def test_score_split_across_streams_equals_single_call():
+    """oit_score_subsample on disjoint view subsets (concurrent streams, scale 1/S each) equals one
+    call over all S views (the mean of R19)."""
+    L = _L()
+    sc = synth.scene_c2(n=6000, n_views=6, res=64)
+    mask = synth.active_mask(sc, 0.3, "uniform")
+    act, ina = np.flatnonzero(mask).astype(np.int32), np.flatnonzero(~mask).astype(np.int32)
+    W, H = 64, 64
+    caches = [_t(plain_to_tile_major(O.render(sc.rows, sc.sigma, ina, c, sc.bg)["state"], W, H).astype(np.float32))
+              for c in sc.cams]
+    targets = [_t(synth.target_image(c, 70 + k)) for k, c in enumerate(sc.cams)]
+    cap = 1 << 18
+    rows, sigma = _t(sc.rows), _t(np.array([sc.sigma], np.float32))
+    views = [0, 2, 3, 5]
+
+    def run(parts):
+        sg = torch.zeros((len(ina), 80), dtype=torch.float32, device=DEV)
+        ds = torch.zeros(1, dtype=torch.float32, device=DEV)
+        mp = torch.zeros(1, dtype=torch.int64, device=DEV)
+        main = torch.cuda.current_stream()
+        streams = [torch.cuda.Stream() for _ in parts]
+        for s_, part in zip(streams, parts):
+            s_.wait_stream(main)
+            ws = torch.empty(L.oit_score_workspace_bytes(sc.cams[0], len(act), len(ina), cap), dtype=torch.uint8,
+                             device=DEV)
+            with torch.cuda.stream(s_):
+                L.oit_score_subsample(rows, sigma, sc.cams, targets, caches, _t(act), _t(ina), part, "l2", sc.bg, sg,
+                                      ds, cap, mp, ws, scale=1.0 / len(views))
+        for s_ in streams:
+            main.wait_stream(s_)
+        torch.cuda.synchronize()
+        return sg.cpu().numpy(), float(ds.item())
+
+    a, da = run([views])
+    b, db = run([views[:2], views[2:]])
+    assert np.abs(a - b).max() <= 1e-5 * np.abs(a).max() and np.abs(a).max() > 0
+    assert abs(da - db) <= 1e-5 * abs(da) + 1e-12
