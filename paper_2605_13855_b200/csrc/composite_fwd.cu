@@ -9,14 +9,14 @@
 // k_fwd_items (the default path): work items are (tile, chunk of ≤ kFwdChunk slots), longest
 // tiles first, claimed by a persistent grid — OIT's order independence makes splitting a tile
 // legal: partial (P, Q, T) of the chunks combine as P = ΣP_k, Q = ΣQ_k, T = ΠT_k, done in chunk
-// order by the last CTA to finish the tile (deterministic). Each thread owns 2 pixels of one row
-// (x and x+8), which shares the record loads and the row terms of the spec test and gives two
-// independent dependency chains. k_fwd (one CTA per tile) serves the BAU route path.
+// order by the last CTA to finish the tile (deterministic). Each thread owns 4 pixels of one row
+// (x, x+4, x+8, x+12), which shares the record loads and the row terms of the spec test across
+// the 4 pixels and gives four independent dependency chains. k_fwd (one CTA per tile) serves the BAU route path.
 #include "kernels.h"
 
 namespace oit {
 
-constexpr int kFwdThreads = 128;   // 2 pixels per thread
+constexpr int kFwdThreads = 64;    // 4 pixels per thread (one tile row: columns c, c+4, c+8, c+12)
 constexpr int kFwdChunk = 256;     // slots per work item
 
 __device__ __forceinline__ void accum_px(float power, float thr_hi, float arg, const float4& q2, float& P0, float& P1,
@@ -28,6 +28,19 @@ __device__ __forceinline__ void accum_px(float power, float thr_hi, float arg, c
   P2 = fmaf(q2.z, aw, P2);
   Q += aw;
   T = fmaf(-alpha, T, T);
+}
+
+struct Px {
+  float P0, P1, P2, Q, T;
+};
+
+__device__ __forceinline__ void load_px(Px& a, const float* base, size_t plane, size_t px) {
+  a.P0 = base[px]; a.P1 = base[plane + px]; a.P2 = base[2 * plane + px]; a.Q = base[3 * plane + px];
+  a.T = base[4 * plane + px];
+}
+__device__ __forceinline__ void store_px(const Px& a, float* dst, size_t plane, size_t px) {
+  dst[px] = a.P0; dst[plane + px] = a.P1; dst[2 * plane + px] = a.P2; dst[3 * plane + px] = a.Q;
+  dst[4 * plane + px] = a.T;
 }
 
 template <bool kBase, bool kCount>
@@ -44,8 +57,8 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
   const int n_tiles = cam.TX * cam.TY;
   const size_t plane = (size_t)n_tiles * kTilePx;
   const int n_items = *n_items_p;
-  const int ly = tid >> 3, lx = tid & 7;     // pixels (lx, ly) and (lx + 8, ly) of the tile
-  const int p0 = ly * kTile + lx, p1 = p0 + 8;
+  const int ly = tid >> 2, lx = tid & 3;  // pixels (lx + 4k, ly), k = 0..3
+  const int p0 = ly * kTile + lx;
   for (;;) {
     if (tid == 0) s_item = atomicAdd(counter, 1);
     __syncthreads();
@@ -56,13 +69,15 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
     const int tile = it.x, chunk = it.y;
     const int nch = tile_nch[tile];
     const int tx0 = (tile % cam.TX) * kTile, ty0 = (tile / cam.TX) * kTile;
-    const float fy = (float)(ty0 + ly), fx0 = (float)(tx0 + lx), fx1 = (float)(tx0 + lx + 8);
-    const size_t px0 = (size_t)tile * kTilePx + p0, px1 = px0 + 8;
-    float A0 = 0.f, A1 = 0.f, A2 = 0.f, AQ = 0.f, AT = 1.f;   // pixel 0
-    float B0 = 0.f, B1 = 0.f, B2 = 0.f, BQ = 0.f, BT = 1.f;   // pixel 1
-    if (kBase && nch == 1) {
-      A0 = base[px0]; A1 = base[plane + px0]; A2 = base[2 * plane + px0]; AQ = base[3 * plane + px0]; AT = base[4 * plane + px0];
-      B0 = base[px1]; B1 = base[plane + px1]; B2 = base[2 * plane + px1]; BQ = base[3 * plane + px1]; BT = base[4 * plane + px1];
+    const float fy = (float)(ty0 + ly), fx0 = (float)(tx0 + lx);
+    const float fx1 = fx0 + 4.0f, fx2 = fx0 + 8.0f, fx3 = fx0 + 12.0f;
+    const size_t pxb = (size_t)tile * kTilePx + p0;
+    Px a[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      a[k].P0 = a[k].P1 = a[k].P2 = a[k].Q = 0.f;
+      a[k].T = 1.f;
+      if (kBase && nch == 1) load_px(a[k], base, plane, pxb + 4 * k);
     }
     int64_t e64 = offs[tile + 1];
     if (e64 > capacity) e64 = capacity;
@@ -87,17 +102,24 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
         const float by = __fmul_rn(q0.w, dy);
         const float cy = __fmul_rn(__fmul_rn(q1.x, dy), dy);
         const float dx0 = __fsub_rn(fx0, q0.x), dx1 = __fsub_rn(fx1, q0.x);
-        const float pw0 = spec_power_row(q0.z, dx0, by, cy);
-        const float pw1 = spec_power_row(q0.z, dx1, by, cy);
-        const bool c0 = pw0 <= 0.0f && pw0 >= q1.y;
-        const bool c1 = pw1 <= 0.0f && pw1 >= q1.y;
-        if (c0 || c1) {
+        const float dx2 = __fsub_rn(fx2, q0.x), dx3 = __fsub_rn(fx3, q0.x);
+        const float pw0 = spec_power_row(q0.z, dx0, by, cy), pw1 = spec_power_row(q0.z, dx1, by, cy);
+        const float pw2 = spec_power_row(q0.z, dx2, by, cy), pw3 = spec_power_row(q0.z, dx3, by, cy);
+        const bool c0 = pw0 <= 0.0f && pw0 >= q1.y, c1 = pw1 <= 0.0f && pw1 >= q1.y;
+        const bool c2 = pw2 <= 0.0f && pw2 >= q1.y, c3 = pw3 <= 0.0f && pw3 >= q1.y;
+        if (c0 || c1 || c2 || c3) {
           const float4 q2 = s_q2[i];  // cR cG cB w
           const float2 kk = s_k[i];   // sub-ulp μ' correction of the exponent (value path)
           const float base_arg = fmaf(-kk.y, dy, q1.w);
-          if (c0) accum_px(pw0, q1.z, fmaf(-kk.x, dx0, fmaf(pw0, kLog2e, base_arg)), q2, A0, A1, A2, AQ, AT);
-          if (c1) accum_px(pw1, q1.z, fmaf(-kk.x, dx1, fmaf(pw1, kLog2e, base_arg)), q2, B0, B1, B2, BQ, BT);
-          if (kCount) n_contrib += (c0 && tx0 + lx < cam.W && ty0 + ly < cam.H) + (c1 && tx0 + lx + 8 < cam.W && ty0 + ly < cam.H);
+          if (c0) accum_px(pw0, q1.z, fmaf(-kk.x, dx0, fmaf(pw0, kLog2e, base_arg)), q2, a[0].P0, a[0].P1, a[0].P2, a[0].Q, a[0].T);
+          if (c1) accum_px(pw1, q1.z, fmaf(-kk.x, dx1, fmaf(pw1, kLog2e, base_arg)), q2, a[1].P0, a[1].P1, a[1].P2, a[1].Q, a[1].T);
+          if (c2) accum_px(pw2, q1.z, fmaf(-kk.x, dx2, fmaf(pw2, kLog2e, base_arg)), q2, a[2].P0, a[2].P1, a[2].P2, a[2].Q, a[2].T);
+          if (c3) accum_px(pw3, q1.z, fmaf(-kk.x, dx3, fmaf(pw3, kLog2e, base_arg)), q2, a[3].P0, a[3].P1, a[3].P2, a[3].Q, a[3].T);
+          if (kCount) {
+            if (ty0 + ly < cam.H)
+              n_contrib += (c0 && tx0 + lx < cam.W) + (c1 && tx0 + lx + 4 < cam.W) + (c2 && tx0 + lx + 8 < cam.W) +
+                           (c3 && tx0 + lx + 12 < cam.W);
+          }
         }
       }
       __syncthreads();
@@ -113,8 +135,8 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
     if (nch > 1) {
       // multi-chunk tile: publish this chunk's partial; the last chunk to finish combines them
       float* pa = partial + (size_t)item * 5 * kTilePx;
-      pa[p0] = A0; pa[kTilePx + p0] = A1; pa[2 * kTilePx + p0] = A2; pa[3 * kTilePx + p0] = AQ; pa[4 * kTilePx + p0] = AT;
-      pa[p1] = B0; pa[kTilePx + p1] = B1; pa[2 * kTilePx + p1] = B2; pa[3 * kTilePx + p1] = BQ; pa[4 * kTilePx + p1] = BT;
+#pragma unroll
+      for (int k = 0; k < 4; k++) store_px(a[k], pa, kTilePx, p0 + 4 * k);
       __threadfence();
       __syncthreads();
       if (tid == 0) s_last = (atomicAdd(done + tile, 1) == nch - 1);
@@ -123,41 +145,35 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
       if (write_final) {
         __threadfence();
         const int first = item - chunk;
-        if (kBase) {
-          A0 = base[px0]; A1 = base[plane + px0]; A2 = base[2 * plane + px0]; AQ = base[3 * plane + px0]; AT = base[4 * plane + px0];
-          B0 = base[px1]; B1 = base[plane + px1]; B2 = base[2 * plane + px1]; BQ = base[3 * plane + px1]; BT = base[4 * plane + px1];
-        } else {
-          A0 = A1 = A2 = AQ = 0.f; AT = 1.f;
-          B0 = B1 = B2 = BQ = 0.f; BT = 1.f;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          if (kBase) load_px(a[k], base, plane, pxb + 4 * k);
+          else { a[k].P0 = a[k].P1 = a[k].P2 = a[k].Q = 0.f; a[k].T = 1.f; }
         }
-        for (int k = 0; k < nch; k++) {  // fixed chunk order: deterministic combination
-          const float* pk = partial + (size_t)(first + k) * 5 * kTilePx;
-          A0 += __ldcg(pk + p0); A1 += __ldcg(pk + kTilePx + p0); A2 += __ldcg(pk + 2 * kTilePx + p0);
-          AQ += __ldcg(pk + 3 * kTilePx + p0); AT *= __ldcg(pk + 4 * kTilePx + p0);
-          B0 += __ldcg(pk + p1); B1 += __ldcg(pk + kTilePx + p1); B2 += __ldcg(pk + 2 * kTilePx + p1);
-          BQ += __ldcg(pk + 3 * kTilePx + p1); BT *= __ldcg(pk + 4 * kTilePx + p1);
+        for (int c = 0; c < nch; c++) {  // fixed chunk order: deterministic combination
+          const float* pk = partial + (size_t)(first + c) * 5 * kTilePx;
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            const int q = p0 + 4 * k;
+            a[k].P0 += __ldcg(pk + q); a[k].P1 += __ldcg(pk + kTilePx + q); a[k].P2 += __ldcg(pk + 2 * kTilePx + q);
+            a[k].Q += __ldcg(pk + 3 * kTilePx + q); a[k].T *= __ldcg(pk + 4 * kTilePx + q);
+          }
         }
         if (tid == 0) done[tile] = 0;  // re-arm for the next call
       }
     }
     if (write_final) {
-      if (state) {
-        state[px0] = A0; state[plane + px0] = A1; state[2 * plane + px0] = A2; state[3 * plane + px0] = AQ; state[4 * plane + px0] = AT;
-        state[px1] = B0; state[plane + px1] = B1; state[2 * plane + px1] = B2; state[3 * plane + px1] = BQ; state[4 * plane + px1] = BT;
-      }
-      if (image) {
-        const size_t hw = (size_t)cam.W * cam.H;
-        const int y = ty0 + ly;
-        float F0, F1, F2, C0, C1, C2;
-        if (y < cam.H && tx0 + lx < cam.W) {
-          resolve_pixel(A0, A1, A2, AQ, AT, cam.bg, F0, F1, F2, C0, C1, C2);
-          const size_t p = (size_t)y * cam.W + tx0 + lx;
-          image[p] = C0; image[hw + p] = C1; image[2 * hw + p] = C2;
-        }
-        if (y < cam.H && tx0 + lx + 8 < cam.W) {
-          resolve_pixel(B0, B1, B2, BQ, BT, cam.bg, F0, F1, F2, C0, C1, C2);
-          const size_t p = (size_t)y * cam.W + tx0 + lx + 8;
-          image[p] = C0; image[hw + p] = C1; image[2 * hw + p] = C2;
+      const size_t hw = (size_t)cam.W * cam.H;
+      const int y = ty0 + ly;
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        if (state) store_px(a[k], state, plane, pxb + 4 * k);
+        const int x = tx0 + lx + 4 * k;
+        if (image && y < cam.H && x < cam.W) {
+          float F0, F1, F2, C0, C1, C2;
+          resolve_pixel(a[k].P0, a[k].P1, a[k].P2, a[k].Q, a[k].T, cam.bg, F0, F1, F2, C0, C1, C2);
+          const size_t pp = (size_t)y * cam.W + x;
+          image[pp] = C0; image[hw + pp] = C1; image[2 * hw + pp] = C2;
         }
       }
     }
@@ -281,7 +297,7 @@ void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pa
     cudaMemsetAsync(done, 0, sizeof(int32_t) * n_tiles, st);
     cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
     launch_build_items(tile_offsets, n_tiles, capacity, kFwdChunk, 1, items, n_items, tile_nch, scratch, st);
-    const int grid = sm_count() * 12;  // persistent; items are claimed dynamically
+    const int grid = sm_count() * 24;  // persistent (64-thread CTAs); items are claimed dynamically
 #define OIT_FWD2(B, K)                                                                                         \
   k_fwd_items<B, K><<<grid, kFwdThreads, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, items, n_items, \
                                                   counter, tile_nch, done, partial, base, image, state, cnt)
