@@ -301,7 +301,6 @@ class Workload:
         assert max_pairs <= cap, "pair capacity overflow"
         self.max_pairs_train = max_pairs
         # ---- buffers of the step ----
-        self.dLdC = [torch.empty((3, H, W), dtype=torch.float32, device=dev) for _ in range(self.n_streams)]
         self.grad = torch.zeros((max(self.n_act, 1), 80), dtype=torch.float32, device=dev)
         self.dsig = torch.zeros(1, dtype=torch.float32, device=dev)
         # refresh: FPS over this rank's view centres, S = 5% of the views, scored set = inactive set
@@ -361,13 +360,14 @@ class Workload:
             p = self.pipes[k]
             with torch.cuda.stream(self.streams[k]):
                 p.set_camera(cam)
-                img, st = p.forward(self.rows, self.sigma, self.act, self.bg, base=self.caches[v],
-                                    events=self.ev_fwd[v])
+                # a3 (no image: the fused a4 below resolves C from the state), then a4+a5+a6 with
+                # the L1 gradient against the view's training image fused into the coefficients
+                _, st = p.forward(self.rows, self.sigma, self.act, self.bg, base=self.caches[v], image=False,
+                                  events=self.ev_fwd[v])
                 if host_targets is not None:
                     self.streams[k].wait_event(self.ev_copy[v])
-                L.oit_loss_grad(cam, img, self.targets[v], "l1", self.dLdC[k])
-                p.backward(self.rows, self.sigma, self.act, self.bg, st, self.dLdC[k], self.grad, self.dsig,
-                           events=self.ev_bwd[v])
+                p.backward(self.rows, self.sigma, self.act, self.bg, st, None, self.grad, self.dsig,
+                           events=self.ev_bwd[v], target=self.targets[v], loss="l1")
         for st_ in self.streams[:ns]:
             main.wait_stream(st_)
         if host_targets is not None:
@@ -414,7 +414,7 @@ class Workload:
         fwd = 3                                            # items hist + emit, k_fwd_items
         # coef | quadrant count, scan, quadrant scatter, items hist + emit, moments, epilogue
         bwd = lambda n: 1 + ((6 + scan_kernels(4 * nt)) if n > 0 else 0)  # noqa: E731
-        train = self.V * (proj(a) + binn(a) + fwd + 1 + bwd(a))
+        train = self.V * (proj(a) + binn(a) + fwd + bwd(a))   # loss fused into the bwd coefficients
         refresh = 1
         if s > 0:
             refresh += self.S * (proj(a) + binn(a) + fwd + 1 + proj(s) + binn(s) + (bwd(s) - 1))

@@ -175,9 +175,13 @@ int oit_composite_bwd(const oit_scene* scene, const oit_camera* cam, const int32
                       float scale, float* grad, float* dL_dsigma, float* dL_dcov, void* ws,
                       size_t ws_bytes, oit_stream_t stream);
 
-/* Same as oit_composite_bwd; ev (nullable) holds two cudaEvent_t recorded on `stream` right
- * before and after the a5 moment kernel (the hot loop), so callers can time it with events
- * (also inside CUDA-graph capture, where they are recorded as external event nodes). */
+/* Same as oit_composite_bwd, plus:
+ *  - target (nullable, [3][H][W] device): if given, dL_dimage is ignored (may be NULL) and the
+ *    pixel gradient is the L1 (loss 0) / L2 (loss 1) gradient of oit_loss_grad, computed from the
+ *    image the state resolves to, inside the coefficient kernel (a4 fused: no image round trip);
+ *  - ev (nullable): two cudaEvent_t recorded on `stream` right before and after the a5 moment
+ *    kernel (the hot loop), so callers can time it with events (also inside CUDA-graph capture,
+ *    where they are recorded as external event nodes). */
 typedef struct {
   void* moments_begin; /* cudaEvent_t or NULL */
   void* moments_end;   /* cudaEvent_t or NULL */
@@ -187,7 +191,8 @@ int oit_composite_bwd_ex(const oit_scene* scene, const oit_camera* cam, const in
                          const int32_t* tile_offsets, int64_t pair_capacity, const float bg_host[3],
                          const float* state, const float* dL_dimage, float scale, float* grad,
                          float* dL_dsigma, float* dL_dcov, void* ws, size_t ws_bytes,
-                         const oit_bwd_events* ev, oit_stream_t stream);
+                         const float* target, int32_t loss, const oit_bwd_events* ev,
+                         oit_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------
  * a7  oit_select_views — farthest point sampling over the camera centres with a Philox4x32-10

@@ -143,16 +143,17 @@ int oit_composite_bwd(const oit_scene* scene, const oit_camera* cam, const int32
                       const float bg_host[3], const float* state, const float* dL_dimage, float scale, float* grad,
                       float* dL_dsigma, float* dL_dcov, void* ws, size_t ws_bytes, oit_stream_t stream) {
   return oit_composite_bwd_ex(scene, cam, idx, n_slots, rec, pair_slot, tile_offsets, pair_capacity, bg_host, state,
-                              dL_dimage, scale, grad, dL_dsigma, dL_dcov, ws, ws_bytes, nullptr, stream);
+                              dL_dimage, scale, grad, dL_dsigma, dL_dcov, ws, ws_bytes, nullptr, 0, nullptr, stream);
 }
 
 int oit_composite_bwd_ex(const oit_scene* scene, const oit_camera* cam, const int32_t* idx, int32_t n_slots,
                          const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
                          int64_t pair_capacity, const float bg_host[3], const float* state, const float* dL_dimage,
                          float scale, float* grad, float* dL_dsigma, float* dL_dcov, void* ws, size_t ws_bytes,
-                         const oit_bwd_events* ev, oit_stream_t stream) {
+                         const float* target, int32_t loss, const oit_bwd_events* ev, oit_stream_t stream) {
   if (!scene || !scene->rows || !scene->sigma || !cam_ok(cam) || n_slots < 0 || pair_capacity < 0) return OIT_EINVAL;
-  if (!tile_offsets || !bg_host || !state || !dL_dimage || !dL_dsigma || !ws) return OIT_EINVAL;
+  if (!tile_offsets || !bg_host || !state || (!dL_dimage && !target) || !dL_dsigma || !ws) return OIT_EINVAL;
+  if (target && loss != 0 && loss != 1) return OIT_EINVAL;
   if (n_slots > 0 && (!idx || !rec || !grad)) return OIT_EINVAL;
   if (pair_capacity > 0 && !pair_slot) return OIT_EINVAL;
   if (!shape_ok(cam) || n_slots > scene->n || oit_num_tiles(cam) > kMaxScan) return OIT_ESHAPE;
@@ -163,7 +164,7 @@ int oit_composite_bwd_ex(const oit_scene* scene, const oit_camera* cam, const in
   float* coef4 = cv.take<float>((size_t)nt * kTilePx * 4);
   float* coefa = cv.take<float>((size_t)nt * kTilePx);
   void* rest = cv.base + cv.off;
-  launch_coef(dc, state, dL_dimage, nullptr, 0, coef4, coefa, S(stream));
+  launch_coef(dc, state, target ? nullptr : dL_dimage, target, loss, coef4, coefa, S(stream));
   launch_composite_bwd(dc, scene->rows, scene->sigma, idx, n_slots, rec, pair_slot, tile_offsets, pair_capacity,
                        coef4, coefa, scale, grad, dL_dsigma, dL_dcov, rest, S(stream),
                        ev ? static_cast<cudaEvent_t>(ev->moments_begin) : nullptr,

@@ -416,3 +416,34 @@ def test_score_split_across_streams_equals_single_call():
     b, db = run([views[:2], views[2:]])
     assert np.abs(a - b).max() <= 1e-5 * np.abs(a).max() and np.abs(a).max() > 0
     assert abs(da - db) <= 1e-5 * abs(da) + 1e-12
+
+
+@pytest.mark.parametrize("loss", ["l1", "l2"])
+def test_fused_loss_backward_equals_two_step(loss):
+    """oit_composite_bwd_ex(target=…) (a4 fused into the coefficients) equals oit_loss_grad on the
+    forward image followed by oit_composite_bwd, and the oracle's loss-gradient backward."""
+    L = _L()
+    sc = SCENES[1]
+    cam = sc.cams[2]
+    idx = np.arange(sc.n, dtype=np.int32)
+    rows, sigma, idx_t = _t(sc.rows), _t(np.array([sc.sigma], np.float32)), _t(idx)
+    tgt = _t(synth.target_image(cam, 77))
+    p = _pipe(cam, sc.n)
+    img, st = p.forward(rows, sigma, idx_t, sc.bg)
+    g = torch.empty_like(img)
+    L.oit_loss_grad(cam, img, tgt, loss, g)
+    out = []
+    for fused in (False, True):
+        grad = torch.zeros((sc.n, 80), dtype=torch.float32, device=DEV)
+        ds = torch.zeros(1, dtype=torch.float32, device=DEV)
+        if fused:
+            p.backward(rows, sigma, idx_t, sc.bg, st, None, grad, ds, target=tgt, loss=loss)
+        else:
+            p.backward(rows, sigma, idx_t, sc.bg, st, g, grad, ds)
+        out.append(grad.cpu().numpy())
+    assert np.abs(out[0] - out[1]).max() <= 1e-6 * max(np.abs(out[0]).max(), 1e-30)
+    ref = O.render(sc.rows, sc.sigma, idx, cam, sc.bg)
+    gref = O.loss_grad(ref["image"], tgt.cpu().numpy().astype(np.float64), loss)
+    gr, _, _, bnd = O.backward_bound(sc.rows, sc.sigma, idx, cam, sc.bg, ref["state"], gref)
+    ok, bad = grad_close(out[1], gr, bnd, atol=1e-6 / (3 * cam["width"] * cam["height"]))
+    assert ok, describe_bad(out[1], gr, bad, bnd)
