@@ -411,9 +411,9 @@ class Workload:
         a, s = self.n_act, self.n_ina
         proj = lambda n: 1 if n > 0 else 0  # noqa: E731
         binn = lambda n: (1 if n > 0 else 0) + scan_kernels(nt) + 1  # noqa: E731
-        fwd = 3                                            # items hist + emit, k_fwd_items
-        # coef | quadrant count, scan, quadrant scatter, items hist + emit, moments, epilogue
-        bwd = lambda n: 1 + ((6 + scan_kernels(4 * nt)) if n > 0 else 0)  # noqa: E731
+        fwd = 2                                            # fused item builder, k_fwd_items
+        # coef | quadrant count, scan, quadrant scatter, fused item builder, moments, epilogue
+        bwd = lambda n: 1 + ((5 + scan_kernels(4 * nt)) if n > 0 else 0)  # noqa: E731
         train = self.V * (proj(a) + binn(a) + fwd + bwd(a))   # loss fused into the bwd coefficients
         refresh = 1
         if s > 0:

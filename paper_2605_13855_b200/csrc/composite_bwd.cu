@@ -467,7 +467,7 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
   int2* items = cv.take<int2>(max_items);
   int32_t* n_items = cv.take<int32_t>(4);
   int32_t* tile_nch = cv.take<int32_t>(4 * n_tiles + 1);
-  int32_t* scratch = cv.take<int32_t>(66);
+  int32_t* scratch = cv.take<int32_t>(68);
   int32_t* counter = cv.take<int32_t>(4);
   int32_t* qcount = cv.take<int32_t>(4 * n_tiles + 1);
   int32_t* qoffs = cv.take<int32_t>(4 * n_tiles + 1);

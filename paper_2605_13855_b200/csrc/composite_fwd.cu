@@ -290,7 +290,7 @@ void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pa
     int2* items = cv.take<int2>(max_items);
     int32_t* n_items = cv.take<int32_t>(4);
     int32_t* tile_nch = cv.take<int32_t>(n_tiles + 1);
-    int32_t* scratch = cv.take<int32_t>(66);
+    int32_t* scratch = cv.take<int32_t>(68);
     int32_t* done = cv.take<int32_t>(n_tiles);
     int32_t* counter = cv.take<int32_t>(4);
     float* partial = cv.take<float>((size_t)max_items * 5 * kTilePx);

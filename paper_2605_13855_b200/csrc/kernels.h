@@ -32,7 +32,7 @@ size_t fwd_ws_bytes(int32_t n_tiles, int64_t capacity);
 // items.cu — (tile, chunk) work lists, longest tiles first
 size_t items_bytes(int32_t n_tiles, int64_t capacity, int chunk);
 void launch_build_items(const int32_t* tile_offsets, int n_tiles, int64_t capacity, int chunk, int empty_items,
-                        int2* items, int32_t* n_items, int32_t* tile_nch, int32_t* scratch66, cudaStream_t st);
+                        int2* items, int32_t* n_items, int32_t* tile_nch, int32_t* scratch68, cudaStream_t st);
 
 // quadrant sub-binning: qoffs[4·n_tiles+1], qslot[4·capacity] (lists of the 8×8 quadrants in
 // list order), qmask[capacity] and qcount[4·n_tiles] scratch, tmp = scan_tmp_bytes(4·n_tiles)
