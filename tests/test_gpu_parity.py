@@ -441,7 +441,8 @@ def test_fused_loss_backward_equals_two_step(loss):
         else:
             p.backward(rows, sigma, idx_t, sc.bg, st, g, grad, ds)
         out.append(grad.cpu().numpy())
-    assert np.abs(out[0] - out[1]).max() <= 1e-6 * max(np.abs(out[0]).max(), 1e-30)
+    # identical coefficients; the two runs differ only by the order of the fp32 atomics
+    assert np.abs(out[0] - out[1]).max() <= 1e-5 * max(np.abs(out[0]).max(), 1e-30)
     ref = O.render(sc.rows, sc.sigma, idx, cam, sc.bg)
     gref = O.loss_grad(ref["image"], tgt.cpu().numpy().astype(np.float64), loss)
     gr, _, _, bnd = O.backward_bound(sc.rows, sc.sigma, idx, cam, sc.bg, ref["state"], gref)
