@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-reconcile", action="store_true", help="skip the NEXT-1 reconciliation measurement")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--profile-once", action="store_true", help="run one eager step (for ncu) and exit")
     return ap.parse_args()
@@ -577,7 +578,66 @@ def time_workload(args, torch, dist, wl, world, headline_run):
                refresh_ms=float(np.mean([b for _, b in seg_ms])) if seg_ms else None)
     if headline_run and not args.no_e2e:
         res["e2e"] = time_e2e(args, torch, dist, wl, step, flush, allred)
+    if headline_run and not args.no_reconcile and wl.n_ina > 0:
+        res["reconcile"] = time_reconcile(args, torch, wl, flush)
     return res
+
+
+def time_reconcile(args, torch, wl, flush):
+    """NEXT-1 (§4.1 P:147 lazy pre-render): cost of bringing one view's cache to a new active set
+    by the delta (oit_active_set_delta + oit_reconcile_cache: FOLD the newly frozen, UNFOLD the
+    re-activated splats) versus re-rendering the new frozen set from scratch (a1-a3, no image).
+    The synthetic change: 10 % of the active set frozen, 2 % of the frozen set re-activated
+    (seeded). Summed over the V views on one stream; L2 flushed before each repetition."""
+    from paper_2605_13855_b200 import synth
+    from paper_2605_13855_b200.pipeline import ViewPipeline
+    L, dev = wl.L, wl.dev
+    mask0 = synth.mask_from_bits(wl.bits0.cpu().numpy().view(np.uint32), wl.n)
+    g = np.random.default_rng(4242)
+    m = mask0.copy()
+    a, i = np.flatnonzero(mask0), np.flatnonzero(~mask0)
+    m[a[g.random(len(a)) < 0.10]] = False
+    m[i[g.random(len(i)) < 0.02]] = True
+    bits_new = torch.from_numpy(synth.bits_from_mask(m).view(np.int32)).to(dev)
+    ina_new = torch.from_numpy(np.flatnonzero(~m).astype(np.int32)).to(dev)
+    fold = torch.empty(wl.n, dtype=torch.int32, device=dev)
+    unfold = torch.empty(wl.n, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int32, device=dev)
+    dws = torch.empty(L.oit_delta_workspace_bytes(wl.n), dtype=torch.uint8, device=dev)
+    L.oit_active_set_delta(wl.bits0, bits_new, wl.n, fold, cnt[0:1], unfold, cnt[1:2], dws)
+    nf, nu = (int(x) for x in cnt.cpu().numpy())
+    cap = wl.score_cap
+    rws = torch.empty(L.oit_reconcile_workspace_bytes(wl.cams[0], nf + nu, cap), dtype=torch.uint8, device=dev)
+    npairs = torch.zeros(1, dtype=torch.int64, device=dev)
+    scratch = torch.empty_like(wl.caches[0])
+    pipe = ViewPipeline(wl.cams[0], wl.n, cap, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2 * wl.V)]
+    rec_ms, rr_ms = [], []
+    max_diff = 0.0
+    for rep in range(args.warmup + args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        for v, cam in enumerate(wl.cams):
+            scratch.copy_(wl.caches[v])
+            ev[2 * v][0].record()
+            L.oit_active_set_delta(wl.bits0, bits_new, wl.n, fold, cnt[0:1], unfold, cnt[1:2], dws)
+            L.oit_reconcile_cache(wl.rows, wl.sigma, cam, fold[:nf], unfold[:nu], scratch, cap, npairs, rws)
+            ev[2 * v][1].record()
+            pipe.set_camera(cam)
+            ev[2 * v + 1][0].record()
+            _, st = pipe.forward(wl.rows, wl.sigma, ina_new, wl.bg, image=False)
+            ev[2 * v + 1][1].record()
+            if rep == 0 and v < 4:   # sanity (GPU vs GPU; parity is tests/test_gpu_parity.py)
+                d = (scratch - st).abs() / (st.abs() + 1e-3)
+                max_diff = max(max_diff, float(d.max()))
+        torch.cuda.synchronize()
+        if rep >= args.warmup:
+            rec_ms.append(sum(event_ms(*ev[2 * v]) for v in range(wl.V)))
+            rr_ms.append(sum(event_ms(*ev[2 * v + 1]) for v in range(wl.V)))
+    assert npairs.item() <= cap and pipe.pairs_used() <= cap
+    return dict(ms_per_view=float(np.mean(rec_ms)) / wl.V, rerender_ms_per_view=float(np.mean(rr_ms)) / wl.V,
+                n_fold=nf, n_unfold=nu, n_frozen_new=int(ina_new.numel()), max_rel_diff_vs_rerender=max_diff,
+                change="10% of the active set frozen, 2% of the frozen set re-activated (seeded)")
 
 
 def time_e2e(args, torch, dist, wl, step, flush, allred):
@@ -696,6 +756,8 @@ def build_line(args, world, res, results):
         "clocks": res["clocks"], "gpu_launches": res["launches"] * args.steps,
         "sweep": sweep,
     }
+    if "reconcile" in res:
+        line["next1_reconcile"] = res["reconcile"]
     if "e2e" in res:
         e = res["e2e"]
         line["e2e"] = {"value": world * res["V"] * res["H"] * res["W"] / (e["ms"] * 1e-3) / 1e6, "unit": UNIT,

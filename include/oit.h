@@ -245,6 +245,30 @@ int oit_update_active_set(const float* score_grad, const int32_t* score_idx, int
                           int32_t* newly_frozen, int32_t* d_n_frozen, int32_t* newly_active,
                           int32_t* d_n_activated, void* ws, size_t ws_bytes, oit_stream_t stream);
 
+/* ---------------------------------------------------------------------------------------
+ * NEXT-1  lazy pre-render reconciliation (§4.1: "delay the update of the pre-rendered image
+ * … until the pre-rendered image is used"; Alg. 2 BAU P:358).
+ *
+ * oit_active_set_delta: from a view's stamp bitmask `old_bits` and the current `bits` (1 = active,
+ * [⌈n_total/32⌉]), the ascending lists of splats to FOLD into the view's cache (active then,
+ * frozen now) and to UNFOLD from it (frozen then, active now); counts in *d_n_fold / *d_n_unfold
+ * (device int32). Scratch: oit_delta_workspace_bytes(n_total).
+ *
+ * oit_reconcile_cache: brings the cache [5][n_tiles][256] of a view up to date in place, in one
+ * routed pass over the fold ∪ unfold splats: FOLD P̄ += cαw, Q̄ += αw, T̄ *= 1−α; UNFOLD P̄ −= cαw,
+ * Q̄ −= αw, T̄ /= 1−α. n_fold / n_unfold are host counts. Pair overflow as in oit_bin_tiles
+ * (*d_n_pairs). Scratch: oit_reconcile_workspace_bytes(cam, n_fold + n_unfold, pair_capacity).
+ * --------------------------------------------------------------------------------------- */
+size_t oit_delta_workspace_bytes(int32_t n_total);
+int oit_active_set_delta(const uint32_t* old_bits, const uint32_t* bits, int32_t n_total, int32_t* fold_idx,
+                         int32_t* d_n_fold, int32_t* unfold_idx, int32_t* d_n_unfold, void* ws,
+                         size_t ws_bytes, oit_stream_t stream);
+size_t oit_reconcile_workspace_bytes(const oit_camera* cam, int32_t n_splats, int64_t pair_capacity);
+int oit_reconcile_cache(const oit_scene* scene, const oit_camera* cam, const int32_t* fold_idx,
+                        int32_t n_fold, const int32_t* unfold_idx, int32_t n_unfold, float* cache,
+                        int64_t pair_capacity, int64_t* d_n_pairs, void* ws, size_t ws_bytes,
+                        oit_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

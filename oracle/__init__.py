@@ -169,6 +169,17 @@ def render(rows32, sigma, idx, cam, bg, base=None, route=None, mode: str = "rect
                 contrib_pairs=int(counters[1]))
 
 
+def reconcile(rows32, sigma, cache, fold_idx, unfold_idx, cam):
+    """Lazy pre-render reconciliation (§4.1, NEXT-1): the cache [5,H,W] of the frozen set with
+    the newly frozen splats folded in and the re-activated ones removed (returns a new array)."""
+    rows32 = _f32(rows32)
+    out = _f64(cache).copy()
+    f, u = _i32(fold_idx), _i32(unfold_idx)
+    lib().orc_reconcile(_p(rows32), _p(_f64(rows32)), C.c_double(sigma), _p(f), C.c_int32(len(f)), _p(u),
+                        C.c_int32(len(u)), C.byref(camera(cam)), _p(out))
+    return out
+
+
 def backward(rows32, sigma, idx, cam, bg, state, dL_dC, mode: str = "rect", rows64=None):
     """Analytic backward: Eq. B.2 per (splat, pixel), then the chain rule to
     μ, q, s, o, h, v (Eq. 8 attribute list) and σ. Returns (grad [n,80], dsigma, dcov [n,6])."""

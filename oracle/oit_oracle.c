@@ -509,6 +509,44 @@ void orc_render(const float* rows_dec, const double* rows_val, double sigma, con
     if (counters) { counters[0] = tile_pairs; counters[1] = contrib_pairs; }
 }
 
+/* Lazy pre-render reconciliation (§4.1 P:147 "delay the update of the pre-rendered image", SURVEY
+ * NEXT-1): bring a view's cache of the frozen set [5][H][W] (P_RGB, Q, T; R16) from stage s to the
+ * current stage by adding the splats frozen since s (FOLD: P += cαw, Q += αw, T *= 1-α) and removing
+ * the splats re-activated since s (UNFOLD: P -= cαw, Q -= αw, T /= 1-α). In place, fp64. */
+void orc_reconcile(const float* rows_dec, const double* rows_val, double sigma, const int32_t* fold_idx,
+                   int32_t n_fold, const int32_t* unfold_idx, int32_t n_unfold, const orc_camera* cam,
+                   double* cache) {
+    int Wd = cam->width, H = cam->height;
+    size_t np = (size_t)Wd * H;
+    for (int pass = 0; pass < 2; pass++) {
+        const int32_t* idx = pass == 0 ? fold_idx : unfold_idx;
+        int32_t n = pass == 0 ? n_fold : n_unfold;
+        for (int32_t k = 0; k < n; k++) {
+            int32_t i = idx[k];
+            orc_spec s;
+            orc_spec_project(rows_dec + (size_t)i * ROW, cam, &s);
+            if (!s.visible) continue;
+            orc_val v;
+            orc_value_project(rows_val + (size_t)i * ROW, sigma, cam, &v);
+            for (int py = s.y0 * 16; py < (s.y1 * 16 < H ? s.y1 * 16 : H); py++)
+                for (int px = s.x0 * 16; px < (s.x1 * 16 < Wd ? s.x1 * 16 : Wd); px++) {
+                    if (!orc_spec_tile_keep(&s, px / 16, py / 16, Wd, H)) continue;
+                    int contrib, clamped;
+                    spec_pixel(&s, px, py, &contrib, &clamped);
+                    if (!contrib) continue;
+                    double dx, dy;
+                    double alpha = value_alpha(&v, px, py, clamped, &dx, &dy);
+                    size_t p = (size_t)py * Wd + px;
+                    double aw = alpha * v.w, sg = pass == 0 ? 1.0 : -1.0;
+                    for (int c = 0; c < 3; c++) cache[c * np + p] += sg * v.col[c] * aw;
+                    cache[3 * np + p] += sg * aw;
+                    if (pass == 0) cache[4 * np + p] *= (1.0 - alpha);
+                    else cache[4 * np + p] /= (1.0 - alpha);
+                }
+        }
+    }
+}
+
 /* 2D gradient accumulators of one splat in one view. */
 typedef struct {
     double gc[3], gw, go;          /* dL/dcolour, dL/dw, dL/do */

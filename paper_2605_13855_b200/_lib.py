@@ -83,6 +83,10 @@ def lib() -> C.CDLL:
             "oit_score_subsample": (C.c_int, [scene_p, cam_p, i32, vp, vp, vp, i32, vp, i32, vp, i32, i32, vp, f32,
                                               vp, vp, i64, vp, vp, sz, vp]),
             "oit_update_workspace_bytes": (sz, [i32]),
+            "oit_delta_workspace_bytes": (sz, [i32]),
+            "oit_active_set_delta": (C.c_int, [vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]),
+            "oit_reconcile_workspace_bytes": (sz, [cam_p, i32, i64]),
+            "oit_reconcile_cache": (C.c_int, [scene_p, cam_p, vp, i32, vp, i32, vp, i64, vp, vp, sz, vp]),
             "oit_update_active_set": (C.c_int, [vp, vp, i32, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         }
         for name, (res, args) in sig.items():
@@ -96,7 +100,8 @@ def lib() -> C.CDLL:
 EXPORTED = ["oit_status_string", "oit_num_tiles", "oit_project_cull", "oit_bin_workspace_bytes", "oit_bin_tiles",
             "oit_fwd_workspace_bytes", "oit_composite_fwd", "oit_composite_fwd_ex", "oit_loss_grad", "oit_bwd_workspace_bytes", "oit_composite_bwd", "oit_composite_bwd_ex",
             "oit_select_views", "oit_score_workspace_bytes", "oit_score_subsample", "oit_update_workspace_bytes",
-            "oit_update_active_set"]
+            "oit_update_active_set", "oit_delta_workspace_bytes", "oit_active_set_delta",
+            "oit_reconcile_workspace_bytes", "oit_reconcile_cache"]
 
 
 # ------------------------------------------------------------------ marshalling helpers ---
@@ -236,3 +241,25 @@ def oit_update_active_set(score_grad, score_idx, eps, mode: str, n_total: int, a
                                        _ptr(active_idx), _ptr(n_active), _ptr(newly_frozen), _ptr(n_frozen),
                                        _ptr(newly_active), _ptr(n_activated), _ptr(ws), int(ws.numel()),
                                        _stream(stream)), "oit_update_active_set")
+
+
+def oit_delta_workspace_bytes(n_total: int) -> int:
+    return int(lib().oit_delta_workspace_bytes(int(n_total)))
+
+
+def oit_active_set_delta(old_bits, bits, n_total: int, fold_idx, n_fold, unfold_idx, n_unfold, ws, stream=None):
+    _check(lib().oit_active_set_delta(_ptr(old_bits), _ptr(bits), int(n_total), _ptr(fold_idx), _ptr(n_fold),
+                                      _ptr(unfold_idx), _ptr(n_unfold), _ptr(ws), int(ws.numel()), _stream(stream)),
+           "oit_active_set_delta")
+
+
+def oit_reconcile_workspace_bytes(cam, n_splats: int, pair_capacity: int) -> int:
+    return int(lib().oit_reconcile_workspace_bytes(C.byref(camera(cam)), int(n_splats), int(pair_capacity)))
+
+
+def oit_reconcile_cache(rows, sigma, cam, fold_idx, unfold_idx, cache, pair_capacity: int, n_pairs, ws, stream=None):
+    sc = scene(rows, sigma)
+    nf, nu = int(fold_idx.numel()), int(unfold_idx.numel())
+    _check(lib().oit_reconcile_cache(C.byref(sc), C.byref(camera(cam)), _ptr(fold_idx) if nf else None, nf,
+                                     _ptr(unfold_idx) if nu else None, nu, _ptr(cache), int(pair_capacity),
+                                     _ptr(n_pairs), _ptr(ws), int(ws.numel()), _stream(stream)), "oit_reconcile_cache")

@@ -272,4 +272,65 @@ int oit_update_active_set(const float* score_grad, const int32_t* score_idx, int
   return launch_status();
 }
 
+size_t oit_delta_workspace_bytes(int32_t n_total) { return n_total < 0 ? 0 : delta_ws_bytes(n_total); }
+
+int oit_active_set_delta(const uint32_t* old_bits, const uint32_t* bits, int32_t n_total, int32_t* fold_idx,
+                         int32_t* d_n_fold, int32_t* unfold_idx, int32_t* d_n_unfold, void* ws, size_t ws_bytes,
+                         oit_stream_t stream) {
+  if (n_total < 0 || !d_n_fold || !d_n_unfold || !ws) return OIT_EINVAL;
+  if (n_total > 0 && (!old_bits || !bits || !fold_idx || !unfold_idx)) return OIT_EINVAL;
+  if (((int64_t)n_total + 31) / 32 > kMaxScan) return OIT_ESHAPE;
+  if (ws_bytes < oit_delta_workspace_bytes(n_total)) return OIT_ECAPACITY;
+  launch_delta(old_bits, bits, n_total, fold_idx, d_n_fold, unfold_idx, d_n_unfold, ws, S(stream));
+  return launch_status();
+}
+
+static size_t reconcile_layout(void* ws, const oit_camera* cam, int32_t n, int64_t cap, int32_t** idx,
+                               uint8_t** route, float** rec, int32_t** tps, int32_t** pairs, int32_t** offs,
+                               void** bin_ws) {
+  const int32_t nt = oit_num_tiles(cam);
+  Carve cv(ws);
+  *idx = cv.take<int32_t>((size_t)n + 1);
+  *route = cv.take<uint8_t>((size_t)n + 1);
+  *rec = cv.take<float>(((size_t)n + 1) * kRec4 * 4);
+  *tps = cv.take<int32_t>((size_t)n + 1);
+  *pairs = cv.take<int32_t>((size_t)cap + 1);
+  *offs = cv.take<int32_t>((size_t)nt + 1);
+  *bin_ws = cv.take<char>(bin_ws_bytes(nt));
+  return cv.off;
+}
+
+size_t oit_reconcile_workspace_bytes(const oit_camera* cam, int32_t n_splats, int64_t pair_capacity) {
+  if (!cam || n_splats < 0 || pair_capacity < 0) return 0;
+  int32_t* a; uint8_t* b; float* c; int32_t *d, *e, *f; void* g;
+  return reconcile_layout(nullptr, cam, n_splats, pair_capacity, &a, &b, &c, &d, &e, &f, &g);
+}
+
+int oit_reconcile_cache(const oit_scene* scene, const oit_camera* cam, const int32_t* fold_idx, int32_t n_fold,
+                        const int32_t* unfold_idx, int32_t n_unfold, float* cache, int64_t pair_capacity,
+                        int64_t* d_n_pairs, void* ws, size_t ws_bytes, oit_stream_t stream) {
+  if (!scene || !scene->rows || !scene->sigma || !cam_ok(cam) || !cache || !d_n_pairs || !ws) return OIT_EINVAL;
+  if (n_fold < 0 || n_unfold < 0 || pair_capacity < 0) return OIT_EINVAL;
+  if ((n_fold > 0 && !fold_idx) || (n_unfold > 0 && !unfold_idx)) return OIT_EINVAL;
+  if (!shape_ok(cam) || n_fold + n_unfold > 2 * scene->n || oit_num_tiles(cam) > kMaxScan) return OIT_ESHAPE;
+  const int32_t n = n_fold + n_unfold;
+  if (ws_bytes < oit_reconcile_workspace_bytes(cam, n, pair_capacity)) return OIT_ECAPACITY;
+  int32_t *idx, *tps, *pairs, *offs;
+  uint8_t* route;
+  float* rec;
+  void* bin_ws;
+  reconcile_layout(ws, cam, n, pair_capacity, &idx, &route, &rec, &tps, &pairs, &offs, &bin_ws);
+  cudaStream_t st = S(stream);
+  if (n_fold) cudaMemcpyAsync(idx, fold_idx, sizeof(int32_t) * n_fold, cudaMemcpyDeviceToDevice, st);
+  if (n_unfold) cudaMemcpyAsync(idx + n_fold, unfold_idx, sizeof(int32_t) * n_unfold, cudaMemcpyDeviceToDevice, st);
+  if (n_fold) cudaMemsetAsync(route, 1, n_fold, st);
+  if (n_unfold) cudaMemsetAsync(route + n_fold, 2, n_unfold, st);
+  DevCam dc = dev_cam(cam);
+  launch_project(dc, scene->rows, scene->sigma, idx, n, rec, tps, st);
+  launch_bin(dc, rec, tps, n, pairs, pair_capacity, offs, d_n_pairs, nullptr, bin_ws, st);
+  launch_composite_fwd(dc, rec, pairs, offs, pair_capacity, cache, route, nullptr, nullptr, cache, st, nullptr,
+                       nullptr);
+  return launch_status();
+}
+
 }  // extern "C"

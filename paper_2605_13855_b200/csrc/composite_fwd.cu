@@ -184,9 +184,10 @@ template <bool kRoute, bool kBase, bool kCount>
 __global__ void __launch_bounds__(256) k_fwd(DevCam cam, const float4* __restrict__ rec,
                                              const int32_t* __restrict__ pair_slot,
                                              const int32_t* __restrict__ offs, int64_t capacity,
-                                             const float* __restrict__ base, const uint8_t* __restrict__ route,
+                                             const float* base, const uint8_t* __restrict__ route,
                                              float* __restrict__ image, float* __restrict__ state,
                                              float* base_out, unsigned long long* __restrict__ counters) {
+  // base_out may alias base (in-place reconciliation): each thread reads its pixel before writing it
   int n_contrib = 0;
   __shared__ float4 s_q0[256], s_q1[256], s_q2[256];
   __shared__ float2 s_k[256];
@@ -239,12 +240,18 @@ __global__ void __launch_bounds__(256) k_fwd(DevCam cam, const float4* __restric
         P2 = fmaf(q2.z, aw, P2);
         Q += aw;
         T = fmaf(-alpha, T, T);
-        if (kRoute && s_route[i] == 1) {
+        if (kRoute && s_route[i] == 1) {         // FOLD: bake into the pre-render (BAU)
           B0 = fmaf(q2.x, aw, B0);
           B1 = fmaf(q2.y, aw, B1);
           B2 = fmaf(q2.z, aw, B2);
           BQ += aw;
           BT = fmaf(-alpha, BT, BT);
+        } else if (kRoute && s_route[i] == 2) {  // UNFOLD: remove a re-activated splat
+          B0 = fmaf(-q2.x, aw, B0);
+          B1 = fmaf(-q2.y, aw, B1);
+          B2 = fmaf(-q2.z, aw, B2);
+          BQ -= aw;
+          BT = BT / (1.0f - alpha);
         }
       }
     }

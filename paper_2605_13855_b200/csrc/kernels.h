@@ -77,6 +77,9 @@ void launch_loss_grad(const DevCam& cam, const float* image, const float* target
 void launch_fps(const float* centers, int32_t V, int32_t S, uint64_t seed, uint32_t refresh, int32_t* out,
                 cudaStream_t st);
 size_t update_ws_bytes(int32_t n_total);
+size_t delta_ws_bytes(int32_t n_total);
+void launch_delta(const uint32_t* old_bits, const uint32_t* bits, int32_t n_total, int32_t* fold, int32_t* d_n_fold,
+                  int32_t* unfold, int32_t* d_n_unfold, void* ws, cudaStream_t st);
 void launch_update(const float* score_grad, const int32_t* score_idx, int32_t n_score, const float eps[6],
                    int32_t mode, int32_t n_total, uint32_t* bits, int32_t* active_idx, int32_t* d_n_active,
                    int32_t* frozen, int32_t* d_n_frozen, int32_t* activated, int32_t* d_n_activated, void* ws,

@@ -182,9 +182,35 @@ __global__ void k_emit3(const uint32_t* __restrict__ old_bits, const uint32_t* _
   if (w >= nw) return;
   uint32_t m = word_mask(w, n_total);
   uint32_t o = old_bits[w] & m, b = bits[w] & m;
-  emit_bits(b, w * 32, active_idx, oa[w]);
+  if (active_idx) emit_bits(b, w * 32, active_idx, oa[w]);
   if (frozen) emit_bits(o & ~b, w * 32, frozen, of_[w]);
   if (activated) emit_bits(b & ~o, w * 32, activated, on[w]);
+}
+
+// Delta between two active-set bitmasks (NEXT-1): splats frozen since `old` (active then, inactive
+// now: to FOLD into a view's cache) and re-activated since `old` (to UNFOLD), ascending.
+void launch_delta(const uint32_t* old_bits, const uint32_t* bits, int32_t n_total, int32_t* fold, int32_t* d_n_fold,
+                  int32_t* unfold, int32_t* d_n_unfold, void* ws, cudaStream_t st) {
+  const int nw = (n_total + 31) / 32;
+  Carve cv(ws);
+  int32_t* ca = cv.take<int32_t>(nw);
+  int32_t* cf = cv.take<int32_t>(nw);
+  int32_t* cn = cv.take<int32_t>(nw);
+  int32_t* of_ = cv.take<int32_t>(nw + 1);
+  int32_t* on = cv.take<int32_t>(nw + 1);
+  void* tmp = cv.take<char>(scan_tmp_bytes(nw));
+  const int wb = (nw + 255) / 256;
+  if (nw > 0) k_popc3<<<wb, 256, 0, st>>>(old_bits, bits, nw, n_total, ca, cf, cn);
+  launch_exclusive_scan(cf, of_, nw, tmp, st);
+  launch_exclusive_scan(cn, on, nw, tmp, st);
+  if (nw > 0) k_emit3<<<wb, 256, 0, st>>>(old_bits, bits, nw, n_total, of_, of_, on, nullptr, fold, unfold);
+  cudaMemcpyAsync(d_n_fold, of_ + nw, sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(d_n_unfold, on + nw, sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
+}
+
+size_t delta_ws_bytes(int32_t n_total) {
+  int64_t nw = ((int64_t)n_total + 31) / 32;
+  return 3 * align_up(nw * 4) + 2 * align_up((nw + 1) * 4) + scan_tmp_bytes(nw);
 }
 
 size_t update_ws_bytes(int32_t n_total) {

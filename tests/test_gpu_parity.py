@@ -448,3 +448,65 @@ def test_fused_loss_backward_equals_two_step(loss):
     gr, _, _, bnd = O.backward_bound(sc.rows, sc.sigma, idx, cam, sc.bg, ref["state"], gref)
     ok, bad = grad_close(out[1], gr, bnd, atol=1e-6 / (3 * cam["width"] * cam["height"]))
     assert ok, describe_bad(out[1], gr, bad, bnd)
+
+
+# ------------------------------------------------------------------ NEXT-1 reconcile ------
+def _state_close(got, ref, rtol=2e-4, frac=1e-5):
+    """Pixel-state bar (as test_composite_fwd_parity) plus a per-channel floor for the P̄/Q̄
+    channels, whose UNFOLD subtraction cancels against the stored sum."""
+    scale = np.abs(ref).reshape(5, -1).max(1)[:, None, None] * frac
+    return np.abs(got - ref) <= rtol * np.abs(ref) + scale + 1e-7
+
+
+def test_reconcile_cache_three_stages():
+    """§4.1 P:147 lazy pre-render: a view's cache stamped at stage s is brought to stage s+1 by the
+    active-set delta (FOLD newly frozen, UNFOLD re-activated) instead of a re-render; the result
+    equals the oracle's from-scratch render of the new frozen set, and the active set composited over
+    it equals the full render. The delta lists are bit-exact; an empty delta leaves the cache as is."""
+    L = _L()
+    sc = SCENES[1]
+    cam = sc.cams[1]
+    W, H = cam["width"], cam["height"]
+    rows, sigma = _t(sc.rows), _t(np.array([sc.sigma], np.float32))
+    g = synth.rng(31)
+    masks = [synth.active_mask(sc, 0.2, "clustered")]
+    for s in range(2):                      # freeze ~30 % of the active set, re-activate ~3 % of the rest
+        m = masks[-1].copy()
+        m[np.flatnonzero(m)[g.random(m.sum()) < 0.3]] = False
+        m[np.flatnonzero(~masks[-1])[g.random((~masks[-1]).sum()) < 0.03]] = True
+        masks.append(m)
+    masks.append(masks[-1].copy())          # stage 3: no change
+    oc = O.render(sc.rows, sc.sigma, np.flatnonzero(~masks[0]), cam, sc.bg)["state"]
+    cache = _t(plain_to_tile_major(oc, W, H).astype(np.float32))
+    ref_cache = oc
+    n = sc.n
+    fold = torch.empty(n, dtype=torch.int32, device=DEV)
+    unfold = torch.empty(n, dtype=torch.int32, device=DEV)
+    cnt = torch.zeros(2, dtype=torch.int32, device=DEV)
+    dws = torch.empty(L.oit_delta_workspace_bytes(n), dtype=torch.uint8, device=DEV)
+    p = _pipe(cam, n)
+    for s in range(1, len(masks)):
+        old_bits, bits = synth.bits_from_mask(masks[s - 1]), synth.bits_from_mask(masks[s])
+        L.oit_active_set_delta(_t(old_bits.view(np.int32)), _t(bits.view(np.int32)), n, fold, cnt[0:1], unfold,
+                               cnt[1:2], dws)
+        nf, nu = cnt.cpu().numpy()
+        ref_f = np.flatnonzero(masks[s - 1] & ~masks[s]).astype(np.int32)
+        ref_u = np.flatnonzero(~masks[s - 1] & masks[s]).astype(np.int32)
+        assert np.array_equal(fold[:nf].cpu().numpy(), ref_f) and np.array_equal(unfold[:nu].cpu().numpy(), ref_u)
+        cap = 1 << 20
+        ws = torch.empty(L.oit_reconcile_workspace_bytes(cam, int(nf + nu), cap), dtype=torch.uint8, device=DEV)
+        npairs = torch.zeros(1, dtype=torch.int64, device=DEV)
+        before = cache.clone()
+        L.oit_reconcile_cache(rows, sigma, cam, fold[:nf], unfold[:nu], cache, cap, npairs, ws)
+        got = tile_major_to_plain(cache.cpu().numpy(), W, H)
+        if nf + nu == 0:
+            assert torch.equal(cache, before)
+        ref_cache = O.reconcile(sc.rows, sc.sigma, ref_cache, ref_f, ref_u, cam)
+        scratch = O.render(sc.rows, sc.sigma, np.flatnonzero(~masks[s]), cam, sc.bg)["state"]
+        assert np.allclose(ref_cache, scratch, rtol=1e-9, atol=1e-12)     # oracle: reconcile == re-render
+        ok = _state_close(got, scratch)
+        assert ok.all(), (s, (~ok).sum(), np.abs(got - scratch).max())
+        img, _ = p.forward(rows, sigma, _t(np.flatnonzero(masks[s]).astype(np.int32)), sc.bg, base=cache)
+        ref = O.render(sc.rows, sc.sigma, np.arange(n), cam, sc.bg)["image"]
+        assert np.abs(img.cpu().numpy() - ref).max() < 1e-5, s
+        assert s == 3 or nf > 0 and nu > 0

@@ -505,3 +505,24 @@ def test_backward_bound_dominates_gradient():
     assert np.array_equal(grad, gplain)
     assert np.all(bnd >= np.abs(grad) * (1 - 1e-12))
     assert (bnd > 10 * np.abs(grad)).any()      # cancellation exists in real scenes
+
+
+def test_reconcile_folds_and_unfolds_exactly():
+    """NEXT-1 (§4.1): a cache reconciled over 3 stages (folds of newly frozen splats, unfolds
+    of re-activated ones) equals a from-scratch render of the final frozen set (fp64)."""
+    sc = synth.scene_c1()
+    cam = sc.cams[1]
+    g = np.random.default_rng(8)
+    frozen = g.random(sc.n) < 0.5
+    cache = O.render(sc.rows, sc.sigma, np.flatnonzero(frozen), cam, sc.bg)["state"]
+    for _ in range(3):
+        nxt = frozen.copy()
+        flip = g.random(sc.n) < 0.15
+        nxt[flip] = ~nxt[flip]
+        fold = np.flatnonzero(nxt & ~frozen)
+        unfold = np.flatnonzero(frozen & ~nxt)
+        cache = O.reconcile(sc.rows, sc.sigma, cache, fold, unfold, cam)
+        frozen = nxt
+        assert len(fold) and len(unfold)
+    ref = O.render(sc.rows, sc.sigma, np.flatnonzero(frozen), cam, sc.bg)["state"]
+    assert np.abs(cache - ref).max() < 1e-10
