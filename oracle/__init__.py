@@ -275,3 +275,30 @@ def score_subsample(rows32, sigma, cams, targets, caches, active_idx, score_idx,
     if with_bound:
         return acc / len(views), dsig / len(views), bnd / len(views)
     return acc / len(views), dsig / len(views)
+
+
+ADAM_LR_3DGS = {"mu": 1.6e-4, "o": 0.01, "q": 1e-3, "s": 5e-3, "v": 0.005, "h_dc": 2.5e-3, "h_rest": 2.5e-3 / 20,
+                "sigma": 0.1}
+ADAM_LR_KEYS = ("mu", "o", "q", "s", "v", "h_dc", "h_rest", "sigma")
+
+
+def adam_step(grad, active_idx, latent, m, v, step, dsigma=0.0, sig_state=None, lr=None, beta1=0.9, beta2=0.999,
+              eps=1e-15):
+    """NEXT-2: masked Adam (Kingma & Ba, Alg. 1) on the compacted active rows, per-splat step
+    counts, with the activations of R25/R33 (Alg. 1 l.6 P:162). Inputs are copied; returns
+    (latent, m, v, step, rows_physical, sig_state, sigma) as fp64 / int32 arrays."""
+    lr = dict(ADAM_LR_3DGS if lr is None else lr)
+    lrv = np.array([lr[k] for k in ADAM_LR_KEYS], np.float64)
+    grad = _f64(grad).reshape(-1, ROW)
+    idx = _i32(active_idx)
+    lat, mm, vv = (_f64(x).reshape(-1, ROW).copy() for x in (latent, m, v))
+    st = np.ascontiguousarray(step, dtype=np.int32).copy()
+    rows = lat.copy()                 # frozen rows: the physical row of the unchanged latent
+    rows[:, 3] = 1.0 / (1.0 + np.exp(-lat[:, 3]))
+    rows[:, 8:11] = np.exp(lat[:, 8:11])
+    ss = None if sig_state is None else _f64(sig_state).copy()
+    sig_out = np.zeros(1)
+    lib().orc_adam_step(_p(grad), _p(idx), C.c_int32(len(idx)), _p(lat), _p(mm), _p(vv), _p(st), _p(rows),
+                        C.c_double(float(dsigma)), _p(ss) if ss is not None else None, _p(sig_out), _p(lrv),
+                        C.c_double(beta1), C.c_double(beta2), C.c_double(eps))
+    return lat, mm, vv, st, rows, ss, (float(sig_out[0]) if ss is not None else None)

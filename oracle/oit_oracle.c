@@ -897,3 +897,70 @@ void orc_update_active(const float* score_grad, const int32_t* score_idx, int32_
     n_out[0] = na; n_out[1] = nf; n_out[2] = nn;
     free(old);
 }
+
+/* ---- NEXT-2: masked Adam on the compacted active rows, with the parameter activations ----
+ * P:220 "We use Adam for parameter optimization … learning rates 0.01 for o, 0.1 for σ, 0.005
+ * for v, with all other settings following the original 3DGS"; Alg. 1 l.6 P:162 (the update
+ * touches 𝒢_𝒜 only). Adam as Kingma & Ba (Alg. 1): per element, with the splat's own step count
+ * t (frozen splats do not advance, R33):
+ *   m ← β1 m + (1−β1) g;  v ← β2 v + (1−β2) g²;  m̂ = m/(1−β1^t);  v̂ = v/(1−β2^t);
+ *   ℓ ← ℓ − lr·m̂/(√v̂ + ε).
+ * The optimiser holds latent values ℓ; the physical row (what the renderer reads, R25) is
+ * μ = ℓ_μ, o = 1/(1+e^(−ℓ_o)), q = ℓ_q (normalised inside the projection), s = e^(ℓ_s), v = ℓ_v,
+ * h = ℓ_h, σ = e^(ℓ_σ); g is the gradient of the physical row pushed through these maps at the
+ * latent value before the update: g_ℓo = g_o·o(1−o), g_ℓs = g_s·s, g_ℓσ = g_σ·σ.
+ * lr[8] = {μ, o, q, s, v, h_dc, h_rest, σ}; pads (fields 11, 76-79) have lr 0.
+ * sig_state = {ℓ_σ, m_σ, v_σ, t_σ}: σ is shared and always advances. */
+static double adam_lr_of(int f, const double* lr) {
+    if (f < R_O) return lr[0];
+    if (f == R_O) return lr[1];
+    if (f < R_S) return lr[2];
+    if (f < R_S + 3) return lr[3];
+    if (f < R_V) return 0.0;
+    if (f < R_H) return lr[4];
+    if (f < R_H + 3) return lr[5];
+    if (f < R_H + 48) return lr[6];
+    return 0.0;
+}
+
+static double adam_one(double* l, double* m, double* v, double g, int32_t t, double lr, double b1, double b2,
+                       double eps) {
+    *m = b1 * *m + (1.0 - b1) * g;
+    *v = b2 * *v + (1.0 - b2) * g * g;
+    double mh = *m / (1.0 - pow(b1, (double)t));
+    double vh = *v / (1.0 - pow(b2, (double)t));
+    *l = *l - lr * mh / (sqrt(vh) + eps);
+    return *l;
+}
+
+static double act_of(int f, double l) {
+    if (f == R_O) return 1.0 / (1.0 + exp(-l));
+    if (f >= R_S && f < R_S + 3) return exp(l);
+    return l;
+}
+
+void orc_adam_step(const double* grad, const int32_t* active_idx, int32_t n_active, double* latent, double* m,
+                   double* v, int32_t* step, double* rows_out, double dsigma, double* sig_state, double* sigma_out,
+                   const double* lr, double beta1, double beta2, double eps) {
+    for (int32_t k = 0; k < n_active; k++) {
+        int32_t i = active_idx[k];
+        int32_t t = step[i] + 1;
+        step[i] = t;
+        for (int f = 0; f < ROW; f++) {
+            size_t e = (size_t)i * ROW + f;
+            double gp = grad[(size_t)k * ROW + f];
+            double g = gp;
+            if (f == R_O) { double o = act_of(f, latent[e]); g = gp * o * (1.0 - o); }
+            else if (f >= R_S && f < R_S + 3) g = gp * act_of(f, latent[e]);
+            adam_one(&latent[e], &m[e], &v[e], g, t, adam_lr_of(f, lr), beta1, beta2, eps);
+            rows_out[e] = act_of(f, latent[e]);
+        }
+    }
+    if (sig_state) {
+        int32_t t = (int32_t)sig_state[3] + 1;
+        sig_state[3] = t;
+        double g = dsigma * exp(sig_state[0]);
+        adam_one(&sig_state[0], &sig_state[1], &sig_state[2], g, t, lr[7], beta1, beta2, eps);
+        *sigma_out = exp(sig_state[0]);
+    }
+}
