@@ -42,6 +42,18 @@ BWD_F_TEST, BWD_F_CONTRIB = 9, 32
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: 148 SMs × 128 FP32 lanes × FMA × 1965 MHz
 
 
+def _hbm_peak():
+    """Measured copy bandwidth (MEASURED_PEAKS.json, driver-written), else the guide's fallback."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"
+    except Exception:
+        return 7700.0, "B200_PROFILING.md nominal 7.7 TB/s (MEASURED_PEAKS.json absent)"
+
+
+HBM_PEAK_GBS, HBM_PEAK_SOURCE = _hbm_peak()
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -58,6 +70,7 @@ def parse():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-adam", action="store_true", help="skip the NEXT-2 Adam measurement")
     ap.add_argument("--no-reconcile", action="store_true", help="skip the NEXT-1 reconciliation measurement")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--profile-once", action="store_true", help="run one eager step (for ncu) and exit")
@@ -580,7 +593,48 @@ def time_workload(args, torch, dist, wl, world, headline_run):
         res["e2e"] = time_e2e(args, torch, dist, wl, step, flush, allred)
     if headline_run and not args.no_reconcile and wl.n_ina > 0:
         res["reconcile"] = time_reconcile(args, torch, wl, flush)
+    if headline_run and not args.no_adam:
+        res["adam"] = time_adam(args, torch, wl, flush)
     return res
+
+
+ADAM_BYTES_PER_ROW = 4 * 320 + 4 * 320 + 4 + 4 + 4   # read g, ℓ, m, v; write ℓ, m, v, row; idx, step r/w
+
+
+def time_adam(args, torch, wl, flush):
+    """NEXT-2: one oit_adam_step over the step's compacted active gradient rows (n_A rows, state
+    for all N splats), event-timed on its stream after an L2 flush; HBM roofline against the
+    measured copy bandwidth (algorithmic bytes: grad/latent/m/v read, latent/m/v/rows written,
+    index and step count)."""
+    L, dev = wl.L, wl.dev
+    g = torch.Generator(device=dev)
+    g.manual_seed(77)
+    lat = torch.randn((wl.n, 80), generator=g, device=dev) * 0.5
+    m = torch.zeros_like(lat)
+    v = torch.zeros_like(lat)
+    step = torch.zeros(wl.n, dtype=torch.int32, device=dev)
+    rows = torch.empty_like(lat)
+    sig = torch.tensor([np.log(4.8), 0.0, 0.0, 0.0], dtype=torch.float32, device=dev)
+    sig_out = torch.zeros(1, dtype=torch.float32, device=dev)
+    cfg = L.adam_cfg()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
+    for rep in range(args.warmup + max(args.steps, 5)):
+        flush.zero_()
+        flush.sum()          # read back: the flush's dirty lines are written back before timing
+        torch.cuda.synchronize()
+        t0.record()
+        L.oit_adam_step(wl.grad, wl.act, lat, m, v, step, rows, cfg, dsigma=wl.dsig, sigma_state=sig, sigma=sig_out)
+        t1.record()
+        torch.cuda.synchronize()
+        if rep >= args.warmup:
+            times.append(t0.elapsed_time(t1))
+    ms = float(np.mean(times))
+    nbytes = wl.n_act * ADAM_BYTES_PER_ROW
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    return {"ms": ms, "rows": wl.n_act, "bytes": nbytes,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": HBM_PEAK_GBS, "unit": "GB/s",
+                         "frac": gbs / HBM_PEAK_GBS, "peak_source": HBM_PEAK_SOURCE}}
 
 
 def time_reconcile(args, torch, wl, flush):
@@ -756,6 +810,8 @@ def build_line(args, world, res, results):
         "clocks": res["clocks"], "gpu_launches": res["launches"] * args.steps,
         "sweep": sweep,
     }
+    if "adam" in res:
+        line["next2_adam"] = res["adam"]
     if "reconcile" in res:
         line["next1_reconcile"] = res["reconcile"]
     if "e2e" in res:

@@ -269,6 +269,32 @@ int oit_reconcile_cache(const oit_scene* scene, const oit_camera* cam, const int
                         int64_t pair_capacity, int64_t* d_n_pairs, void* ws, size_t ws_bytes,
                         oit_stream_t stream);
 
+/* ---------------------------------------------------------------------------------------
+ * NEXT-2  oit_adam_step — masked Adam on the compacted active rows, fused with the parameter
+ * activations ("We use Adam … learning rates 0.01 for o, 0.1 for σ, 0.005 for v, all other
+ * settings following the original 3DGS"; Alg. 1 l.6 P:162: only 𝒢_𝒜 is updated; R33).
+ *
+ * The optimiser state is latent: latent/m/v [N][80] fp32 (row layout of DESIGN.md §2) with
+ * μ, q, v, h stored as is, ℓ_o = logit(o), ℓ_s = log(s); step [N] int32 per-splat Adam step counts.
+ * For k < n (n = min(*d_n_active, n_active) when d_n_active is non-NULL, else n_active), splat
+ * i = active_idx[k] (distinct) takes gradient row grad[k] — the gradient w.r.t. its PHYSICAL row as
+ * oit_composite_bwd writes it — and: t = ++step[i]; g_ℓ = g·(∂physical/∂ℓ) at the old latent
+ * (o(1−o) for o, s for s, 1 otherwise); m ← β1m + (1−β1)g_ℓ; v ← β2v + (1−β2)g_ℓ²;
+ * ℓ ← ℓ − lr·(m/(1−β1^t)) / (√(v/(1−β2^t)) + ε); rows[i] ← physical(ℓ) (sigmoid o, exp s, the rest
+ * as is). Rows not in the list are not touched. cfg->lr[8] = {μ, o, q, s, v, h_dc, h_rest, σ}
+ * (padding fields get lr 0). σ (optional, all three or none): sigma_state [4] = {log σ, m, v, t}
+ * (16-B aligned, t as float), dsigma the device scalar ∂L/∂σ; σ always advances and *sigma is
+ * written = exp(log σ). All pointers device, 16-B aligned rows.
+ * --------------------------------------------------------------------------------------- */
+typedef struct {
+    float lr[8];
+    float beta1, beta2, eps;
+} oit_adam_cfg;
+
+int oit_adam_step(const float* grad, const int32_t* active_idx, int32_t n_active, const int32_t* d_n_active,
+                  float* latent, float* m, float* v, int32_t* step, float* rows, const float* dsigma,
+                  float* sigma_state, float* sigma, const oit_adam_cfg* cfg, oit_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

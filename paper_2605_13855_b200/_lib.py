@@ -51,6 +51,10 @@ def camera(cam: dict) -> Camera:
     return c
 
 
+class AdamCfg(C.Structure):
+    _fields_ = [("lr", C.c_float * 8), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float)]
+
+
 _lib = None
 
 
@@ -87,6 +91,7 @@ def lib() -> C.CDLL:
             "oit_active_set_delta": (C.c_int, [vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]),
             "oit_reconcile_workspace_bytes": (sz, [cam_p, i32, i64]),
             "oit_reconcile_cache": (C.c_int, [scene_p, cam_p, vp, i32, vp, i32, vp, i64, vp, vp, sz, vp]),
+            "oit_adam_step": (C.c_int, [vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.POINTER(AdamCfg), vp]),
             "oit_update_active_set": (C.c_int, [vp, vp, i32, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         }
         for name, (res, args) in sig.items():
@@ -101,7 +106,7 @@ EXPORTED = ["oit_status_string", "oit_num_tiles", "oit_project_cull", "oit_bin_w
             "oit_fwd_workspace_bytes", "oit_composite_fwd", "oit_composite_fwd_ex", "oit_loss_grad", "oit_bwd_workspace_bytes", "oit_composite_bwd", "oit_composite_bwd_ex",
             "oit_select_views", "oit_score_workspace_bytes", "oit_score_subsample", "oit_update_workspace_bytes",
             "oit_update_active_set", "oit_delta_workspace_bytes", "oit_active_set_delta",
-            "oit_reconcile_workspace_bytes", "oit_reconcile_cache"]
+            "oit_reconcile_workspace_bytes", "oit_reconcile_cache", "oit_adam_step"]
 
 
 # ------------------------------------------------------------------ marshalling helpers ---
@@ -263,3 +268,25 @@ def oit_reconcile_cache(rows, sigma, cam, fold_idx, unfold_idx, cache, pair_capa
     _check(lib().oit_reconcile_cache(C.byref(sc), C.byref(camera(cam)), _ptr(fold_idx) if nf else None, nf,
                                      _ptr(unfold_idx) if nu else None, nu, _ptr(cache), int(pair_capacity),
                                      _ptr(n_pairs), _ptr(ws), int(ws.numel()), _stream(stream)), "oit_reconcile_cache")
+
+
+ADAM_LR_KEYS = ("mu", "o", "q", "s", "v", "h_dc", "h_rest", "sigma")
+ADAM_LR_3DGS = {"mu": 1.6e-4, "o": 0.01, "q": 1e-3, "s": 5e-3, "v": 0.005, "h_dc": 2.5e-3, "h_rest": 2.5e-3 / 20,
+                "sigma": 0.1}   # P:220 (o, σ, v) + the 3DGS defaults for the rest
+
+
+def adam_cfg(lr=None, beta1=0.9, beta2=0.999, eps=1e-15) -> AdamCfg:
+    lr = dict(ADAM_LR_3DGS if lr is None else lr)
+    c = AdamCfg()
+    for k, key in enumerate(ADAM_LR_KEYS):
+        c.lr[k] = float(lr[key])
+    c.beta1, c.beta2, c.eps = float(beta1), float(beta2), float(eps)
+    return c
+
+
+def oit_adam_step(grad, active_idx, latent, m, v, step, rows, cfg: AdamCfg, n_active=None, d_n_active=None,
+                  dsigma=None, sigma_state=None, sigma=None, stream=None):
+    n = int(active_idx.numel()) if n_active is None else int(n_active)
+    _check(lib().oit_adam_step(_ptr(grad) if n else None, _ptr(active_idx) if n else None, n, _ptr(d_n_active),
+                               _ptr(latent), _ptr(m), _ptr(v), _ptr(step), _ptr(rows), _ptr(dsigma),
+                               _ptr(sigma_state), _ptr(sigma), C.byref(cfg), _stream(stream)), "oit_adam_step")

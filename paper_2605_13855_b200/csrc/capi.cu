@@ -272,6 +272,26 @@ int oit_update_active_set(const float* score_grad, const int32_t* score_idx, int
   return launch_status();
 }
 
+int oit_adam_step(const float* grad, const int32_t* active_idx, int32_t n_active, const int32_t* d_n_active,
+                  float* latent, float* m, float* v, int32_t* step, float* rows, const float* dsigma,
+                  float* sigma_state, float* sigma, const oit_adam_cfg* cfg, oit_stream_t stream) {
+  if (!cfg || n_active < 0) return OIT_EINVAL;
+  if (n_active > 0 && (!grad || !active_idx || !latent || !m || !v || !step || !rows)) return OIT_EINVAL;
+  const int nsig = (dsigma != nullptr) + (sigma_state != nullptr) + (sigma != nullptr);
+  if (nsig != 0 && nsig != 3) return OIT_EINVAL;
+  if (!(cfg->beta1 >= 0.0f && cfg->beta1 < 1.0f && cfg->beta2 >= 0.0f && cfg->beta2 < 1.0f && cfg->eps >= 0.0f))
+    return OIT_EINVAL;
+  for (int k = 0; k < 8; k++)
+    if (!(cfg->lr[k] >= 0.0f)) return OIT_EINVAL;
+  auto misaligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) != 0; };
+  if (misaligned(grad) || misaligned(latent) || misaligned(m) || misaligned(v) || misaligned(rows) ||
+      misaligned(sigma_state))
+    return OIT_EINVAL;
+  launch_adam(grad, active_idx, n_active, d_n_active, latent, m, v, step, rows, dsigma, sigma_state, sigma, cfg->lr,
+              cfg->beta1, cfg->beta2, cfg->eps, S(stream));
+  return launch_status();
+}
+
 size_t oit_delta_workspace_bytes(int32_t n_total) { return n_total < 0 ? 0 : delta_ws_bytes(n_total); }
 
 int oit_active_set_delta(const uint32_t* old_bits, const uint32_t* bits, int32_t n_total, int32_t* fold_idx,

@@ -78,6 +78,11 @@ void launch_fps(const float* centers, int32_t V, int32_t S, uint64_t seed, uint3
                 cudaStream_t st);
 size_t update_ws_bytes(int32_t n_total);
 size_t delta_ws_bytes(int32_t n_total);
+
+// optim.cu — NEXT-2 masked Adam + activations
+void launch_adam(const float* grad, const int32_t* active_idx, int32_t n_cap, const int32_t* d_n, float* latent,
+                 float* m, float* v, int32_t* step, float* rows, const float* dsigma, float* sig_state, float* sigma,
+                 const float lr[8], float beta1, float beta2, float eps, cudaStream_t st);
 void launch_delta(const uint32_t* old_bits, const uint32_t* bits, int32_t n_total, int32_t* fold, int32_t* d_n_fold,
                   int32_t* unfold, int32_t* d_n_unfold, void* ws, cudaStream_t st);
 void launch_update(const float* score_grad, const int32_t* score_idx, int32_t n_score, const float eps[6],

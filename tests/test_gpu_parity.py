@@ -510,3 +510,106 @@ def test_reconcile_cache_three_stages():
         ref = O.render(sc.rows, sc.sigma, np.arange(n), cam, sc.bg)["image"]
         assert np.abs(img.cpu().numpy() - ref).max() < 1e-5, s
         assert s == 3 or nf > 0 and nu > 0
+
+
+# ------------------------------------------------------------------ NEXT-2 Adam ----------
+def _adam_state(n, g):
+    lat = (g.normal(size=(n, 80)) * 0.5).astype(np.float32)
+    lat[:, [11, 76, 77, 78, 79]] = 0.0
+    m = (g.normal(size=(n, 80)) * 1e-2).astype(np.float32)
+    v = (np.abs(g.normal(size=(n, 80))) * 1e-4 + m.astype(np.float64) ** 2).astype(np.float32)
+    step = g.integers(0, 60, size=n).astype(np.int32)
+    m[step == 0] = 0.0
+    v[step == 0] = 0.0
+    return lat, m, v, step
+
+
+def _adam_check(got, ref, lr_f, g_lat):
+    """fp32-rounding bar (R33): moments ≤ 1e-6 of what was summed, latent ≤ 1e-6·|ℓ| +
+    2e-5·lr·|Adam direction|, physical = activation of the latent within its own bar."""
+    lat, m, v, rows = got
+    rl, rm, rv, rrows, u = ref
+    assert np.all(np.abs(m - rm) <= 1e-6 * (np.abs(rm) + np.abs(g_lat)) + 1e-37)
+    assert np.all(np.abs(v - rv) <= 1e-6 * (np.abs(rv) + g_lat ** 2) + 1e-37)
+    bar_l = 1e-6 * np.abs(rl) + 2e-5 * lr_f * (np.abs(u) + 1e-3) + 1e-37
+    assert np.all(np.abs(lat - rl) <= bar_l), np.max(np.abs(lat - rl) / bar_l)
+    assert np.all(np.abs(rows - rrows) <= 2e-6 * np.abs(rrows) + np.maximum(1, np.abs(rrows)) * bar_l)
+
+
+def test_adam_step_parity_masked_and_device_count():
+    L = _L()
+    g = synth.rng(2025)
+    n = 100_003
+    lat, m, v, step = _adam_state(n, g)
+    lr = dict(L.ADAM_LR_3DGS)
+    cfg = L.adam_cfg(lr)
+    lr_f = np.zeros(80)
+    for key, cols in {"mu": range(0, 3), "o": [3], "q": range(4, 8), "s": range(8, 11), "v": range(12, 28),
+                      "h_dc": range(28, 31), "h_rest": range(31, 76)}.items():
+        lr_f[list(cols)] = np.float32(lr[key])
+    b1, b2, eps = float(np.float32(0.9)), float(np.float32(0.999)), float(np.float32(1e-15))
+    d = {k: _t(x) for k, x in dict(lat=lat, m=m, v=v, step=step).items()}
+    rows = torch.full((n, 80), -7.0, dtype=torch.float32, device=DEV)          # sentinel: untouched rows
+    sig = _t(np.array([np.log(4.8), 1e-3, 1e-6, 7.0], np.float32))
+    sig_out = torch.zeros(1, dtype=torch.float32, device=DEV)
+    for call in range(3):
+        mask = g.random(n) < 0.2
+        act = np.flatnonzero(mask).astype(np.int32)
+        gr = (g.normal(size=(len(act), 80)) * 10.0 ** g.integers(-6, 1, size=(len(act), 1))).astype(np.float32)
+        gr[call::7] = 0.0                                                           # some zero-gradient rows
+        dsig = np.float32(g.normal())
+        before = {k: x.cpu().numpy().copy() for k, x in d.items()}
+        rows_before = rows.cpu().numpy().copy()
+        sig_before = sig.cpu().numpy().copy()
+        if call == 1:   # count on the device, larger capacity (the post-refresh graph path)
+            cap_idx = np.concatenate([act, np.zeros(5000, np.int32)])
+            gpad = np.concatenate([gr, np.zeros((5000, 80), np.float32)])
+            L.oit_adam_step(_t(gpad), _t(cap_idx), d["lat"], d["m"], d["v"], d["step"], rows, cfg,
+                            n_active=len(cap_idx), d_n_active=_t(np.array([len(act)], np.int32)),
+                            dsigma=_t(np.array([dsig])), sigma_state=sig, sigma=sig_out)
+        else:
+            L.oit_adam_step(_t(gr), _t(act), d["lat"], d["m"], d["v"], d["step"], rows, cfg,
+                            dsigma=_t(np.array([dsig])), sigma_state=sig, sigma=sig_out)
+        got = {k: x.cpu().numpy() for k, x in d.items()}
+        r_lat, r_m, r_v, r_step, r_rows, r_ss, r_sig = O.adam_step(
+            gr, act, before["lat"], before["m"], before["v"], before["step"], float(dsig),
+            sig_before.astype(np.float64), lr={k: float(np.float32(x)) for k, x in lr.items()}, beta1=b1, beta2=b2,
+            eps=eps)
+        fro = ~mask
+        for k in ("lat", "m", "v", "step"):
+            assert np.array_equal(got[k][fro], before[k][fro]), k                 # frozen: bit-unchanged
+        rws = rows.cpu().numpy()
+        assert np.array_equal(rws[fro], rows_before[fro])
+        assert np.array_equal(got["step"][act], r_step[act])
+        # Adam direction u and the latent-space gradient (for the bars), from the oracle's inputs
+        gl = gr.astype(np.float64)
+        o = 1 / (1 + np.exp(-before["lat"][act, 3].astype(np.float64)))
+        gl[:, 3] *= o * (1 - o)
+        gl[:, 8:11] *= np.exp(before["lat"][act, 8:11].astype(np.float64))
+        t = r_step[act][:, None].astype(np.float64)
+        u = (r_m[act] / (1 - b1 ** t)) / (np.sqrt(r_v[act] / (1 - b2 ** t)) + eps)
+        _adam_check((got["lat"][act], got["m"][act], got["v"][act], rws[act]),
+                    (r_lat[act], r_m[act], r_v[act], r_rows[act], u), lr_f[None, :], gl)
+        s = sig.cpu().numpy()
+        assert s[3] == r_ss[3] and abs(s[0] - r_ss[0]) <= 1e-6 * abs(r_ss[0]) + 2e-5 * lr["sigma"]
+        assert abs(sig_out.item() - r_sig) <= 1e-5 * r_sig
+
+
+def test_adam_step_empty_and_errors():
+    L = _L()
+    cfg = L.adam_cfg()
+    z = torch.zeros((4, 80), dtype=torch.float32, device=DEV)
+    st = torch.zeros(4, dtype=torch.int32, device=DEV)
+    sig = _t(np.array([0.0, 0.0, 0.0, 0.0], np.float32))
+    out = torch.zeros(1, dtype=torch.float32, device=DEV)
+    empty = torch.empty(0, dtype=torch.int32, device=DEV)
+    L.oit_adam_step(z, empty, z, z.clone(), z.clone(), st, z.clone(), cfg, dsigma=_t(np.array([2.0], np.float32)),
+                    sigma_state=sig, sigma=out)
+    s = sig.cpu().numpy()
+    assert s[3] == 1.0 and s[0] == pytest.approx(-0.1, rel=1e-6)                # t=1: −lr_σ·sign(g)
+    assert out.item() == pytest.approx(np.exp(-0.1), rel=1e-6)
+    with pytest.raises(L.OitError):
+        L.oit_adam_step(z, empty, z, z, z, st, z, cfg, dsigma=_t(np.array([1.0], np.float32)))
+    bad = L.adam_cfg(beta1=1.0)
+    with pytest.raises(L.OitError):
+        L.oit_adam_step(z, _t(np.arange(2, dtype=np.int32)), z, z, z, st, z, bad)
