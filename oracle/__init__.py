@@ -302,3 +302,15 @@ def adam_step(grad, active_idx, latent, m, v, step, dsigma=0.0, sig_state=None, 
                         C.c_double(float(dsigma)), _p(ss) if ss is not None else None, _p(sig_out), _p(lrv),
                         C.c_double(beta1), C.c_double(beta2), C.c_double(eps))
     return lat, mm, vv, st, rows, ss, (float(sig_out[0]) if ss is not None else None)
+
+
+def loss_dssim(image, target, lam: float = 0.2, with_map: bool = False):
+    """NEXT-3: the 3DGS loss (1−λ)·L1 + λ·(1 − SSIM) (11×11 Gaussian window σ 1.5,
+    zero padding, C1 = 0.01², C2 = 0.03²) and dL/dC. image, target [3,H,W]. Returns (L, g[, ssim])."""
+    x, y = _f64(image), _f64(target)
+    H, W = x.shape[1], x.shape[2]
+    g = np.zeros_like(x)
+    smap = np.zeros_like(x)
+    lib().orc_loss_dssim.restype = C.c_double
+    L = lib().orc_loss_dssim(_p(x), _p(y), C.c_int32(H), C.c_int32(W), C.c_double(lam), _p(g), _p(smap))
+    return (L, g, smap) if with_map else (L, g)

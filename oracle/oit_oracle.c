@@ -964,3 +964,79 @@ void orc_adam_step(const double* grad, const int32_t* active_idx, int32_t n_acti
         *sigma_out = exp(sig_state[0]);
     }
 }
+
+/* ---- NEXT-3: the 3DGS loss L = (1−λ)·L1 + λ·(1 − SSIM) and its gradient dL/dC ----
+ * P:161 / P:220 "The loss function is the same as in the original 3DGS formulation … λ_ssim kept
+ * consistent" (R24 → NEXT-3). SSIM (Wang et al. 2004) as 3DGS evaluates it: per channel, an
+ * 11×11 Gaussian window (σ = 1.5, normalised to sum 1) with zero padding, C1 = 0.01², C2 = 0.03²,
+ *   S(p) = (2μxμy + C1)(2σxy + C2) / ((μx² + μy² + C1)(σx² + σy² + C2)),
+ *   μx = Σ_u w(u) x(p+u), σx² = Σ_u w(u) x(p+u)² − μx², σxy = Σ_u w(u) x(p+u) y(p+u) − μxμy;
+ * L1 and SSIM are means over the 3·H·W entries. x = image, y = target (layout [3][H][W]).
+ * The gradient is the plain derivative: with E = Σ w x², F = Σ w x y held as window sums,
+ *   ∂S/∂μx = 2μy(a2 − a1)/(b1 b2) − 2μx S (1/b1 − 1/b2),  ∂S/∂E = −S/b2,  ∂S/∂F = 2a1/(b1 b2)
+ * (a1 = 2μxμy + C1, a2 = 2σxy + C2, b1 = μx² + μy² + C1, b2 = σx² + σy² + C2), and
+ *   dL/dx(q) = (1−λ)/M·sign(x(q) − y(q)) − λ/M·Σ_{p in image} w(q−p)[∂S/∂μx(p) + 2x(q)∂S/∂E(p)
+ *              + y(q)∂S/∂F(p)].
+ * Direct 2D window sums (no separable blocking). Returns L; g [3HW] and ssim_map [3HW] (nullable). */
+static void gauss_window(double w[11][11]) {
+    double g[11], s = 0.0;
+    for (int i = 0; i < 11; i++) { g[i] = exp(-((double)(i - 5) * (i - 5)) / (2.0 * 1.5 * 1.5)); s += g[i]; }
+    for (int i = 0; i < 11; i++)
+        for (int j = 0; j < 11; j++) w[i][j] = (g[i] / s) * (g[j] / s);
+}
+
+double orc_loss_dssim(const double* image, const double* target, int32_t H, int32_t W, double lambda, double* g,
+                      double* ssim_map) {
+    const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+    double w[11][11];
+    gauss_window(w);
+    const size_t hw = (size_t)H * W, M = 3 * hw;
+    double* dmu = (double*)calloc(M, sizeof(double));
+    double* dE = (double*)calloc(M, sizeof(double));
+    double* dF = (double*)calloc(M, sizeof(double));
+    double l1 = 0.0, ssum = 0.0;
+    for (int c = 0; c < 3; c++) {
+        const double* X = image + c * hw;
+        const double* Y = target + c * hw;
+        for (int py = 0; py < H; py++)
+            for (int px = 0; px < W; px++) {
+                double mx = 0, my = 0, exx = 0, eyy = 0, exy = 0;
+                for (int u = -5; u <= 5; u++)
+                    for (int v = -5; v <= 5; v++) {
+                        int qy = py + u, qx = px + v;
+                        if (qy < 0 || qy >= H || qx < 0 || qx >= W) continue;
+                        double ww = w[u + 5][v + 5], x = X[(size_t)qy * W + qx], y = Y[(size_t)qy * W + qx];
+                        mx += ww * x; my += ww * y; exx += ww * x * x; eyy += ww * y * y; exy += ww * x * y;
+                    }
+                double sx = exx - mx * mx, sy = eyy - my * my, sxy = exy - mx * my;
+                double a1 = 2 * mx * my + C1, a2 = 2 * sxy + C2, b1 = mx * mx + my * my + C1, b2 = sx + sy + C2;
+                double S = (a1 * a2) / (b1 * b2);
+                size_t p = c * hw + (size_t)py * W + px;
+                if (ssim_map) ssim_map[p] = S;
+                ssum += S;
+                dmu[p] = 2 * my * (a2 - a1) / (b1 * b2) - 2 * mx * S * (1.0 / b1 - 1.0 / b2);
+                dE[p] = -S / b2;
+                dF[p] = 2 * a1 / (b1 * b2);
+            }
+    }
+    for (size_t p = 0; p < M; p++) l1 += fabs(image[p] - target[p]);
+    if (g) {
+        for (int c = 0; c < 3; c++)
+            for (int qy = 0; qy < H; qy++)
+                for (int qx = 0; qx < W; qx++) {
+                    size_t q = c * hw + (size_t)qy * W + qx;
+                    double x = image[q], y = target[q], acc = 0.0;
+                    for (int u = -5; u <= 5; u++)
+                        for (int v = -5; v <= 5; v++) {
+                            int py = qy + u, px = qx + v;
+                            if (py < 0 || py >= H || px < 0 || px >= W) continue;
+                            size_t p = c * hw + (size_t)py * W + px;
+                            acc += w[u + 5][v + 5] * (dmu[p] + 2 * x * dE[p] + y * dF[p]);
+                        }
+                    double d = x - y, sg = d > 0 ? 1.0 : (d < 0 ? -1.0 : 0.0);
+                    g[q] = (1.0 - lambda) / (double)M * sg - lambda / (double)M * acc;
+                }
+    }
+    free(dmu); free(dE); free(dF);
+    return (1.0 - lambda) * l1 / (double)M + lambda * (1.0 - ssum / (double)M);
+}
