@@ -70,6 +70,9 @@ def parse():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--loss", choices=["l1", "dssim"], default="l1",
+                    help="training/score loss: L1 (north-star config) or the 3DGS (1-λ)L1 + λ·D-SSIM (NEXT-3)")
+    ap.add_argument("--no-dssim", action="store_true", help="skip the NEXT-3 D-SSIM loss measurement")
     ap.add_argument("--no-adam", action="store_true", help="skip the NEXT-2 Adam measurement")
     ap.add_argument("--no-reconcile", action="store_true", help="skip the NEXT-1 reconciliation measurement")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
@@ -264,6 +267,7 @@ class Workload:
         self.V = len(cams)
         self.rho = rho
         self.world, self.rank = world, rank
+        self.loss = args.loss
         mask = synth.active_mask(sc, rho, args.kind)
         self.n = sc.n
         act = np.flatnonzero(mask).astype(np.int32)
@@ -381,7 +385,7 @@ class Workload:
                 if host_targets is not None:
                     self.streams[k].wait_event(self.ev_copy[v])
                 p.backward(self.rows, self.sigma, self.act, self.bg, st, None, self.grad, self.dsig,
-                           events=self.ev_bwd[v], target=self.targets[v], loss="l1")
+                           events=self.ev_bwd[v], target=self.targets[v], loss=self.loss)
         for st_ in self.streams[:ns]:
             main.wait_stream(st_)
         if host_targets is not None:
@@ -404,7 +408,7 @@ class Workload:
                 self.streams[k].wait_stream(main)
                 with torch.cuda.stream(self.streams[k]):
                     L.oit_score_subsample(self.rows, self.sigma, self.cams, self.targets_list, self.caches_list,
-                                          self.act, self.ina, part, "l1", self.bg, self.score_grad, self.score_dsig,
+                                          self.act, self.ina, part, self.loss, self.bg, self.score_grad, self.score_dsig,
                                           self.score_cap, self.max_pairs, self.score_ws[k], scale=1.0 / self.S)
             for k, part in enumerate(parts):
                 if part:
@@ -428,10 +432,11 @@ class Workload:
         fwd = 2                                            # fused item builder, k_fwd_items
         # coef | quadrant count, scan, quadrant scatter, fused item builder, moments, epilogue
         bwd = lambda n: 1 + ((5 + scan_kernels(4 * nt)) if n > 0 else 0)  # noqa: E731
-        train = self.V * (proj(a) + binn(a) + fwd + bwd(a))   # loss fused into the bwd coefficients
+        lossk = 3 if self.loss == "dssim" else 0   # resolve + 2 SSIM stencil passes (L1/L2: fused in k_coef)
+        train = self.V * (proj(a) + binn(a) + fwd + bwd(a) + lossk)
         refresh = 1
         if s > 0:
-            refresh += self.S * (proj(a) + binn(a) + fwd + 1 + proj(s) + binn(s) + (bwd(s) - 1))
+            refresh += self.S * (proj(a) + binn(a) + fwd + 1 + lossk + proj(s) + binn(s) + (bwd(s) - 1))
             refresh += 1 + 1 + 3 * scan_kernels(nw) + 1
         return train + refresh
 
@@ -595,7 +600,42 @@ def time_workload(args, torch, dist, wl, world, headline_run):
         res["reconcile"] = time_reconcile(args, torch, wl, flush)
     if headline_run and not args.no_adam:
         res["adam"] = time_adam(args, torch, wl, flush)
+    if headline_run and not args.no_dssim:
+        res["dssim"] = time_dssim(args, torch, wl, flush)
     return res
+
+
+DSSIM_BYTES_PER_PX = 3 * (8 + 12 + 12 + 8 + 4)   # per pixel (3 channels): stats pass in/out, grad pass in/out
+
+
+def time_dssim(args, torch, wl, flush):
+    """NEXT-3: oit_loss_dssim (the 3DGS (1−λ)L1 + λ·D-SSIM loss and dL/dC) on one 800×800 view,
+    event-timed after an L2 flush; HBM roofline on the stencil passes' algorithmic bytes."""
+    L, dev = wl.L, wl.dev
+    cam = wl.cams[0]
+    img = wl.targets[1 % wl.V].contiguous()
+    tgt = wl.targets[0].contiguous()
+    g = torch.empty_like(tgt)
+    loss = torch.zeros(1, dtype=torch.float32, device=dev)
+    ws = torch.empty(L.oit_dssim_workspace_bytes(cam), dtype=torch.uint8, device=dev)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
+    for rep in range(args.warmup + max(args.steps, 5)):
+        flush.zero_()
+        flush.sum()
+        torch.cuda.synchronize()
+        t0.record()
+        L.oit_loss_dssim(cam, img, tgt, g, ws, 0.2, loss)
+        t1.record()
+        torch.cuda.synchronize()
+        if rep >= args.warmup:
+            times.append(t0.elapsed_time(t1))
+    ms = float(np.mean(times))
+    nbytes = wl.H * wl.W * DSSIM_BYTES_PER_PX
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    return {"ms_per_view": ms, "res": [wl.W, wl.H], "bytes": nbytes, "loss": float(loss.item()),
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": HBM_PEAK_GBS, "unit": "GB/s",
+                         "frac": gbs / HBM_PEAK_GBS, "peak_source": HBM_PEAK_SOURCE}}
 
 
 ADAM_BYTES_PER_ROW = 4 * 320 + 4 * 320 + 4 + 4 + 4   # read g, ℓ, m, v; write ℓ, m, v, row; idx, step r/w
@@ -794,7 +834,7 @@ def build_line(args, world, res, results):
                    "step": "I=100 iterations (one view each, fwd+bwd) + one refresh (a7 score over the inactive "
                            "set on S views, a8 update)",
                    "l2": "flushed between timed steps (256 MB write)", "graph": not args.no_graph,
-                   "streams": args.streams},
+                   "streams": args.streams, "loss": args.loss},
         "splat_pixel_evals_per_s": evals / (res["ms"] * 1e-3),
         "contributing_fraction_f_c": f_c,
         "evaluated_splat_pixels_per_view": res["tile_evals"] / res["V"],
@@ -810,6 +850,8 @@ def build_line(args, world, res, results):
         "clocks": res["clocks"], "gpu_launches": res["launches"] * args.steps,
         "sweep": sweep,
     }
+    if "dssim" in res:
+        line["next3_dssim"] = res["dssim"]
     if "adam" in res:
         line["next2_adam"] = res["adam"]
     if "reconcile" in res:

@@ -178,7 +178,9 @@ int oit_composite_bwd(const oit_scene* scene, const oit_camera* cam, const int32
 /* Same as oit_composite_bwd, plus:
  *  - target (nullable, [3][H][W] device): if given, dL_dimage is ignored (may be NULL) and the
  *    pixel gradient is the L1 (loss 0) / L2 (loss 1) gradient of oit_loss_grad, computed from the
- *    image the state resolves to, inside the coefficient kernel (a4 fused: no image round trip);
+ *    image the state resolves to, inside the coefficient kernel (a4 fused: no image round trip),
+ *    or (loss 2) the 3DGS loss gradient of oit_loss_dssim with λ = 0.2 (the image is resolved
+ *    into the workspace first: D-SSIM is not pixel-local);
  *  - ev (nullable): two cudaEvent_t recorded on `stream` right before and after the a5 moment
  *    kernel (the hot loop), so callers can time it with events (also inside CUDA-graph capture,
  *    where they are recorded as external event nodes). */
@@ -206,7 +208,8 @@ int oit_select_views(const float* centers, int32_t n_views, int32_t n_sub, uint6
 /* ---------------------------------------------------------------------------------------
  * a7  oit_score_subsample — the subsampled gradient score of Alg. 1 l.8-12.
  * For each subsampled view j = views_host[s]: the full-G pixel state is caches[j] ⊕ the active
- * set (Rasterize(G, I^pre_j), R16); the L1/L2 loss gradient against targets[j] (R20, R24) is
+ * set (Rasterize(G, I^pre_j), R16); the loss gradient against targets[j] (R20, R24; loss 0 = L1,
+ * 1 = L2, 2 = the 3DGS (1−λ)L1 + λ·D-SSIM with λ = 0.2, NEXT-3) is
  * back-propagated to the scored splats score_idx (normally the inactive set);
  *   score_grad[n_score][80] += scale·Σ_j ∂L_j/∂row, *dL_dsigma += scale·Σ_j ∂L_j/∂σ
  * (scale = 1/S gives the mean over the S subsampled views of R19; disjoint subsets of the S views
@@ -268,6 +271,18 @@ int oit_reconcile_cache(const oit_scene* scene, const oit_camera* cam, const int
                         int32_t n_fold, const int32_t* unfold_idx, int32_t n_unfold, float* cache,
                         int64_t pair_capacity, int64_t* d_n_pairs, void* ws, size_t ws_bytes,
                         oit_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * NEXT-3  oit_loss_dssim — the 3DGS loss L = (1−λ)·mean|C−I| + λ·(1 − mean SSIM(C, I)) and dL/dC
+ * ("the loss function is the same as in the original 3DGS"; R34): SSIM per
+ * channel with an 11×11 Gaussian window (σ = 1.5, normalised), zero padding, C1 = 0.01²,
+ * C2 = 0.03²; means over the 3·H·W entries; sign(0) = 0 in the L1 term. image, target,
+ * dL_dimage [3][H][W] device fp32 (dL_dimage overwritten); d_loss (nullable) device float ← L.
+ * Only cam->width / height are read. Scratch: oit_dssim_workspace_bytes(cam). λ ∈ [0, 1].
+ * --------------------------------------------------------------------------------------- */
+size_t oit_dssim_workspace_bytes(const oit_camera* cam);
+int oit_loss_dssim(const oit_camera* cam, const float* image, const float* target, float lambda,
+                   float* dL_dimage, float* d_loss, void* ws, size_t ws_bytes, oit_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------
  * NEXT-2  oit_adam_step — masked Adam on the compacted active rows, fused with the parameter

@@ -267,7 +267,7 @@ def score_subsample(rows32, sigma, cams, targets, caches, active_idx, score_idx,
     for j in views:
         cam = cams[j]
         fwd = render(rows32, sigma, active_idx, cam, bg, base=caches[j], mode=mode)
-        g = loss_grad(fwd["image"], targets[j], loss)
+        g = loss_dssim(fwd["image"], targets[j], 0.2)[1] if loss == "dssim" else loss_grad(fwd["image"], targets[j], loss)
         gr, ds, _, b = backward_bound(rows32, sigma, score_idx, cam, bg, fwd["state"], g, mode=mode)
         acc += gr
         bnd += b

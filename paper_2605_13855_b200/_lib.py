@@ -55,6 +55,9 @@ class AdamCfg(C.Structure):
     _fields_ = [("lr", C.c_float * 8), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float)]
 
 
+LOSS_CODE = {"l1": 0, "l2": 1, "dssim": 2}   # "dssim" = the 3DGS (1−λ)L1 + λ·D-SSIM, λ = 0.2
+
+
 _lib = None
 
 
@@ -91,6 +94,8 @@ def lib() -> C.CDLL:
             "oit_active_set_delta": (C.c_int, [vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]),
             "oit_reconcile_workspace_bytes": (sz, [cam_p, i32, i64]),
             "oit_reconcile_cache": (C.c_int, [scene_p, cam_p, vp, i32, vp, i32, vp, i64, vp, vp, sz, vp]),
+            "oit_dssim_workspace_bytes": (sz, [cam_p]),
+            "oit_loss_dssim": (C.c_int, [cam_p, vp, vp, C.c_float, vp, vp, vp, sz, vp]),
             "oit_adam_step": (C.c_int, [vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.POINTER(AdamCfg), vp]),
             "oit_update_active_set": (C.c_int, [vp, vp, i32, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         }
@@ -106,7 +111,8 @@ EXPORTED = ["oit_status_string", "oit_num_tiles", "oit_project_cull", "oit_bin_w
             "oit_fwd_workspace_bytes", "oit_composite_fwd", "oit_composite_fwd_ex", "oit_loss_grad", "oit_bwd_workspace_bytes", "oit_composite_bwd", "oit_composite_bwd_ex",
             "oit_select_views", "oit_score_workspace_bytes", "oit_score_subsample", "oit_update_workspace_bytes",
             "oit_update_active_set", "oit_delta_workspace_bytes", "oit_active_set_delta",
-            "oit_reconcile_workspace_bytes", "oit_reconcile_cache", "oit_adam_step"]
+            "oit_reconcile_workspace_bytes", "oit_reconcile_cache", "oit_adam_step",
+            "oit_dssim_workspace_bytes", "oit_loss_dssim"]
 
 
 # ------------------------------------------------------------------ marshalling helpers ---
@@ -201,7 +207,7 @@ def oit_composite_bwd(rows, sigma, cam, idx, rec, pair_slot, tile_offsets, bg, s
     else:
         ev = None if events is None else C.byref(BwdEvents(C.c_void_p(events[0].cuda_event),
                                                            C.c_void_p(events[1].cuda_event)))
-        _check(lib().oit_composite_bwd_ex(*args, _ptr(target), 0 if loss == "l1" else 1, ev, _stream(stream)),
+        _check(lib().oit_composite_bwd_ex(*args, _ptr(target), LOSS_CODE[loss], ev, _stream(stream)),
                "oit_composite_bwd_ex")
 
 
@@ -226,7 +232,7 @@ def oit_score_subsample(rows, sigma, cams, targets, caches, active_idx, score_id
     vw = (C.c_int32 * len(views))(*[int(v) for v in views])
     _check(lib().oit_score_subsample(C.byref(sc), cam_arr, V, tg, ch, _ptr(active_idx), int(active_idx.numel()),
                                      _ptr(score_idx), int(score_idx.numel()), vw, len(views),
-                                     0 if loss == "l1" else 1, _f3(bg),
+                                     LOSS_CODE[loss], _f3(bg),
                                      C.c_float(1.0 / len(views) if scale is None else scale), _ptr(score_grad),
                                      _ptr(dL_dsigma),
                                      int(pair_capacity), _ptr(max_pairs), _ptr(ws), int(ws.numel()),
@@ -290,3 +296,12 @@ def oit_adam_step(grad, active_idx, latent, m, v, step, rows, cfg: AdamCfg, n_ac
     _check(lib().oit_adam_step(_ptr(grad) if n else None, _ptr(active_idx) if n else None, n, _ptr(d_n_active),
                                _ptr(latent), _ptr(m), _ptr(v), _ptr(step), _ptr(rows), _ptr(dsigma),
                                _ptr(sigma_state), _ptr(sigma), C.byref(cfg), _stream(stream)), "oit_adam_step")
+
+
+def oit_dssim_workspace_bytes(cam) -> int:
+    return int(lib().oit_dssim_workspace_bytes(C.byref(camera(cam))))
+
+
+def oit_loss_dssim(cam, image, target, dL_dimage, ws, lam: float = 0.2, loss=None, stream=None):
+    _check(lib().oit_loss_dssim(C.byref(camera(cam)), _ptr(image), _ptr(target), float(lam), _ptr(dL_dimage),
+                                _ptr(loss), _ptr(ws), int(ws.numel()), _stream(stream)), "oit_loss_dssim")

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "lib", "liboit.so")
 SOURCES = ["capi.cu", "project.cu", "scan.cu", "bin.cu", "items.cu", "composite_fwd.cu", "composite_bwd.cu",
-           "score_update.cu", "optim.cu"]
+           "score_update.cu", "optim.cu", "ssim.cu"]
 HEADERS = ["common.cuh", "kernels.h", os.path.join("..", "..", "include", "oit.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]

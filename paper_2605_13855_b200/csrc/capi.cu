@@ -132,10 +132,34 @@ static size_t coef_bytes(int32_t n_tiles) {
   return align_up((size_t)n_tiles * kTilePx * sizeof(float4)) + align_up((size_t)n_tiles * kTilePx * sizeof(float));
 }
 
+// D-SSIM scratch (loss 2): the resolved image, its gradient and the SSIM stencil maps
+static size_t dssim_bytes(const oit_camera* cam) {
+  const size_t n = (size_t)3 * cam->width * cam->height;
+  return 2 * align_up(n * 4) + ssim_ws_bytes(cam->width, cam->height);
+}
+
+// Pixel coefficients from a state and a target: L1/L2 fused into k_coef; D-SSIM (not pixel-local)
+// resolves the image, runs the two SSIM stencil passes, then k_coef from dL/dC.
+static void coef_from_target(const DevCam& dc, const oit_camera* cam, const float* state, const float* target,
+                             int32_t loss, float* coef4, float* coefa, void* dssim_ws, cudaStream_t st) {
+  if (loss != 2) {
+    launch_coef(dc, state, nullptr, target, loss, coef4, coefa, st);
+    return;
+  }
+  const size_t n = (size_t)3 * cam->width * cam->height;
+  Carve cv(dssim_ws);
+  float* image = cv.take<float>(n);
+  float* g = cv.take<float>(n);
+  void* sws = cv.take<char>(ssim_ws_bytes(cam->width, cam->height));
+  launch_resolve(dc, state, image, st);
+  launch_ssim(image, target, cam->width, cam->height, kLambdaSsim, g, nullptr, sws, st);
+  launch_coef(dc, state, g, nullptr, 0, coef4, coefa, st);
+}
+
 size_t oit_bwd_workspace_bytes(const oit_camera* cam, int32_t n_slots, int64_t pair_capacity) {
   if (!cam || n_slots < 0 || pair_capacity < 0) return 0;
   int32_t nt = oit_num_tiles(cam);
-  return coef_bytes(nt) + bwd_ws_bytes(nt, n_slots, pair_capacity);
+  return coef_bytes(nt) + dssim_bytes(cam) + bwd_ws_bytes(nt, n_slots, pair_capacity);
 }
 
 int oit_composite_bwd(const oit_scene* scene, const oit_camera* cam, const int32_t* idx, int32_t n_slots,
@@ -153,7 +177,7 @@ int oit_composite_bwd_ex(const oit_scene* scene, const oit_camera* cam, const in
                          const float* target, int32_t loss, const oit_bwd_events* ev, oit_stream_t stream) {
   if (!scene || !scene->rows || !scene->sigma || !cam_ok(cam) || n_slots < 0 || pair_capacity < 0) return OIT_EINVAL;
   if (!tile_offsets || !bg_host || !state || (!dL_dimage && !target) || !dL_dsigma || !ws) return OIT_EINVAL;
-  if (target && loss != 0 && loss != 1) return OIT_EINVAL;
+  if (target && loss != 0 && loss != 1 && loss != 2) return OIT_EINVAL;
   if (n_slots > 0 && (!idx || !rec || !grad)) return OIT_EINVAL;
   if (pair_capacity > 0 && !pair_slot) return OIT_EINVAL;
   if (!shape_ok(cam) || n_slots > scene->n || oit_num_tiles(cam) > kMaxScan) return OIT_ESHAPE;
@@ -163,8 +187,10 @@ int oit_composite_bwd_ex(const oit_scene* scene, const oit_camera* cam, const in
   Carve cv(ws);
   float* coef4 = cv.take<float>((size_t)nt * kTilePx * 4);
   float* coefa = cv.take<float>((size_t)nt * kTilePx);
+  void* dssim_ws = cv.take<char>(dssim_bytes(cam));
   void* rest = cv.base + cv.off;
-  launch_coef(dc, state, target ? nullptr : dL_dimage, target, loss, coef4, coefa, S(stream));
+  if (target) coef_from_target(dc, cam, state, target, loss, coef4, coefa, dssim_ws, S(stream));
+  else launch_coef(dc, state, dL_dimage, nullptr, 0, coef4, coefa, S(stream));
   launch_composite_bwd(dc, scene->rows, scene->sigma, idx, n_slots, rec, pair_slot, tile_offsets, pair_capacity,
                        coef4, coefa, scale, grad, dL_dsigma, dL_dcov, rest, S(stream),
                        ev ? static_cast<cudaEvent_t>(ev->moments_begin) : nullptr,
@@ -184,7 +210,7 @@ struct ScoreWs {
   float *rec_a, *rec_s, *state, *coef4, *coefa;
   int32_t *tps_a, *tps_s, *pairs, *offs;
   int64_t* npairs;
-  void *bin_ws, *bwd_ws, *fwd_ws;
+  void *bin_ws, *bwd_ws, *fwd_ws, *dssim_ws;
   size_t total;
 };
 
@@ -205,6 +231,7 @@ static ScoreWs score_layout(void* ws, const oit_camera* cam, int32_t n_active, i
   w.bin_ws = cv.take<char>(bin_ws_bytes(nt));
   w.fwd_ws = cv.take<char>(fwd_ws_bytes(nt, cap));
   w.bwd_ws = cv.take<char>(bwd_ws_bytes(nt, n_score, cap));
+  w.dssim_ws = cv.take<char>(dssim_bytes(cam));
   w.total = cv.off;
   return w;
 }
@@ -223,7 +250,7 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
   if (!scene || !scene->rows || !scene->sigma || !cams_host || !targets_host || !views_host || !bg_host ||
       !dL_dsigma || !d_max_pairs || !ws)
     return OIT_EINVAL;
-  if (n_views <= 0 || n_sub <= 0 || n_active < 0 || n_score < 0 || pair_capacity < 0 || (loss != 0 && loss != 1))
+  if (n_views <= 0 || n_sub <= 0 || n_active < 0 || n_score < 0 || pair_capacity < 0 || loss < 0 || loss > 2)
     return OIT_EINVAL;
   if ((n_active > 0 && !active_idx) || (n_score > 0 && (!score_idx || !score_grad))) return OIT_EINVAL;
   if (n_active > scene->n || n_score > scene->n) return OIT_ESHAPE;
@@ -245,7 +272,7 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
     launch_composite_fwd(dc, w.rec_a, w.pairs, w.offs, pair_capacity, caches_host ? caches_host[j] : nullptr, nullptr,
                          nullptr, w.state, nullptr, st, nullptr, w.fwd_ws);
     // L_j and its pixel gradient (fused with the backward coefficients)
-    launch_coef(dc, w.state, nullptr, targets_host[j], loss, w.coef4, w.coefa, st);
+    coef_from_target(dc, &cams_host[j], w.state, targets_host[j], loss, w.coef4, w.coefa, w.dssim_ws, st);
     // back-propagate L_j to the scored splats (R20)
     launch_project(dc, scene->rows, scene->sigma, score_idx, n_score, w.rec_s, w.tps_s, st);
     launch_bin(dc, w.rec_s, w.tps_s, n_score, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st);
@@ -289,6 +316,20 @@ int oit_adam_step(const float* grad, const int32_t* active_idx, int32_t n_active
     return OIT_EINVAL;
   launch_adam(grad, active_idx, n_active, d_n_active, latent, m, v, step, rows, dsigma, sigma_state, sigma, cfg->lr,
               cfg->beta1, cfg->beta2, cfg->eps, S(stream));
+  return launch_status();
+}
+
+size_t oit_dssim_workspace_bytes(const oit_camera* cam) {
+  if (!cam || cam->width <= 0 || cam->height <= 0) return 0;
+  return ssim_ws_bytes(cam->width, cam->height);
+}
+
+int oit_loss_dssim(const oit_camera* cam, const float* image, const float* target, float lambda, float* dL_dimage,
+                   float* d_loss, void* ws, size_t ws_bytes, oit_stream_t stream) {
+  if (!cam || !image || !target || !dL_dimage || !ws || !(lambda >= 0.0f && lambda <= 1.0f)) return OIT_EINVAL;
+  if (cam->width <= 0 || cam->height <= 0) return OIT_ESHAPE;
+  if (ws_bytes < oit_dssim_workspace_bytes(cam)) return OIT_ECAPACITY;
+  launch_ssim(image, target, cam->width, cam->height, lambda, dL_dimage, d_loss, ws, S(stream));
   return launch_status();
 }
 

@@ -62,6 +62,24 @@ __global__ void __launch_bounds__(256) k_coef(DevCam cam, const float* __restric
   coefa[pix] = a;
 }
 
+// The image [3][H][W] of a pixel state (for the non-pixel-local D-SSIM loss, NEXT-3).
+__global__ void __launch_bounds__(256) k_resolve(DevCam cam, const float* __restrict__ state, float* __restrict__ image) {
+  const int tile = blockIdx.x, tid = threadIdx.x;
+  const int n_tiles = cam.TX * cam.TY;
+  const int x = (tile % cam.TX) * kTile + (tid & 15), y = (tile / cam.TX) * kTile + (tid >> 4);
+  if (x >= cam.W || y >= cam.H) return;
+  const size_t plane = (size_t)n_tiles * kTilePx, pix = (size_t)tile * kTilePx + tid;
+  float F0, F1, F2, C0, C1, C2;
+  resolve_pixel(state[pix], state[plane + pix], state[2 * plane + pix], state[3 * plane + pix],
+                state[4 * plane + pix], cam.bg, F0, F1, F2, C0, C1, C2);
+  const size_t hw = (size_t)cam.W * cam.H, p = (size_t)y * cam.W + x;
+  image[p] = C0; image[hw + p] = C1; image[2 * hw + p] = C2;
+}
+
+void launch_resolve(const DevCam& cam, const float* state, float* image, cudaStream_t st) {
+  k_resolve<<<cam.TX * cam.TY, 256, 0, st>>>(cam, state, image);
+}
+
 // ------------------------------------------------------------------------- a5 moments ----
 struct Moments {
   float U0, U1, U2, S, Od, M1, M2, XX, XY, YY;

@@ -79,6 +79,14 @@ void launch_fps(const float* centers, int32_t V, int32_t S, uint64_t seed, uint3
 size_t update_ws_bytes(int32_t n_total);
 size_t delta_ws_bytes(int32_t n_total);
 
+// ssim.cu — NEXT-3 3DGS loss (1−λ)L1 + λ(1−SSIM): dL/dC (g, [3][H][W]) and optionally L (device
+// float); ws = ssim_ws_bytes(W, H). launch_resolve: image [3][H][W] from a pixel state.
+size_t ssim_ws_bytes(int32_t W, int32_t H);
+void launch_ssim(const float* image, const float* target, int32_t W, int32_t H, float lambda, float* g, float* loss,
+                 void* ws, cudaStream_t st);
+void launch_resolve(const DevCam& cam, const float* state, float* image, cudaStream_t st);
+constexpr float kLambdaSsim = 0.2f;  // 3DGS λ_ssim ("kept consistent with those of 3DGS")
+
 // optim.cu — NEXT-2 masked Adam + activations
 void launch_adam(const float* grad, const int32_t* active_idx, int32_t n_cap, const int32_t* d_n, float* latent,
                  float* m, float* v, int32_t* step, float* rows, const float* dsigma, float* sig_state, float* sigma,

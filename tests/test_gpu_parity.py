@@ -248,7 +248,7 @@ def test_select_views_bitexact(V, S, seed, refresh):
     assert np.array_equal(out.cpu().numpy(), O.fps(centers, S, seed, refresh))
 
 
-@pytest.mark.parametrize("loss", ["l1", "l2"])
+@pytest.mark.parametrize("loss", ["l1", "l2", "dssim"])
 def test_score_subsample_parity(loss):
     L = _L()
     sc = synth.scene_c2(n=8000, n_views=6, res=96)
@@ -613,3 +613,60 @@ def test_adam_step_empty_and_errors():
     bad = L.adam_cfg(beta1=1.0)
     with pytest.raises(L.OitError):
         L.oit_adam_step(z, _t(np.arange(2, dtype=np.int32)), z, z, z, st, z, bad)
+
+
+# ------------------------------------------------------------------ NEXT-3 D-SSIM --------
+def _dssim_bar(ref):
+    """fp32 bar for dL/dC of the 3DGS loss (R34): the window sums of x², xy enter
+    σ² = E[x²] − μ² with cancellation ε32·E[x²]/C2 ≈ 2e-5, so entries are held to 3e-5 of the
+    largest |dL/dC| plus 1e-3 relative (measured: ≤ 7.6e-6 of the largest, 800×800)."""
+    return 3e-5 * np.abs(ref).max() + 1e-3 * np.abs(ref)
+
+
+@pytest.mark.parametrize("W,H", [(33, 17), (100, 75), (200, 200), (800, 800)])
+def test_loss_dssim_parity(W, H):
+    L = _L()
+    g = synth.rng(W * 7 + H)
+    cam = {"width": W, "height": H, "fx": 1.0, "fy": 1.0, "cx": 0.0, "cy": 0.0, "R": np.eye(3).ravel(),
+           "t": np.zeros(3), "center": np.zeros(3)}
+    # rendered-like content: smooth blobs + noise, target = image + structured perturbation
+    yy, xx = np.mgrid[0:H, 0:W]
+    base = np.stack([0.5 + 0.4 * np.sin(xx / (5 + 3 * c) + yy / (7 + c)) for c in range(3)])
+    img = np.clip(base + 0.05 * g.normal(size=base.shape), 0, 1).astype(np.float32)
+    tgt = np.clip(img + 0.1 * g.normal(size=base.shape), 0, 1).astype(np.float32)
+    ref_l, ref_g = O.loss_dssim(img, tgt, 0.2)
+    out = torch.empty((3, H, W), dtype=torch.float32, device=DEV)
+    loss = torch.zeros(1, dtype=torch.float32, device=DEV)
+    ws = torch.empty(L.oit_dssim_workspace_bytes(cam), dtype=torch.uint8, device=DEV)
+    L.oit_loss_dssim(cam, _t(img), _t(tgt), out, ws, 0.2, loss)
+    got = out.cpu().numpy()
+    err = np.abs(got - ref_g)
+    print("dssim", W, H, "max err / max|g|", err.max() / np.abs(ref_g).max(), "loss", loss.item(), ref_l)
+    assert np.all(err <= _dssim_bar(ref_g))
+    assert abs(loss.item() - ref_l) <= 1e-5 * abs(ref_l)
+    # identical images: L = 0 and dL/dC = 0 up to fp32 rounding
+    L.oit_loss_dssim(cam, _t(img), _t(img), out, ws, 0.2, loss)
+    assert abs(loss.item()) < 1e-6 and np.abs(out.cpu().numpy()).max() < 1e-3 * np.abs(ref_g).max()
+
+
+def test_fused_dssim_backward_parity():
+    """oit_composite_bwd_ex(target, loss=2): resolve → D-SSIM stencils → coefficients → a5/a6,
+    against the oracle's D-SSIM gradient pushed through its backward (R31 bar)."""
+    sc = SCENES[1]
+    cam = sc.cams[0]
+    idx = np.arange(sc.n, dtype=np.int32)
+    rows, sigma, idx_t = _t(sc.rows), _t(np.array([sc.sigma], np.float32)), _t(idx)
+    tgt = synth.target_image(cam, 91)
+    p = _pipe(cam, sc.n)
+    _, st = p.forward(rows, sigma, idx_t, sc.bg, image=False)
+    grad = torch.zeros((sc.n, 80), dtype=torch.float32, device=DEV)
+    ds = torch.zeros(1, dtype=torch.float32, device=DEV)
+    p.backward(rows, sigma, idx_t, sc.bg, st, None, grad, ds, target=_t(tgt), loss="dssim")
+    ref = O.render(sc.rows, sc.sigma, idx, cam, sc.bg)
+    gref = O.loss_dssim(ref["image"], tgt.astype(np.float64), 0.2)[1]
+    gr, dsr, _, bnd = O.backward_bound(sc.rows, sc.sigma, idx, cam, sc.bg, ref["state"], gref)
+    out = grad.cpu().numpy()
+    ok, bad = grad_close(out, gr, bnd, atol=1e-6 / (3 * cam["width"] * cam["height"]))
+    print("fused dssim strict fraction", strict_fraction(out, gr, atol=1e-6 / (3 * cam["width"] * cam["height"])))
+    assert ok, describe_bad(out, gr, bad, bnd)
+    assert abs(ds.item() - dsr) <= 1e-4 * abs(dsr) + 1e-9
