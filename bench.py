@@ -72,6 +72,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--loss", choices=["l1", "dssim"], default="l1",
                     help="training/score loss: L1 (north-star config) or the 3DGS (1-λ)L1 + λ·D-SSIM (NEXT-3)")
+    ap.add_argument("--no-ablation", action="store_true", help="skip the NEXT-4 per-pixel backward ablation")
     ap.add_argument("--no-dssim", action="store_true", help="skip the NEXT-3 D-SSIM loss measurement")
     ap.add_argument("--no-adam", action="store_true", help="skip the NEXT-2 Adam measurement")
     ap.add_argument("--no-reconcile", action="store_true", help="skip the NEXT-1 reconciliation measurement")
@@ -602,7 +603,41 @@ def time_workload(args, torch, dist, wl, world, headline_run):
         res["adam"] = time_adam(args, torch, wl, flush)
     if headline_run and not args.no_dssim:
         res["dssim"] = time_dssim(args, torch, wl, flush)
+    if headline_run and not args.no_ablation:
+        res["ablation"] = time_ablation(args, torch, wl, flush)
     return res
+
+
+def time_ablation(args, torch, wl, flush, n_views=10):
+    """NEXT-4 (Table 2 analogue): the a5 moment kernel of our lane = splat backward vs
+    the 3DGS-style per-pixel backward (oit_composite_bwd_perpixel), same views, same dL/dC, one
+    stream, event-timed around the moment kernel; L2 flushed before each view's backward."""
+    L, dev = wl.L, wl.dev
+    p = wl.pipe
+    grad = torch.zeros_like(wl.grad)
+    ds = torch.zeros(1, dtype=torch.float32, device=dev)
+    g = torch.empty((3, wl.H, wl.W), dtype=torch.float32, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
+          for _ in range(2)]
+    for e in ev:
+        e[0].record(); e[1].record()
+    ms = {False: [], True: []}
+    for rep in range(2):
+        for v in range(min(n_views, wl.V)):
+            p.set_camera(wl.cams[v])
+            img, st = p.forward(wl.rows, wl.sigma, wl.act, wl.bg, base=wl.caches[v])
+            L.oit_loss_grad(wl.cams[v], img, wl.targets[v], "l1", g)
+            for k, per_pixel in enumerate((False, True)):
+                flush.zero_()
+                flush.sum()
+                torch.cuda.synchronize()
+                p.backward(wl.rows, wl.sigma, wl.act, wl.bg, st, g, grad, ds, events=ev[k], per_pixel=per_pixel)
+                torch.cuda.synchronize()
+                if rep > 0:
+                    ms[per_pixel].append(event_ms(*ev[k]))
+    ours, pix = float(np.mean(ms[False])), float(np.mean(ms[True]))
+    return {"views": min(n_views, wl.V), "moments_ms_per_view_ours": ours, "moments_ms_per_view_per_pixel": pix,
+            "speedup": pix / ours}
 
 
 DSSIM_BYTES_PER_PX = 3 * (8 + 12 + 12 + 8 + 4)   # per pixel (3 channels): stats pass in/out, grad pass in/out
@@ -850,6 +885,8 @@ def build_line(args, world, res, results):
         "clocks": res["clocks"], "gpu_launches": res["launches"] * args.steps,
         "sweep": sweep,
     }
+    if "ablation" in res:
+        line["next4_bwd_ablation"] = res["ablation"]
     if "dssim" in res:
         line["next3_dssim"] = res["dssim"]
     if "adam" in res:

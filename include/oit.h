@@ -196,6 +196,18 @@ int oit_composite_bwd_ex(const oit_scene* scene, const oit_camera* cam, const in
                          const float* target, int32_t loss, const oit_bwd_events* ev,
                          oit_stream_t stream);
 
+/* NEXT-4 ablation (§4.2, Table 2 "Per-pixel"): the same backward as oit_composite_bwd_ex
+ * (same arguments and workspace, dL_dimage required, no fused loss) with the a5 moments computed
+ * 3DGS-style — thread = pixel over the whole tile list, per-(splat, warp) shuffle reduction and
+ * vector atomics — instead of lane = splat. Results equal oit_composite_bwd up to summation order.
+ * For measurement only; the hot path never uses it. */
+int oit_composite_bwd_perpixel(const oit_scene* scene, const oit_camera* cam, const int32_t* idx,
+                               int32_t n_slots, const float* rec, const int32_t* pair_slot,
+                               const int32_t* tile_offsets, int64_t pair_capacity, const float bg_host[3],
+                               const float* state, const float* dL_dimage, float scale, float* grad,
+                               float* dL_dsigma, float* dL_dcov, void* ws, size_t ws_bytes,
+                               const oit_bwd_events* ev, oit_stream_t stream);
+
 /* ---------------------------------------------------------------------------------------
  * a7  oit_select_views — farthest point sampling over the camera centres with a Philox4x32-10
  * random start (§4.1; R22; DESIGN.md §3 FPS spec). Runs as one CUDA block.

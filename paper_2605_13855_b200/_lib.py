@@ -85,6 +85,8 @@ def lib() -> C.CDLL:
                                             vp, vp, sz, vp]),
             "oit_composite_bwd_ex": (C.c_int, [scene_p, cam_p, vp, i32, vp, vp, vp, i64, vp, vp, vp, f32, vp, vp,
                                                vp, vp, sz, vp, i32, C.POINTER(BwdEvents), vp]),
+            "oit_composite_bwd_perpixel": (C.c_int, [scene_p, cam_p, vp, i32, vp, vp, vp, i64, vp, vp, vp, f32, vp,
+                                                     vp, vp, vp, sz, C.POINTER(BwdEvents), vp]),
             "oit_select_views": (C.c_int, [vp, i32, i32, C.c_uint64, C.c_uint32, vp, vp]),
             "oit_score_workspace_bytes": (sz, [cam_p, i32, i32, i64]),
             "oit_score_subsample": (C.c_int, [scene_p, cam_p, i32, vp, vp, vp, i32, vp, i32, vp, i32, i32, vp, f32,
@@ -112,7 +114,7 @@ EXPORTED = ["oit_status_string", "oit_num_tiles", "oit_project_cull", "oit_bin_w
             "oit_select_views", "oit_score_workspace_bytes", "oit_score_subsample", "oit_update_workspace_bytes",
             "oit_update_active_set", "oit_delta_workspace_bytes", "oit_active_set_delta",
             "oit_reconcile_workspace_bytes", "oit_reconcile_cache", "oit_adam_step",
-            "oit_dssim_workspace_bytes", "oit_loss_dssim"]
+            "oit_dssim_workspace_bytes", "oit_loss_dssim", "oit_composite_bwd_perpixel"]
 
 
 # ------------------------------------------------------------------ marshalling helpers ---
@@ -194,7 +196,8 @@ def oit_bwd_workspace_bytes(cam, n_slots: int, pair_capacity: int) -> int:
 
 
 def oit_composite_bwd(rows, sigma, cam, idx, rec, pair_slot, tile_offsets, bg, state, dL_dimage, grad, dL_dsigma,
-                      ws, dL_dcov=None, scale: float = 1.0, stream=None, events=None, target=None, loss="l1"):
+                      ws, dL_dcov=None, scale: float = 1.0, stream=None, events=None, target=None, loss="l1",
+                      per_pixel: bool = False):
     """events: optional (begin, end) torch.cuda.Event pair recorded around the a5 moment kernel;
     target: optional training image — the L1/L2 pixel gradient is then fused into the backward
     (dL_dimage may be None). Both select oit_composite_bwd_ex."""
@@ -202,7 +205,11 @@ def oit_composite_bwd(rows, sigma, cam, idx, rec, pair_slot, tile_offsets, bg, s
     args = (C.byref(sc), C.byref(c), _ptr(idx), int(idx.numel()), _ptr(rec), _ptr(pair_slot), _ptr(tile_offsets),
             int(pair_slot.numel()), _f3(bg), _ptr(state), _ptr(dL_dimage), C.c_float(scale), _ptr(grad),
             _ptr(dL_dsigma), _ptr(dL_dcov), _ptr(ws), int(ws.numel()))
-    if events is None and target is None:
+    if per_pixel:   # NEXT-4 ablation (3DGS-style per-pixel moments)
+        ev = None if events is None else C.byref(BwdEvents(C.c_void_p(events[0].cuda_event),
+                                                           C.c_void_p(events[1].cuda_event)))
+        _check(lib().oit_composite_bwd_perpixel(*args, ev, _stream(stream)), "oit_composite_bwd_perpixel")
+    elif events is None and target is None:
         _check(lib().oit_composite_bwd(*args, _stream(stream)), "oit_composite_bwd")
     else:
         ev = None if events is None else C.byref(BwdEvents(C.c_void_p(events[0].cuda_event),

@@ -198,6 +198,32 @@ int oit_composite_bwd_ex(const oit_scene* scene, const oit_camera* cam, const in
   return launch_status();
 }
 
+int oit_composite_bwd_perpixel(const oit_scene* scene, const oit_camera* cam, const int32_t* idx, int32_t n_slots,
+                               const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
+                               int64_t pair_capacity, const float bg_host[3], const float* state,
+                               const float* dL_dimage, float scale, float* grad, float* dL_dsigma, float* dL_dcov,
+                               void* ws, size_t ws_bytes, const oit_bwd_events* ev, oit_stream_t stream) {
+  if (!scene || !scene->rows || !scene->sigma || !cam_ok(cam) || n_slots < 0 || pair_capacity < 0) return OIT_EINVAL;
+  if (!tile_offsets || !bg_host || !state || !dL_dimage || !dL_dsigma || !ws) return OIT_EINVAL;
+  if (n_slots > 0 && (!idx || !rec || !grad)) return OIT_EINVAL;
+  if (pair_capacity > 0 && !pair_slot) return OIT_EINVAL;
+  if (!shape_ok(cam) || n_slots > scene->n || oit_num_tiles(cam) > kMaxScan) return OIT_ESHAPE;
+  if (ws_bytes < oit_bwd_workspace_bytes(cam, n_slots, pair_capacity)) return OIT_ECAPACITY;
+  const int32_t nt = oit_num_tiles(cam);
+  DevCam dc = dev_cam(cam, bg_host);
+  Carve cv(ws);
+  float* coef4 = cv.take<float>((size_t)nt * kTilePx * 4);
+  float* coefa = cv.take<float>((size_t)nt * kTilePx);
+  cv.take<char>(dssim_bytes(cam));
+  void* rest = cv.base + cv.off;
+  launch_coef(dc, state, dL_dimage, nullptr, 0, coef4, coefa, S(stream));
+  launch_composite_bwd(dc, scene->rows, scene->sigma, idx, n_slots, rec, pair_slot, tile_offsets, pair_capacity,
+                       coef4, coefa, scale, grad, dL_dsigma, dL_dcov, rest, S(stream),
+                       ev ? static_cast<cudaEvent_t>(ev->moments_begin) : nullptr,
+                       ev ? static_cast<cudaEvent_t>(ev->moments_end) : nullptr, 1);
+  return launch_status();
+}
+
 int oit_select_views(const float* centers, int32_t n_views, int32_t n_sub, uint64_t seed, uint32_t refresh_index,
                      int32_t* views_out, oit_stream_t stream) {
   if (!centers || !views_out || n_sub <= 0 || n_sub > n_views || n_views > 8192) return OIT_EINVAL;

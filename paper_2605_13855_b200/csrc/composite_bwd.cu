@@ -228,6 +228,76 @@ __global__ void __launch_bounds__(kMomentsThreads, 8) k_moments(DevCam cam, cons
   }
 }
 
+// ------------------------------------------------- NEXT-4 ablation: per-pixel backward ----
+// The 3DGS-style parallelisation the paper ablates against (§4.2, Table 2 "Per-pixel"): a
+// CTA per tile, THREAD = PIXEL, walking the tile's whole splat list (records staged in smem as in
+// the forward); every (splat, warp) with a contributing pixel reduces its 10 moments across the
+// warp with shuffles and one lane adds them with 3 vector atomics into the same per-slot moment
+// rows k_moments produces (so the epilogue is shared). B200 analogue of 3DGS's per-pixel atomics
+// (warp-aggregated rather than one atomic per pixel). Ablation only: not used by the hot path.
+__global__ void __launch_bounds__(256) k_moments_pixel(DevCam cam, const float4* __restrict__ rec,
+                                                       const int32_t* __restrict__ pair_slot,
+                                                       const int32_t* __restrict__ offs, int64_t capacity,
+                                                       const float4* __restrict__ coef4,
+                                                       const float* __restrict__ coefa, float* __restrict__ acc2d) {
+  __shared__ float4 s_q0[256], s_q1[256], s_q2[256];
+  __shared__ float2 s_k[256];
+  __shared__ int s_slot[256];
+  const unsigned FULL = 0xffffffffu;
+  const int tile = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  const int x = (tile % cam.TX) * kTile + (tid & 15), y = (tile / cam.TX) * kTile + (tid >> 4);
+  const bool inimg = x < cam.W && y < cam.H;
+  const size_t pix = (size_t)tile * kTilePx + tid;
+  const float4 cu = coef4[pix];
+  const float ca = coefa[pix];
+  int start = offs[tile], end = offs[tile + 1];
+  if ((int64_t)end > capacity) end = (int)capacity;
+  if (start > end) start = end;
+  const float fx = (float)x, fy = (float)y;
+  for (int b = start; b < end; b += 256) {
+    const int n = min(256, end - b);
+    __syncthreads();
+    if (tid < n) {
+      const int slot = pair_slot[b + tid];
+      const float4* r = rec + (size_t)slot * kRec4;
+      s_q0[tid] = r[0];
+      s_q1[tid] = r[1];
+      s_q2[tid] = r[2];
+      s_k[tid] = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(r + 3) + 2);
+      s_slot[tid] = slot;
+    }
+    __syncthreads();
+    for (int i = 0; i < n; i++) {
+      const float4 q0 = s_q0[i], q1 = s_q1[i];
+      const float dx = __fsub_rn(fx, q0.x), dy = __fsub_rn(fy, q0.y);
+      const float power = spec_power(q0.z, q0.w, q1.x, dx, dy);
+      const bool contrib = inimg && power <= 0.0f && power >= q1.y;
+      if (!__any_sync(FULL, contrib)) continue;
+      const float2 kk = s_k[i];
+      const float4 q2 = s_q2[i];
+      const bool clamp = power >= q1.z;
+      float alpha = clamp ? 0.99f : ex2_approx(fmaf(-kk.x, dx, fmaf(power, kLog2e, fmaf(-kk.y, dy, q1.w))));
+      alpha = contrib ? alpha : 0.0f;
+      const float rinv = rcp_approx(1.0f - alpha);
+      const float dot = fmaf(cu.x, q2.x, fmaf(cu.y, q2.y, fmaf(cu.z, q2.z, -cu.w)));
+      float d = fmaf(ca, rinv, q2.w * dot) * alpha;
+      d = clamp ? 0.0f : d;
+      float v[10] = {alpha * cu.x, alpha * cu.y, alpha * cu.z, alpha * cu.w, d, d * dx, d * dy,
+                     d * dx * dx, d * dx * dy, d * dy * dy};
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < 10; q++) v[q] += __shfl_xor_sync(FULL, v[q], o);
+      if (lane == 0) {
+        float* a = acc2d + (size_t)s_slot[i] * 12;
+        red_add_v4(a, v[0], v[1], v[2], v[3]);
+        red_add_v4(a + 4, v[4], v[5], v[6], v[7]);
+        red_add_v4(a + 8, v[8], v[9], 0.f, 0.f);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------------ a6 epilogue ----
 // One thread per slot. Phase 1 (appearance): view direction, SH colour/weight and their
 // gradients, the h/v rows are updated while streaming the coefficients, and the direction's
@@ -471,7 +541,7 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
                           int32_t n_slots, const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
                           int64_t capacity, const float* coef4, const float* coefa, float scale, float* grad,
                           float* dL_dsigma, float* dL_dcov, void* ws, cudaStream_t st, cudaEvent_t ev_begin,
-                          cudaEvent_t ev_end) {
+                          cudaEvent_t ev_end, int variant) {
   if (n_slots <= 0) {
     record_event(ev_begin, st);
     record_event(ev_end, st);
@@ -493,16 +563,23 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
   uint8_t* qmask = cv.take<uint8_t>(capacity);
   void* tmp = cv.take<char>(scan_tmp_bytes(4 * (int64_t)n_tiles));
   cudaMemsetAsync(acc2d, 0, sizeof(float) * 12 * (size_t)n_slots, st);
-  cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
-  // quadrant sub-binning of the tile lists, then (quadrant, 32-slot chunk) items
-  launch_quad_bin(cam, rec, pair_slot, tile_offsets, capacity, qmask, qcount, qoffs, qslot, tmp, st);
-  launch_build_items(qoffs, 4 * n_tiles, qcap, 32, 0, items, n_items, tile_nch, scratch, st);
-  const int blocks = sm_count() * 8;  // persistent: 8 × 4 warps per SM, dynamic item claiming
-  record_event(ev_begin, st);
-  k_moments<<<blocks, kMomentsThreads, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), qslot, qoffs,
-                                                qcap, items, n_items, counter,
-                                                reinterpret_cast<const float4*>(coef4), coefa, acc2d);
-  record_event(ev_end, st);
+  if (variant == 1) {  // NEXT-4 ablation: per-pixel backward over the tile lists
+    record_event(ev_begin, st);
+    k_moments_pixel<<<n_tiles, 256, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), pair_slot, tile_offsets,
+                                             capacity, reinterpret_cast<const float4*>(coef4), coefa, acc2d);
+    record_event(ev_end, st);
+  } else {
+    cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
+    // quadrant sub-binning of the tile lists, then (quadrant, 32-slot chunk) items
+    launch_quad_bin(cam, rec, pair_slot, tile_offsets, capacity, qmask, qcount, qoffs, qslot, tmp, st);
+    launch_build_items(qoffs, 4 * n_tiles, qcap, 32, 0, items, n_items, tile_nch, scratch, st);
+    const int blocks = sm_count() * 8;  // persistent: 8 × 4 warps per SM, dynamic item claiming
+    record_event(ev_begin, st);
+    k_moments<<<blocks, kMomentsThreads, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), qslot, qoffs,
+                                                  qcap, items, n_items, counter,
+                                                  reinterpret_cast<const float4*>(coef4), coefa, acc2d);
+    record_event(ev_end, st);
+  }
   k_epilogue<<<(n_slots + 127) / 128, 128, 0, st>>>(cam, reinterpret_cast<const float4*>(rows), sigma, idx, n_slots,
                                                     reinterpret_cast<const float4*>(rec),
                                                     reinterpret_cast<const float4*>(acc2d), scale,

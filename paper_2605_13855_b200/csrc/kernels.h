@@ -60,7 +60,7 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
                           int32_t n_slots, const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
                           int64_t capacity, const float* coef4, const float* coefa, float scale, float* grad,
                           float* dL_dsigma, float* dL_dcov, void* ws, cudaStream_t st,
-                          cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr);
+                          cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr, int variant = 0);
 
 // Record an event on a stream, as an external event node when the stream is being captured.
 inline void record_event(cudaEvent_t ev, cudaStream_t st) {

@@ -63,14 +63,14 @@ class ViewPipeline:
         return (self.image if image else None), self.state
 
     def backward(self, rows, sigma, idx, bg, state, dL_dimage, grad, dL_dsigma, dL_dcov=None, scale=1.0,
-                 reuse_bins=True, stream=None, events=None, target=None, loss="l1"):
+                 reuse_bins=True, stream=None, events=None, target=None, loss="l1", per_pixel=False):
         """a4-a6 for the splats idx (grad rows += ...). With reuse_bins the records/pairs of the
         preceding forward over the same idx are reused."""
         n = int(idx.numel())
         rec = (self.rec[:n] if n > 0 else self.rec) if reuse_bins else self.project_bin(rows, sigma, idx, stream)
         L.oit_composite_bwd(rows, sigma, self.cam, idx, rec, self.pairs, self.offs, bg, state, dL_dimage, grad,
                             dL_dsigma, self.bwd_ws, dL_dcov=dL_dcov, scale=scale, stream=stream, events=events,
-                            target=target, loss=loss)
+                            target=target, loss=loss, per_pixel=per_pixel)
 
     def pairs_used(self) -> int:
         return int(self.n_pairs.item())

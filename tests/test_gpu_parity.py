@@ -176,7 +176,7 @@ def test_composite_fwd_empty_and_permutation():
 
 
 # ------------------------------------------------------------------ a4-a6 backward -------
-def _bwd_case(sc, cam, idx, seed=5, base=None):
+def _bwd_case(sc, cam, idx, seed=5, base=None, per_pixel=False):
     rows, sigma = _t(sc.rows), _t(np.array([sc.sigma], np.float32))
     p = _pipe(cam, len(idx))
     _, state = p.forward(rows, sigma, _t(idx), sc.bg, base=base)
@@ -184,7 +184,7 @@ def _bwd_case(sc, cam, idx, seed=5, base=None):
     grad = torch.zeros((len(idx), 80), dtype=torch.float32, device=DEV)
     dsig = torch.zeros(1, dtype=torch.float32, device=DEV)
     dcov = torch.zeros((len(idx), 6), dtype=torch.float32, device=DEV)
-    p.backward(rows, sigma, _t(idx), sc.bg, state, _t(g), grad, dsig, dL_dcov=dcov)
+    p.backward(rows, sigma, _t(idx), sc.bg, state, _t(g), grad, dsig, dL_dcov=dcov, per_pixel=per_pixel)
     return grad.cpu().numpy(), float(dsig.item()), dcov.cpu().numpy(), g
 
 
@@ -670,3 +670,17 @@ def test_fused_dssim_backward_parity():
     print("fused dssim strict fraction", strict_fraction(out, gr, atol=1e-6 / (3 * cam["width"] * cam["height"])))
     assert ok, describe_bad(out, gr, bad, bnd)
     assert abs(ds.item() - dsr) <= 1e-4 * abs(dsr) + 1e-9
+
+
+# ------------------------------------------------------------------ NEXT-4 ablation ------
+def test_per_pixel_backward_ablation_parity(scene):
+    """The 3DGS-style per-pixel backward (Table 2 ablation variant) meets the same bar as ours."""
+    idx = np.arange(scene.n, dtype=np.int32)
+    cam = scene.cams[0]
+    grad, dsig, dcov, g = _bwd_case(scene, cam, idx, per_pixel=True)
+    ref = O.render(scene.rows, scene.sigma, idx, cam, scene.bg)
+    gref, dsref, cref, bnd = O.backward_bound(scene.rows, scene.sigma, idx, cam, scene.bg, ref["state"], g)
+    ok, bad = grad_close(grad, gref, bnd)
+    assert ok, describe_bad(grad, gref, bad, bnd)
+    assert strict_fraction(grad, gref) > 0.99
+    assert abs(dsig - dsref) <= 1e-4 * abs(dsref) + 1e-6
