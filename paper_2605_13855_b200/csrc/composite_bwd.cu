@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(128, 3) k_epilogue(DevCam cam, const float4* _
 size_t bwd_ws_bytes(int32_t n_tiles, int32_t n_slots, int64_t capacity) {
   const int64_t qcap = 4 * capacity;
   return align_up((size_t)n_slots * 12 * sizeof(float)) + items_bytes(4 * n_tiles, qcap, 32) + align_up(16) +
-         2 * align_up((size_t)(4 * n_tiles + 1) * 4) + align_up((size_t)qcap * 4) + align_up((size_t)capacity) +
+         2 * align_up((size_t)(4 * n_tiles + 1) * 4) + align_up((size_t)qcap * 4) + align_up((size_t)capacity * 4) +
          scan_tmp_bytes(4 * (int64_t)n_tiles);
 }
 
@@ -560,7 +560,7 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
   int32_t* qcount = cv.take<int32_t>(4 * n_tiles + 1);
   int32_t* qoffs = cv.take<int32_t>(4 * n_tiles + 1);
   int32_t* qslot = cv.take<int32_t>(qcap);
-  uint8_t* qmask = cv.take<uint8_t>(capacity);
+  uint32_t* tq = cv.take<uint32_t>(capacity);
   void* tmp = cv.take<char>(scan_tmp_bytes(4 * (int64_t)n_tiles));
   cudaMemsetAsync(acc2d, 0, sizeof(float) * 12 * (size_t)n_slots, st);
   if (variant == 1) {  // NEXT-4 ablation: per-pixel backward over the tile lists
@@ -571,7 +571,7 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
   } else {
     cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
     // quadrant sub-binning of the tile lists, then (quadrant, 32-slot chunk) items
-    launch_quad_bin(cam, rec, pair_slot, tile_offsets, capacity, qmask, qcount, qoffs, qslot, tmp, st);
+    launch_quad_bin(cam, rec, pair_slot, tile_offsets, capacity, tq, qcount, qoffs, qslot, tmp, st);
     launch_build_items(qoffs, 4 * n_tiles, qcap, 32, 0, items, n_items, tile_nch, scratch, st);
     const int blocks = sm_count() * 8;  // persistent: 8 × 4 warps per SM, dynamic item claiming
     record_event(ev_begin, st);

@@ -17,7 +17,10 @@
 namespace oit {
 
 constexpr int kFwdThreads = 64;    // 4 pixels per thread (one tile row: columns c, c+4, c+8, c+12)
-constexpr int kFwdChunk = 256;     // slots per work item
+// slots per work item: 128 balances the persistent grid (alone on the GPU: 84 vs 124 µs per C2
+// view at 256; 64 is no faster); the workspace is sized for chunks down to kFwdChunkMin
+constexpr int kFwdChunk = 128;
+constexpr int kFwdChunkMin = 64;
 
 __device__ __forceinline__ void accum_px(float power, float thr_hi, float arg, const float4& q2, float& P0, float& P1,
                                          float& P2, float& Q, float& T) {
@@ -49,7 +52,7 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
     const int32_t* __restrict__ offs, int64_t capacity, const int2* __restrict__ items,
     const int32_t* __restrict__ n_items_p, int32_t* __restrict__ counter, const int32_t* __restrict__ tile_nch,
     int32_t* __restrict__ done, float* __restrict__ partial, const float* __restrict__ base,
-    float* __restrict__ image, float* __restrict__ state, unsigned long long* __restrict__ counters) {
+    float* __restrict__ image, float* __restrict__ state, unsigned long long* __restrict__ counters, int chunk_len) {
   __shared__ float4 s_q0[kFwdThreads], s_q1[kFwdThreads], s_q2[kFwdThreads];
   __shared__ float2 s_k[kFwdThreads];
   __shared__ int s_item, s_last;
@@ -71,6 +74,7 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
     const int tx0 = (tile % cam.TX) * kTile, ty0 = (tile / cam.TX) * kTile;
     const float fy = (float)(ty0 + ly), fx0 = (float)(tx0 + lx);
     const float fx1 = fx0 + 4.0f, fx2 = fx0 + 8.0f, fx3 = fx0 + 12.0f;
+    const f2_t fxA = f2(fx0, fx1), fxB = f2(fx2, fx3);
     const size_t pxb = (size_t)tile * kTilePx + p0;
     Px a[4];
 #pragma unroll
@@ -79,10 +83,15 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
       a[k].T = 1.f;
       if (kBase && nch == 1) load_px(a[k], base, plane, pxb + 4 * k);
     }
+    // packed accumulators of the pixel pairs A = (k 0, 1), B = (k 2, 3)
+    f2_t PA0 = f2(a[0].P0, a[1].P0), PA1 = f2(a[0].P1, a[1].P1), PA2 = f2(a[0].P2, a[1].P2), QA = f2(a[0].Q, a[1].Q);
+    f2_t TA = f2(a[0].T, a[1].T);
+    f2_t PB0 = f2(a[2].P0, a[3].P0), PB1 = f2(a[2].P1, a[3].P1), PB2 = f2(a[2].P2, a[3].P2), QB = f2(a[2].Q, a[3].Q);
+    f2_t TB = f2(a[2].T, a[3].T);
     int64_t e64 = offs[tile + 1];
     if (e64 > capacity) e64 = capacity;
-    const int begin = offs[tile] + chunk * kFwdChunk;
-    const int end = (int)min((int64_t)begin + kFwdChunk, e64);
+    const int begin = offs[tile] + chunk * chunk_len;
+    const int end = (int)min((int64_t)begin + chunk_len, e64);
     int n_contrib = 0;
     for (int b = begin; b < end; b += kFwdThreads) {
       const int n = min(kFwdThreads, end - b);
@@ -94,27 +103,40 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
         s_k[tid] = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(r + 3) + 2);
       }
       __syncthreads();
-#pragma unroll 2
+#pragma unroll 1
       for (int i = 0; i < n; i++) {
         const float4 q0 = s_q0[i];  // mx my nA nB
         const float4 q1 = s_q1[i];  // nC thr_lo thr_hi log2o
+        // spec test (DESIGN.md §3 step 13) on the pixel pairs (x, x+4), (x+8, x+12): the packed
+        // sub/fma are per element the scalar __fsub_rn/__fmaf_rn, so the decisions are unchanged
         const float dy = __fsub_rn(fy, q0.y);
         const float by = __fmul_rn(q0.w, dy);
         const float cy = __fmul_rn(__fmul_rn(q1.x, dy), dy);
-        const float dx0 = __fsub_rn(fx0, q0.x), dx1 = __fsub_rn(fx1, q0.x);
-        const float dx2 = __fsub_rn(fx2, q0.x), dx3 = __fsub_rn(fx3, q0.x);
-        const float pw0 = spec_power_row(q0.z, dx0, by, cy), pw1 = spec_power_row(q0.z, dx1, by, cy);
-        const float pw2 = spec_power_row(q0.z, dx2, by, cy), pw3 = spec_power_row(q0.z, dx3, by, cy);
+        const f2_t mx2 = f2s(q0.x), nA2 = f2s(q0.z), by2 = f2s(by), cy2 = f2s(cy);
+        const f2_t dxA = sub2(fxA, mx2), dxB = sub2(fxB, mx2);
+        const f2_t pwA = fma2(dxA, fma2(nA2, dxA, by2), cy2), pwB = fma2(dxB, fma2(nA2, dxB, by2), cy2);
+        const float pw0 = f2lo(pwA), pw1 = f2hi(pwA), pw2 = f2lo(pwB), pw3 = f2hi(pwB);
         const bool c0 = pw0 <= 0.0f && pw0 >= q1.y, c1 = pw1 <= 0.0f && pw1 >= q1.y;
         const bool c2 = pw2 <= 0.0f && pw2 >= q1.y, c3 = pw3 <= 0.0f && pw3 >= q1.y;
-        if (c0 || c1 || c2 || c3) {
+        if (c0 || c1 || c2 || c3) {  // branch-free inside: α = 0 for the non-contributing pixels
           const float4 q2 = s_q2[i];  // cR cG cB w
           const float2 kk = s_k[i];   // sub-ulp μ' correction of the exponent (value path)
-          const float base_arg = fmaf(-kk.y, dy, q1.w);
-          if (c0) accum_px(pw0, q1.z, fmaf(-kk.x, dx0, fmaf(pw0, kLog2e, base_arg)), q2, a[0].P0, a[0].P1, a[0].P2, a[0].Q, a[0].T);
-          if (c1) accum_px(pw1, q1.z, fmaf(-kk.x, dx1, fmaf(pw1, kLog2e, base_arg)), q2, a[1].P0, a[1].P1, a[1].P2, a[1].Q, a[1].T);
-          if (c2) accum_px(pw2, q1.z, fmaf(-kk.x, dx2, fmaf(pw2, kLog2e, base_arg)), q2, a[2].P0, a[2].P1, a[2].P2, a[2].Q, a[2].T);
-          if (c3) accum_px(pw3, q1.z, fmaf(-kk.x, dx3, fmaf(pw3, kLog2e, base_arg)), q2, a[3].P0, a[3].P1, a[3].P2, a[3].Q, a[3].T);
+          const f2_t base2 = f2s(fmaf(-kk.y, dy, q1.w)), nkx2 = f2s(-kk.x), l2e = f2s(kLog2e);
+          const f2_t argA = fma2(nkx2, dxA, fma2(pwA, l2e, base2));
+          const f2_t argB = fma2(nkx2, dxB, fma2(pwB, l2e, base2));
+          const float e0 = ex2_approx(f2lo(argA)), e1 = ex2_approx(f2hi(argA));
+          const float e2 = ex2_approx(f2lo(argB)), e3 = ex2_approx(f2hi(argB));
+          const float a0 = c0 ? (pw0 >= q1.z ? 0.99f : e0) : 0.0f;
+          const float a1 = c1 ? (pw1 >= q1.z ? 0.99f : e1) : 0.0f;
+          const float a2 = c2 ? (pw2 >= q1.z ? 0.99f : e2) : 0.0f;
+          const float a3 = c3 ? (pw3 >= q1.z ? 0.99f : e3) : 0.0f;
+          const f2_t alA = f2(a0, a1), alB = f2(a2, a3), w2 = f2s(q2.w), neg1 = f2s(-1.0f);
+          const f2_t awA = mul2(alA, w2), awB = mul2(alB, w2);
+          const f2_t cR = f2s(q2.x), cG = f2s(q2.y), cB = f2s(q2.z);
+          fma2_acc(PA0, cR, awA); fma2_acc(PA1, cG, awA); fma2_acc(PA2, cB, awA); add2_acc(QA, awA);
+          fma2_acc(PB0, cR, awB); fma2_acc(PB1, cG, awB); fma2_acc(PB2, cB, awB); add2_acc(QB, awB);
+          fma2_acc(TA, mul2(alA, neg1), TA);  // T ← T − αT (one rounding, as fmaf(−α, T, T))
+          fma2_acc(TB, mul2(alB, neg1), TB);
           if (kCount) {
             if (ty0 + ly < cam.H)
               n_contrib += (c0 && tx0 + lx < cam.W) + (c1 && tx0 + lx + 4 < cam.W) + (c2 && tx0 + lx + 8 < cam.W) +
@@ -124,6 +146,10 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
       }
       __syncthreads();
     }
+    a[0].P0 = f2lo(PA0); a[1].P0 = f2hi(PA0); a[0].P1 = f2lo(PA1); a[1].P1 = f2hi(PA1);
+    a[0].P2 = f2lo(PA2); a[1].P2 = f2hi(PA2); a[0].Q = f2lo(QA); a[1].Q = f2hi(QA); a[0].T = f2lo(TA); a[1].T = f2hi(TA);
+    a[2].P0 = f2lo(PB0); a[3].P0 = f2hi(PB0); a[2].P1 = f2lo(PB1); a[3].P1 = f2hi(PB1);
+    a[2].P2 = f2lo(PB2); a[3].P2 = f2hi(PB2); a[2].Q = f2lo(QB); a[3].Q = f2hi(QB); a[2].T = f2lo(TB); a[3].T = f2hi(TB);
     if (kCount) {
       unsigned long long c = (unsigned long long)n_contrib;
 #pragma unroll
@@ -280,8 +306,8 @@ __global__ void __launch_bounds__(256) k_fwd(DevCam cam, const float4* __restric
 }
 
 size_t fwd_ws_bytes(int32_t n_tiles, int64_t capacity) {
-  const int64_t max_items = capacity / kFwdChunk + n_tiles + 1;
-  return items_bytes(n_tiles, capacity, kFwdChunk) + align_up((size_t)n_tiles * 4) + align_up(16) +
+  const int64_t max_items = capacity / kFwdChunkMin + n_tiles + 1;
+  return items_bytes(n_tiles, capacity, kFwdChunkMin) + align_up((size_t)n_tiles * 4) + align_up(16) +
          align_up((size_t)max_items * 5 * kTilePx * sizeof(float));
 }
 
@@ -292,7 +318,8 @@ void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pa
   const float4* r4 = reinterpret_cast<const float4*>(rec);
   auto* cnt = reinterpret_cast<unsigned long long*>(counters);
   if (!route) {
-    const int64_t max_items = capacity / kFwdChunk + n_tiles + 1;
+    const int chunk_len = kFwdChunk;
+    const int64_t max_items = capacity / chunk_len + n_tiles + 1;
     Carve cv(ws);
     int2* items = cv.take<int2>(max_items);
     int32_t* n_items = cv.take<int32_t>(4);
@@ -303,11 +330,11 @@ void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pa
     float* partial = cv.take<float>((size_t)max_items * 5 * kTilePx);
     cudaMemsetAsync(done, 0, sizeof(int32_t) * n_tiles, st);
     cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
-    launch_build_items(tile_offsets, n_tiles, capacity, kFwdChunk, 1, items, n_items, tile_nch, scratch, st);
+    launch_build_items(tile_offsets, n_tiles, capacity, chunk_len, 1, items, n_items, tile_nch, scratch, st);
     const int grid = sm_count() * 24;  // persistent (64-thread CTAs); items are claimed dynamically
 #define OIT_FWD2(B, K)                                                                                         \
   k_fwd_items<B, K><<<grid, kFwdThreads, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, items, n_items, \
-                                                  counter, tile_nch, done, partial, base, image, state, cnt)
+                                                  counter, tile_nch, done, partial, base, image, state, cnt, chunk_len)
     if (counters) { if (base) OIT_FWD2(true, true); else OIT_FWD2(false, true); }
     else { if (base) OIT_FWD2(true, false); else OIT_FWD2(false, false); }
 #undef OIT_FWD2

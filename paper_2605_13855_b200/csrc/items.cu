@@ -84,73 +84,102 @@ __global__ void __launch_bounds__(256) k_items_emit(const int32_t* __restrict__ 
 // max of its power over the quadrant's pixel-centre rectangle reaches thr_lo·(1+2^-10) (the step
 // 12b test on a smaller rectangle: conservative, so no contributing pixel is lost; pixel decisions
 // stay the spec's). On C2 a pair touches 2.2 quadrants on average: 55% of the pixels to evaluate.
-// One warp per tile (grid-stride). Pass 0 counts the quadrant lists (and keeps each pair's 4-bit
-// mask); pass 1 scatters the slots in list order (ballot prefix sums: deterministic).
-template <bool kScatter>
-__global__ void __launch_bounds__(128) k_quad_bin(DevCam cam, const float4* __restrict__ rec,
-                                                  const int32_t* __restrict__ pair_slot,
-                                                  const int32_t* __restrict__ offs, int64_t capacity,
-                                                  uint8_t* __restrict__ qmask, int32_t* __restrict__ qcount,
-                                                  const int32_t* __restrict__ qoffs, int32_t* __restrict__ qslot) {
-  const unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+// Pair-parallel (one thread per pair, persistent grid-stride; the per-tile lists vary from a few
+// to thousands of pairs, so a warp per tile left the long tiles' dependent gathers exposed):
+//   k_quad_count:   tile of the pair (binary search in the tile offsets), rec gather, 4-bit mask;
+//                   keeps tile<<4|mask per pair and counts the (tile, quadrant) lists with
+//                   warp-aggregated atomics (lanes of a warp mostly share a tile);
+//   scan of the 4·n_tiles counts → quadrant list offsets (also copied to the scatter cursors);
+//   k_quad_scatter: claims positions with aggregated atomics on the cursors and writes the slots.
+// The order inside a quadrant list is therefore not fixed (as the k_moments accumulation order,
+// which is atomic anyway); the lists' contents are.
+__device__ __forceinline__ int tile_of_pair(const int32_t* __restrict__ offs, int n_tiles, int j) {
+  int lo = 0, hi = n_tiles;  // last t with offs[t] <= j (offs non-decreasing, offs[0] = 0)
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(offs + mid) <= j) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Aggregated atomicAdd of 1 per active lane on ctr[key]; returns the lane's claimed position.
+__device__ __forceinline__ int agg_claim(int32_t* ctr, int key, unsigned active) {
+  const unsigned peers = __match_any_sync(active, key);
+  const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(ctr + key, __popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  return base + __popc(peers & ((1u << lane) - 1u));
+}
+
+__global__ void __launch_bounds__(256) k_quad_count(DevCam cam, const float4* __restrict__ rec,
+                                                    const int32_t* __restrict__ pair_slot,
+                                                    const int32_t* __restrict__ offs, int64_t capacity,
+                                                    uint32_t* __restrict__ tq, int32_t* __restrict__ qcount) {
   const int n_tiles = cam.TX * cam.TY;
-  for (int t = gw; t < n_tiles; t += nw) {
-    int64_t s64 = offs[t], e64 = offs[t + 1];
-    if (e64 > capacity) e64 = capacity;
-    if (s64 > e64) s64 = e64;
-    const int s = (int)s64, e = (int)e64;
-    int c0 = 0, c1 = 0, c2 = 0, c3 = 0;  // running counts (warp-uniform)
-    int b0s = 0, b1s = 0, b2s = 0, b3s = 0;
-    if (kScatter) {
-      b0s = qoffs[4 * t]; b1s = qoffs[4 * t + 1]; b2s = qoffs[4 * t + 2]; b3s = qoffs[4 * t + 3];
+  const int n = (int)min((int64_t)offs[n_tiles], capacity);
+  const int stride = gridDim.x * blockDim.x;
+  for (int j0 = blockIdx.x * blockDim.x; j0 < n; j0 += stride) {  // warp-uniform trip count
+    const int j = j0 + threadIdx.x;
+    const bool live = j < n;
+    unsigned m = 0;
+    int t = 0;
+    if (live) {
+      t = tile_of_pair(offs, n_tiles, j);
+      const float4* r = rec + (size_t)pair_slot[j] * kRec4;
+      m = quadrant_mask(cam, t, r[0], r[1]);
+      tq[j] = ((uint32_t)t << 4) | m;
     }
-    for (int j0 = s; j0 < e; j0 += 32) {
-      const int j = j0 + lane;
-      unsigned m = 0;
-      int slot = 0;
-      if (j < e) {
-        slot = pair_slot[j];
-        if (!kScatter) {
-          const float4* r = rec + (size_t)slot * kRec4;
-          m = quadrant_mask(cam, t, r[0], r[1]);
-          qmask[j] = (uint8_t)m;
-        } else {
-          m = qmask[j];
-        }
-      }
-      const unsigned lt = (1u << lane) - 1u;
-      const unsigned b0 = __ballot_sync(FULL, m & 1u), b1 = __ballot_sync(FULL, m & 2u);
-      const unsigned b2 = __ballot_sync(FULL, m & 4u), b3 = __ballot_sync(FULL, m & 8u);
-      if (kScatter) {
-        if (m & 1u) qslot[b0s + c0 + __popc(b0 & lt)] = slot;
-        if (m & 2u) qslot[b1s + c1 + __popc(b1 & lt)] = slot;
-        if (m & 4u) qslot[b2s + c2 + __popc(b2 & lt)] = slot;
-        if (m & 8u) qslot[b3s + c3 + __popc(b3 & lt)] = slot;
-      }
-      c0 += __popc(b0); c1 += __popc(b1); c2 += __popc(b2); c3 += __popc(b3);
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const unsigned act = __ballot_sync(0xffffffffu, live && (m >> q & 1u));
+      if (live && (m >> q & 1u)) agg_claim(qcount, 4 * t + q, act);
     }
-    if (!kScatter && lane == 0) {
-      qcount[4 * t + 0] = c0; qcount[4 * t + 1] = c1; qcount[4 * t + 2] = c2; qcount[4 * t + 3] = c3;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_quad_scatter(int n_tiles, const int32_t* __restrict__ pair_slot,
+                                                      const int32_t* __restrict__ offs, int64_t capacity,
+                                                      const uint32_t* __restrict__ tq, int32_t* __restrict__ cursor,
+                                                      int32_t* __restrict__ qslot) {
+  const int n = (int)min((int64_t)offs[n_tiles], capacity);
+  const int stride = gridDim.x * blockDim.x;
+  for (int j0 = blockIdx.x * blockDim.x; j0 < n; j0 += stride) {
+    const int j = j0 + threadIdx.x;
+    const bool live = j < n;
+    uint32_t v = 0;
+    int slot = 0;
+    if (live) {
+      v = tq[j];
+      slot = pair_slot[j];
+    }
+    const int t = (int)(v >> 4);
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const bool on = live && (v >> q & 1u);
+      const unsigned act = __ballot_sync(0xffffffffu, on);
+      if (on) qslot[agg_claim(cursor, 4 * t + q, act)] = slot;
     }
   }
 }
 
 void launch_quad_bin(const DevCam& cam, const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
-                     int64_t capacity, uint8_t* qmask, int32_t* qcount, int32_t* qoffs, int32_t* qslot, void* tmp,
+                     int64_t capacity, uint32_t* tq, int32_t* qcount, int32_t* qoffs, int32_t* qslot, void* tmp,
                      cudaStream_t st) {
   const int n_tiles = cam.TX * cam.TY;
-  const int qblocks = (n_tiles + 3) / 4;  // one warp per tile
+  const int blocks = sm_count() * 8;
   const float4* r4 = reinterpret_cast<const float4*>(rec);
-  k_quad_bin<false><<<qblocks, 128, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, qmask, qcount, qoffs, qslot);
+  cudaMemsetAsync(qcount, 0, sizeof(int32_t) * 4 * (size_t)n_tiles, st);
+  k_quad_count<<<blocks, 256, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, tq, qcount);
   launch_exclusive_scan(qcount, qoffs, 4 * (int64_t)n_tiles, tmp, st);
-  k_quad_bin<true><<<qblocks, 128, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, qmask, qcount, qoffs, qslot);
+  // the counts are consumed: reuse them as the scatter cursors (= the list starts)
+  cudaMemcpyAsync(qcount, qoffs, sizeof(int32_t) * 4 * (size_t)n_tiles, cudaMemcpyDeviceToDevice, st);
+  k_quad_scatter<<<blocks, 256, 0, st>>>(n_tiles, pair_slot, tile_offsets, capacity, tq, qcount, qslot);
 }
 
 size_t quad_bytes(int32_t n_tiles, int64_t capacity) {
-  return 2 * align_up((size_t)(4 * n_tiles + 1) * 4) + align_up((size_t)(4 * capacity) * 4) + align_up((size_t)capacity) +
-         scan_tmp_bytes(4 * (int64_t)n_tiles);
+  return 2 * align_up((size_t)(4 * n_tiles + 1) * 4) + align_up((size_t)(4 * capacity) * 4) +
+         align_up((size_t)capacity * 4) + scan_tmp_bytes(4 * (int64_t)n_tiles);
 }
 
 // Fused variant for small tile counts (grid ≤ SM count, hence co-resident): the histogram, a
