@@ -85,65 +85,85 @@ struct Moments {
   float U0, U1, U2, S, Od, M1, M2, XX, XY, YY;
 };
 
-// One lane = one splat; walks the pixel window [py0,py1]×[px0,px1] of its tile. The tile's
-// coefficients sit in this warp's shared-memory slice (broadcast reads). kClamp: some lane of the
-// warp may hit the 0.99 clamp (only splats with o ≥ 0.99 can: thr_hi ≤ 0).
+// One lane = one splat; walks the pixel window [py0,py1]×[px0,px1] of its tile, two pixels at a
+// time in packed f32x2 arithmetic (the pair (px, px+1), px even; the decision ops are per element
+// the scalar spec ops). The tile's coefficients sit in this warp's shared-memory slice as five
+// 8×8 planes (u_R, u_G, u_B, −s, a), read as 64-bit broadcasts. kClamp: some lane of the warp may
+// hit the 0.99 clamp (only splats with o ≥ 0.99 can: thr_hi ≤ 0).
 template <bool kClamp>
-__device__ __forceinline__ void moments_window(Moments& m, const float4* __restrict__ s_cu,
-                                               const float* __restrict__ s_ca, int qx0, int qy0, int tx0, int ty0,
-                                               int px0, int px1,
-                                               int py0, int py1, bool valid, float mx, float my, float nA, float nB,
-                                               float nC, float thr_lo, float thr_hi, float log2o, float cR, float cG,
-                                               float cB, float w, float kx, float ky, float ey) {
+__device__ __forceinline__ void moments_window(Moments& m, const float* __restrict__ s_u, int qx0, int qy0, int tx0,
+                                               int ty0, int px0, int px1, int py0, int py1, bool valid, float mx,
+                                               float my, float nA, float nB, float nC, float thr_lo, float thr_hi,
+                                               float log2o, float cR, float cG, float cB, float w, float kx, float ky,
+                                               float ey) {
   const unsigned FULL = 0xffffffffu;
+  const int pxe = px0 & ~1;
+  const f2_t mx2 = f2s(mx), nA2 = f2s(nA), nkx2 = f2s(-kx), l2e = f2s(kLog2e), one2 = f2s(1.0f);
+  const f2_t cR2 = f2s(cR), cG2 = f2s(cG), cB2 = f2s(cB), w2 = f2s(w);
+  f2_t U0 = 0ull, U1 = 0ull, U2 = 0ull, NS = 0ull;  // packed (even, odd pixel) partial sums; NS = −S
   for (int py = py0; py <= py1; py++) {
     const float dy = __fsub_rn((float)(ty0 + py), my);
     const bool ract = valid && fabsf(dy) <= ey;
     if (!__any_sync(FULL, ract)) continue;
-    const float by = __fmul_rn(nB, dy);
-    const float cyv = __fmul_rn(__fmul_rn(nC, dy), dy);
-    const float row_arg = fmaf(-ky, dy, log2o);
+    const f2_t by2 = f2s(__fmul_rn(nB, dy));
+    const f2_t cy2 = f2s(__fmul_rn(__fmul_rn(nC, dy), dy));
+    const f2_t ra2 = f2s(fmaf(-ky, dy, log2o));
     const float lo = ract ? thr_lo : 1.0f;  // folds the row test into the pixel test
-    float Rd = 0.f, Rdx = 0.f, Rdxx = 0.f;
-    const float4* cu_row = s_cu + (py - qy0) * 8 - qx0;  // the staged 8×8 quadrant
-    const float* ca_row = s_ca + (py - qy0) * 8 - qx0;
-#pragma unroll 4
-    for (int px = px0; px <= px1; px++) {
-      const float dx = __fsub_rn((float)(tx0 + px), mx);
-      const float power = spec_power_row(nA, dx, by, cyv);
-      const bool contrib = power <= 0.0f && power >= lo;
-      float alpha = ex2_approx(fmaf(-kx, dx, fmaf(power, kLog2e, row_arg)));
-      bool clamp = false;
+    f2_t Rd = 0ull, Rdx = 0ull, Rdxx = 0ull;
+    const float* row = s_u + (py - qy0) * 8 - qx0;
+    f2_t dx2 = sub2(f2((float)(tx0 + pxe), (float)(tx0 + pxe + 1)), mx2);
+    const f2_t two2 = f2s(2.0f);
+#pragma unroll 2
+    for (int px = pxe; px <= px1; px += 2) {
+      const f2_t pw2 = fma2(dx2, fma2(nA2, dx2, by2), cy2);
+      const float pl = f2lo(pw2), ph = f2hi(pw2);
+      const bool cl = pl <= 0.0f && pl >= lo, ch = ph <= 0.0f && ph >= lo;
+      const f2_t arg2 = fma2(nkx2, dx2, fma2(pw2, l2e, ra2));
+      const float el = ex2_approx(f2lo(arg2)), eh = ex2_approx(f2hi(arg2));
+      float al = cl ? el : 0.0f, ah = ch ? eh : 0.0f;
+      bool kl = false, kh = false;
       if (kClamp) {
-        clamp = power >= thr_hi;
-        alpha = clamp ? 0.99f : alpha;
+        kl = pl >= thr_hi;
+        kh = ph >= thr_hi;
+        al = cl ? (kl ? 0.99f : el) : 0.0f;
+        ah = ch ? (kh ? 0.99f : eh) : 0.0f;
       }
-      alpha = contrib ? alpha : 0.0f;
-      const float4 cu = cu_row[px];  // (u_R, u_G, u_B, s): broadcast
-      const float ca = ca_row[px];   // a
-      const float rinv = rcp_approx(1.0f - alpha);
-      const float dot = fmaf(cu.x, cR, fmaf(cu.y, cG, fmaf(cu.z, cB, -cu.w)));
-      float d = fmaf(ca, rinv, w * dot) * alpha;  // dL/dα · α (0 where α = 0)
-      if (kClamp) d = clamp ? 0.0f : d;
-      m.U0 = fmaf(alpha, cu.x, m.U0);
-      m.U1 = fmaf(alpha, cu.y, m.U1);
-      m.U2 = fmaf(alpha, cu.z, m.U2);
-      m.S = fmaf(alpha, cu.w, m.S);
-      const float t = d * dx;
-      Rd += d;
-      Rdx += t;
-      Rdxx = fmaf(t, dx, Rdxx);
+      const f2_t a2 = f2(al, ah);
+      const f2_t uR = *reinterpret_cast<const f2_t*>(row + px);  // broadcasts (64-bit)
+      const f2_t uG = *reinterpret_cast<const f2_t*>(row + 64 + px);
+      const f2_t uB = *reinterpret_cast<const f2_t*>(row + 128 + px);
+      const f2_t ns = *reinterpret_cast<const f2_t*>(row + 192 + px);
+      const f2_t ca = *reinterpret_cast<const f2_t*>(row + 256 + px);
+      const f2_t om = sub2(one2, a2);
+      const f2_t rinv = f2(rcp_approx(f2lo(om)), rcp_approx(f2hi(om)));
+      const f2_t dot = fma2(uR, cR2, fma2(uG, cG2, fma2(uB, cB2, ns)));
+      f2_t d = mul2(fma2(ca, rinv, mul2(w2, dot)), a2);  // dL/dα · α (0 where α = 0)
+      if (kClamp) d = f2(kl ? 0.0f : f2lo(d), kh ? 0.0f : f2hi(d));
+      fma2_acc(U0, a2, uR);
+      fma2_acc(U1, a2, uG);
+      fma2_acc(U2, a2, uB);
+      fma2_acc(NS, a2, ns);
+      const f2_t t = mul2(d, dx2);
+      add2_acc(Rd, d);
+      add2_acc(Rdx, t);
+      fma2_acc(Rdxx, t, dx2);
+      add2_acc(dx2, two2);  // next pair: dx + 2 (exact: small integers minus the same mx)
     }
-    m.Od += Rd;
-    m.M1 += Rdx;
-    m.M2 = fmaf(dy, Rd, m.M2);
-    m.XX += Rdxx;
-    m.XY = fmaf(dy, Rdx, m.XY);
-    m.YY = fmaf(dy * dy, Rd, m.YY);
+    const float rd = f2lo(Rd) + f2hi(Rd), rdx = f2lo(Rdx) + f2hi(Rdx), rdxx = f2lo(Rdxx) + f2hi(Rdxx);
+    m.Od += rd;
+    m.M1 += rdx;
+    m.M2 = fmaf(dy, rd, m.M2);
+    m.XX += rdxx;
+    m.XY = fmaf(dy, rdx, m.XY);
+    m.YY = fmaf(dy * dy, rd, m.YY);
   }
+  m.U0 += f2lo(U0) + f2hi(U0);
+  m.U1 += f2lo(U1) + f2hi(U1);
+  m.U2 += f2lo(U2) + f2hi(U2);
+  m.S -= f2lo(NS) + f2hi(NS);
 }
 
-__global__ void __launch_bounds__(kMomentsThreads, 8) k_moments(DevCam cam, const float4* __restrict__ rec,
+__global__ void __launch_bounds__(kMomentsThreads, 6) k_moments(DevCam cam, const float4* __restrict__ rec,
                                                              const int32_t* __restrict__ pair_slot,
                                                              const int32_t* __restrict__ offs, int64_t capacity,
                                                              const int2* __restrict__ items,
@@ -152,11 +172,9 @@ __global__ void __launch_bounds__(kMomentsThreads, 8) k_moments(DevCam cam, cons
                                                              const float4* __restrict__ coef4,
                                                              const float* __restrict__ coefa,
                                                              float* __restrict__ acc2d) {
-  __shared__ float4 s_cu_all[kMomentsThreads / 32][64];
-  __shared__ float s_ca_all[kMomentsThreads / 32][64];
+  __shared__ __align__(16) float s_u_all[kMomentsThreads / 32][5 * 64];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  float4* s_cu = s_cu_all[wid];
-  float* s_ca = s_ca_all[wid];
+  float* s_u = s_u_all[wid];
   const int n_items = *n_items_p;
   const unsigned FULL = 0xffffffffu;
   int staged = -1;
@@ -178,10 +196,9 @@ __global__ void __launch_bounds__(kMomentsThreads, 8) k_moments(DevCam cam, cons
       const float4 v1 = __ldcg(g4 + (qy0 + r0 + 4) * kTile + qx0 + c0);
       const float a0 = __ldcg(ga + (qy0 + r0) * kTile + qx0 + c0);
       const float a1 = __ldcg(ga + (qy0 + r0 + 4) * kTile + qx0 + c0);
-      s_cu[r0 * 8 + c0] = v0;
-      s_cu[(r0 + 4) * 8 + c0] = v1;
-      s_ca[r0 * 8 + c0] = a0;
-      s_ca[(r0 + 4) * 8 + c0] = a1;
+      const int i0 = r0 * 8 + c0, i1 = (r0 + 4) * 8 + c0;  // planes u_R, u_G, u_B, −s, a
+      s_u[i0] = v0.x; s_u[64 + i0] = v0.y; s_u[128 + i0] = v0.z; s_u[192 + i0] = -v0.w; s_u[256 + i0] = a0;
+      s_u[i1] = v1.x; s_u[64 + i1] = v1.y; s_u[128 + i1] = v1.z; s_u[192 + i1] = -v1.w; s_u[256 + i1] = a1;
       __syncwarp();
       staged = vt;
     }
@@ -214,10 +231,10 @@ __global__ void __launch_bounds__(kMomentsThreads, 8) k_moments(DevCam cam, cons
     const int py1 = min(qy0 + 7, (int)ceilf(fminf(hi_y - (float)ty0, 16.f)));
     Moments m = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (__any_sync(FULL, valid && q1.z <= 0.0f))
-      moments_window<true>(m, s_cu, s_ca, qx0, qy0, tx0, ty0, px0, px1, py0, py1, valid, mx, my, q0.z, q0.w, q1.x, q1.y, q1.z,
+      moments_window<true>(m, s_u, qx0, qy0, tx0, ty0, px0, px1, py0, py1, valid, mx, my, q0.z, q0.w, q1.x, q1.y, q1.z,
                            q1.w, q2.x, q2.y, q2.z, q2.w, q3.z, q3.w, ey);
     else
-      moments_window<false>(m, s_cu, s_ca, qx0, qy0, tx0, ty0, px0, px1, py0, py1, valid, mx, my, q0.z, q0.w, q1.x, q1.y, q1.z,
+      moments_window<false>(m, s_u, qx0, qy0, tx0, ty0, px0, px1, py0, py1, valid, mx, my, q0.z, q0.w, q1.x, q1.y, q1.z,
                             q1.w, q2.x, q2.y, q2.z, q2.w, q3.z, q3.w, ey);
     if (valid && (m.U0 != 0.f || m.U1 != 0.f || m.U2 != 0.f || m.S != 0.f || m.Od != 0.f)) {
       float* a = acc2d + (size_t)slot * 12;
@@ -573,7 +590,7 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
     // quadrant sub-binning of the tile lists, then (quadrant, 32-slot chunk) items
     launch_quad_bin(cam, rec, pair_slot, tile_offsets, capacity, tq, qcount, qoffs, qslot, tmp, st);
     launch_build_items(qoffs, 4 * n_tiles, qcap, 32, 0, items, n_items, tile_nch, scratch, st);
-    const int blocks = sm_count() * 8;  // persistent: 8 × 4 warps per SM, dynamic item claiming
+    const int blocks = sm_count() * 6;  // persistent: 6 × 4 warps per SM (80 regs), dynamic item claiming
     record_event(ev_begin, st);
     k_moments<<<blocks, kMomentsThreads, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), qslot, qoffs,
                                                   qcap, items, n_items, counter,
