@@ -254,41 +254,22 @@ constexpr float kLog2e = 1.4426950408889634f;
 // ---------------------------------------------------------------- packed f32x2 (sm_100a) -----
 // Blackwell's FFMA2 / FADD2 / FMUL2 do two IEEE round-to-nearest fp32 operations per instruction
 // (per element identical to the scalar __fmaf_rn / __fadd_rn / __fmul_rn), halving the issue
-// slots of the ALU-bound per-pixel loops. A pair lives in one 64-bit register pair.
-typedef unsigned long long f2_t;
-__device__ __forceinline__ f2_t f2(float lo, float hi) {
-  f2_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ f2_t f2s(float v) { return f2(v, v); }
-__device__ __forceinline__ float f2lo(f2_t r) { return __uint_as_float((unsigned)(r & 0xffffffffull)); }
-__device__ __forceinline__ float f2hi(f2_t r) { return __uint_as_float((unsigned)(r >> 32)); }
-__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
-  f2_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-// in place: acc ← fma(a, b, acc) / acc ← acc + b (keeps loop-carried pairs in their registers)
-__device__ __forceinline__ void fma2_acc(f2_t& acc, f2_t a, f2_t b) {
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
-}
-__device__ __forceinline__ void add2_acc(f2_t& acc, f2_t b) { asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(b)); }
-__device__ __forceinline__ f2_t add2(f2_t a, f2_t b) {
-  f2_t d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f2_t sub2(f2_t a, f2_t b) {
-  f2_t d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
-  f2_t d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
+// slots of the ALU-bound per-pixel loops. A pair is a float2 (one 64-bit register pair); the __ffma2_rn / __fadd2_rn /
+// __fmul2_rn builtins let the compiler keep loop-carried pairs in place and fold negations.
+typedef float2 f2_t;
+__device__ __forceinline__ f2_t f2(float lo, float hi) { return make_float2(lo, hi); }
+__device__ __forceinline__ f2_t f2s(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float f2lo(f2_t r) { return r.x; }
+__device__ __forceinline__ float f2hi(f2_t r) { return r.y; }
+__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ f2_t add2(f2_t a, f2_t b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ f2_t sub2(f2_t a, f2_t b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) { return __fmul2_rn(a, b); }
+// in place: acc ← fma(a, b, acc) / acc ← acc + b
+__device__ __forceinline__ void fma2_acc(f2_t& acc, f2_t a, f2_t b) { acc = __ffma2_rn(a, b, acc); }
+__device__ __forceinline__ void add2_acc(f2_t& acc, f2_t b) { acc = __fadd2_rn(acc, b); }
+// T ← T − α·T in one rounding (= fmaf(−α, T, T) per element)
+__device__ __forceinline__ void decay2(f2_t& T, f2_t al) { T = __ffma2_rn(make_float2(-al.x, -al.y), T, T); }
 
 // 3DGS real SH basis, degree 3 (Eq. 4).
 constexpr float SH_C0 = 0.28209479177387814f;

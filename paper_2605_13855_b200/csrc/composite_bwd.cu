@@ -100,7 +100,7 @@ __device__ __forceinline__ void moments_window(Moments& m, const float* __restri
   const int pxe = px0 & ~1;
   const f2_t mx2 = f2s(mx), nA2 = f2s(nA), nkx2 = f2s(-kx), l2e = f2s(kLog2e), one2 = f2s(1.0f);
   const f2_t cR2 = f2s(cR), cG2 = f2s(cG), cB2 = f2s(cB), w2 = f2s(w);
-  f2_t U0 = 0ull, U1 = 0ull, U2 = 0ull, NS = 0ull;  // packed (even, odd pixel) partial sums; NS = −S
+  f2_t U0 = f2s(0.f), U1 = f2s(0.f), U2 = f2s(0.f), NS = f2s(0.f);  // packed (even, odd pixel) partial sums; NS = −S
   for (int py = py0; py <= py1; py++) {
     const float dy = __fsub_rn((float)(ty0 + py), my);
     const bool ract = valid && fabsf(dy) <= ey;
@@ -109,7 +109,7 @@ __device__ __forceinline__ void moments_window(Moments& m, const float* __restri
     const f2_t cy2 = f2s(__fmul_rn(__fmul_rn(nC, dy), dy));
     const f2_t ra2 = f2s(fmaf(-ky, dy, log2o));
     const float lo = ract ? thr_lo : 1.0f;  // folds the row test into the pixel test
-    f2_t Rd = 0ull, Rdx = 0ull, Rdxx = 0ull;
+    f2_t Rd = f2s(0.f), Rdx = f2s(0.f), Rdxx = f2s(0.f);
     const float* row = s_u + (py - qy0) * 8 - qx0;
     f2_t dx2 = sub2(f2((float)(tx0 + pxe), (float)(tx0 + pxe + 1)), mx2);
     const f2_t two2 = f2s(2.0f);

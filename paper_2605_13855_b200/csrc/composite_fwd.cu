@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
         const float pw0 = f2lo(pwA), pw1 = f2hi(pwA), pw2 = f2lo(pwB), pw3 = f2hi(pwB);
         const bool c0 = pw0 <= 0.0f && pw0 >= q1.y, c1 = pw1 <= 0.0f && pw1 >= q1.y;
         const bool c2 = pw2 <= 0.0f && pw2 >= q1.y, c3 = pw3 <= 0.0f && pw3 >= q1.y;
-        if (c0 || c1 || c2 || c3) {  // branch-free inside: α = 0 for the non-contributing pixels
+        if (__any_sync(0xffffffffu, c0 || c1 || c2 || c3)) {  // warp-uniform; α = 0 for the others
           const float4 q2 = s_q2[i];  // cR cG cB w
           const float2 kk = s_k[i];   // sub-ulp μ' correction of the exponent (value path)
           const f2_t base2 = f2s(fmaf(-kk.y, dy, q1.w)), nkx2 = f2s(-kk.x), l2e = f2s(kLog2e);
@@ -126,17 +126,22 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
           const f2_t argB = fma2(nkx2, dxB, fma2(pwB, l2e, base2));
           const float e0 = ex2_approx(f2lo(argA)), e1 = ex2_approx(f2hi(argA));
           const float e2 = ex2_approx(f2lo(argB)), e3 = ex2_approx(f2hi(argB));
-          const float a0 = c0 ? (pw0 >= q1.z ? 0.99f : e0) : 0.0f;
-          const float a1 = c1 ? (pw1 >= q1.z ? 0.99f : e1) : 0.0f;
-          const float a2 = c2 ? (pw2 >= q1.z ? 0.99f : e2) : 0.0f;
-          const float a3 = c3 ? (pw3 >= q1.z ? 0.99f : e3) : 0.0f;
-          const f2_t alA = f2(a0, a1), alB = f2(a2, a3), w2 = f2s(q2.w), neg1 = f2s(-1.0f);
+          float a0, a1, a2, a3;
+          if (q1.z > 0.0f) {  // o < 0.99: a contributing power (≤ 0) never reaches thr_hi (warp-uniform)
+            a0 = c0 ? e0 : 0.0f; a1 = c1 ? e1 : 0.0f; a2 = c2 ? e2 : 0.0f; a3 = c3 ? e3 : 0.0f;
+          } else {
+            a0 = c0 ? (pw0 >= q1.z ? 0.99f : e0) : 0.0f;
+            a1 = c1 ? (pw1 >= q1.z ? 0.99f : e1) : 0.0f;
+            a2 = c2 ? (pw2 >= q1.z ? 0.99f : e2) : 0.0f;
+            a3 = c3 ? (pw3 >= q1.z ? 0.99f : e3) : 0.0f;
+          }
+          const f2_t alA = f2(a0, a1), alB = f2(a2, a3), w2 = f2s(q2.w);
           const f2_t awA = mul2(alA, w2), awB = mul2(alB, w2);
           const f2_t cR = f2s(q2.x), cG = f2s(q2.y), cB = f2s(q2.z);
           fma2_acc(PA0, cR, awA); fma2_acc(PA1, cG, awA); fma2_acc(PA2, cB, awA); add2_acc(QA, awA);
           fma2_acc(PB0, cR, awB); fma2_acc(PB1, cG, awB); fma2_acc(PB2, cB, awB); add2_acc(QB, awB);
-          fma2_acc(TA, mul2(alA, neg1), TA);  // T ← T − αT (one rounding, as fmaf(−α, T, T))
-          fma2_acc(TB, mul2(alB, neg1), TB);
+          decay2(TA, alA);  // T ← T − αT (one rounding, as fmaf(−α, T, T))
+          decay2(TB, alB);
           if (kCount) {
             if (ty0 + ly < cam.H)
               n_contrib += (c0 && tx0 + lx < cam.W) + (c1 && tx0 + lx + 4 < cam.W) + (c2 && tx0 + lx + 8 < cam.W) +
