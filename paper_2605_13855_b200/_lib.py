@@ -234,7 +234,7 @@ def oit_score_subsample(rows, sigma, cams, targets, caches, active_idx, score_id
     sc = scene(rows, sigma)
     V = len(cams)
     cam_arr = (Camera * V)(*[camera(c) for c in cams])
-    tg = (C.c_void_p * V)(*[t.data_ptr() for t in targets])
+    tg = (C.c_void_p * V)(*[(t.data_ptr() if t is not None else None) for t in targets])
     ch = (C.c_void_p * V)(*[(c.data_ptr() if c is not None else None) for c in caches]) if caches is not None else None
     vw = (C.c_int32 * len(views))(*[int(v) for v in views])
     _check(lib().oit_score_subsample(C.byref(sc), cam_arr, V, tg, ch, _ptr(active_idx), int(active_idx.numel()),

@@ -166,7 +166,7 @@ __device__ __forceinline__ void moments_window(Moments& m, const float* __restri
 __global__ void __launch_bounds__(kMomentsThreads, 6) k_moments(DevCam cam, const float4* __restrict__ rec,
                                                              const int32_t* __restrict__ pair_slot,
                                                              const int32_t* __restrict__ offs, int64_t capacity,
-                                                             const int2* __restrict__ items,
+                                                             const int4* __restrict__ items,
                                                              const int32_t* __restrict__ n_items_p,
                                                              int32_t* __restrict__ counter,
                                                              const float4* __restrict__ coef4,
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kMomentsThreads, 6) k_moments(DevCam cam, cons
     if (lane == 0) item = atomicAdd(counter, 1);
     item = __shfl_sync(FULL, item, 0);
     if (item >= n_items) return;
-    const int2 it = items[item];
+    const int4 it = items[item];
     const int vt = it.x, chunk = it.y;  // vt = 4·tile + quadrant
     const int tile = vt >> 2, quad = vt & 3;
     const int qx0 = 8 * (quad & 1), qy0 = 8 * (quad >> 1);
@@ -569,7 +569,7 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
   const int64_t max_items = qcap / 32 + 4 * n_tiles + 1;
   Carve cv(ws);
   float* acc2d = cv.take<float>((size_t)n_slots * 12);
-  int2* items = cv.take<int2>(max_items);
+  int4* items = cv.take<int4>(max_items);
   int32_t* n_items = cv.take<int32_t>(4);
   int32_t* tile_nch = cv.take<int32_t>(4 * n_tiles + 1);
   int32_t* scratch = cv.take<int32_t>(68);

@@ -49,7 +49,7 @@ __device__ __forceinline__ void store_px(const Px& a, float* dst, size_t plane, 
 template <bool kBase, bool kCount>
 __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
     DevCam cam, const float4* __restrict__ rec, const int32_t* __restrict__ pair_slot,
-    const int32_t* __restrict__ offs, int64_t capacity, const int2* __restrict__ items,
+    const int32_t* __restrict__ offs, int64_t capacity, const int4* __restrict__ items,
     const int32_t* __restrict__ n_items_p, int32_t* __restrict__ counter, const int32_t* __restrict__ tile_nch,
     int32_t* __restrict__ done, float* __restrict__ partial, const float* __restrict__ base,
     float* __restrict__ image, float* __restrict__ state, unsigned long long* __restrict__ counters, int chunk_len) {
@@ -68,8 +68,8 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
     const int item = s_item;
     __syncthreads();
     if (item >= n_items) return;
-    const int2 it = items[item];
-    const int tile = it.x, chunk = it.y;
+    const int4 it = items[item];
+    const int tile = it.x;
     const int nch = tile_nch[tile];
     const int tx0 = (tile % cam.TX) * kTile, ty0 = (tile / cam.TX) * kTile;
     const float fy = (float)(ty0 + ly), fx0 = (float)(tx0 + lx);
@@ -88,10 +88,7 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
     f2_t TA = f2(a[0].T, a[1].T);
     f2_t PB0 = f2(a[2].P0, a[3].P0), PB1 = f2(a[2].P1, a[3].P1), PB2 = f2(a[2].P2, a[3].P2), QB = f2(a[2].Q, a[3].Q);
     f2_t TB = f2(a[2].T, a[3].T);
-    int64_t e64 = offs[tile + 1];
-    if (e64 > capacity) e64 = capacity;
-    const int begin = offs[tile] + chunk * chunk_len;
-    const int end = (int)min((int64_t)begin + chunk_len, e64);
+    const int begin = it.z, end = it.w;  // the chunk's pair range (clipped to capacity by the builder)
     int n_contrib = 0;
     for (int b = begin; b < end; b += kFwdThreads) {
       const int n = min(kFwdThreads, end - b);
@@ -175,7 +172,7 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
       write_final = s_last;
       if (write_final) {
         __threadfence();
-        const int first = item - chunk;
+        const int first = item - it.y;  // chunks of a tile are contiguous items
 #pragma unroll
         for (int k = 0; k < 4; k++) {
           if (kBase) load_px(a[k], base, plane, pxb + 4 * k);
@@ -326,7 +323,7 @@ void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pa
     const int chunk_len = kFwdChunk;
     const int64_t max_items = capacity / chunk_len + n_tiles + 1;
     Carve cv(ws);
-    int2* items = cv.take<int2>(max_items);
+    int4* items = cv.take<int4>(max_items);
     int32_t* n_items = cv.take<int32_t>(4);
     int32_t* tile_nch = cv.take<int32_t>(n_tiles + 1);
     int32_t* scratch = cv.take<int32_t>(68);

@@ -5,7 +5,9 @@
 // of at most `chunk` slots and the items are ordered by descending list length (bucketed by
 // ⌈log2 L⌉): persistent CTAs/warps claim items from an atomic counter, heavy tiles start first and
 // the light ones fill the tail. Items of one tile are contiguous, so chunk k of the tile whose
-// first item is f sits at f + k. Two grid-wide kernels: a bucket histogram, then the emission.
+// first item is f sits at f + k. An item is int4 (tile, chunk, first pair, end pair), so a consumer
+// reaches its pair range with one load. Two grid-wide kernels: a bucket histogram, then the
+// emission (fused into one launch with a grid barrier when the grid is co-resident).
 #include "kernels.h"
 
 namespace oit {
@@ -13,10 +15,12 @@ namespace oit {
 constexpr int kNB = 33;  // buckets: 0 (empty tile) and 1..32 (= bit length of L)
 
 __device__ __forceinline__ void tile_len(const int32_t* offs, int t, int64_t capacity, int chunk, int empty_items,
-                                         int& nch, int& b) {
+                                         int& nch, int& b, int& js, int& je) {
   int64_t s = offs[t], e = offs[t + 1];
   if (e > capacity) e = capacity;
   if (s > e) s = e;
+  js = (int)s;
+  je = (int)e;
   const int L = (int)(e - s);
   nch = L > 0 ? (L + chunk - 1) / chunk : empty_items;
   b = L > 0 ? 32 - __clz(L) : 0;
@@ -30,8 +34,8 @@ __global__ void __launch_bounds__(256) k_items_hist(const int32_t* __restrict__ 
   __syncthreads();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < n_tiles) {
-    int nch, b;
-    tile_len(offs, t, capacity, chunk, empty_items, nch, b);
+    int nch, b, js, je;
+    tile_len(offs, t, capacity, chunk, empty_items, nch, b, js, je);
     if (nch) atomicAdd(&s_cnt[b], nch);
   }
   __syncthreads();
@@ -40,7 +44,7 @@ __global__ void __launch_bounds__(256) k_items_hist(const int32_t* __restrict__ 
 
 __global__ void __launch_bounds__(256) k_items_emit(const int32_t* __restrict__ offs, int n_tiles, int64_t capacity,
                                                     int chunk, int empty_items, int32_t* __restrict__ g,
-                                                    int2* __restrict__ items, int32_t* __restrict__ n_items,
+                                                    int4* __restrict__ items, int32_t* __restrict__ n_items,
                                                     int32_t* __restrict__ tile_nch) {
   __shared__ int s_off[kNB];
   if (threadIdx.x == 0) {  // descending bucket order: longest lists first
@@ -54,8 +58,8 @@ __global__ void __launch_bounds__(256) k_items_emit(const int32_t* __restrict__ 
   __syncthreads();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_tiles) return;
-  int nch, b;
-  tile_len(offs, t, capacity, chunk, empty_items, nch, b);
+  int nch, b, js, je;
+  tile_len(offs, t, capacity, chunk, empty_items, nch, b, js, je);
   if (tile_nch) tile_nch[t] = nch;
   if (!nch) return;
   // one cursor claim per (warp, bucket)
@@ -75,7 +79,7 @@ __global__ void __launch_bounds__(256) k_items_emit(const int32_t* __restrict__ 
   if (lane == leader) base = atomicAdd(g + kNB + b, total);
   base = __shfl_sync(peers, base, leader);
   const int pos = s_off[b] + base + before;
-  for (int c = 0; c < nch; c++) items[pos + c] = make_int2(t, c);
+  for (int c = 0; c < nch; c++) items[pos + c] = make_int4(t, c, js + c * chunk, min(je, js + (c + 1) * chunk));
 }
 
 // ------------------------------------------------------------- quadrant sub-binning ----
@@ -186,16 +190,16 @@ size_t quad_bytes(int32_t n_tiles, int64_t capacity) {
 // software grid barrier and the emission in one launch. g[66] is the barrier counter.
 __global__ void __launch_bounds__(256) k_items_fused(const int32_t* __restrict__ offs, int n_tiles, int64_t capacity,
                                                      int chunk, int empty_items, int32_t* __restrict__ g,
-                                                     int2* __restrict__ items, int32_t* __restrict__ n_items,
+                                                     int4* __restrict__ items, int32_t* __restrict__ n_items,
                                                      int32_t* __restrict__ tile_nch) {
   __shared__ int s_cnt[kNB];
   __shared__ int s_off[kNB];
   if (threadIdx.x < kNB) s_cnt[threadIdx.x] = 0;
   __syncthreads();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  int nch = 0, b = 0;
+  int nch = 0, b = 0, js = 0, je = 0;
   if (t < n_tiles) {
-    tile_len(offs, t, capacity, chunk, empty_items, nch, b);
+    tile_len(offs, t, capacity, chunk, empty_items, nch, b, js, je);
     if (tile_nch) tile_nch[t] = nch;
     if (nch) atomicAdd(&s_cnt[b], nch);
   }
@@ -233,19 +237,19 @@ __global__ void __launch_bounds__(256) k_items_fused(const int32_t* __restrict__
     if (lane == leader) base = atomicAdd(g + kNB + b, total);
     base = __shfl_sync(peers, base, leader);
     const int pos = s_off[b] + base + before;
-    for (int c = 0; c < nch; c++) items[pos + c] = make_int2(t, c);
+    for (int c = 0; c < nch; c++) items[pos + c] = make_int4(t, c, js + c * chunk, min(je, js + (c + 1) * chunk));
   }
 }
 
 size_t items_bytes(int32_t n_tiles, int64_t capacity, int chunk) {
   const int64_t max_items = capacity / chunk + n_tiles + 1;
-  return align_up((size_t)max_items * sizeof(int2)) + align_up(16) + align_up((size_t)(n_tiles + 1) * 4) +
+  return align_up((size_t)max_items * sizeof(int4)) + align_up(16) + align_up((size_t)(n_tiles + 1) * 4) +
          align_up((2 * kNB + 2) * sizeof(int32_t));
 }
 
 // items [capacity/chunk + n_tiles + 1], n_items [1], tile_nch [n_tiles], g = 2·kNB ints of scratch
 void launch_build_items(const int32_t* tile_offsets, int n_tiles, int64_t capacity, int chunk, int empty_items,
-                        int2* items, int32_t* n_items, int32_t* tile_nch, int32_t* g, cudaStream_t st) {
+                        int4* items, int32_t* n_items, int32_t* tile_nch, int32_t* g, cudaStream_t st) {
   const int blocks = (n_tiles + 255) / 256;
   cudaMemsetAsync(g, 0, (2 * kNB + 2) * sizeof(int32_t), st);
   if (blocks <= sm_count()) {

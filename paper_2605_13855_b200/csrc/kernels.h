@@ -32,7 +32,7 @@ size_t fwd_ws_bytes(int32_t n_tiles, int64_t capacity);
 // items.cu — (tile, chunk) work lists, longest tiles first
 size_t items_bytes(int32_t n_tiles, int64_t capacity, int chunk);
 void launch_build_items(const int32_t* tile_offsets, int n_tiles, int64_t capacity, int chunk, int empty_items,
-                        int2* items, int32_t* n_items, int32_t* tile_nch, int32_t* scratch68, cudaStream_t st);
+                        int4* items, int32_t* n_items, int32_t* tile_nch, int32_t* scratch68, cudaStream_t st);
 
 // quadrant sub-binning: qoffs[4·n_tiles+1], qslot[4·capacity] (lists of the 8×8 quadrants; order
 // within a list unspecified), tq[capacity] and qcount[4·n_tiles] scratch, tmp = scan_tmp_bytes(4·n_tiles)
@@ -101,6 +101,10 @@ void launch_update(const float* score_grad, const int32_t* score_idx, int32_t n_
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 // Bump allocator over a caller workspace.
+// DEV: kernel-variant selector for in-process A/B timing (0 = product kernels); set through
+// oit_dev_set_variant. Not part of the hot-path contract.
+int dev_variant();
+
 struct Carve {
   char* base;
   size_t off = 0;

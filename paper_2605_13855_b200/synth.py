@@ -177,6 +177,23 @@ def target_image(cam: dict, seed: int) -> np.ndarray:
     return rng(seed).uniform(0.0, 1.0, (3, cam["height"], cam["width"])).astype(np.float32)
 
 
+def pixel_state(cam: dict, seed: int) -> np.ndarray:
+    """Synthetic pre-render cache [5,H,W] fp32 (planes P_R, P_G, P_B, Q, T) shaped
+    like the frozen-set accumulators of Eq. 7: with A = Σα ~ U[0,3] per pixel, T = e^{−A·U[0.8,1.2]}
+    (≥ 0.01), Q = A·U[0.3,1.5] (w in the synthetic range) and P = F·Q with F ~ U[0,1]³ — so a pixel
+    with little coverage has both Q ≈ 0 and T ≈ 1, as a real cache does. A seeded input for parity
+    tests at sizes where the oracle cannot render the frozen set."""
+    g = rng(seed)
+    H, W = cam["height"], cam["width"]
+    a = g.uniform(0.0, 3.0, (H, W))
+    q = a * g.uniform(0.3, 1.5, (H, W))
+    out = np.empty((5, H, W))
+    out[0:3] = g.uniform(0.0, 1.0, (3, H, W)) * q[None]
+    out[3] = q
+    out[4] = np.maximum(np.exp(-a * g.uniform(0.8, 1.2, (H, W))), 0.01)
+    return out.astype(np.float32)
+
+
 def bits_from_mask(mask: np.ndarray) -> np.ndarray:
     n = len(mask)
     padded = np.zeros(((n + 31) // 32) * 32, bool)
