@@ -835,6 +835,20 @@ def time_e2e(args, torch, dist, wl, step, flush, allred):
     return dict(ms=ms, h2d=h2d, d2h=d2h)
 
 
+def _ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the newest committed
+    ncu --set full capture summary (profiles/<round>_traffic.json, tools/traffic_json.py), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
+    if not files:
+        return None, None
+    try:
+        d = json.load(open(files[-1]))[kernel]
+        return d["dram_bytes_per_launch"], f"profiles/{os.path.basename(files[-1])} ({d['report']}, one C2 view)"
+    except Exception:
+        return None, None
+
+
 def mpix_per_s(res, world):
     return world * res["V"] * res["H"] * res["W"] / (res["ms"] * 1e-3) / 1e6
 
@@ -847,9 +861,10 @@ def build_line(args, world, res, results):
     fwd_flops = res["tile_evals"] * FWD_F_TEST + res["contrib"] * FWD_F_CONTRIB
     bwd_flops = res["tile_evals"] * BWD_F_TEST + res["contrib"] * BWD_F_CONTRIB
     if res["ser_bwd_ms"] >= res["ser_fwd_ms"]:
-        kern, flops, kms = "k_moments (oit_composite_bwd a5)", bwd_flops, res["ser_bwd_ms"]
+        kern, flops, kms, tkey = "k_moments (oit_composite_bwd a5)", bwd_flops, res["ser_bwd_ms"], "k_moments"
     else:
-        kern, flops, kms = "k_fwd_items (oit_composite_fwd a3)", fwd_flops, res["ser_fwd_ms"]
+        kern, flops, kms, tkey = "k_fwd_items (oit_composite_fwd a3)", fwd_flops, res["ser_fwd_ms"], "k_fwd_items<1, 0>"
+    traffic, traffic_src = _ncu_traffic(tkey)
     achieved = flops / (kms * 1e-3) / 1e12
     sweep = {}
     for rho, r in sorted(results.items(), reverse=True):
@@ -880,7 +895,8 @@ def build_line(args, world, res, results):
         "segments_ms": {"train_views": res["train_ms"], "refresh": res["refresh_ms"]},
         "roofline": {"kernel": kern, "bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
                      "algorithmic_flops_per_step": flops, "kernel_ms_per_step": kms,
-                     "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS, "traffic": None,
+                     "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "peak_source": "148 SMs x 128 FP32 lanes x 2 (FMA) x 1965 MHz (B200_PROFILING.md unit counts)"},
         "clocks": res["clocks"], "gpu_launches": res["launches"] * args.steps,
         "sweep": sweep,
