@@ -153,6 +153,52 @@ def scene_c3(seed: int = 3, n: int = 3_000_000, n_views: int = 200, width: int =
     return Scene("C3", rows, 25.0, cams, np.array([0.0, 0.0, 0.0]), dict(seed=seed))
 
 
+def scene_degenerate(seed: int = 5) -> Scene:
+    """C1 (300 splats, 4 views 64×64) plus hand-set edge-case splats: zero quaternion, opacity at
+    and just above 1/255, opacity 1 and 0.995 (the 0.99 clamp at the centre), a splat at the look-at
+    point (centre on the principal point), one huge splat covering every view, needle-thin and
+    flat splats, a splat behind/at the near plane of every view, far off-screen splats whose extent
+    reaches the border, exact duplicates, a colour channel clamped at 0 (h DC very negative), a
+    weight SH that is negative in some directions (the v⁺ guard, R4) and splats beyond σ (w = 0)."""
+    base = scene_c1(seed=seed, n=300, n_views=4)
+    rows = [r for r in base.rows]
+
+    def splat(mu, s=(0.05, 0.05, 0.05), o=0.7, q=(1.0, 0.0, 0.0, 0.0), dc=(0.3, 0.2, -0.1), vdc=4.0, vrest=None):
+        r = np.zeros(ROW, np.float32)
+        r[MU:MU + 3] = mu
+        r[O] = o
+        r[Q:Q + 4] = q
+        r[S:S + 3] = s
+        r[H:H + 3] = dc
+        r[V] = vdc
+        if vrest is not None:
+            r[V + 1:V + 4] = vrest
+        rows.append(r)
+
+    splat((0.1, 0.1, 0.1), q=(0.0, 0.0, 0.0, 0.0))                  # zero quaternion → culled
+    splat((0.2, -0.1, 0.0), o=np.float32(1.0 / 255.0))              # 255·o ≤ 1 → culled
+    splat((0.2, -0.2, 0.1), o=np.nextafter(np.float32(1.0 / 255.0), np.float32(1)) * np.float32(1.001))
+    splat((-0.3, 0.2, 0.0), o=1.0)                                  # α clamped to 0.99 near the centre
+    splat((0.3, 0.3, -0.2), o=0.995)
+    splat((0.0, 0.0, 0.0), s=(0.08, 0.08, 0.08))                    # on the look-at point: centre on (cx, cy)
+    splat((0.0, 0.0, 0.0), s=(3.0, 3.0, 3.0), o=0.05)               # covers every view (huge extent)
+    splat((0.4, 0.0, 0.2), s=(1e-4, 0.3, 0.3))                      # flat disc
+    splat((-0.4, 0.1, 0.2), s=(1e-4, 1e-4, 0.4), q=(0.7, 0.1, 0.7, 0.1))   # needle
+    for c in base.cams:                                             # at / behind every camera centre
+        ctr = np.asarray(c["center"], np.float64)
+        splat(tuple(ctr * 1.0001))
+        splat(tuple(ctr * 1.3))
+    splat((6.0, 0.0, 0.3), s=(0.6, 0.6, 0.6))                       # off-screen centre, extent on screen
+    splat((0.0, -6.0, 0.3), s=(0.6, 0.6, 0.6))
+    for _ in range(2):
+        splat((0.15, 0.25, -0.05), o=0.6, dc=(0.1, 0.4, 0.2))       # exact duplicates
+    splat((-0.1, -0.3, 0.1), dc=(-3.0, 0.5, 0.5))                   # red channel clamped at 0
+    splat((0.25, -0.25, -0.1), vdc=0.3, vrest=(2.0, 2.0, 2.0))      # v(r) < 0 for some directions
+    for c in base.cams:                                             # on the view axis beyond σ: w = 0, still in T
+        splat(tuple(-0.35 * np.asarray(c["center"], np.float64)), s=(0.15, 0.15, 0.15))
+    return Scene("degenerate", np.stack(rows).astype(np.float32), base.sigma, base.cams, base.bg, dict(seed=seed))
+
+
 def active_mask(scene: Scene, rho: float, kind: str = "clustered", seed: int = 11) -> np.ndarray:
     """Forced active set of fraction ρ: 'uniform' (Bernoulli(ρ)) or 'clustered' (μ_x in the top ρ
     quantile — the paper's "small objects … large number of iterations")."""

@@ -287,7 +287,7 @@ def test_order_independence():
 
 def test_brute_force_equals_tiled():
     """R9: the conservative opacity-aware rectangle loses no contributing pair (all-pairs == tiled)."""
-    for sc in (synth.scene_c1(), synth.scene_c1(seed=5, n=3000, res=96)):
+    for sc in (synth.scene_c1(), synth.scene_c1(seed=5, n=3000, res=96), synth.scene_degenerate()):
         idx = np.arange(sc.n)
         for cam in sc.cams:
             a = O.render(sc.rows, sc.sigma, idx, cam, sc.bg, mode="brute")
