@@ -66,7 +66,9 @@ def parse():
     ap.add_argument("--splats", type=int, default=300_000)
     ap.add_argument("--res", type=int, default=800)
     ap.add_argument("--sub-rate", type=float, default=0.05, help="refresh subsample rate S/V")
-    ap.add_argument("--streams", type=int, default=8, help="training views processed concurrently (one stream each)")
+    ap.add_argument("--streams", type=int, default=16, help="training views processed concurrently (one stream each)")
+    ap.add_argument("--targets", choices=["u8", "f32"], default="u8",
+                    help="training-image format: 8-bit (the datasets' PNGs, OIT_TARGET_U8) or fp32")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -297,7 +299,10 @@ class Workload:
         self.caches = torch.empty((self.V, 5, nt, 256), dtype=torch.float32, device=dev)
         gen = torch.Generator(device=dev)
         gen.manual_seed(1234 + rank)
-        self.targets = torch.rand((self.V, 3, H, W), generator=gen, device=dev, dtype=torch.float32)
+        if args.targets == "u8":   # 8-bit training images (OIT_TARGET_U8: read as u8/255 by the loss kernels)
+            self.targets = torch.randint(0, 256, (self.V, 3, H, W), generator=gen, device=dev, dtype=torch.uint8)
+        else:
+            self.targets = torch.rand((self.V, 3, H, W), generator=gen, device=dev, dtype=torch.float32)
         self.pairs_act = []
         for v, cam in enumerate(cams):
             self.pipe.set_camera(cam)
@@ -356,6 +361,11 @@ class Workload:
         torch.cuda.synchronize()
 
     # ---------------------------------------------------------------------------------------
+    def target_f32(self, v):
+        """fp32 copy of training image v (for the measurement legs that call oit_loss_grad / SSIM)."""
+        t = self.targets[v]
+        return t.float() / 255.0 if t.dtype == self.torch.uint8 else t.contiguous()
+
     def train_views(self, n_streams=None, host_targets=None):
         """a1-a6 over every training view (Alg. 1 l.3-6, one view per iteration); views are dealt
         round-robin to n_streams streams (fork/join on the current stream). host_targets (e2e):
@@ -626,7 +636,7 @@ def time_ablation(args, torch, wl, flush, n_views=10):
         for v in range(min(n_views, wl.V)):
             p.set_camera(wl.cams[v])
             img, st = p.forward(wl.rows, wl.sigma, wl.act, wl.bg, base=wl.caches[v])
-            L.oit_loss_grad(wl.cams[v], img, wl.targets[v], "l1", g)
+            L.oit_loss_grad(wl.cams[v], img, wl.target_f32(v), "l1", g)
             for k, per_pixel in enumerate((False, True)):
                 flush.zero_()
                 flush.sum()
@@ -648,8 +658,8 @@ def time_dssim(args, torch, wl, flush):
     event-timed after an L2 flush; HBM roofline on the stencil passes' algorithmic bytes."""
     L, dev = wl.L, wl.dev
     cam = wl.cams[0]
-    img = wl.targets[1 % wl.V].contiguous()
-    tgt = wl.targets[0].contiguous()
+    img = wl.target_f32(1 % wl.V)
+    tgt = wl.target_f32(0)
     g = torch.empty_like(tgt)
     loss = torch.zeros(1, dtype=torch.float32, device=dev)
     ws = torch.empty(L.oit_dssim_workspace_bytes(cam), dtype=torch.uint8, device=dev)
@@ -779,7 +789,7 @@ def time_e2e(args, torch, dist, wl, step, flush, allred):
     targets_h = wl.targets.cpu().pin_memory()
     grad_h = torch.empty_like(wl.grad, device="cpu").pin_memory()
     bits_h = torch.empty_like(wl.bits, device="cpu").pin_memory()
-    h2d = rows_h.numel() * 4 + targets_h.numel() * 4
+    h2d = rows_h.numel() * rows_h.element_size() + targets_h.numel() * targets_h.element_size()
     d2h = grad_h.numel() * 4 + bits_h.numel() * 4
     host_views = [targets_h[v] for v in range(wl.V)]
 
@@ -884,7 +894,9 @@ def build_line(args, world, res, results):
                    "step": "I=100 iterations (one view each, fwd+bwd) + one refresh (a7 score over the inactive "
                            "set on S views, a8 update)",
                    "l2": "flushed between timed steps (256 MB write)", "graph": not args.no_graph,
-                   "streams": args.streams, "loss": args.loss},
+                   "streams": args.streams, "loss": args.loss,
+                   "targets": ("uint8 [3][H][W] 8-bit training images (OIT_TARGET_U8)" if args.targets == "u8"
+                               else "fp32 [3][H][W]")},
         "splat_pixel_evals_per_s": evals / (res["ms"] * 1e-3),
         "contributing_fraction_f_c": f_c,
         "evaluated_splat_pixels_per_view": res["tile_evals"] / res["V"],

@@ -176,14 +176,18 @@ int oit_composite_bwd(const oit_scene* scene, const oit_camera* cam, const int32
                       size_t ws_bytes, oit_stream_t stream);
 
 /* Same as oit_composite_bwd, plus:
- *  - target (nullable, [3][H][W] device): if given, dL_dimage is ignored (may be NULL) and the
+ *  - target (nullable, [3][H][W] device, fp32 — or uint8 with OIT_TARGET_U8): if given, dL_dimage
+ *    is ignored (may be NULL) and the
  *    pixel gradient is the L1 (loss 0) / L2 (loss 1) gradient of oit_loss_grad, computed from the
  *    image the state resolves to, inside the coefficient kernel (a4 fused: no image round trip),
  *    or (loss 2) the 3DGS loss gradient of oit_loss_dssim with λ = 0.2 (the image is resolved
  *    into the workspace first: D-SSIM is not pixel-local);
+ *    loss | OIT_TARGET_U8: target is an 8-bit image (uint8 [3][H][W], the training images of
+ *    the paper's datasets), read as the fp32 value u8/255 (one correctly rounded division);
  *  - ev (nullable): two cudaEvent_t recorded on `stream` right before and after the a5 moment
  *    kernel (the hot loop), so callers can time it with events (also inside CUDA-graph capture,
  *    where they are recorded as external event nodes). */
+#define OIT_TARGET_U8 0x100 /* loss flag: targets are uint8 [3][H][W], value u8/255 */
 typedef struct {
   void* moments_begin; /* cudaEvent_t or NULL */
   void* moments_end;   /* cudaEvent_t or NULL */
@@ -193,7 +197,7 @@ int oit_composite_bwd_ex(const oit_scene* scene, const oit_camera* cam, const in
                          const int32_t* tile_offsets, int64_t pair_capacity, const float bg_host[3],
                          const float* state, const float* dL_dimage, float scale, float* grad,
                          float* dL_dsigma, float* dL_dcov, void* ws, size_t ws_bytes,
-                         const float* target, int32_t loss, const oit_bwd_events* ev,
+                         const void* target, int32_t loss, const oit_bwd_events* ev,
                          oit_stream_t stream);
 
 /* NEXT-4 ablation (§4.2, Table 2 "Per-pixel"): the same backward as oit_composite_bwd_ex
@@ -221,12 +225,13 @@ int oit_select_views(const float* centers, int32_t n_views, int32_t n_sub, uint6
  * a7  oit_score_subsample — the subsampled gradient score of Alg. 1 l.8-12.
  * For each subsampled view j = views_host[s]: the full-G pixel state is caches[j] ⊕ the active
  * set (Rasterize(G, I^pre_j), R16); the loss gradient against targets[j] (R20, R24; loss 0 = L1,
- * 1 = L2, 2 = the 3DGS (1−λ)L1 + λ·D-SSIM with λ = 0.2, NEXT-3) is
+ * 1 = L2, 2 = the 3DGS (1−λ)L1 + λ·D-SSIM with λ = 0.2, NEXT-3; | OIT_TARGET_U8 for 8-bit targets) is
  * back-propagated to the scored splats score_idx (normally the inactive set);
  *   score_grad[n_score][80] += scale·Σ_j ∂L_j/∂row, *dL_dsigma += scale·Σ_j ∂L_j/∂σ
  * (scale = 1/S gives the mean over the S subsampled views of R19; disjoint subsets of the S views
  * may be scored by concurrent calls on different streams, each with scale = 1/S).
- * cams_host [n_views]; targets/caches: HOST arrays of n_views DEVICE pointers ([3][H][W] and
+ * cams_host [n_views]; targets/caches: HOST arrays of n_views DEVICE pointers ([3][H][W] fp32, or
+ * uint8 with loss | OIT_TARGET_U8, and
  * [5][n_tiles][256]; caches[j] may be NULL = nothing frozen). All views share W and H.
  * *d_max_pairs (device int64) receives the largest pair count met; if > pair_capacity the
  * result is invalid and the caller re-calls with more room.
@@ -235,7 +240,7 @@ int oit_select_views(const float* centers, int32_t n_views, int32_t n_sub, uint6
 size_t oit_score_workspace_bytes(const oit_camera* cam, int32_t n_active, int32_t n_score,
                                  int64_t pair_capacity);
 int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int32_t n_views,
-                        const float* const* targets_host, const float* const* caches_host,
+                        const void* const* targets_host, const float* const* caches_host,
                         const int32_t* active_idx, int32_t n_active, const int32_t* score_idx,
                         int32_t n_score, const int32_t* views_host, int32_t n_sub, int32_t loss,
                         const float bg_host[3], float scale, float* score_grad, float* dL_dsigma,

@@ -56,6 +56,13 @@ class AdamCfg(C.Structure):
 
 
 LOSS_CODE = {"l1": 0, "l2": 1, "dssim": 2}   # "dssim" = the 3DGS (1−λ)L1 + λ·D-SSIM, λ = 0.2
+OIT_TARGET_U8 = 0x100                          # loss flag: 8-bit targets (uint8 [3][H][W], value u8/255)
+
+
+def _loss_flags(loss: str, targets) -> int:
+    """Loss code plus OIT_TARGET_U8 when the (first non-None) target tensor is uint8."""
+    t = next((x for x in targets if x is not None), None)
+    return LOSS_CODE[loss] | (OIT_TARGET_U8 if t is not None and t.dtype == torch.uint8 else 0)
 
 
 _lib = None
@@ -214,7 +221,7 @@ def oit_composite_bwd(rows, sigma, cam, idx, rec, pair_slot, tile_offsets, bg, s
     else:
         ev = None if events is None else C.byref(BwdEvents(C.c_void_p(events[0].cuda_event),
                                                            C.c_void_p(events[1].cuda_event)))
-        _check(lib().oit_composite_bwd_ex(*args, _ptr(target), LOSS_CODE[loss], ev, _stream(stream)),
+        _check(lib().oit_composite_bwd_ex(*args, _ptr(target), _loss_flags(loss, [target]), ev, _stream(stream)),
                "oit_composite_bwd_ex")
 
 
@@ -239,7 +246,7 @@ def oit_score_subsample(rows, sigma, cams, targets, caches, active_idx, score_id
     vw = (C.c_int32 * len(views))(*[int(v) for v in views])
     _check(lib().oit_score_subsample(C.byref(sc), cam_arr, V, tg, ch, _ptr(active_idx), int(active_idx.numel()),
                                      _ptr(score_idx), int(score_idx.numel()), vw, len(views),
-                                     LOSS_CODE[loss], _f3(bg),
+                                     _loss_flags(loss, targets), _f3(bg),
                                      C.c_float(1.0 / len(views) if scale is None else scale), _ptr(score_grad),
                                      _ptr(dL_dsigma),
                                      int(pair_capacity), _ptr(max_pairs), _ptr(ws), int(ws.numel()),

@@ -137,28 +137,42 @@ static size_t coef_bytes(int32_t n_tiles) {
   return align_up((size_t)n_tiles * kTilePx * sizeof(float4)) + align_up((size_t)n_tiles * kTilePx * sizeof(float));
 }
 
-// D-SSIM scratch (loss 2): the resolved image, its gradient and the SSIM stencil maps
+// D-SSIM scratch (loss 2): the resolved image, its gradient, an fp32 copy of an 8-bit target and
+// the SSIM stencil maps
 static size_t dssim_bytes(const oit_camera* cam) {
   const size_t n = (size_t)3 * cam->width * cam->height;
-  return 2 * align_up(n * 4) + ssim_ws_bytes(cam->width, cam->height);
+  return 3 * align_up(n * 4) + ssim_ws_bytes(cam->width, cam->height);
 }
 
 // Pixel coefficients from a state and a target: L1/L2 fused into k_coef; D-SSIM (not pixel-local)
 // resolves the image, runs the two SSIM stencil passes, then k_coef from dL/dC.
-static void coef_from_target(const DevCam& dc, const oit_camera* cam, const float* state, const float* target,
-                             int32_t loss, float* coef4, float* coefa, void* dssim_ws, cudaStream_t st) {
+static void coef_from_target(const DevCam& dc, const oit_camera* cam, const float* state, const void* target,
+                             int32_t loss_flags, float* coef4, float* coefa, void* dssim_ws, cudaStream_t st) {
+  const bool u8 = (loss_flags & OIT_TARGET_U8) != 0;
+  const int32_t loss = loss_flags & ~OIT_TARGET_U8;
   if (loss != 2) {
-    launch_coef(dc, state, nullptr, target, loss, coef4, coefa, st);
+    launch_coef(dc, state, nullptr, target, u8, loss, coef4, coefa, st);
     return;
   }
   const size_t n = (size_t)3 * cam->width * cam->height;
   Carve cv(dssim_ws);
   float* image = cv.take<float>(n);
   float* g = cv.take<float>(n);
+  float* t32 = cv.take<float>(n);
   void* sws = cv.take<char>(ssim_ws_bytes(cam->width, cam->height));
+  const float* tf = static_cast<const float*>(target);
+  if (u8) {
+    launch_u8_to_f32(static_cast<const uint8_t*>(target), (int64_t)n, t32, st);
+    tf = t32;
+  }
   launch_resolve(dc, state, image, st);
-  launch_ssim(image, target, cam->width, cam->height, kLambdaSsim, g, nullptr, sws, st);
-  launch_coef(dc, state, g, nullptr, 0, coef4, coefa, st);
+  launch_ssim(image, tf, cam->width, cam->height, kLambdaSsim, g, nullptr, sws, st);
+  launch_coef(dc, state, g, nullptr, false, 0, coef4, coefa, st);
+}
+
+static bool loss_ok(int32_t loss_flags) {
+  const int32_t l = loss_flags & ~OIT_TARGET_U8;
+  return l == 0 || l == 1 || l == 2;
 }
 
 size_t oit_bwd_workspace_bytes(const oit_camera* cam, int32_t n_slots, int64_t pair_capacity) {
@@ -179,10 +193,10 @@ int oit_composite_bwd_ex(const oit_scene* scene, const oit_camera* cam, const in
                          const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
                          int64_t pair_capacity, const float bg_host[3], const float* state, const float* dL_dimage,
                          float scale, float* grad, float* dL_dsigma, float* dL_dcov, void* ws, size_t ws_bytes,
-                         const float* target, int32_t loss, const oit_bwd_events* ev, oit_stream_t stream) {
+                         const void* target, int32_t loss, const oit_bwd_events* ev, oit_stream_t stream) {
   if (!scene || !scene->rows || !scene->sigma || !cam_ok(cam) || n_slots < 0 || pair_capacity < 0) return OIT_EINVAL;
   if (!tile_offsets || !bg_host || !state || (!dL_dimage && !target) || !dL_dsigma || !ws) return OIT_EINVAL;
-  if (target && loss != 0 && loss != 1 && loss != 2) return OIT_EINVAL;
+  if (target && !loss_ok(loss)) return OIT_EINVAL;
   if (n_slots > 0 && (!idx || !rec || !grad)) return OIT_EINVAL;
   if (pair_capacity > 0 && !pair_slot) return OIT_EINVAL;
   if (!shape_ok(cam) || n_slots > scene->n || oit_num_tiles(cam) > kMaxScan) return OIT_ESHAPE;
@@ -195,7 +209,7 @@ int oit_composite_bwd_ex(const oit_scene* scene, const oit_camera* cam, const in
   void* dssim_ws = cv.take<char>(dssim_bytes(cam));
   void* rest = cv.base + cv.off;
   if (target) coef_from_target(dc, cam, state, target, loss, coef4, coefa, dssim_ws, S(stream));
-  else launch_coef(dc, state, dL_dimage, nullptr, 0, coef4, coefa, S(stream));
+  else launch_coef(dc, state, dL_dimage, nullptr, false, 0, coef4, coefa, S(stream));
   launch_composite_bwd(dc, scene->rows, scene->sigma, idx, n_slots, rec, pair_slot, tile_offsets, pair_capacity,
                        coef4, coefa, scale, grad, dL_dsigma, dL_dcov, rest, S(stream),
                        ev ? static_cast<cudaEvent_t>(ev->moments_begin) : nullptr,
@@ -221,7 +235,7 @@ int oit_composite_bwd_perpixel(const oit_scene* scene, const oit_camera* cam, co
   float* coefa = cv.take<float>((size_t)nt * kTilePx);
   cv.take<char>(dssim_bytes(cam));
   void* rest = cv.base + cv.off;
-  launch_coef(dc, state, dL_dimage, nullptr, 0, coef4, coefa, S(stream));
+  launch_coef(dc, state, dL_dimage, nullptr, false, 0, coef4, coefa, S(stream));
   launch_composite_bwd(dc, scene->rows, scene->sigma, idx, n_slots, rec, pair_slot, tile_offsets, pair_capacity,
                        coef4, coefa, scale, grad, dL_dsigma, dL_dcov, rest, S(stream),
                        ev ? static_cast<cudaEvent_t>(ev->moments_begin) : nullptr,
@@ -273,7 +287,7 @@ size_t oit_score_workspace_bytes(const oit_camera* cam, int32_t n_active, int32_
 }
 
 int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int32_t n_views,
-                        const float* const* targets_host, const float* const* caches_host, const int32_t* active_idx,
+                        const void* const* targets_host, const float* const* caches_host, const int32_t* active_idx,
                         int32_t n_active, const int32_t* score_idx, int32_t n_score, const int32_t* views_host,
                         int32_t n_sub, int32_t loss, const float bg_host[3], float scale, float* score_grad, float* dL_dsigma,
                         int64_t pair_capacity, int64_t* d_max_pairs, void* ws, size_t ws_bytes,
@@ -281,7 +295,7 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
   if (!scene || !scene->rows || !scene->sigma || !cams_host || !targets_host || !views_host || !bg_host ||
       !dL_dsigma || !d_max_pairs || !ws)
     return OIT_EINVAL;
-  if (n_views <= 0 || n_sub <= 0 || n_active < 0 || n_score < 0 || pair_capacity < 0 || loss < 0 || loss > 2)
+  if (n_views <= 0 || n_sub <= 0 || n_active < 0 || n_score < 0 || pair_capacity < 0 || !loss_ok(loss))
     return OIT_EINVAL;
   if ((n_active > 0 && !active_idx) || (n_score > 0 && (!score_idx || !score_grad))) return OIT_EINVAL;
   if (n_active > scene->n || n_score > scene->n) return OIT_ESHAPE;

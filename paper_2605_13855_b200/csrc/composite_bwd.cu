@@ -24,8 +24,12 @@ namespace oit {
 constexpr int kMomentsThreads = 128;
 
 // ------------------------------------------------------------------------------ a4 coef ---
+__device__ __forceinline__ float target_value(const float* t, size_t i) { return t[i]; }
+__device__ __forceinline__ float target_value(const uint8_t* t, size_t i) { return __fdiv_rn((float)t[i], 255.0f); }
+
+template <class TT>
 __global__ void __launch_bounds__(256) k_coef(DevCam cam, const float* __restrict__ state,
-                                              const float* __restrict__ dL_dimage, const float* __restrict__ target,
+                                              const float* __restrict__ dL_dimage, const TT* __restrict__ target,
                                               int32_t loss, float4* __restrict__ coef4, float* __restrict__ coefa) {
   const int tile = blockIdx.x, tid = threadIdx.x;
   const int n_tiles = cam.TX * cam.TY;
@@ -46,7 +50,8 @@ __global__ void __launch_bounds__(256) k_coef(DevCam cam, const float* __restric
     g0 = dL_dimage[p]; g1 = dL_dimage[hw + p]; g2 = dL_dimage[2 * hw + p];
   } else {
     const float inv = 1.0f / (3.0f * (float)hw);
-    const float d0 = C0 - target[p], d1 = C1 - target[hw + p], d2 = C2 - target[2 * hw + p];
+    const float d0 = C0 - target_value(target, p), d1 = C1 - target_value(target, hw + p);
+    const float d2 = C2 - target_value(target, 2 * hw + p);
     if (loss == 0) {
       g0 = (d0 > 0.f ? inv : (d0 < 0.f ? -inv : 0.f));
       g1 = (d1 > 0.f ? inv : (d1 < 0.f ? -inv : 0.f));
@@ -548,10 +553,23 @@ size_t bwd_ws_bytes(int32_t n_tiles, int32_t n_slots, int64_t capacity) {
          scan_tmp_bytes(4 * (int64_t)n_tiles);
 }
 
-void launch_coef(const DevCam& cam, const float* state, const float* dL_dimage, const float* target, int32_t loss,
-                 float* coef4, float* coefa, cudaStream_t st) {
-  int n_tiles = cam.TX * cam.TY;
-  k_coef<<<n_tiles, 256, 0, st>>>(cam, state, dL_dimage, target, loss, reinterpret_cast<float4*>(coef4), coefa);
+void launch_coef(const DevCam& cam, const float* state, const float* dL_dimage, const void* target, bool target_u8,
+                 int32_t loss, float* coef4, float* coefa, cudaStream_t st) {
+  const int n_tiles = cam.TX * cam.TY;
+  float4* c4 = reinterpret_cast<float4*>(coef4);
+  if (target_u8)
+    k_coef<uint8_t><<<n_tiles, 256, 0, st>>>(cam, state, dL_dimage, static_cast<const uint8_t*>(target), loss, c4, coefa);
+  else
+    k_coef<float><<<n_tiles, 256, 0, st>>>(cam, state, dL_dimage, static_cast<const float*>(target), loss, c4, coefa);
+}
+
+__global__ void k_u8_to_f32(const uint8_t* __restrict__ src, int64_t n, float* __restrict__ dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = __fdiv_rn((float)src[i], 255.0f);
+}
+
+void launch_u8_to_f32(const uint8_t* src, int64_t n, float* dst, cudaStream_t st) {
+  if (n > 0) k_u8_to_f32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, n, dst);
 }
 
 void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sigma, const int32_t* idx,

@@ -54,8 +54,10 @@ inline int sm_count() {
 
 // composite_bwd.cu — a4 coefficients, a5 moments, a6 epilogue
 size_t bwd_ws_bytes(int32_t n_tiles, int32_t n_slots, int64_t capacity);
-void launch_coef(const DevCam& cam, const float* state, const float* dL_dimage, const float* target, int32_t loss,
-                 float* coef4, float* coefa, cudaStream_t st);
+// target: fp32 [3][H][W], or (target_u8) uint8 [3][H][W] read as u8/255
+void launch_coef(const DevCam& cam, const float* state, const float* dL_dimage, const void* target, bool target_u8,
+                 int32_t loss, float* coef4, float* coefa, cudaStream_t st);
+void launch_u8_to_f32(const uint8_t* src, int64_t n, float* dst, cudaStream_t st);
 void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sigma, const int32_t* idx,
                           int32_t n_slots, const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
                           int64_t capacity, const float* coef4, const float* coefa, float scale, float* grad,

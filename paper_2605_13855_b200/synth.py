@@ -223,6 +223,11 @@ def target_image(cam: dict, seed: int) -> np.ndarray:
     return rng(seed).uniform(0.0, 1.0, (3, cam["height"], cam["width"])).astype(np.float32)
 
 
+def target_image_u8(cam: dict, seed: int) -> np.ndarray:
+    """Synthetic 8-bit training image (uint8 [3,H,W], uniform 0..255) — the datasets' PNG format."""
+    return rng(seed).integers(0, 256, (3, cam["height"], cam["width"]), dtype=np.uint8)
+
+
 def pixel_state(cam: dict, seed: int) -> np.ndarray:
     """Synthetic pre-render cache [5,H,W] fp32 (planes P_R, P_G, P_B, Q, T) shaped
     like the frozen-set accumulators of Eq. 7: with A = Σα ~ U[0,3] per pixel, T = e^{−A·U[0.8,1.2]}

@@ -577,6 +577,43 @@ def test_fused_loss_backward_equals_two_step(loss):
     assert ok, describe_bad(out[1], gr, bad, bnd)
 
 
+@pytest.mark.parametrize("loss", ["l1", "l2", "dssim"])
+def test_u8_targets_equal_fp32_targets(loss):
+    """loss | OIT_TARGET_U8: an 8-bit target gives the backward of the fp32 target u8/255 (one
+    correctly rounded division on both sides), in the fused backward and in the score."""
+    L = _L()
+    sc = SCENES[1]
+    cam = sc.cams[1]
+    idx = np.arange(sc.n, dtype=np.int32)
+    rows, sigma, idx_t = _t(sc.rows), _t(np.array([sc.sigma], np.float32)), _t(idx)
+    t8 = synth.target_image_u8(cam, 123)
+    t32 = t8.astype(np.float32) / np.float32(255.0)
+    p = _pipe(cam, sc.n)
+    _, st = p.forward(rows, sigma, idx_t, sc.bg, image=False)
+    out = []
+    for tgt in (_t(t8), _t(t32)):
+        grad = torch.zeros((sc.n, 80), dtype=torch.float32, device=DEV)
+        ds = torch.zeros(1, dtype=torch.float32, device=DEV)
+        p.backward(rows, sigma, idx_t, sc.bg, st, None, grad, ds, target=tgt, loss=loss)
+        out.append(grad.cpu().numpy())
+    assert np.abs(out[0] - out[1]).max() <= 1e-5 * max(np.abs(out[1]).max(), 1e-30)
+    assert np.abs(out[1]).max() > 0
+    # score with 8-bit targets (the inactive half over a cache, one view)
+    mask = synth.active_mask(sc, 0.5, "uniform")
+    act, ina = _t(np.flatnonzero(mask).astype(np.int32)), _t(np.flatnonzero(~mask).astype(np.int32))
+    cap = 1 << 20
+    ws = torch.empty(L.oit_score_workspace_bytes(cam, int(act.numel()), int(ina.numel()), cap), dtype=torch.uint8,
+                     device=DEV)
+    res = []
+    for tgt in (_t(t8), _t(t32)):
+        sg = torch.zeros((int(ina.numel()), 80), dtype=torch.float32, device=DEV)
+        ds = torch.zeros(1, dtype=torch.float32, device=DEV)
+        mp = torch.zeros(1, dtype=torch.int64, device=DEV)
+        L.oit_score_subsample(rows, sigma, [cam], [tgt], None, act, ina, [0], loss, sc.bg, sg, ds, cap, mp, ws)
+        res.append(sg.cpu().numpy())
+    assert np.abs(res[0] - res[1]).max() <= 1e-5 * max(np.abs(res[1]).max(), 1e-30)
+
+
 # ------------------------------------------------------------------ NEXT-1 reconcile ------
 def _state_close(got, ref, rtol=2e-4, frac=1e-5):
     """Pixel-state bar (as test_composite_fwd_parity) plus a per-channel floor for the P̄/Q̄
