@@ -79,6 +79,8 @@ def parse():
     ap.add_argument("--no-adam", action="store_true", help="skip the NEXT-2 Adam measurement")
     ap.add_argument("--no-reconcile", action="store_true", help="skip the NEXT-1 reconciliation measurement")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-c3", action="store_true", help="skip the configs[2] (C3, 3M splats) measurement")
+    ap.add_argument("--no-c4", action="store_true", help="skip the configs[3] (C4 score sweep) measurement")
     ap.add_argument("--profile-once", action="store_true", help="run one eager step (for ncu) and exit")
     return ap.parse_args()
 
@@ -259,19 +261,21 @@ def scan_kernels(n):
 class Workload:
     """One rank's share: scene, active set, per-view caches/targets, buffers and the step."""
 
-    def __init__(self, args, torch, L, synth, rho, cams, rank, world):
+    def __init__(self, args, torch, L, synth, rho, cams, rank, world, scene=None, cap=1 << 22, cache_cap=None,
+                 with_refresh=True, kind=None):
         from paper_2605_13855_b200.pipeline import ViewPipeline
         self.torch, self.L = torch, L
         dev = torch.device("cuda", torch.cuda.current_device())
         self.dev = dev
-        sc = synth.scene_c2(n=args.splats, n_views=1, res=args.res)   # scene content (cameras passed in)
+        # scene content (cameras passed in): C2 by default, or a given scene (C3 measurements)
+        sc = synth.scene_c2(n=args.splats, n_views=1, res=args.res) if scene is None else scene
         self.sc = sc
         self.cams = cams
         self.V = len(cams)
         self.rho = rho
         self.world, self.rank = world, rank
         self.loss = args.loss
-        mask = synth.active_mask(sc, rho, args.kind)
+        mask = synth.active_mask(sc, rho, args.kind if kind is None else kind)
         self.n = sc.n
         act = np.flatnonzero(mask).astype(np.int32)
         ina = np.flatnonzero(~mask).astype(np.int32)
@@ -281,10 +285,11 @@ class Workload:
         self.act = torch.from_numpy(act).to(dev)
         self.ina = torch.from_numpy(ina).to(dev)
         self.bg = sc.bg
-        H = W = args.res
+        H, W = int(cams[0]["height"]), int(cams[0]["width"])
         self.H, self.W = H, W
-        cap = 1 << 22   # ≥ 2× the largest per-view pair count of C2 (checked below)
-        self.pipe = ViewPipeline(cams[0], max(self.n_act, self.n_ina, 1), cap, device=dev)
+        # cap ≥ 2× the largest per-view pair count of the training views (checked below); the
+        # frozen-set caches are built on the first pipeline, sized for them (cache_cap)
+        self.pipe = ViewPipeline(cams[0], max(self.n_act, self.n_ina, 1), cache_cap or cap, device=dev)
         # independent views run concurrently: one pipeline (buffers + workspaces) per stream; the
         # gradient rows are accumulated with vector atomics, so all streams share grad / dσ
         self.n_streams = max(1, args.streams)
@@ -309,6 +314,7 @@ class Workload:
             if self.n_ina > 0:
                 _, st = self.pipe.forward(self.rows, self.sigma, self.ina, self.bg, image=False)
                 self.caches[v].copy_(st)
+                assert self.pipe.pairs_used() <= self.pipe.capacity, "cache pair capacity overflow"
             else:
                 self.caches[v, :3].zero_(); self.caches[v, 3].zero_(); self.caches[v, 4].fill_(1.0)
         # work counters of the training views (untimed)
@@ -327,6 +333,20 @@ class Workload:
         # ---- buffers of the step ----
         self.grad = torch.zeros((max(self.n_act, 1), 80), dtype=torch.float32, device=dev)
         self.dsig = torch.zeros(1, dtype=torch.float32, device=dev)
+        self.with_refresh = with_refresh
+        self._setup_refresh(args, synth, mask, cams, cap) if with_refresh else None
+        # events around the two hot kernels of every training view (external nodes in the graph)
+        mk = lambda: torch.cuda.Event(enable_timing=True, external=True)  # noqa: E731
+        self.ev_fwd = [(mk(), mk()) for _ in range(self.V)]
+        self.ev_bwd = [(mk(), mk()) for _ in range(self.V)]
+        self.ev_seg = [mk() for _ in range(3)]
+        for pair in self.ev_fwd + self.ev_bwd + [tuple(self.ev_seg[:2]), tuple(self.ev_seg[1:])]:
+            pair[0].record()                      # torch creates the CUDA event lazily on first record
+            pair[1].record()
+        torch.cuda.synchronize()
+
+    def _setup_refresh(self, args, synth, mask, cams, cap):
+        torch, L, dev = self.torch, self.L, self.dev
         # refresh: FPS over this rank's view centres, S = 5% of the views, scored set = inactive set
         self.S = max(1, int(round(args.sub_rate * self.V)))
         self.centers = torch.from_numpy(synth.camera_centers(cams)).to(dev)
@@ -350,15 +370,6 @@ class Workload:
         self.eps = [1e-7, 1e-7, 1e-7, 1e-7, 1e-7, 1e-7]
         self.caches_list = [self.caches[v] for v in range(self.V)]
         self.targets_list = [self.targets[v] for v in range(self.V)]
-        # events around the two hot kernels of every training view (external nodes in the graph)
-        mk = lambda: torch.cuda.Event(enable_timing=True, external=True)  # noqa: E731
-        self.ev_fwd = [(mk(), mk()) for _ in range(self.V)]
-        self.ev_bwd = [(mk(), mk()) for _ in range(self.V)]
-        self.ev_seg = [mk() for _ in range(3)]
-        for pair in self.ev_fwd + self.ev_bwd + [tuple(self.ev_seg[:2]), tuple(self.ev_seg[1:])]:
-            pair[0].record()                      # torch creates the CUDA event lazily on first record
-            pair[1].record()
-        torch.cuda.synchronize()
 
     # ---------------------------------------------------------------------------------------
     def target_f32(self, v):
@@ -482,8 +493,21 @@ def run_ours(args):
         del wl
         torch.cuda.empty_cache()
     wl, res = headline
+    del wl
+    torch.cuda.empty_cache()
+    extra = {}
+    if world == 1:
+        flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+        if not args.no_c3:
+            extra["c3_mip360_shaped"] = time_c3(args, torch, L, synth, flush)
+            torch.cuda.empty_cache()
+        if not args.no_c4:
+            extra["c4_score_sweep"] = time_c4(args, torch, L, synth, flush)
+            torch.cuda.empty_cache()
+        del flush
     if rank == 0:
         line = build_line(args, world, res, results)
+        line.update(extra)
         if not args.no_cpu and world == 1:
             try:
                 line["cpu_baseline"] = {k: v for k, v in cpu_leg(args, args.views, 1, 0).items() if k != "ms_per_step"}
@@ -616,6 +640,141 @@ def time_workload(args, torch, dist, wl, world, headline_run):
     if headline_run and not args.no_ablation:
         res["ablation"] = time_ablation(args, torch, wl, flush)
     return res
+
+
+def _graph_time(torch, fn, flush, warmup, steps):
+    """Capture fn in a CUDA graph, replay warmup + steps times between L2 flushes; mean ms."""
+    fn()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
+    for i in range(warmup + steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0.record()
+        g.replay()
+        t1.record()
+        torch.cuda.synchronize()
+        if i >= warmup:
+            times.append(t0.elapsed_time(t1))
+    del g
+    return float(np.mean(times))
+
+
+def time_c3(args, torch, L, synth, flush, n_views=16):
+    """configs[2] (Mip-NeRF360-shaped: 3M splats, 1600×1064, ρ = 0.1): training views a1-a6 over
+    their frozen-set caches, 16 streams in one CUDA graph (no refresh), clustered and uniform masks."""
+    sc = synth.scene_c3(n_views=n_views)
+    out = {"views": n_views, "splats": sc.n, "res": [1600, 1064], "rho": 0.1}
+    for kind in ("clustered", "uniform"):
+        wl = Workload(args, torch, L, synth, 0.1, sc.cams, 0, 1, scene=sc, cap=1 << 22, cache_cap=1 << 25,
+                      with_refresh=False, kind=kind)
+        ms = _graph_time(torch, wl.train_views, flush, args.warmup, args.steps)
+        px = n_views * wl.H * wl.W
+        out[kind] = {"ms_per_view": ms / n_views, "mpix_per_s": px / (ms * 1e-3) / 1e6,
+                     "splat_pixel_evals_per_s": 256 * sum(wl.pairs_act) / (ms * 1e-3),
+                     "pairs_per_view": sum(wl.pairs_act) / n_views, "n_active": wl.n_act,
+                     "f_c": wl.contrib / max(wl.tile_evals, 1)}
+        del wl
+        torch.cuda.empty_cache()
+    return out
+
+
+def time_c4(args, torch, L, synth, flush, rates=(0.01, 0.02, 0.05, 0.10), n_views=300, refresh_every=100):
+    """configs[3] (score sweep: 1M inactive + 111k active splats on the C3 rig, 300 views): one
+    refresh = FPS (a7) + the subsampled gradient score of all 1M inactive splats over S = rate·V
+    views (concurrent streams, each view over its cache) + the Eq. 8 update (a8). Reports ms per
+    refresh, amortized per iteration (refresh every 100 iterations) and the ratio to one training
+    iteration (one view's a1-a6 over the 111k active splats)."""
+    n_ina, n_act = 1_000_000, 111_000
+    sc = synth.scene_c3(n=n_ina + n_act, n_views=n_views)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    mask = synth.active_mask(sc, n_act / sc.n, "clustered")
+    act = torch.from_numpy(np.flatnonzero(mask).astype(np.int32)).to(dev)
+    ina = torch.from_numpy(np.flatnonzero(~mask).astype(np.int32)).to(dev)
+    rows = torch.from_numpy(sc.rows).to(dev)
+    sigma = torch.tensor([sc.sigma], dtype=torch.float32, device=dev)
+    centers = torch.from_numpy(synth.camera_centers(sc.cams)).to(dev)
+    S_max = max(1, int(round(max(rates) * n_views)))
+    vd = torch.empty(S_max, dtype=torch.int32, device=dev)
+    L.oit_select_views(centers, S_max, 2605, 1, vd)
+    picked = [int(x) for x in vd.cpu().numpy()]          # FPS is greedy: the first S picks are FPS(S)
+    from paper_2605_13855_b200.pipeline import ViewPipeline
+    cam0 = sc.cams[0]
+    big = ViewPipeline(cam0, max(n_ina, n_act), 1 << 24, device=dev)
+    caches, targets = [None] * n_views, [None] * n_views
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(4321)
+    for j in picked:
+        big.set_camera(sc.cams[j])
+        _, st = big.forward(rows, sigma, ina, sc.bg, image=False)
+        assert big.pairs_used() <= big.capacity
+        caches[j] = st.clone()
+        targets[j] = torch.randint(0, 256, (3, cam0["height"], cam0["width"]), generator=gen, device=dev,
+                                   dtype=torch.uint8)
+    # one training iteration of this scene: a view's a1-a6 over the active set (single stream)
+    grad = torch.zeros((n_act, 80), dtype=torch.float32, device=dev)
+    dsig = torch.zeros(1, dtype=torch.float32, device=dev)
+
+    def one_iter():
+        for j in picked[:4]:
+            big.set_camera(sc.cams[j])
+            _, st = big.forward(rows, sigma, act, sc.bg, base=caches[j], image=False)
+            big.backward(rows, sigma, act, sc.bg, st, None, grad, dsig, target=targets[j], loss="l1")
+    iter_ms = _graph_time(torch, one_iter, flush, args.warmup, args.steps) / 4
+    del big
+    torch.cuda.empty_cache()
+    cap = 1 << 24
+    n_str = 8
+    streams = [torch.cuda.Stream() for _ in range(n_str)]
+    ws = [torch.empty(L.oit_score_workspace_bytes(cam0, n_act, n_ina, cap), dtype=torch.uint8, device=dev)
+          for _ in range(n_str)]
+    sg = torch.zeros((n_ina, 80), dtype=torch.float32, device=dev)
+    sds = torch.zeros(1, dtype=torch.float32, device=dev)
+    mp = torch.zeros(1, dtype=torch.int64, device=dev)
+    bits0 = torch.from_numpy(synth.bits_from_mask(mask).view(np.int32)).to(dev)
+    bits = bits0.clone()
+    n = sc.n
+    act_out, fro, new = (torch.empty(n, dtype=torch.int32, device=dev) for _ in range(3))
+    cnt = torch.zeros(3, dtype=torch.int32, device=dev)
+    uws = torch.empty(L.oit_update_workspace_bytes(n), dtype=torch.uint8, device=dev)
+    out = {"splats": sc.n, "n_inactive_scored": n_ina, "n_active": n_act, "views": n_views,
+           "refresh_every": refresh_every, "iteration_ms": iter_ms, "sweep": {}}
+    for rate in rates:
+        S = max(1, int(round(rate * n_views)))
+        views = picked[:S]
+
+        def refresh():
+            L.oit_select_views(centers, S, 2605, 1, vd)
+            sg.zero_()
+            sds.zero_()
+            main = torch.cuda.current_stream()
+            k_used = min(S, n_str)
+            for k in range(k_used):
+                part = views[k::k_used]
+                streams[k].wait_stream(main)
+                with torch.cuda.stream(streams[k]):
+                    L.oit_score_subsample(rows, sigma, sc.cams, targets, caches, act, ina, part, "l1", sc.bg, sg, sds,
+                                          cap, mp, ws[k], scale=1.0 / S)
+            for k in range(k_used):
+                main.wait_stream(streams[k])
+            bits.copy_(bits0)
+            L.oit_update_active_set(sg, ina, [1e-7] * 6, "fresh", n, bits, act_out, cnt[0:1], fro, cnt[1:2], new,
+                                    cnt[2:3], uws)
+        ms = _graph_time(torch, refresh, flush, args.warmup, args.steps)
+        assert int(mp.item()) <= cap, "score pair capacity overflow"
+        out["sweep"][f"{rate:g}"] = {"S": S, "ms_per_refresh": ms, "amortized_ms_per_iteration": ms / refresh_every,
+                                     "ratio_to_iteration": ms / refresh_every / iter_ms,
+                                     "ms_per_scored_view": ms / S}
+    return out
 
 
 def time_ablation(args, torch, wl, flush, n_views=10):
