@@ -8,11 +8,6 @@
 
 using namespace oit;
 
-namespace oit {
-static int g_dev_variant = 0;
-int dev_variant() { return g_dev_variant; }
-}  // namespace oit
-
 namespace {
 
 bool cam_ok(const oit_camera* c) {
@@ -440,8 +435,3 @@ int oit_reconcile_cache(const oit_scene* scene, const oit_camera* cam, const int
 }
 
 }  // extern "C"
-
-extern "C" int oit_dev_set_variant(int v) {
-  oit::g_dev_variant = v;
-  return OIT_OK;
-}

@@ -103,10 +103,6 @@ void launch_update(const float* score_grad, const int32_t* score_idx, int32_t n_
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 // Bump allocator over a caller workspace.
-// DEV: kernel-variant selector for in-process A/B timing (0 = product kernels); set through
-// oit_dev_set_variant. Not part of the hot-path contract.
-int dev_variant();
-
 struct Carve {
   char* base;
   size_t off = 0;

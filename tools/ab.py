@@ -1,4 +1,6 @@
-"""DEV: in-process A/B timing of kernel variants (oit_dev_set_variant) on the bench workload.
+"""DEV: in-process A/B timing of kernel variants on the bench workload. Variants are selected by an
+`oit_dev_set_variant(int)` export that experimental builds add temporarily (the product library has
+none: variant 0 only).
 
 Prepares C2 (300k splats, 800², ρ = 0.2 clustered) views over their pre-render caches, then times
 the a3 composite (fwd) and a5 moments (bwd) kernels with CUDA events, single stream, alternating
@@ -44,14 +46,19 @@ def main():
     grad = torch.zeros((len(act), 80), dtype=torch.float32, device=dev)
     dsig = torch.zeros(1, dtype=torch.float32, device=dev)
     lib = L.lib()
-    lib.oit_dev_set_variant.argtypes = [ctypes.c_int]
+    set_variant = getattr(lib, "oit_dev_set_variant", None)
+    if set_variant is None:
+        assert a.variants == [0], "this library has no kernel variants"
+        set_variant = lambda v: None  # noqa: E731
+    else:
+        set_variant.argtypes = [ctypes.c_int]
     res = {v: {"fwd": [], "bwd": []} for v in a.variants}
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     for e in ev:
         e.record()  # creates the underlying cudaEvent_t
     for r in range(a.rounds):
         for var in a.variants:
-            lib.oit_dev_set_variant(var)
+            set_variant(var)
             tf = tb = 0.0
             for v, cam in enumerate(sc.cams):
                 p.set_camera(cam)
@@ -63,7 +70,7 @@ def main():
             if r > 0:
                 res[var]["fwd"].append(tf / len(sc.cams) * 1e3)
                 res[var]["bwd"].append(tb / len(sc.cams) * 1e3)
-    lib.oit_dev_set_variant(0)
+    set_variant(0)
     for var in a.variants:
         f, b = np.array(res[var]["fwd"]), np.array(res[var]["bwd"])
         print(f"variant {var}: fwd {np.median(f):7.2f} us/view (min {f.min():.2f})   "
