@@ -403,11 +403,11 @@ class Workload:
                 # a3 (no image: the fused a4 below resolves C from the state), then a4+a5+a6 with
                 # the L1 gradient against the view's training image fused into the coefficients
                 _, st = p.forward(self.rows, self.sigma, self.act, self.bg, base=self.caches[v], image=False,
-                                  events=self.ev_fwd[v])
+                                  events=self.ev_fwd[v], concurrency=ns)
                 if host_targets is not None:
                     self.streams[k].wait_event(self.ev_copy[v])
                 p.backward(self.rows, self.sigma, self.act, self.bg, st, None, self.grad, self.dsig,
-                           events=self.ev_bwd[v], target=self.targets[v], loss=self.loss)
+                           events=self.ev_bwd[v], target=self.targets[v], loss=self.loss, concurrency=ns)
         for st_ in self.streams[:ns]:
             main.wait_stream(st_)
         if host_targets is not None:
@@ -1067,6 +1067,9 @@ def build_line(args, world, res, results):
         "roofline": {"kernel": kern, "bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
                      "algorithmic_flops_per_step": flops, "kernel_ms_per_step": kms,
                      "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
+                     "timing": "the step's training views replayed on ONE stream (between L2 flushes), the kernel "
+                               "with its full-GPU persistent grid (concurrency 1); the timed step launches it "
+                               f"with concurrency = {args.streams} (smaller grids, views sharing the SMs)",
                      "traffic_source": traffic_src,
                      "peak_source": "148 SMs x 128 FP32 lanes x 2 (FMA) x 1965 MHz (B200_PROFILING.md unit counts)"},
         "clocks": res["clocks"], "gpu_launches": res["launches"] * args.steps,

@@ -181,16 +181,17 @@ def oit_fwd_workspace_bytes(cam, pair_capacity: int) -> int:
 
 
 def oit_composite_fwd(cam, rec, pair_slot, tile_offsets, bg, ws, base=None, route=None, image=None, state=None,
-                      base_out=None, stream=None, counters=None):
-    """counters: optional int64[2] device tensor (+=): contributing pairs, tile-granular evals
-    (oit_composite_fwd_ex)."""
+                      base_out=None, stream=None, counters=None, concurrency: int = 1):
+    """counters: optional int64[2] device tensor (+=): contributing pairs, tile-granular evals;
+    concurrency: calls the caller keeps in flight on other streams (grid sizing). Either selects
+    oit_composite_fwd_ex."""
     args = (C.byref(camera(cam)), _ptr(rec), _ptr(pair_slot), _ptr(tile_offsets), int(pair_slot.numel()), _f3(bg),
             _ptr(base), _ptr(route), _ptr(image), _ptr(state), _ptr(base_out))
-    if counters is None:
+    if counters is None and concurrency == 1:
         _check(lib().oit_composite_fwd(*args, _ptr(ws), int(ws.numel()), _stream(stream)), "oit_composite_fwd")
     else:
-        _check(lib().oit_composite_fwd_ex(*args, _ptr(counters), _ptr(ws), int(ws.numel()), _stream(stream)),
-               "oit_composite_fwd_ex")
+        _check(lib().oit_composite_fwd_ex(*args, _ptr(counters), _ptr(ws), int(ws.numel()), int(concurrency),
+                                          _stream(stream)), "oit_composite_fwd_ex")
 
 
 def oit_loss_grad(cam, image, target, loss: str, dL_dimage, stream=None):
@@ -204,10 +205,11 @@ def oit_bwd_workspace_bytes(cam, n_slots: int, pair_capacity: int) -> int:
 
 def oit_composite_bwd(rows, sigma, cam, idx, rec, pair_slot, tile_offsets, bg, state, dL_dimage, grad, dL_dsigma,
                       ws, dL_dcov=None, scale: float = 1.0, stream=None, events=None, target=None, loss="l1",
-                      per_pixel: bool = False):
+                      per_pixel: bool = False, concurrency: int = 1):
     """events: optional (begin, end) torch.cuda.Event pair recorded around the a5 moment kernel;
     target: optional training image — the L1/L2 pixel gradient is then fused into the backward
-    (dL_dimage may be None). Both select oit_composite_bwd_ex."""
+    (dL_dimage may be None); concurrency: calls in flight on other streams (grid sizing). Any of
+    them selects oit_composite_bwd_ex."""
     sc, c = scene(rows, sigma), camera(cam)
     args = (C.byref(sc), C.byref(c), _ptr(idx), int(idx.numel()), _ptr(rec), _ptr(pair_slot), _ptr(tile_offsets),
             int(pair_slot.numel()), _f3(bg), _ptr(state), _ptr(dL_dimage), C.c_float(scale), _ptr(grad),
@@ -216,12 +218,13 @@ def oit_composite_bwd(rows, sigma, cam, idx, rec, pair_slot, tile_offsets, bg, s
         ev = None if events is None else C.byref(BwdEvents(C.c_void_p(events[0].cuda_event),
                                                            C.c_void_p(events[1].cuda_event)))
         _check(lib().oit_composite_bwd_perpixel(*args, ev, _stream(stream)), "oit_composite_bwd_perpixel")
-    elif events is None and target is None:
+    elif events is None and target is None and concurrency == 1:
         _check(lib().oit_composite_bwd(*args, _stream(stream)), "oit_composite_bwd")
     else:
         ev = None if events is None else C.byref(BwdEvents(C.c_void_p(events[0].cuda_event),
                                                            C.c_void_p(events[1].cuda_event)))
-        _check(lib().oit_composite_bwd_ex(*args, _ptr(target), _loss_flags(loss, [target]), ev, _stream(stream)),
+        _check(lib().oit_composite_bwd_ex(*args, _ptr(target), _loss_flags(loss, [target]), ev, int(concurrency),
+                                          _stream(stream)),
                "oit_composite_bwd_ex")
 
 

@@ -102,13 +102,13 @@ int oit_composite_fwd(const oit_camera* cam, const float* rec, const int32_t* pa
                       int64_t pair_capacity, const float bg_host[3], const float* base, const uint8_t* route,
                       float* image, float* state, float* base_out, void* ws, size_t ws_bytes, oit_stream_t stream) {
   return oit_composite_fwd_ex(cam, rec, pair_slot, tile_offsets, pair_capacity, bg_host, base, route, image, state,
-                              base_out, nullptr, ws, ws_bytes, stream);
+                              base_out, nullptr, ws, ws_bytes, 1, stream);
 }
 
 int oit_composite_fwd_ex(const oit_camera* cam, const float* rec, const int32_t* pair_slot,
                          const int32_t* tile_offsets, int64_t pair_capacity, const float bg_host[3], const float* base,
                          const uint8_t* route, float* image, float* state, float* base_out, int64_t* d_counters,
-                         void* ws, size_t ws_bytes, oit_stream_t stream) {
+                         void* ws, size_t ws_bytes, int32_t concurrency, oit_stream_t stream) {
   if (!cam_ok(cam) || !tile_offsets || !bg_host || pair_capacity < 0) return OIT_EINVAL;
   if (pair_capacity > 0 && (!rec || !pair_slot)) return OIT_EINVAL;
   if (route && !base_out) return OIT_EINVAL;
@@ -116,7 +116,7 @@ int oit_composite_fwd_ex(const oit_camera* cam, const float* rec, const int32_t*
   if (!shape_ok(cam)) return OIT_ESHAPE;
   if (!route && ws_bytes < oit_fwd_workspace_bytes(cam, pair_capacity)) return OIT_ECAPACITY;
   launch_composite_fwd(dev_cam(cam, bg_host), rec, pair_slot, tile_offsets, pair_capacity, base, route, image, state,
-                       base_out, S(stream), d_counters, ws);
+                       base_out, S(stream), d_counters, ws, concurrency);
   return launch_status();
 }
 
@@ -181,14 +181,15 @@ int oit_composite_bwd(const oit_scene* scene, const oit_camera* cam, const int32
                       const float bg_host[3], const float* state, const float* dL_dimage, float scale, float* grad,
                       float* dL_dsigma, float* dL_dcov, void* ws, size_t ws_bytes, oit_stream_t stream) {
   return oit_composite_bwd_ex(scene, cam, idx, n_slots, rec, pair_slot, tile_offsets, pair_capacity, bg_host, state,
-                              dL_dimage, scale, grad, dL_dsigma, dL_dcov, ws, ws_bytes, nullptr, 0, nullptr, stream);
+                              dL_dimage, scale, grad, dL_dsigma, dL_dcov, ws, ws_bytes, nullptr, 0, nullptr, 1, stream);
 }
 
 int oit_composite_bwd_ex(const oit_scene* scene, const oit_camera* cam, const int32_t* idx, int32_t n_slots,
                          const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
                          int64_t pair_capacity, const float bg_host[3], const float* state, const float* dL_dimage,
                          float scale, float* grad, float* dL_dsigma, float* dL_dcov, void* ws, size_t ws_bytes,
-                         const void* target, int32_t loss, const oit_bwd_events* ev, oit_stream_t stream) {
+                         const void* target, int32_t loss, const oit_bwd_events* ev, int32_t concurrency,
+                         oit_stream_t stream) {
   if (!scene || !scene->rows || !scene->sigma || !cam_ok(cam) || n_slots < 0 || pair_capacity < 0) return OIT_EINVAL;
   if (!tile_offsets || !bg_host || !state || (!dL_dimage && !target) || !dL_dsigma || !ws) return OIT_EINVAL;
   if (target && !loss_ok(loss)) return OIT_EINVAL;
@@ -208,7 +209,7 @@ int oit_composite_bwd_ex(const oit_scene* scene, const oit_camera* cam, const in
   launch_composite_bwd(dc, scene->rows, scene->sigma, idx, n_slots, rec, pair_slot, tile_offsets, pair_capacity,
                        coef4, coefa, scale, grad, dL_dsigma, dL_dcov, rest, S(stream),
                        ev ? static_cast<cudaEvent_t>(ev->moments_begin) : nullptr,
-                       ev ? static_cast<cudaEvent_t>(ev->moments_end) : nullptr);
+                       ev ? static_cast<cudaEvent_t>(ev->moments_end) : nullptr, 0, concurrency);
   return launch_status();
 }
 

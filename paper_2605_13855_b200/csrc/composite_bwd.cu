@@ -576,7 +576,7 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
                           int32_t n_slots, const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
                           int64_t capacity, const float* coef4, const float* coefa, float scale, float* grad,
                           float* dL_dsigma, float* dL_dcov, void* ws, cudaStream_t st, cudaEvent_t ev_begin,
-                          cudaEvent_t ev_end, int variant) {
+                          cudaEvent_t ev_end, int variant, int concurrency) {
   if (n_slots <= 0) {
     record_event(ev_begin, st);
     record_event(ev_end, st);
@@ -608,7 +608,8 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
     // quadrant sub-binning of the tile lists, then (quadrant, 32-slot chunk) items
     launch_quad_bin(cam, rec, pair_slot, tile_offsets, capacity, tq, qcount, qoffs, qslot, tmp, st);
     launch_build_items(qoffs, 4 * n_tiles, qcap, 32, 0, items, n_items, tile_nch, scratch, st);
-    const int blocks = sm_count() * 6;  // persistent: 6 × 4 warps per SM (80 regs), dynamic item claiming
+    // persistent: up to 6 × 4 warps per SM (80 regs), fewer when views run concurrently; dynamic item claiming
+    const int blocks = sm_count() * persistent_ctas(6, concurrency);
     record_event(ev_begin, st);
     k_moments<<<blocks, kMomentsThreads, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), qslot, qoffs,
                                                   qcap, items, n_items, counter,

@@ -315,7 +315,8 @@ size_t fwd_ws_bytes(int32_t n_tiles, int64_t capacity) {
 
 void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pair_slot,
                           const int32_t* tile_offsets, int64_t capacity, const float* base, const uint8_t* route,
-                          float* image, float* state, float* base_out, cudaStream_t st, int64_t* counters, void* ws) {
+                          float* image, float* state, float* base_out, cudaStream_t st, int64_t* counters, void* ws,
+                          int concurrency) {
   const int n_tiles = cam.TX * cam.TY;
   const float4* r4 = reinterpret_cast<const float4*>(rec);
   auto* cnt = reinterpret_cast<unsigned long long*>(counters);
@@ -333,7 +334,9 @@ void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pa
     cudaMemsetAsync(done, 0, sizeof(int32_t) * n_tiles, st);
     cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
     launch_build_items(tile_offsets, n_tiles, capacity, chunk_len, 1, items, n_items, tile_nch, scratch, st);
-    const int grid = sm_count() * 24;  // persistent (64-thread CTAs); items are claimed dynamically
+    // persistent (64-thread CTAs, up to 24 per SM; fewer when views run concurrently); items are
+    // claimed dynamically
+    const int grid = sm_count() * persistent_ctas(24, concurrency);
 #define OIT_FWD2(B, K)                                                                                         \
   k_fwd_items<B, K><<<grid, kFwdThreads, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, items, n_items, \
                                                   counter, tile_nch, done, partial, base, image, state, cnt, chunk_len)

@@ -26,7 +26,15 @@ void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_sl
 // composite_fwd.cu — a3
 void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pair_slot,
                           const int32_t* tile_offsets, int64_t capacity, const float* base, const uint8_t* route,
-                          float* image, float* state, float* base_out, cudaStream_t st, int64_t* counters, void* ws);
+                          float* image, float* state, float* base_out, cudaStream_t st, int64_t* counters, void* ws,
+                          int concurrency = 1);
+// Persistent-grid CTAs per SM for `full` (the kernel's resident maximum) when `concurrency` calls
+// run at once on different streams: about 2·full/concurrency, at least 2, at most full.
+inline int persistent_ctas(int full, int concurrency) {
+  const int c = concurrency < 1 ? 1 : concurrency;
+  int k = (2 * full + c - 1) / c;
+  return k < 2 ? 2 : (k > full ? full : k);
+}
 size_t fwd_ws_bytes(int32_t n_tiles, int64_t capacity);
 
 // items.cu — (tile, chunk) work lists, longest tiles first
@@ -62,7 +70,8 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
                           int32_t n_slots, const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
                           int64_t capacity, const float* coef4, const float* coefa, float scale, float* grad,
                           float* dL_dsigma, float* dL_dcov, void* ws, cudaStream_t st,
-                          cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr, int variant = 0);
+                          cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr, int variant = 0,
+                          int concurrency = 1);
 
 // Record an event on a stream, as an external event node when the stream is being captured.
 inline void record_event(cudaEvent_t ev, cudaStream_t st) {

@@ -49,7 +49,7 @@ class ViewPipeline:
         return rec
 
     def forward(self, rows, sigma, idx, bg, base=None, route=None, base_out=None, image=True, stream=None,
-                counters=None, events=None):
+                counters=None, events=None, concurrency=1):
         """a1-a3: returns (image or None, state). ``state`` is this pipeline's buffer. ``events``:
         optional (begin, end) torch events recorded around the a3 composite kernel."""
         rec = self.project_bin(rows, sigma, idx, stream)
@@ -57,20 +57,20 @@ class ViewPipeline:
             events[0].record()
         L.oit_composite_fwd(self.cam, rec, self.pairs, self.offs, bg, self.fwd_ws, base=base, route=route,
                             image=self.image if image else None, state=self.state, base_out=base_out,
-                            stream=stream, counters=counters)
+                            stream=stream, counters=counters, concurrency=concurrency)
         if events is not None:
             events[1].record()
         return (self.image if image else None), self.state
 
     def backward(self, rows, sigma, idx, bg, state, dL_dimage, grad, dL_dsigma, dL_dcov=None, scale=1.0,
-                 reuse_bins=True, stream=None, events=None, target=None, loss="l1", per_pixel=False):
+                 reuse_bins=True, stream=None, events=None, target=None, loss="l1", per_pixel=False, concurrency=1):
         """a4-a6 for the splats idx (grad rows += ...). With reuse_bins the records/pairs of the
         preceding forward over the same idx are reused."""
         n = int(idx.numel())
         rec = (self.rec[:n] if n > 0 else self.rec) if reuse_bins else self.project_bin(rows, sigma, idx, stream)
         L.oit_composite_bwd(rows, sigma, self.cam, idx, rec, self.pairs, self.offs, bg, state, dL_dimage, grad,
                             dL_dsigma, self.bwd_ws, dL_dcov=dL_dcov, scale=scale, stream=stream, events=events,
-                            target=target, loss=loss, per_pixel=per_pixel)
+                            target=target, loss=loss, per_pixel=per_pixel, concurrency=concurrency)
 
     def pairs_used(self) -> int:
         return int(self.n_pairs.item())

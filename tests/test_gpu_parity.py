@@ -506,6 +506,29 @@ def test_concurrent_views_accumulate_like_sequential():
     assert ok, describe_bad(g3, ref, bad, bnd)
 
 
+def test_concurrency_hint_does_not_change_results():
+    """concurrency only sizes the persistent grids: forward state and backward equal up to fp32
+    summation order (the order inside a tile list comes from atomics, R15; the gradient rows
+    accumulate with atomics)."""
+    sc = SCENES[1]
+    cam = sc.cams[0]
+    idx = _t(np.arange(sc.n, dtype=np.int32))
+    rows, sigma = _t(sc.rows), _t(np.array([sc.sigma], np.float32))
+    g = _t(synth.dl_dimage(cam, 3))
+    p = _pipe(cam, sc.n)
+    out = []
+    for conc in (1, 16, 1000):
+        _, st = p.forward(rows, sigma, idx, sc.bg, image=False, concurrency=conc)
+        st = st.clone()
+        grad = torch.zeros((sc.n, 80), dtype=torch.float32, device=DEV)
+        ds = torch.zeros(1, dtype=torch.float32, device=DEV)
+        p.backward(rows, sigma, idx, sc.bg, st, g, grad, ds, concurrency=conc)
+        out.append((st.cpu().numpy(), grad.cpu().numpy()))
+    for st, gr in out[1:]:
+        assert np.allclose(st, out[0][0], rtol=1e-5, atol=1e-7)
+        assert np.abs(gr - out[0][1]).max() <= 1e-5 * np.abs(out[0][1]).max()
+
+
 def test_score_split_across_streams_equals_single_call():
     """oit_score_subsample on disjoint view subsets (concurrent streams, scale 1/S each) equals one
     call over all S views (the mean of R19)."""
