@@ -431,7 +431,8 @@ class Workload:
                 with torch.cuda.stream(self.streams[k]):
                     L.oit_score_subsample(self.rows, self.sigma, self.cams, self.targets_list, self.caches_list,
                                           self.act, self.ina, part, self.loss, self.bg, self.score_grad, self.score_dsig,
-                                          self.score_cap, self.max_pairs, self.score_ws[k], scale=1.0 / self.S)
+                                          self.score_cap, self.max_pairs, self.score_ws[k], scale=1.0 / self.S,
+                                          concurrency=sum(1 for q in parts if q))
             for k, part in enumerate(parts):
                 if part:
                     main.wait_stream(self.streams[k])
@@ -763,7 +764,7 @@ def time_c4(args, torch, L, synth, flush, rates=(0.01, 0.02, 0.05, 0.10), n_view
                 streams[k].wait_stream(main)
                 with torch.cuda.stream(streams[k]):
                     L.oit_score_subsample(rows, sigma, sc.cams, targets, caches, act, ina, part, "l1", sc.bg, sg, sds,
-                                          cap, mp, ws[k], scale=1.0 / S)
+                                          cap, mp, ws[k], scale=1.0 / S, concurrency=k_used)
             for k in range(k_used):
                 main.wait_stream(streams[k])
             bits.copy_(bits0)

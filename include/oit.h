@@ -241,6 +241,8 @@ int oit_select_views(const float* centers, int32_t n_views, int32_t n_sub, uint6
  * [5][n_tiles][256]; caches[j] may be NULL = nothing frozen). All views share W and H.
  * *d_max_pairs (device int64) receives the largest pair count met; if > pair_capacity the
  * result is invalid and the caller re-calls with more room.
+ * concurrency (≥ 1): score calls in flight on other streams — sizes the persistent grids as in
+ * oit_composite_bwd_ex (results do not depend on it).
  * Scratch: ws of oit_score_workspace_bytes(...) bytes.
  * --------------------------------------------------------------------------------------- */
 size_t oit_score_workspace_bytes(const oit_camera* cam, int32_t n_active, int32_t n_score,
@@ -251,7 +253,7 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
                         int32_t n_score, const int32_t* views_host, int32_t n_sub, int32_t loss,
                         const float bg_host[3], float scale, float* score_grad, float* dL_dsigma,
                         int64_t pair_capacity, int64_t* d_max_pairs, void* ws, size_t ws_bytes,
-                        oit_stream_t stream);
+                        int32_t concurrency, oit_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------
  * a8  oit_update_active_set — Eq. 8 with the text's ∃ reading (R18), Alg. 1 l.13

@@ -239,8 +239,10 @@ def oit_score_workspace_bytes(cam, n_active: int, n_score: int, pair_capacity: i
 
 
 def oit_score_subsample(rows, sigma, cams, targets, caches, active_idx, score_idx, views, loss: str, bg,
-                        score_grad, dL_dsigma, pair_capacity: int, max_pairs, ws, stream=None, scale=None):
-    """scale: weight of each view's gradient (default 1/len(views): the mean over these views)."""
+                        score_grad, dL_dsigma, pair_capacity: int, max_pairs, ws, stream=None, scale=None,
+                        concurrency: int = 1):
+    """scale: weight of each view's gradient (default 1/len(views): the mean over these views);
+    concurrency: score calls in flight on other streams (grid sizing only)."""
     sc = scene(rows, sigma)
     V = len(cams)
     cam_arr = (Camera * V)(*[camera(c) for c in cams])
@@ -253,7 +255,7 @@ def oit_score_subsample(rows, sigma, cams, targets, caches, active_idx, score_id
                                      C.c_float(1.0 / len(views) if scale is None else scale), _ptr(score_grad),
                                      _ptr(dL_dsigma),
                                      int(pair_capacity), _ptr(max_pairs), _ptr(ws), int(ws.numel()),
-                                     _stream(stream)), "oit_score_subsample")
+                                     int(concurrency), _stream(stream)), "oit_score_subsample")
 
 
 def oit_update_workspace_bytes(n_total: int) -> int:

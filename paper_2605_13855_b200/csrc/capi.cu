@@ -287,7 +287,7 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
                         int32_t n_active, const int32_t* score_idx, int32_t n_score, const int32_t* views_host,
                         int32_t n_sub, int32_t loss, const float bg_host[3], float scale, float* score_grad, float* dL_dsigma,
                         int64_t pair_capacity, int64_t* d_max_pairs, void* ws, size_t ws_bytes,
-                        oit_stream_t stream) {
+                        int32_t concurrency, oit_stream_t stream) {
   if (!scene || !scene->rows || !scene->sigma || !cams_host || !targets_host || !views_host || !bg_host ||
       !dL_dsigma || !d_max_pairs || !ws)
     return OIT_EINVAL;
@@ -311,14 +311,15 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
     launch_project(dc, scene->rows, scene->sigma, active_idx, n_active, w.rec_a, w.tps_a, st);
     launch_bin(dc, w.rec_a, w.tps_a, n_active, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st);
     launch_composite_fwd(dc, w.rec_a, w.pairs, w.offs, pair_capacity, caches_host ? caches_host[j] : nullptr, nullptr,
-                         nullptr, w.state, nullptr, st, nullptr, w.fwd_ws);
+                         nullptr, w.state, nullptr, st, nullptr, w.fwd_ws, concurrency);
     // L_j and its pixel gradient (fused with the backward coefficients)
     coef_from_target(dc, &cams_host[j], w.state, targets_host[j], loss, w.coef4, w.coefa, w.dssim_ws, st);
     // back-propagate L_j to the scored splats (R20)
     launch_project(dc, scene->rows, scene->sigma, score_idx, n_score, w.rec_s, w.tps_s, st);
     launch_bin(dc, w.rec_s, w.tps_s, n_score, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st);
     launch_composite_bwd(dc, scene->rows, scene->sigma, score_idx, n_score, w.rec_s, w.pairs, w.offs, pair_capacity,
-                         w.coef4, w.coefa, scale, score_grad, dL_dsigma, nullptr, w.bwd_ws, st);
+                         w.coef4, w.coefa, scale, score_grad, dL_dsigma, nullptr, w.bwd_ws, st, nullptr, nullptr, 0,
+                         concurrency);
   }
   return launch_status();
 }

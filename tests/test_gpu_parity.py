@@ -556,7 +556,7 @@ def test_score_split_across_streams_equals_single_call():
                              device=DEV)
             with torch.cuda.stream(s_):
                 L.oit_score_subsample(rows, sigma, sc.cams, targets, caches, _t(act), _t(ina), part, "l2", sc.bg, sg,
-                                      ds, cap, mp, ws, scale=1.0 / len(views))
+                                      ds, cap, mp, ws, scale=1.0 / len(views), concurrency=len(parts))
         for s_ in streams:
             main.wait_stream(s_)
         torch.cuda.synchronize()
