@@ -349,6 +349,38 @@ def test_degenerate_scene_parity():
         assert abs(dsig - dsref) <= 1e-4 * abs(dsref) + 1e-6
 
 
+@pytest.mark.parametrize("W,H", [(32767, 17), (19, 32767)])
+def test_maximum_image_extent(W, H):
+    """The largest width/height the ABI accepts (32767) with a ragged other side:
+    tile sets exact, image within 1e-5, gradients within R31; one more pixel is OIT_ESHAPE."""
+    L = _L()
+    sc = synth.scene_c1(seed=21, n=400, n_views=1, res=64)
+    cam = dict(sc.cams[0])
+    cam["width"], cam["height"] = W, H
+    cam["cx"], cam["cy"] = W / 2.0, H / 2.0
+    cam["fx"] = cam["fy"] = 80.0 * max(W, H) / 64.0 / 64.0 * 8.0   # the scene spans a few hundred pixels
+    idx = np.arange(sc.n, dtype=np.int32)
+    rows, sigma = _t(sc.rows), _t(np.array([sc.sigma], np.float32))
+    p = _pipe(cam, sc.n)
+    img, st = p.forward(rows, sigma, _t(idx), sc.bg)
+    ref = O.render(sc.rows, sc.sigma, idx, cam, sc.bg)
+    assert p.pairs_used() == ref["tile_pairs"] > 0
+    assert np.abs(img.cpu().numpy() - ref["image"]).max() < 1e-5
+    g = synth.dl_dimage(cam, 4)
+    grad = torch.zeros((sc.n, 80), dtype=torch.float32, device=DEV)
+    dsig = torch.zeros(1, dtype=torch.float32, device=DEV)
+    p.backward(rows, sigma, _t(idx), sc.bg, st, _t(g), grad, dsig)
+    gref, _, _, bnd = O.backward_bound(sc.rows, sc.sigma, idx, cam, sc.bg, ref["state"], g)
+    ok, bad = grad_close(grad.cpu().numpy(), gref, bnd)
+    assert ok, describe_bad(grad.cpu().numpy(), gref, bad, bnd)
+    big = dict(cam)
+    big["width" if W > H else "height"] = 32768
+    rec = torch.empty((sc.n, 20), dtype=torch.float32, device=DEV)
+    tps = torch.empty(sc.n, dtype=torch.int32, device=DEV)
+    with pytest.raises(L.OitError):
+        L.oit_project_cull(rows, sigma, big, _t(idx), rec, tps)
+
+
 # ------------------------------------------------------------------ full-size sampled ----
 @pytest.mark.slow
 def test_c2_full_size_parity_sampled():
