@@ -183,10 +183,9 @@ __global__ void __launch_bounds__(kMomentsThreads, 6) k_moments(DevCam cam, cons
   const int n_items = *n_items_p;
   const unsigned FULL = 0xffffffffu;
   int staged = -1;
-  for (;;) {
-    int item = 0;
-    if (lane == 0) item = atomicAdd(counter, 1);
-    item = __shfl_sync(FULL, item, 0);
+  const int n_warps = gridDim.x * (kMomentsThreads / 32);
+  // first item static (warp g takes item g), then dynamic claims offset by the number of warps
+  for (int item = blockIdx.x * (kMomentsThreads / 32) + wid;;) {
     if (item >= n_items) return;
     const int4 it = items[item];
     const int vt = it.x, chunk = it.y;  // vt = 4·tile + quadrant
@@ -247,6 +246,9 @@ __global__ void __launch_bounds__(kMomentsThreads, 6) k_moments(DevCam cam, cons
       red_add_v4(a + 4, m.Od, m.M1, m.M2, m.XX);
       red_add_v4(a + 8, m.XY, m.YY, 0.f, 0.f);
     }
+    int nxt = 0;
+    if (lane == 0) nxt = n_warps + atomicAdd(counter, 1);
+    item = __shfl_sync(FULL, nxt, 0);
   }
 }
 

@@ -62,8 +62,10 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
   const int n_items = *n_items_p;
   const int ly = tid >> 2, lx = tid & 3;  // pixels (lx + 4k, ly), k = 0..3
   const int p0 = ly * kTile + lx;
-  for (;;) {
-    if (tid == 0) s_item = atomicAdd(counter, 1);
+  // first item static (CTA b takes item b: no claim on the critical start), then dynamic claims
+  // from the shared counter offset by the grid size
+  for (int first = 1;; first = 0) {
+    if (tid == 0) s_item = first ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(counter, 1);
     __syncthreads();
     const int item = s_item;
     __syncthreads();
