@@ -402,12 +402,20 @@ class Workload:
                 p.set_camera(cam)
                 # a3 (no image: the fused a4 below resolves C from the state), then a4+a5+a6 with
                 # the L1 gradient against the view's training image fused into the coefficients
-                _, st = p.forward(self.rows, self.sigma, self.act, self.bg, base=self.caches[v], image=False,
-                                  events=self.ev_fwd[v], concurrency=ns)
                 if host_targets is not None:
                     self.streams[k].wait_event(self.ev_copy[v])
-                p.backward(self.rows, self.sigma, self.act, self.bg, st, None, self.grad, self.dsig,
-                           events=self.ev_bwd[v], target=self.targets[v], loss=self.loss, concurrency=ns)
+                if self.loss in ("l1", "l2"):
+                    # a3 + a4 fused: the forward's epilogue applies the pixel-local loss and writes the
+                    # backward coefficients into the backward workspace (no pixel-state round trip)
+                    p.forward_loss(self.rows, self.sigma, self.act, self.bg, self.targets[v], self.loss,
+                                   base=self.caches[v], events=self.ev_fwd[v], concurrency=ns)
+                    p.backward(self.rows, self.sigma, self.act, self.bg, None, None, self.grad, self.dsig,
+                               events=self.ev_bwd[v], coef_ready=True, concurrency=ns)
+                else:   # D-SSIM is not pixel-local: state → resolve → SSIM stencils → coefficients
+                    _, st = p.forward(self.rows, self.sigma, self.act, self.bg, base=self.caches[v], image=False,
+                                      events=self.ev_fwd[v], concurrency=ns)
+                    p.backward(self.rows, self.sigma, self.act, self.bg, st, None, self.grad, self.dsig,
+                               events=self.ev_bwd[v], target=self.targets[v], loss=self.loss, concurrency=ns)
         for st_ in self.streams[:ns]:
             main.wait_stream(st_)
         if host_targets is not None:
@@ -456,7 +464,8 @@ class Workload:
         # coef | quadrant count, scan, quadrant scatter, fused item builder, moments, epilogue
         bwd = lambda n: 1 + ((5 + scan_kernels(4 * nt)) if n > 0 else 0)  # noqa: E731
         lossk = 3 if self.loss == "dssim" else 0   # resolve + 2 SSIM stencil passes (L1/L2: fused in k_coef)
-        train = self.V * (proj(a) + binn(a) + fwd + bwd(a) + lossk)
+        # training views with L1/L2: a4 fused into the forward's epilogue (no k_coef launch)
+        train = self.V * (proj(a) + binn(a) + fwd + bwd(a) - (1 if self.loss in ("l1", "l2") else 0) + lossk)
         refresh = 1
         if s > 0:
             refresh += self.S * (proj(a) + binn(a) + fwd + 1 + lossk + proj(s) + binn(s) + (bwd(s) - 1))

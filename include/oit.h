@@ -147,6 +147,22 @@ int oit_composite_fwd_ex(const oit_camera* cam, const float* rec, const int32_t*
                          float* base_out, int64_t* d_counters, void* ws, size_t ws_bytes,
                          int32_t concurrency, oit_stream_t stream);
 
+/* a3 + a4 fused for a training view (Alg. 1 l.4-5; Eq. B.1-B.2): the forward
+ * of oit_composite_fwd_ex (no route, no image) whose epilogue resolves each pixel (Eq. 7), applies
+ * the pixel-local loss (loss 0 = L1, 1 = L2, | OIT_TARGET_U8 for an 8-bit target; as
+ * oit_loss_grad) against target [3][H][W] and writes the backward coefficients (K, u, s, a) straight
+ * into bwd_ws — the workspace (of oit_bwd_workspace_bytes(cam, n_slots, pair_capacity) bytes) the
+ * following oit_composite_bwd_ex call on the same stream receives with target = NULL,
+ * dL_dimage = NULL and loss = OIT_COEF_IN_WS. No pixel-state round trip; state (nullable) is still
+ * written if given. ws: oit_fwd_workspace_bytes scratch. D-SSIM (loss 2) is not pixel-local: use
+ * oit_composite_bwd_ex with a target for it. */
+#define OIT_COEF_IN_WS 0x200 /* oit_composite_bwd_ex: the coefficients are already in ws */
+int oit_composite_fwd_loss(const oit_camera* cam, const float* rec, const int32_t* pair_slot,
+                           const int32_t* tile_offsets, int64_t pair_capacity, const float bg_host[3],
+                           const float* base, const void* target, int32_t loss, float* state, void* ws,
+                           size_t ws_bytes, void* bwd_ws, size_t bwd_ws_bytes, int32_t n_slots,
+                           int32_t concurrency, oit_stream_t stream);
+
 /* ---------------------------------------------------------------------------------------
  * a4  oit_loss_grad — pixel loss gradient dL/dC of L = mean_{3HW} |C - I| (loss 0, sign(0)=0)
  * or mean (C - I)² (loss 1): the L1 term of the 3DGS loss (R24).
@@ -177,6 +193,8 @@ int oit_composite_bwd(const oit_scene* scene, const oit_camera* cam, const int32
                       size_t ws_bytes, oit_stream_t stream);
 
 /* Same as oit_composite_bwd, plus:
+ *  - loss = OIT_COEF_IN_WS with target = NULL (dL_dimage and state may then be NULL): the pixel
+ *    coefficients were written into ws by oit_composite_fwd_loss (a4 fused into the forward);
  *  - target (nullable, [3][H][W] device, fp32 — or uint8 with OIT_TARGET_U8): if given, dL_dimage
  *    is ignored (may be NULL) and the
  *    pixel gradient is the L1 (loss 0) / L2 (loss 1) gradient of oit_loss_grad, computed from the

@@ -57,6 +57,7 @@ class AdamCfg(C.Structure):
 
 LOSS_CODE = {"l1": 0, "l2": 1, "dssim": 2}   # "dssim" = the 3DGS (1−λ)L1 + λ·D-SSIM, λ = 0.2
 OIT_TARGET_U8 = 0x100                          # loss flag: 8-bit targets (uint8 [3][H][W], value u8/255)
+OIT_COEF_IN_WS = 0x200                         # bwd_ex: coefficients already in ws (oit_composite_fwd_loss)
 
 
 def _loss_flags(loss: str, targets) -> int:
@@ -85,19 +86,21 @@ def lib() -> C.CDLL:
             "oit_bin_tiles": (C.c_int, [cam_p, vp, vp, i32, vp, i64, vp, vp, vp, sz, vp]),
             "oit_fwd_workspace_bytes": (sz, [cam_p, i64]),
             "oit_composite_fwd": (C.c_int, [cam_p, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
-            "oit_composite_fwd_ex": (C.c_int, [cam_p, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+            "oit_composite_fwd_ex": (C.c_int, [cam_p, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, sz, i32, vp]),
+            "oit_composite_fwd_loss": (C.c_int, [cam_p, vp, vp, vp, i64, vp, vp, vp, i32, vp, vp, sz, vp, sz, i32, i32,
+                                                 vp]),
             "oit_loss_grad": (C.c_int, [cam_p, vp, vp, i32, vp, vp]),
             "oit_bwd_workspace_bytes": (sz, [cam_p, i32, i64]),
             "oit_composite_bwd": (C.c_int, [scene_p, cam_p, vp, i32, vp, vp, vp, i64, vp, vp, vp, f32, vp, vp,
                                             vp, vp, sz, vp]),
             "oit_composite_bwd_ex": (C.c_int, [scene_p, cam_p, vp, i32, vp, vp, vp, i64, vp, vp, vp, f32, vp, vp,
-                                               vp, vp, sz, vp, i32, C.POINTER(BwdEvents), vp]),
+                                               vp, vp, sz, vp, i32, C.POINTER(BwdEvents), i32, vp]),
             "oit_composite_bwd_perpixel": (C.c_int, [scene_p, cam_p, vp, i32, vp, vp, vp, i64, vp, vp, vp, f32, vp,
                                                      vp, vp, vp, sz, C.POINTER(BwdEvents), vp]),
             "oit_select_views": (C.c_int, [vp, i32, i32, C.c_uint64, C.c_uint32, vp, vp]),
             "oit_score_workspace_bytes": (sz, [cam_p, i32, i32, i64]),
             "oit_score_subsample": (C.c_int, [scene_p, cam_p, i32, vp, vp, vp, i32, vp, i32, vp, i32, i32, vp, f32,
-                                              vp, vp, i64, vp, vp, sz, vp]),
+                                              vp, vp, i64, vp, vp, sz, i32, vp]),
             "oit_update_workspace_bytes": (sz, [i32]),
             "oit_delta_workspace_bytes": (sz, [i32]),
             "oit_active_set_delta": (C.c_int, [vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]),
@@ -117,7 +120,7 @@ def lib() -> C.CDLL:
 
 
 EXPORTED = ["oit_status_string", "oit_num_tiles", "oit_project_cull", "oit_bin_workspace_bytes", "oit_bin_tiles",
-            "oit_fwd_workspace_bytes", "oit_composite_fwd", "oit_composite_fwd_ex", "oit_loss_grad", "oit_bwd_workspace_bytes", "oit_composite_bwd", "oit_composite_bwd_ex",
+            "oit_fwd_workspace_bytes", "oit_composite_fwd", "oit_composite_fwd_ex", "oit_composite_fwd_loss", "oit_loss_grad", "oit_bwd_workspace_bytes", "oit_composite_bwd", "oit_composite_bwd_ex",
             "oit_select_views", "oit_score_workspace_bytes", "oit_score_subsample", "oit_update_workspace_bytes",
             "oit_update_active_set", "oit_delta_workspace_bytes", "oit_active_set_delta",
             "oit_reconcile_workspace_bytes", "oit_reconcile_cache", "oit_adam_step",
@@ -194,6 +197,18 @@ def oit_composite_fwd(cam, rec, pair_slot, tile_offsets, bg, ws, base=None, rout
                                           _stream(stream)), "oit_composite_fwd_ex")
 
 
+def oit_composite_fwd_loss(cam, rec, pair_slot, tile_offsets, bg, ws, bwd_ws, n_slots: int, target, loss: str,
+                           base=None, state=None, stream=None, concurrency: int = 1):
+    """a3 + a4 fused (training view): the forward whose epilogue applies the L1/L2 loss against
+    target (fp32 or uint8) and writes the backward coefficients into bwd_ws; follow with
+    oit_composite_bwd(..., coef_ready=True) on the same bwd_ws."""
+    _check(lib().oit_composite_fwd_loss(C.byref(camera(cam)), _ptr(rec), _ptr(pair_slot), _ptr(tile_offsets),
+                                        int(pair_slot.numel()), _f3(bg), _ptr(base), _ptr(target),
+                                        _loss_flags(loss, [target]), _ptr(state), _ptr(ws), int(ws.numel()),
+                                        _ptr(bwd_ws), int(bwd_ws.numel()), int(n_slots), int(concurrency),
+                                        _stream(stream)), "oit_composite_fwd_loss")
+
+
 def oit_loss_grad(cam, image, target, loss: str, dL_dimage, stream=None):
     _check(lib().oit_loss_grad(C.byref(camera(cam)), _ptr(image), _ptr(target), 0 if loss == "l1" else 1,
                                _ptr(dL_dimage), _stream(stream)), "oit_loss_grad")
@@ -205,11 +220,12 @@ def oit_bwd_workspace_bytes(cam, n_slots: int, pair_capacity: int) -> int:
 
 def oit_composite_bwd(rows, sigma, cam, idx, rec, pair_slot, tile_offsets, bg, state, dL_dimage, grad, dL_dsigma,
                       ws, dL_dcov=None, scale: float = 1.0, stream=None, events=None, target=None, loss="l1",
-                      per_pixel: bool = False, concurrency: int = 1):
+                      per_pixel: bool = False, concurrency: int = 1, coef_ready: bool = False):
     """events: optional (begin, end) torch.cuda.Event pair recorded around the a5 moment kernel;
     target: optional training image — the L1/L2 pixel gradient is then fused into the backward
-    (dL_dimage may be None); concurrency: calls in flight on other streams (grid sizing). Any of
-    them selects oit_composite_bwd_ex."""
+    (dL_dimage may be None); concurrency: calls in flight on other streams (grid sizing);
+    coef_ready: oit_composite_fwd_loss already wrote the coefficients into ws (state, dL_dimage
+    and target unused). Any of them selects oit_composite_bwd_ex."""
     sc, c = scene(rows, sigma), camera(cam)
     args = (C.byref(sc), C.byref(c), _ptr(idx), int(idx.numel()), _ptr(rec), _ptr(pair_slot), _ptr(tile_offsets),
             int(pair_slot.numel()), _f3(bg), _ptr(state), _ptr(dL_dimage), C.c_float(scale), _ptr(grad),
@@ -218,13 +234,13 @@ def oit_composite_bwd(rows, sigma, cam, idx, rec, pair_slot, tile_offsets, bg, s
         ev = None if events is None else C.byref(BwdEvents(C.c_void_p(events[0].cuda_event),
                                                            C.c_void_p(events[1].cuda_event)))
         _check(lib().oit_composite_bwd_perpixel(*args, ev, _stream(stream)), "oit_composite_bwd_perpixel")
-    elif events is None and target is None and concurrency == 1:
+    elif events is None and target is None and concurrency == 1 and not coef_ready:
         _check(lib().oit_composite_bwd(*args, _stream(stream)), "oit_composite_bwd")
     else:
         ev = None if events is None else C.byref(BwdEvents(C.c_void_p(events[0].cuda_event),
                                                            C.c_void_p(events[1].cuda_event)))
-        _check(lib().oit_composite_bwd_ex(*args, _ptr(target), _loss_flags(loss, [target]), ev, int(concurrency),
-                                          _stream(stream)),
+        flags = OIT_COEF_IN_WS if coef_ready else _loss_flags(loss, [target])
+        _check(lib().oit_composite_bwd_ex(*args, _ptr(target), flags, ev, int(concurrency), _stream(stream)),
                "oit_composite_bwd_ex")
 
 

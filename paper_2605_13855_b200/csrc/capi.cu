@@ -120,6 +120,32 @@ int oit_composite_fwd_ex(const oit_camera* cam, const float* rec, const int32_t*
   return launch_status();
 }
 
+int oit_composite_fwd_loss(const oit_camera* cam, const float* rec, const int32_t* pair_slot,
+                           const int32_t* tile_offsets, int64_t pair_capacity, const float bg_host[3], const float* base,
+                           const void* target, int32_t loss, float* state, void* ws, size_t ws_bytes, void* bwd_ws,
+                           size_t bwd_ws_bytes, int32_t n_slots, int32_t concurrency, oit_stream_t stream) {
+  if (!cam_ok(cam) || !tile_offsets || !bg_host || pair_capacity < 0 || !target || !ws || !bwd_ws || n_slots < 0)
+    return OIT_EINVAL;
+  const int32_t l = loss & ~OIT_TARGET_U8;
+  if (l != 0 && l != 1) return OIT_EINVAL;
+  if (pair_capacity > 0 && (!rec || !pair_slot)) return OIT_EINVAL;
+  if (!shape_ok(cam)) return OIT_ESHAPE;
+  if (ws_bytes < oit_fwd_workspace_bytes(cam, pair_capacity) ||
+      bwd_ws_bytes < oit_bwd_workspace_bytes(cam, n_slots, pair_capacity))
+    return OIT_ECAPACITY;
+  const int32_t nt = oit_num_tiles(cam);
+  Carve cv(bwd_ws);  // the coefficient region oit_composite_bwd_ex carves first
+  FwdLoss fl;
+  fl.target = target;
+  fl.target_u8 = (loss & OIT_TARGET_U8) != 0;
+  fl.loss = l;
+  fl.coef4 = reinterpret_cast<float4*>(cv.take<float>((size_t)nt * kTilePx * 4));
+  fl.coefa = cv.take<float>((size_t)nt * kTilePx);
+  launch_composite_fwd(dev_cam(cam, bg_host), rec, pair_slot, tile_offsets, pair_capacity, base, nullptr, nullptr,
+                       state, nullptr, S(stream), nullptr, ws, concurrency, fl);
+  return launch_status();
+}
+
 int oit_loss_grad(const oit_camera* cam, const float* image, const float* target, int32_t loss, float* dL_dimage,
                   oit_stream_t stream) {
   if (!cam || !image || !target || !dL_dimage || (loss != 0 && loss != 1)) return OIT_EINVAL;
@@ -191,8 +217,11 @@ int oit_composite_bwd_ex(const oit_scene* scene, const oit_camera* cam, const in
                          const void* target, int32_t loss, const oit_bwd_events* ev, int32_t concurrency,
                          oit_stream_t stream) {
   if (!scene || !scene->rows || !scene->sigma || !cam_ok(cam) || n_slots < 0 || pair_capacity < 0) return OIT_EINVAL;
-  if (!tile_offsets || !bg_host || !state || (!dL_dimage && !target) || !dL_dsigma || !ws) return OIT_EINVAL;
+  if (!tile_offsets || !bg_host || !dL_dsigma || !ws) return OIT_EINVAL;
+  if (target && !state) return OIT_EINVAL;
   if (target && !loss_ok(loss)) return OIT_EINVAL;
+  if (!target && !(loss & OIT_COEF_IN_WS) && !dL_dimage) return OIT_EINVAL;
+  if (!target && !(loss & OIT_COEF_IN_WS) && !state) return OIT_EINVAL;
   if (n_slots > 0 && (!idx || !rec || !grad)) return OIT_EINVAL;
   if (pair_capacity > 0 && !pair_slot) return OIT_EINVAL;
   if (!shape_ok(cam) || n_slots > scene->n || oit_num_tiles(cam) > kMaxScan) return OIT_ESHAPE;
@@ -205,7 +234,8 @@ int oit_composite_bwd_ex(const oit_scene* scene, const oit_camera* cam, const in
   void* dssim_ws = cv.take<char>(dssim_bytes(cam));
   void* rest = cv.base + cv.off;
   if (target) coef_from_target(dc, cam, state, target, loss, coef4, coefa, dssim_ws, S(stream));
-  else launch_coef(dc, state, dL_dimage, nullptr, false, 0, coef4, coefa, S(stream));
+  else if (!(loss & OIT_COEF_IN_WS)) launch_coef(dc, state, dL_dimage, nullptr, false, 0, coef4, coefa, S(stream));
+  // else: oit_composite_fwd_loss wrote the coefficients into this workspace
   launch_composite_bwd(dc, scene->rows, scene->sigma, idx, n_slots, rec, pair_slot, tile_offsets, pair_capacity,
                        coef4, coefa, scale, grad, dL_dsigma, dL_dcov, rest, S(stream),
                        ev ? static_cast<cudaEvent_t>(ev->moments_begin) : nullptr,

@@ -350,6 +350,23 @@ __device__ __forceinline__ void resolve_pixel(float P0, float P1, float P2, floa
   C2 = __fmaf_rn(T, bg[2], omT * F2);
 }
 
+// a4 per pixel: the pixel gradient g of the L1 (loss 0, sign(0) = 0) / L2 (loss 1) loss against the
+// target value t (both mean over 3HW; inv = 1/(3HW)), then the backward coefficients of Eq. B.2:
+// K = (1−T)/Q (0 if Q = 0), (u, s) = (K g, K g·F), a = T g·(F − c0).
+__device__ __forceinline__ float target_value(const float* t, size_t i) { return t[i]; }
+__device__ __forceinline__ float target_value(const uint8_t* t, size_t i) { return __fdiv_rn((float)t[i], 255.0f); }
+__device__ __forceinline__ float loss_grad_px(float c, float t, int32_t loss, float inv) {
+  const float d = c - t;
+  return loss == 0 ? (d > 0.f ? inv : (d < 0.f ? -inv : 0.f)) : 2.f * d * inv;
+}
+__device__ __forceinline__ void pixel_coef(float F0, float F1, float F2, float Q, float T, const float* bg, float g0,
+                                           float g1, float g2, float4& c4, float& ca) {
+  const float K = Q > 0.f ? (1.f - T) / Q : 0.f;
+  const float gF = g0 * F0 + g1 * F1 + g2 * F2;
+  ca = T * (g0 * (F0 - bg[0]) + g1 * (F1 - bg[1]) + g2 * (F2 - bg[2]));
+  c4 = make_float4(K * g0, K * g1, K * g2, K * gF);
+}
+
 // 128-bit vector reduction to global memory (sm_90+): one L2 atomic per 16 B.
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)

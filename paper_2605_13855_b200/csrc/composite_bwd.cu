@@ -24,9 +24,6 @@ namespace oit {
 constexpr int kMomentsThreads = 128;
 
 // ------------------------------------------------------------------------------ a4 coef ---
-__device__ __forceinline__ float target_value(const float* t, size_t i) { return t[i]; }
-__device__ __forceinline__ float target_value(const uint8_t* t, size_t i) { return __fdiv_rn((float)t[i], 255.0f); }
-
 template <class TT>
 __global__ void __launch_bounds__(256) k_coef(DevCam cam, const float* __restrict__ state,
                                               const float* __restrict__ dL_dimage, const TT* __restrict__ target,
@@ -50,21 +47,15 @@ __global__ void __launch_bounds__(256) k_coef(DevCam cam, const float* __restric
     g0 = dL_dimage[p]; g1 = dL_dimage[hw + p]; g2 = dL_dimage[2 * hw + p];
   } else {
     const float inv = 1.0f / (3.0f * (float)hw);
-    const float d0 = C0 - target_value(target, p), d1 = C1 - target_value(target, hw + p);
-    const float d2 = C2 - target_value(target, 2 * hw + p);
-    if (loss == 0) {
-      g0 = (d0 > 0.f ? inv : (d0 < 0.f ? -inv : 0.f));
-      g1 = (d1 > 0.f ? inv : (d1 < 0.f ? -inv : 0.f));
-      g2 = (d2 > 0.f ? inv : (d2 < 0.f ? -inv : 0.f));
-    } else {
-      g0 = 2.f * d0 * inv; g1 = 2.f * d1 * inv; g2 = 2.f * d2 * inv;
-    }
+    g0 = loss_grad_px(C0, target_value(target, p), loss, inv);
+    g1 = loss_grad_px(C1, target_value(target, hw + p), loss, inv);
+    g2 = loss_grad_px(C2, target_value(target, 2 * hw + p), loss, inv);
   }
-  const float K = Q > 0.f ? (1.f - T) / Q : 0.f;
-  const float gF = g0 * F0 + g1 * F1 + g2 * F2;
-  const float a = T * (g0 * (F0 - cam.bg[0]) + g1 * (F1 - cam.bg[1]) + g2 * (F2 - cam.bg[2]));
-  coef4[pix] = make_float4(K * g0, K * g1, K * g2, K * gF);
-  coefa[pix] = a;
+  float4 c4;
+  float ca;
+  pixel_coef(F0, F1, F2, Q, T, cam.bg, g0, g1, g2, c4, ca);
+  coef4[pix] = c4;
+  coefa[pix] = ca;
 }
 
 // The image [3][H][W] of a pixel state (for the non-pixel-local D-SSIM loss, NEXT-3).

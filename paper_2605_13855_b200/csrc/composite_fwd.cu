@@ -46,13 +46,16 @@ __device__ __forceinline__ void store_px(const Px& a, float* dst, size_t plane, 
   dst[4 * plane + px] = a.T;
 }
 
-template <bool kBase, bool kCount>
-__global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
+// kLoss (a4 fused into the epilogue, training views): 0 none; 1 / 2 — the L1/L2 loss against an
+// fp32 / 8-bit target, the backward coefficients (coef4, coefa) written instead of a state round trip.
+template <bool kBase, bool kCount, int kLoss = 0>
+__global__ void __launch_bounds__(kFwdThreads, kLoss ? 16 : 1) k_fwd_items(
     DevCam cam, const float4* __restrict__ rec, const int32_t* __restrict__ pair_slot,
     const int32_t* __restrict__ offs, int64_t capacity, const int4* __restrict__ items,
     const int32_t* __restrict__ n_items_p, int32_t* __restrict__ counter, const int32_t* __restrict__ tile_nch,
     int32_t* __restrict__ done, float* __restrict__ partial, const float* __restrict__ base,
-    float* __restrict__ image, float* __restrict__ state, unsigned long long* __restrict__ counters, int chunk_len) {
+    float* __restrict__ image, float* __restrict__ state, unsigned long long* __restrict__ counters, int chunk_len,
+    FwdLoss fl) {
   __shared__ float4 s_q0[kFwdThreads], s_q1[kFwdThreads], s_q2[kFwdThreads];
   __shared__ float2 s_k[kFwdThreads];
   __shared__ int s_item, s_last;
@@ -199,11 +202,32 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_items(
       for (int k = 0; k < 4; k++) {
         if (state) store_px(a[k], state, plane, pxb + 4 * k);
         const int x = tx0 + lx + 4 * k;
-        if (image && y < cam.H && x < cam.W) {
+        const bool in = y < cam.H && x < cam.W;
+        if ((image || kLoss) && in) {
           float F0, F1, F2, C0, C1, C2;
           resolve_pixel(a[k].P0, a[k].P1, a[k].P2, a[k].Q, a[k].T, cam.bg, F0, F1, F2, C0, C1, C2);
           const size_t pp = (size_t)y * cam.W + x;
-          image[pp] = C0; image[hw + pp] = C1; image[2 * hw + pp] = C2;
+          if (image) { image[pp] = C0; image[hw + pp] = C1; image[2 * hw + pp] = C2; }
+          if (kLoss) {
+            const float inv = 1.0f / (3.0f * (float)hw);
+            float t0, t1, t2;
+            if (kLoss == 1) {
+              const float* tg = static_cast<const float*>(fl.target);
+              t0 = target_value(tg, pp); t1 = target_value(tg, hw + pp); t2 = target_value(tg, 2 * hw + pp);
+            } else {
+              const uint8_t* tg = static_cast<const uint8_t*>(fl.target);
+              t0 = target_value(tg, pp); t1 = target_value(tg, hw + pp); t2 = target_value(tg, 2 * hw + pp);
+            }
+            float4 c4;
+            float ca;
+            pixel_coef(F0, F1, F2, a[k].Q, a[k].T, cam.bg, loss_grad_px(C0, t0, fl.loss, inv),
+                       loss_grad_px(C1, t1, fl.loss, inv), loss_grad_px(C2, t2, fl.loss, inv), c4, ca);
+            fl.coef4[pxb + 4 * k] = c4;
+            fl.coefa[pxb + 4 * k] = ca;
+          }
+        } else if (kLoss) {  // padding pixel of an edge tile
+          fl.coef4[pxb + 4 * k] = make_float4(0.f, 0.f, 0.f, 0.f);
+          fl.coefa[pxb + 4 * k] = 0.f;
         }
       }
     }
@@ -318,7 +342,7 @@ size_t fwd_ws_bytes(int32_t n_tiles, int64_t capacity) {
 void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pair_slot,
                           const int32_t* tile_offsets, int64_t capacity, const float* base, const uint8_t* route,
                           float* image, float* state, float* base_out, cudaStream_t st, int64_t* counters, void* ws,
-                          int concurrency) {
+                          int concurrency, FwdLoss fl) {
   const int n_tiles = cam.TX * cam.TY;
   const float4* r4 = reinterpret_cast<const float4*>(rec);
   auto* cnt = reinterpret_cast<unsigned long long*>(counters);
@@ -339,11 +363,16 @@ void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pa
     // persistent (64-thread CTAs, up to 24 per SM; fewer when views run concurrently); items are
     // claimed dynamically
     const int grid = sm_count() * persistent_ctas(24, concurrency);
-#define OIT_FWD2(B, K)                                                                                         \
-  k_fwd_items<B, K><<<grid, kFwdThreads, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, items, n_items, \
-                                                  counter, tile_nch, done, partial, base, image, state, cnt, chunk_len)
-    if (counters) { if (base) OIT_FWD2(true, true); else OIT_FWD2(false, true); }
-    else { if (base) OIT_FWD2(true, false); else OIT_FWD2(false, false); }
+#define OIT_FWD2(B, K, L)                                                                                   \
+  k_fwd_items<B, K, L><<<grid, kFwdThreads, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, items, n_items, \
+                                                     counter, tile_nch, done, partial, base, image, state, cnt,   \
+                                                     chunk_len, fl)
+    if (fl.target) {
+      const bool u8 = fl.target_u8;
+      if (base) { if (u8) OIT_FWD2(true, false, 2); else OIT_FWD2(true, false, 1); }
+      else { if (u8) OIT_FWD2(false, false, 2); else OIT_FWD2(false, false, 1); }
+    } else if (counters) { if (base) OIT_FWD2(true, true, 0); else OIT_FWD2(false, true, 0); }
+    else { if (base) OIT_FWD2(true, false, 0); else OIT_FWD2(false, false, 0); }
 #undef OIT_FWD2
     return;
   }

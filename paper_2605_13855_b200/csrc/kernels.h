@@ -24,10 +24,19 @@ void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_sl
                 int64_t* d_max_pairs, void* ws, cudaStream_t st);
 
 // composite_fwd.cu — a3
+// Fused a4 for training views (pixel-local L1/L2 loss): target fp32 or uint8 [3][H][W]; the
+// backward coefficients go to coef4 [n_tiles·256] float4 / coefa [n_tiles·256].
+struct FwdLoss {
+  const void* target = nullptr;
+  bool target_u8 = false;
+  int32_t loss = 0;
+  float4* coef4 = nullptr;
+  float* coefa = nullptr;
+};
 void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pair_slot,
                           const int32_t* tile_offsets, int64_t capacity, const float* base, const uint8_t* route,
                           float* image, float* state, float* base_out, cudaStream_t st, int64_t* counters, void* ws,
-                          int concurrency = 1);
+                          int concurrency = 1, FwdLoss fl = FwdLoss());
 // Persistent-grid CTAs per SM for `full` (the kernel's resident maximum) when `concurrency` calls
 // run at once on different streams: about 2·full/concurrency, at least 2, at most full.
 inline int persistent_ctas(int full, int concurrency) {

@@ -669,6 +669,47 @@ def test_u8_targets_equal_fp32_targets(loss):
     assert np.abs(res[0] - res[1]).max() <= 1e-5 * max(np.abs(res[1]).max(), 1e-30)
 
 
+@pytest.mark.parametrize("loss,u8", [("l1", False), ("l2", False), ("l1", True), ("l2", True)])
+def test_forward_loss_fusion_equals_separate_calls(loss, u8):
+    """oit_composite_fwd_loss (a4 in the forward's epilogue, coefficients into the backward
+    workspace) + oit_composite_bwd_ex(OIT_COEF_IN_WS) equals oit_composite_fwd + the backward with
+    the target, over a pre-render cache; the optional state equals the plain forward's."""
+    sc = SCENES[1]
+    cam = sc.cams[2]
+    mask = synth.active_mask(sc, 0.4, "uniform")
+    act, ina = _t(np.flatnonzero(mask).astype(np.int32)), _t(np.flatnonzero(~mask).astype(np.int32))
+    rows, sigma = _t(sc.rows), _t(np.array([sc.sigma], np.float32))
+    tgt = _t(synth.target_image_u8(cam, 55)) if u8 else _t(synth.target_image(cam, 55))
+    p = _pipe(cam, sc.n)
+    _, st0 = p.forward(rows, sigma, ina, sc.bg, image=False)
+    cache = st0.clone()
+    n = int(act.numel())
+    out = []
+    for fused in (False, True):
+        grad = torch.zeros((n, 80), dtype=torch.float32, device=DEV)
+        ds = torch.zeros(1, dtype=torch.float32, device=DEV)
+        if fused:
+            st = p.forward_loss(rows, sigma, act, sc.bg, tgt, loss, base=cache, state=True, concurrency=4)
+            p.backward(rows, sigma, act, sc.bg, None, None, grad, ds, coef_ready=True, concurrency=4)
+        else:
+            _, st = p.forward(rows, sigma, act, sc.bg, base=cache, image=False)
+            p.backward(rows, sigma, act, sc.bg, st, None, grad, ds, target=tgt, loss=loss)
+        out.append((st.cpu().numpy().copy(), grad.cpu().numpy(), ds.item()))
+    assert np.allclose(out[1][0], out[0][0], rtol=1e-5, atol=1e-7)
+    assert np.abs(out[1][1] - out[0][1]).max() <= 1e-5 * np.abs(out[0][1]).max()
+    assert abs(out[1][2] - out[0][2]) <= 1e-5 * abs(out[0][2]) + 1e-12
+    assert np.abs(out[0][1]).max() > 0
+    # and against the oracle (loss gradient of the oracle's image pushed through its backward)
+    full = O.render(sc.rows, sc.sigma, np.arange(sc.n), cam, sc.bg)
+    t64 = tgt.cpu().numpy()
+    t64 = (t64.astype(np.float32) / np.float32(255.0)).astype(np.float64) if u8 else t64.astype(np.float64)
+    gimg = O.loss_grad(full["image"], t64, loss)
+    a = np.flatnonzero(mask).astype(np.int32)
+    gr, _, _, bnd = O.backward_bound(sc.rows, sc.sigma, a, cam, sc.bg, full["state"], gimg)
+    ok, bad = grad_close(out[1][1], gr, bnd, atol=1e-6 / (3 * cam["width"] * cam["height"]))
+    assert ok, describe_bad(out[1][1], gr, bad, bnd)
+
+
 # ------------------------------------------------------------------ NEXT-1 reconcile ------
 def _state_close(got, ref, rtol=2e-4, frac=1e-5):
     """Pixel-state bar (as test_composite_fwd_parity) plus a per-channel floor for the P̄/Q̄
