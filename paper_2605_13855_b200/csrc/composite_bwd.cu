@@ -161,7 +161,6 @@ __device__ __forceinline__ void moments_window(Moments& m, const float* __restri
 
 __global__ void __launch_bounds__(kMomentsThreads, 6) k_moments(DevCam cam, const float4* __restrict__ rec,
                                                              const int32_t* __restrict__ pair_slot,
-                                                             const int32_t* __restrict__ offs, int64_t capacity,
                                                              const int4* __restrict__ items,
                                                              const int32_t* __restrict__ n_items_p,
                                                              int32_t* __restrict__ counter,
@@ -179,7 +178,7 @@ __global__ void __launch_bounds__(kMomentsThreads, 6) k_moments(DevCam cam, cons
   for (int item = blockIdx.x * (kMomentsThreads / 32) + wid;;) {
     if (item >= n_items) return;
     const int4 it = items[item];
-    const int vt = it.x, chunk = it.y;  // vt = 4·tile + quadrant
+    const int vt = it.x;  // vt = 4·tile + quadrant; it.z, it.w: the chunk's range in the quadrant slot array
     const int tile = vt >> 2, quad = vt & 3;
     const int qx0 = 8 * (quad & 1), qy0 = 8 * (quad >> 1);
     if (vt != staged) {  // stage the quadrant's 64 pixel coefficients (1.25 KB), coalesced
@@ -198,9 +197,8 @@ __global__ void __launch_bounds__(kMomentsThreads, 6) k_moments(DevCam cam, cons
       staged = vt;
     }
 
-    const int end = offs[vt + 1];   // quadrant lists (built within capacity)
-    const int j = offs[vt] + chunk * 32 + lane;
-    const bool valid = j < end;
+    const int j = it.z + lane;
+    const bool valid = j < it.w;
     float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0, q2 = q0, q3 = q0, q4 = q0;
     int slot = -1;
     if (valid) {
@@ -542,8 +540,7 @@ __global__ void __launch_bounds__(128, 3) k_epilogue(DevCam cam, const float4* _
 size_t bwd_ws_bytes(int32_t n_tiles, int32_t n_slots, int64_t capacity) {
   const int64_t qcap = 4 * capacity;
   return align_up((size_t)n_slots * 12 * sizeof(float)) + items_bytes(4 * n_tiles, qcap, 32) + align_up(16) +
-         2 * align_up((size_t)(4 * n_tiles + 1) * 4) + align_up((size_t)qcap * 4) + align_up((size_t)capacity * 4) +
-         scan_tmp_bytes(4 * (int64_t)n_tiles);
+         align_up((size_t)(4 * n_tiles + 1) * 4) + align_up((size_t)qcap * 4);
 }
 
 void launch_coef(const DevCam& cam, const float* state, const float* dL_dimage, const void* target, bool target_u8,
@@ -585,11 +582,8 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
   int32_t* tile_nch = cv.take<int32_t>(4 * n_tiles + 1);
   int32_t* scratch = cv.take<int32_t>(68);
   int32_t* counter = cv.take<int32_t>(4);
-  int32_t* qcount = cv.take<int32_t>(4 * n_tiles + 1);
-  int32_t* qoffs = cv.take<int32_t>(4 * n_tiles + 1);
+  int32_t* qlen = cv.take<int32_t>(4 * n_tiles + 1);
   int32_t* qslot = cv.take<int32_t>(qcap);
-  uint32_t* tq = cv.take<uint32_t>(capacity);
-  void* tmp = cv.take<char>(scan_tmp_bytes(4 * (int64_t)n_tiles));
   cudaMemsetAsync(acc2d, 0, sizeof(float) * 12 * (size_t)n_slots, st);
   if (variant == 1) {  // NEXT-4 ablation: per-pixel backward over the tile lists
     record_event(ev_begin, st);
@@ -599,13 +593,13 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
   } else {
     cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
     // quadrant sub-binning of the tile lists, then (quadrant, 32-slot chunk) items
-    launch_quad_bin(cam, rec, pair_slot, tile_offsets, capacity, tq, qcount, qoffs, qslot, tmp, st);
-    launch_build_items(qoffs, 4 * n_tiles, qcap, 32, 0, items, n_items, tile_nch, scratch, st);
+    launch_quad_bin(cam, rec, pair_slot, tile_offsets, capacity, qlen, qslot, st);
+    launch_build_items(tile_offsets, qlen, 4 * n_tiles, capacity, 32, 0, items, n_items, tile_nch, scratch, st);
     // persistent: up to 6 × 4 warps per SM (80 regs), fewer when views run concurrently; dynamic item claiming
     const int blocks = sm_count() * persistent_ctas(6, concurrency);
     record_event(ev_begin, st);
-    k_moments<<<blocks, kMomentsThreads, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), qslot, qoffs,
-                                                  qcap, items, n_items, counter,
+    k_moments<<<blocks, kMomentsThreads, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), qslot, items, n_items,
+                                                  counter,
                                                   reinterpret_cast<const float4*>(coef4), coefa, acc2d);
     record_event(ev_end, st);
   }

@@ -14,20 +14,33 @@ namespace oit {
 
 constexpr int kNB = 33;  // buckets: 0 (empty tile) and 1..32 (= bit length of L)
 
-__device__ __forceinline__ void tile_len(const int32_t* offs, int t, int64_t capacity, int chunk, int empty_items,
-                                         int& nch, int& b, int& js, int& je) {
-  int64_t s = offs[t], e = offs[t + 1];
-  if (e > capacity) e = capacity;
-  if (s > e) s = e;
-  js = (int)s;
-  je = (int)e;
-  const int L = (int)(e - s);
+// Work-list entry u: a tile's list [offs[u], offs[u+1]) (qlen == nullptr), or (qlen != nullptr) the
+// 8×8-quadrant list u = 4·t + q laid out inside its tile's region of the quadrant slot array:
+// start 4·offs[t] + q·L_t (L_t = the tile list's length), qlen[u] entries.
+__device__ __forceinline__ void tile_len(const int32_t* offs, const int32_t* qlen, int u, int64_t capacity, int chunk,
+                                         int empty_items, int& nch, int& b, int& js, int& je) {
+  if (qlen) {
+    const int t = u >> 2, q = u & 3;
+    int64_t s = offs[t], e = offs[t + 1];
+    if (e > capacity) e = capacity;
+    if (s > e) s = e;
+    js = (int)(4 * s + q * (e - s));
+    je = js + qlen[u];
+  } else {
+    int64_t s = offs[u], e = offs[u + 1];
+    if (e > capacity) e = capacity;
+    if (s > e) s = e;
+    js = (int)s;
+    je = (int)e;
+  }
+  const int L = je - js;
   nch = L > 0 ? (L + chunk - 1) / chunk : empty_items;
   b = L > 0 ? 32 - __clz(L) : 0;
 }
 
 // ws layout: g[0..32] bucket item counts, g[33..65] bucket cursors (zeroed by the launcher).
-__global__ void __launch_bounds__(256) k_items_hist(const int32_t* __restrict__ offs, int n_tiles, int64_t capacity,
+__global__ void __launch_bounds__(256) k_items_hist(const int32_t* __restrict__ offs, const int32_t* __restrict__ qlen,
+                                                    int n_tiles, int64_t capacity,
                                                     int chunk, int empty_items, int32_t* __restrict__ g) {
   __shared__ int s_cnt[kNB];
   if (threadIdx.x < kNB) s_cnt[threadIdx.x] = 0;
@@ -35,14 +48,15 @@ __global__ void __launch_bounds__(256) k_items_hist(const int32_t* __restrict__ 
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < n_tiles) {
     int nch, b, js, je;
-    tile_len(offs, t, capacity, chunk, empty_items, nch, b, js, je);
+    tile_len(offs, qlen, t, capacity, chunk, empty_items, nch, b, js, je);
     if (nch) atomicAdd(&s_cnt[b], nch);
   }
   __syncthreads();
   if (threadIdx.x < kNB && s_cnt[threadIdx.x]) atomicAdd(g + threadIdx.x, s_cnt[threadIdx.x]);
 }
 
-__global__ void __launch_bounds__(256) k_items_emit(const int32_t* __restrict__ offs, int n_tiles, int64_t capacity,
+__global__ void __launch_bounds__(256) k_items_emit(const int32_t* __restrict__ offs, const int32_t* __restrict__ qlen,
+                                                    int n_tiles, int64_t capacity,
                                                     int chunk, int empty_items, int32_t* __restrict__ g,
                                                     int4* __restrict__ items, int32_t* __restrict__ n_items,
                                                     int32_t* __restrict__ tile_nch) {
@@ -59,7 +73,7 @@ __global__ void __launch_bounds__(256) k_items_emit(const int32_t* __restrict__ 
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_tiles) return;
   int nch, b, js, je;
-  tile_len(offs, t, capacity, chunk, empty_items, nch, b, js, je);
+  tile_len(offs, qlen, t, capacity, chunk, empty_items, nch, b, js, je);
   if (tile_nch) tile_nch[t] = nch;
   if (!nch) return;
   // one cursor claim per (warp, bucket)
@@ -84,19 +98,13 @@ __global__ void __launch_bounds__(256) k_items_emit(const int32_t* __restrict__ 
 
 // ------------------------------------------------------------- quadrant sub-binning ----
 // Both composite kernels evaluate every pixel of a tile for every slot of its list; for C2-sized
-// splats the ellipse covers ~30% of the tile. Each tile list is therefore split into four 8×8 quadrant lists, keeping a slot in a quadrant iff the continuous
-// max of its power over the quadrant's pixel-centre rectangle reaches thr_lo·(1+2^-10) (the step
-// 12b test on a smaller rectangle: conservative, so no contributing pixel is lost; pixel decisions
-// stay the spec's). On C2 a pair touches 2.2 quadrants on average: 55% of the pixels to evaluate.
-// Pair-parallel (one thread per pair, persistent grid-stride; the per-tile lists vary from a few
-// to thousands of pairs, so a warp per tile left the long tiles' dependent gathers exposed):
-//   k_quad_count:   tile of the pair (binary search in the tile offsets), rec gather, 4-bit mask;
-//                   keeps tile<<4|mask per pair and counts the (tile, quadrant) lists with
-//                   warp-aggregated atomics (lanes of a warp mostly share a tile);
-//   scan of the 4·n_tiles counts → quadrant list offsets (also copied to the scatter cursors);
-//   k_quad_scatter: claims positions with aggregated atomics on the cursors and writes the slots.
-// The order inside a quadrant list is therefore not fixed (as the k_moments accumulation order,
-// which is atomic anyway); the lists' contents are.
+// splats the ellipse covers ~30% of the tile. For the backward each tile list is therefore split
+// into four 8×8 quadrant lists, keeping a slot in a quadrant iff the continuous max of its power
+// over the quadrant's pixel-centre rectangle reaches thr_lo·(1+2^-10) (the step 12b test on a
+// smaller rectangle: conservative, so no contributing pixel is lost; pixel decisions stay the
+// spec's). On C2 a pair touches 2.2 quadrants on average: 55% of the pixels to evaluate.
+// k_quad_bin (below) does it in one pair-parallel pass. The order inside a quadrant list is not
+// fixed (as the k_moments accumulation order, which is atomic anyway); the lists' contents are.
 __device__ __forceinline__ int tile_of_pair(const int32_t* __restrict__ offs, int n_tiles, int j) {
   int lo = 0, hi = n_tiles;  // last t with offs[t] <= j (offs non-decreasing, offs[0] = 0)
   while (hi - lo > 1) {
@@ -116,10 +124,14 @@ __device__ __forceinline__ int agg_claim(int32_t* ctr, int key, unsigned active)
   return base + __popc(peers & ((1u << lane) - 1u));
 }
 
-__global__ void __launch_bounds__(256) k_quad_count(DevCam cam, const float4* __restrict__ rec,
-                                                    const int32_t* __restrict__ pair_slot,
-                                                    const int32_t* __restrict__ offs, int64_t capacity,
-                                                    uint32_t* __restrict__ tq, int32_t* __restrict__ qcount) {
+// One pass, pair-parallel: the tile of pair j (binary search in the tile offsets), its record, the
+// 4-bit quadrant mask; each quadrant list of tile t gets a fixed region of the quadrant slot
+// array (start 4·offs[t] + q·L_t, room for the whole tile list), so positions are claimed with
+// warp-aggregated atomics on the per-quadrant lengths — no global scan, no second pass.
+__global__ void __launch_bounds__(256) k_quad_bin(DevCam cam, const float4* __restrict__ rec,
+                                                  const int32_t* __restrict__ pair_slot,
+                                                  const int32_t* __restrict__ offs, int64_t capacity,
+                                                  int32_t* __restrict__ qlen, int32_t* __restrict__ qslot) {
   const int n_tiles = cam.TX * cam.TY;
   const int n = (int)min((int64_t)offs[n_tiles], capacity);
   const int stride = gridDim.x * blockDim.x;
@@ -127,68 +139,39 @@ __global__ void __launch_bounds__(256) k_quad_count(DevCam cam, const float4* __
     const int j = j0 + threadIdx.x;
     const bool live = j < n;
     unsigned m = 0;
-    int t = 0;
+    int t = 0, slot = 0, base = 0, L = 0;
     if (live) {
       t = tile_of_pair(offs, n_tiles, j);
-      const float4* r = rec + (size_t)pair_slot[j] * kRec4;
-      m = quadrant_mask(cam, t, r[0], r[1]);
-      tq[j] = ((uint32_t)t << 4) | m;
-    }
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-      const unsigned act = __ballot_sync(0xffffffffu, live && (m >> q & 1u));
-      if (live && (m >> q & 1u)) agg_claim(qcount, 4 * t + q, act);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(256) k_quad_scatter(int n_tiles, const int32_t* __restrict__ pair_slot,
-                                                      const int32_t* __restrict__ offs, int64_t capacity,
-                                                      const uint32_t* __restrict__ tq, int32_t* __restrict__ cursor,
-                                                      int32_t* __restrict__ qslot) {
-  const int n = (int)min((int64_t)offs[n_tiles], capacity);
-  const int stride = gridDim.x * blockDim.x;
-  for (int j0 = blockIdx.x * blockDim.x; j0 < n; j0 += stride) {
-    const int j = j0 + threadIdx.x;
-    const bool live = j < n;
-    uint32_t v = 0;
-    int slot = 0;
-    if (live) {
-      v = tq[j];
       slot = pair_slot[j];
+      const float4* r = rec + (size_t)slot * kRec4;
+      m = quadrant_mask(cam, t, r[0], r[1]);
+      const int s0 = __ldg(offs + t);
+      const int e0 = (int)min((int64_t)__ldg(offs + t + 1), capacity);
+      base = 4 * s0;
+      L = e0 - s0;
     }
-    const int t = (int)(v >> 4);
 #pragma unroll
     for (int q = 0; q < 4; q++) {
-      const bool on = live && (v >> q & 1u);
+      const bool on = live && (m >> q & 1u);
       const unsigned act = __ballot_sync(0xffffffffu, on);
-      if (on) qslot[agg_claim(cursor, 4 * t + q, act)] = slot;
+      if (on) qslot[base + q * L + agg_claim(qlen, 4 * t + q, act)] = slot;
     }
   }
 }
 
 void launch_quad_bin(const DevCam& cam, const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
-                     int64_t capacity, uint32_t* tq, int32_t* qcount, int32_t* qoffs, int32_t* qslot, void* tmp,
-                     cudaStream_t st) {
+                     int64_t capacity, int32_t* qlen, int32_t* qslot, cudaStream_t st) {
   const int n_tiles = cam.TX * cam.TY;
-  const int blocks = sm_count() * 8;
-  const float4* r4 = reinterpret_cast<const float4*>(rec);
-  cudaMemsetAsync(qcount, 0, sizeof(int32_t) * 4 * (size_t)n_tiles, st);
-  k_quad_count<<<blocks, 256, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, tq, qcount);
-  launch_exclusive_scan(qcount, qoffs, 4 * (int64_t)n_tiles, tmp, st);
-  // the counts are consumed: reuse them as the scatter cursors (= the list starts)
-  cudaMemcpyAsync(qcount, qoffs, sizeof(int32_t) * 4 * (size_t)n_tiles, cudaMemcpyDeviceToDevice, st);
-  k_quad_scatter<<<blocks, 256, 0, st>>>(n_tiles, pair_slot, tile_offsets, capacity, tq, qcount, qslot);
+  cudaMemsetAsync(qlen, 0, sizeof(int32_t) * 4 * (size_t)n_tiles, st);
+  k_quad_bin<<<sm_count() * 8, 256, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), pair_slot, tile_offsets,
+                                             capacity, qlen, qslot);
 }
 
-size_t quad_bytes(int32_t n_tiles, int64_t capacity) {
-  return 2 * align_up((size_t)(4 * n_tiles + 1) * 4) + align_up((size_t)(4 * capacity) * 4) +
-         align_up((size_t)capacity * 4) + scan_tmp_bytes(4 * (int64_t)n_tiles);
-}
 
 // Fused variant for small tile counts (grid ≤ SM count, hence co-resident): the histogram, a
 // software grid barrier and the emission in one launch. g[66] is the barrier counter.
-__global__ void __launch_bounds__(256) k_items_fused(const int32_t* __restrict__ offs, int n_tiles, int64_t capacity,
+__global__ void __launch_bounds__(256) k_items_fused(const int32_t* __restrict__ offs, const int32_t* __restrict__ qlen,
+                                                     int n_tiles, int64_t capacity,
                                                      int chunk, int empty_items, int32_t* __restrict__ g,
                                                      int4* __restrict__ items, int32_t* __restrict__ n_items,
                                                      int32_t* __restrict__ tile_nch) {
@@ -199,7 +182,7 @@ __global__ void __launch_bounds__(256) k_items_fused(const int32_t* __restrict__
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   int nch = 0, b = 0, js = 0, je = 0;
   if (t < n_tiles) {
-    tile_len(offs, t, capacity, chunk, empty_items, nch, b, js, je);
+    tile_len(offs, qlen, t, capacity, chunk, empty_items, nch, b, js, je);
     if (tile_nch) tile_nch[t] = nch;
     if (nch) atomicAdd(&s_cnt[b], nch);
   }
@@ -247,18 +230,19 @@ size_t items_bytes(int32_t n_tiles, int64_t capacity, int chunk) {
          align_up((2 * kNB + 2) * sizeof(int32_t));
 }
 
-// items [capacity/chunk + n_tiles + 1], n_items [1], tile_nch [n_tiles], g = 2·kNB ints of scratch
-void launch_build_items(const int32_t* tile_offsets, int n_tiles, int64_t capacity, int chunk, int empty_items,
-                        int4* items, int32_t* n_items, int32_t* tile_nch, int32_t* g, cudaStream_t st) {
+// items [capacity/chunk + n_tiles + 1], n_items [1], tile_nch [n_tiles], g = 2·kNB ints of scratch;
+// qlen (nullable): quadrant mode (n_tiles = 4 × the tile count, offs = the TILE offsets)
+void launch_build_items(const int32_t* tile_offsets, const int32_t* qlen, int n_tiles, int64_t capacity, int chunk,
+                        int empty_items, int4* items, int32_t* n_items, int32_t* tile_nch, int32_t* g, cudaStream_t st) {
   const int blocks = (n_tiles + 255) / 256;
   cudaMemsetAsync(g, 0, (2 * kNB + 2) * sizeof(int32_t), st);
   if (blocks <= sm_count()) {
-    k_items_fused<<<blocks, 256, 0, st>>>(tile_offsets, n_tiles, capacity, chunk, empty_items, g, items, n_items,
+    k_items_fused<<<blocks, 256, 0, st>>>(tile_offsets, qlen, n_tiles, capacity, chunk, empty_items, g, items, n_items,
                                           tile_nch);
     return;
   }
-  k_items_hist<<<blocks, 256, 0, st>>>(tile_offsets, n_tiles, capacity, chunk, empty_items, g);
-  k_items_emit<<<blocks, 256, 0, st>>>(tile_offsets, n_tiles, capacity, chunk, empty_items, g, items, n_items,
+  k_items_hist<<<blocks, 256, 0, st>>>(tile_offsets, qlen, n_tiles, capacity, chunk, empty_items, g);
+  k_items_emit<<<blocks, 256, 0, st>>>(tile_offsets, qlen, n_tiles, capacity, chunk, empty_items, g, items, n_items,
                                        tile_nch);
 }
 

@@ -48,15 +48,14 @@ size_t fwd_ws_bytes(int32_t n_tiles, int64_t capacity);
 
 // items.cu — (tile, chunk) work lists, longest tiles first
 size_t items_bytes(int32_t n_tiles, int64_t capacity, int chunk);
-void launch_build_items(const int32_t* tile_offsets, int n_tiles, int64_t capacity, int chunk, int empty_items,
-                        int4* items, int32_t* n_items, int32_t* tile_nch, int32_t* scratch68, cudaStream_t st);
+void launch_build_items(const int32_t* tile_offsets, const int32_t* qlen, int n_tiles, int64_t capacity, int chunk,
+                        int empty_items, int4* items, int32_t* n_items, int32_t* tile_nch, int32_t* scratch68,
+                        cudaStream_t st);
 
 // quadrant sub-binning: qoffs[4·n_tiles+1], qslot[4·capacity] (lists of the 8×8 quadrants; order
 // within a list unspecified), tq[capacity] and qcount[4·n_tiles] scratch, tmp = scan_tmp_bytes(4·n_tiles)
 void launch_quad_bin(const DevCam& cam, const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
-                     int64_t capacity, uint32_t* tq, int32_t* qcount, int32_t* qoffs, int32_t* qslot, void* tmp,
-                     cudaStream_t st);
-size_t quad_bytes(int32_t n_tiles, int64_t capacity);
+                     int64_t capacity, int32_t* qlen, int32_t* qslot, cudaStream_t st);
 
 inline int sm_count() {
   static int n = 0;
