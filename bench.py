@@ -1042,7 +1042,8 @@ def build_line(args, world, res, results):
     if res["ser_bwd_ms"] >= res["ser_fwd_ms"]:
         kern, flops, kms, tkey = "k_moments (oit_composite_bwd a5)", bwd_flops, res["ser_bwd_ms"], "k_moments"
     else:
-        kern, flops, kms, tkey = "k_fwd_items (oit_composite_fwd a3)", fwd_flops, res["ser_fwd_ms"], "k_fwd_items<1, 0>"
+        kern, flops, kms = "k_fwd_items (oit_composite_fwd_loss a3+a4)", fwd_flops, res["ser_fwd_ms"]
+        tkey = "k_fwd_items<1, 0, 2>" if args.targets == "u8" else "k_fwd_items<1, 0, 1>"
     traffic, traffic_src = _ncu_traffic(tkey)
     achieved = flops / (kms * 1e-3) / 1e12
     sweep = {}

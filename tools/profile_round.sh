@@ -12,7 +12,11 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   $BENCH > $OUT/${TAG}_launches_bench.log 2>&1
 echo "launch list rc=$?"
 # full sets: the kernels as the roofline pass launches them (one stream, full grid: --streams 1)
-KS=${@:-'k_fwd_items<\(bool\)1, \(bool\)0>' '^oit::k_moments' '^oit::k_epilogue' '^oit::k_project' 'k_bin_expand<\(bool\)1>' '^oit::k_quad_count' '^oit::k_coef'}
+KS=("$@")
+if [ ${#KS[@]} -eq 0 ]; then
+  KS=('k_fwd_items<\(bool\)1, \(bool\)0, \(int\)2>' 'oit::k_moments\(' 'oit::k_epilogue' 'oit::k_project'
+      'k_bin_expand<\(bool\)1>' 'oit::k_quad_bin' 'oit::k_items_fused')
+fi
 i=0
 for k in "${KS[@]}"; do
   i=$((i+1))
