@@ -360,14 +360,15 @@ void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pa
     cudaMemsetAsync(done, 0, sizeof(int32_t) * n_tiles, st);
     cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
     launch_build_items(tile_offsets, nullptr, n_tiles, capacity, chunk_len, 1, items, n_items, tile_nch, scratch, st);
-    // persistent (64-thread CTAs, 16 per SM alone — measured 7.48 vs 7.67 ms per 100 views at 24 —, fewer
-    // when views run concurrently); items are
-    // claimed dynamically
-    const int grid = sm_count() * persistent_ctas(16, concurrency);
+    // persistent grid: as many 64-thread CTAs per SM as the instantiation's registers let reside
+    // (16-18), fewer when views run concurrently; items are claimed dynamically
 #define OIT_FWD2(B, K, L)                                                                                   \
-  k_fwd_items<B, K, L><<<grid, kFwdThreads, 0, st>>>(cam, r4, pair_slot, tile_offsets, capacity, items, n_items, \
-                                                     counter, tile_nch, done, partial, base, image, state, cnt,   \
-                                                     chunk_len, fl)
+  do {                                                                                                      \
+    static const int occ = resident_ctas(k_fwd_items<B, K, L>, kFwdThreads);                                \
+    k_fwd_items<B, K, L><<<sm_count() * persistent_ctas(occ, concurrency), kFwdThreads, 0, st>>>(           \
+        cam, r4, pair_slot, tile_offsets, capacity, items, n_items, counter, tile_nch, done, partial, base,  \
+        image, state, cnt, chunk_len, fl);                                                                  \
+  } while (0)
     if (fl.target) {
       const bool u8 = fl.target_u8;
       if (base) { if (u8) OIT_FWD2(true, false, 2); else OIT_FWD2(true, false, 1); }

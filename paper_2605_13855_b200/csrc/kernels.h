@@ -39,6 +39,12 @@ void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pa
                           int concurrency = 1, FwdLoss fl = FwdLoss());
 // Persistent-grid CTAs per SM for `full` (the kernel's resident maximum) when `concurrency` calls
 // run at once on different streams: about 2·full/concurrency, at least 2, at most full.
+template <class Kernel>
+inline int resident_ctas(Kernel kernel, int threads) {  // CTAs of `kernel` one SM holds (≥ 1)
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, 0) != cudaSuccess || n < 1) n = 1;
+  return n;
+}
 inline int persistent_ctas(int full, int concurrency) {
   const int c = concurrency < 1 ? 1 : concurrency;
   int k = (2 * full + c - 1) / c;
