@@ -340,10 +340,23 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
     // Rasterize(G, I^pre_j): the active set over the view's cache of the frozen set (R16)
     launch_project(dc, scene->rows, scene->sigma, active_idx, n_active, w.rec_a, w.tps_a, st);
     launch_bin(dc, w.rec_a, w.tps_a, n_active, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st);
-    launch_composite_fwd(dc, w.rec_a, w.pairs, w.offs, pair_capacity, caches_host ? caches_host[j] : nullptr, nullptr,
-                         nullptr, w.state, nullptr, st, nullptr, w.fwd_ws, concurrency);
-    // L_j and its pixel gradient (fused with the backward coefficients)
-    coef_from_target(dc, &cams_host[j], w.state, targets_host[j], loss, w.coef4, w.coefa, w.dssim_ws, st);
+    const float* cache = caches_host ? caches_host[j] : nullptr;
+    if ((loss & ~OIT_TARGET_U8) != 2) {
+      // L_j (L1/L2, pixel-local) and the backward coefficients in the forward's epilogue (a3 + a4)
+      FwdLoss fl;
+      fl.target = targets_host[j];
+      fl.target_u8 = (loss & OIT_TARGET_U8) != 0;
+      fl.loss = loss & ~OIT_TARGET_U8;
+      fl.coef4 = reinterpret_cast<float4*>(w.coef4);
+      fl.coefa = w.coefa;
+      launch_composite_fwd(dc, w.rec_a, w.pairs, w.offs, pair_capacity, cache, nullptr, nullptr, nullptr, nullptr, st,
+                           nullptr, w.fwd_ws, concurrency, fl);
+    } else {
+      // D-SSIM is not pixel-local: the state, then resolve → SSIM stencils → coefficients
+      launch_composite_fwd(dc, w.rec_a, w.pairs, w.offs, pair_capacity, cache, nullptr, nullptr, w.state, nullptr, st,
+                           nullptr, w.fwd_ws, concurrency);
+      coef_from_target(dc, &cams_host[j], w.state, targets_host[j], loss, w.coef4, w.coefa, w.dssim_ws, st);
+    }
     // back-propagate L_j to the scored splats (R20)
     launch_project(dc, scene->rows, scene->sigma, score_idx, n_score, w.rec_s, w.tps_s, st);
     launch_bin(dc, w.rec_s, w.tps_s, n_score, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st);
