@@ -52,6 +52,14 @@ def test_status_strings_and_argument_errors_without_gpu():
     assert L.oit_select_views(None, 4, 2, 0, 0, None, None) == 1
     assert L.oit_update_workspace_bytes(1000) > 0
     assert L.oit_bwd_workspace_bytes(ctypes.byref(cam), 100, 1000) > 0
+    # fused forward loss: no target / D-SSIM (not pixel-local) / missing workspaces are rejected
+    # synchronously (OIT_EINVAL = 1), before anything is launched
+    bg = (ctypes.c_float * 3)(0, 0, 0)
+    args = lambda tgt, loss, ws: (ctypes.byref(cam), None, None, ctypes.c_void_p(8), 0, bg, None, tgt, loss, None,  # noqa: E731
+                                  ws, 1 << 20, ws, 1 << 20, 10, 1, None)
+    assert L.oit_composite_fwd_loss(*args(None, 0, ctypes.c_void_p(8))) == 1
+    assert L.oit_composite_fwd_loss(*args(ctypes.c_void_p(8), 2, ctypes.c_void_p(8))) == 1
+    assert L.oit_composite_fwd_loss(*args(ctypes.c_void_p(8), 0 | _lib.OIT_TARGET_U8, None)) == 1
 
 
 def test_product_package_never_imports_the_oracle():
