@@ -407,6 +407,40 @@ def test_c2_full_size_parity_sampled():
     assert strict_fraction(grad.cpu().numpy()[sample], gref) > 0.99
 
 
+@pytest.mark.slow
+def test_c2_full_size_bench_configuration_parity():
+    """configs[1] in the exact launch configuration of bench.py's training step: a3 + a4 fused
+    (oit_composite_fwd_loss, 8-bit target, over a pre-render cache), concurrency = 16 grids, the
+    backward from the coefficients in its workspace (OIT_COEF_IN_WS); L2 loss (continuous, so no
+    sign decision sits on a rounding boundary). State within the state bar, sampled gradient rows
+    within R31 of the oracle's loss gradient pushed through its backward."""
+    sc = synth.scene_c2(n_views=2)
+    mask = synth.active_mask(sc, 0.2, "clustered")
+    act = np.flatnonzero(mask).astype(np.int32)
+    cam = sc.cams[1]
+    W, H = cam["width"], cam["height"]
+    cache = synth.pixel_state(cam, 31)
+    t8 = synth.target_image_u8(cam, 32)
+    rows, sigma = _t(sc.rows), _t(np.array([sc.sigma], np.float32))
+    p = _pipe(cam, len(act), cap=1 << 22)
+    st = p.forward_loss(rows, sigma, _t(act), sc.bg, _t(t8), "l2", base=_t(plain_to_tile_major(cache, W, H)),
+                        state=True, concurrency=16)
+    grad = torch.zeros((len(act), 80), dtype=torch.float32, device=DEV)
+    dsig = torch.zeros(1, dtype=torch.float32, device=DEV)
+    p.backward(rows, sigma, _t(act), sc.bg, None, None, grad, dsig, coef_ready=True, concurrency=16)
+    ref = O.render(sc.rows, sc.sigma, act, cam, sc.bg, base=cache)
+    assert p.pairs_used() == ref["tile_pairs"]
+    assert np.allclose(tile_major_to_plain(st.cpu().numpy(), W, H), ref["state"], rtol=2e-4, atol=1e-7)
+    t64 = (t8.astype(np.float32) / np.float32(255.0)).astype(np.float64)
+    gimg = O.loss_grad(ref["image"], t64, "l2")
+    sample = np.sort(synth.rng(9).choice(len(act), 2000, replace=False))
+    gref, _, _, bnd = O.backward_bound(sc.rows, sc.sigma, act[sample], cam, sc.bg, ref["state"], gimg)
+    got = grad.cpu().numpy()[sample]
+    ok, bad = grad_close(got, gref, bnd, atol=1e-6 / (3 * W * H))
+    assert ok, describe_bad(got, gref, bad, bnd)
+    assert np.abs(gref).max() > 0
+
+
 _C3 = {}
 
 
