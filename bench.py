@@ -483,9 +483,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # OIT_BENCH_BACKEND=gloo + OIT_BENCH_SAME_DEVICE=1: exercise the N > 1 path (sharding, barriers,
+    # all-reduces, max-over-ranks timing) with several ranks on ONE GPU — a test hook, not a bench mode
+    backend = os.environ.get("OIT_BENCH_BACKEND", "nccl")
+    if os.environ.get("OIT_BENCH_SAME_DEVICE"):
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     L.lib()  # fail loudly if liboit.so is missing
     from paper_2605_13855_b200 import dist as D
     all_cams = synth.scene_c2(n=10, n_views=args.views * world, res=args.res).cams
