@@ -174,10 +174,22 @@ __global__ void __launch_bounds__(kMomentsThreads, 6) k_moments(DevCam cam, cons
   const unsigned FULL = 0xffffffffu;
   int staged = -1;
   const int n_warps = gridDim.x * (kMomentsThreads / 32);
-  // first item static (warp g takes item g), then dynamic claims offset by the number of warps
-  for (int item = blockIdx.x * (kMomentsThreads / 32) + wid;;) {
+  // Static interleaved assignment (warp g: items g, g + n_warps, …; the list is longest-first, so
+  // every warp gets one item of each length class) and a software pipeline over it: while item k
+  // is computed, the descriptor of item k+2 and the pair slots of item k+1 are in flight, so only
+  // the record gather sits on an item's critical path.
+  const int4 kNone = make_int4(0, 0, 0, 0);
+  int item = blockIdx.x * (kMomentsThreads / 32) + wid;
+  int4 it1 = item < n_items ? items[item] : kNone;                        // item k
+  int slot1 = it1.z + lane < it1.w ? __ldcg(pair_slot + it1.z + lane) : -1;
+  int4 it2 = item + n_warps < n_items ? items[item + n_warps] : kNone;    // item k+1
+  for (;; item += n_warps) {
     if (item >= n_items) return;
-    const int4 it = items[item];
+    const int4 it = it1;
+    const int slot_k = slot1;
+    it1 = it2;
+    slot1 = it1.z + lane < it1.w ? __ldcg(pair_slot + it1.z + lane) : -1;
+    it2 = item + 2 * n_warps < n_items ? items[item + 2 * n_warps] : kNone;
     const int vt = it.x;  // vt = 4·tile + quadrant; it.z, it.w: the chunk's range in the quadrant slot array
     const int tile = vt >> 2, quad = vt & 3;
     const int qx0 = 8 * (quad & 1), qy0 = 8 * (quad >> 1);
@@ -197,12 +209,10 @@ __global__ void __launch_bounds__(kMomentsThreads, 6) k_moments(DevCam cam, cons
       staged = vt;
     }
 
-    const int j = it.z + lane;
-    const bool valid = j < it.w;
+    const int slot = slot_k;
+    const bool valid = slot >= 0;
     float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0, q2 = q0, q3 = q0, q4 = q0;
-    int slot = -1;
     if (valid) {
-      slot = pair_slot[j];
       const float4* r = rec + (size_t)slot * kRec4;
       q0 = r[0]; q1 = r[1]; q2 = r[2]; q3 = r[3]; q4 = r[4];
     }
@@ -235,9 +245,6 @@ __global__ void __launch_bounds__(kMomentsThreads, 6) k_moments(DevCam cam, cons
       red_add_v4(a + 4, m.Od, m.M1, m.M2, m.XX);
       red_add_v4(a + 8, m.XY, m.YY, 0.f, 0.f);
     }
-    int nxt = 0;
-    if (lane == 0) nxt = n_warps + atomicAdd(counter, 1);
-    item = __shfl_sync(FULL, nxt, 0);
   }
 }
 
