@@ -5,14 +5,15 @@
 // Structure (B200-first; the paper's Fig. 3 design is prior art, not the blueprint):
 //  * k_coef (a4): per pixel, from the forward state (P, Q, T) and dL/dC (or the L1/L2 loss
 //    against a target) — K = (1-T)/Q, u = K g, s = K (g·F), a = T (g·(F - c0)). 20 B/px.
-//  * k_moments (a5): work item = (tile, chunk of 32 slots of the tile's list); one warp per
-//    item, LANE = SPLAT (the paper's "recursive per-splat" idea): each lane keeps its
-//    splat's 10 moments in registers and walks the tile's pixels, whose coefficients are
-//    warp-uniform (broadcast) loads. No shuffle reduction and no per-pixel atomics: every
-//    lane issues exactly 3 × red.global.add.v4.f32 per (splat, tile) — atomic traffic scales
-//    with tiles touched, not pixels. Rows/columns outside the union of the 32 splats'
-//    α = 1/255 extents are skipped warp-uniformly. Items are claimed dynamically (atomic
-//    counter) by a persistent grid sized to the SM count.
+//  * k_moments (a5): work item = (8×8 quadrant of a tile, chunk of 32 slots of its quadrant
+//    list); one warp per item, LANE = SPLAT (the paper's "recursive per-splat" idea): each
+//    lane keeps its splat's 10 moments in registers and walks the quadrant's pixels, whose
+//    coefficients are warp-uniform (broadcast) loads. No shuffle reduction and no per-pixel
+//    atomics: every lane issues exactly 3 × red.global.add.v4.f32 per (splat, quadrant) —
+//    atomic traffic scales with tiles touched, not pixels. Rows/columns outside the union of the
+//    32 splats' α = 1/255 extents are skipped warp-uniformly. A persistent grid takes the
+//    longest-first item list in a static interleave, with the next items' descriptors and pair
+//    slots prefetched.
 //  * k_epilogue (a6): one thread per slot chains the moments to μ, q, s, o, h, v, σ (and Σ).
 // Moments per (slot, tile): U_RGB = Σ α u, S = Σ α s, Od = Σ d, M1 = Σ d dx, M2 = Σ d dy,
 // XX = Σ d dx², XY = Σ d dx dy, YY = Σ d dy², with dL/dα = a/(1-α) + w (u·c - s) and
@@ -163,7 +164,6 @@ __global__ void __launch_bounds__(kMomentsThreads, 6) k_moments(DevCam cam, cons
                                                              const int32_t* __restrict__ pair_slot,
                                                              const int4* __restrict__ items,
                                                              const int32_t* __restrict__ n_items_p,
-                                                             int32_t* __restrict__ counter,
                                                              const float4* __restrict__ coef4,
                                                              const float* __restrict__ coefa,
                                                              float* __restrict__ acc2d) {
@@ -588,7 +588,7 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
   int32_t* n_items = cv.take<int32_t>(4);
   int32_t* tile_nch = cv.take<int32_t>(4 * n_tiles + 1);
   int32_t* scratch = cv.take<int32_t>(68);
-  int32_t* counter = cv.take<int32_t>(4);
+  cv.take<int32_t>(4);  // (formerly the item counter; keeps the workspace layout)
   int32_t* qlen = cv.take<int32_t>(4 * n_tiles + 1);
   int32_t* qslot = cv.take<int32_t>(qcap);
   cudaMemsetAsync(acc2d, 0, sizeof(float) * 12 * (size_t)n_slots, st);
@@ -598,15 +598,13 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
                                              capacity, reinterpret_cast<const float4*>(coef4), coefa, acc2d);
     record_event(ev_end, st);
   } else {
-    cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
     // quadrant sub-binning of the tile lists, then (quadrant, 32-slot chunk) items
     launch_quad_bin(cam, rec, pair_slot, tile_offsets, capacity, qlen, qslot, st);
     launch_build_items(tile_offsets, qlen, 4 * n_tiles, capacity, 32, 0, items, n_items, tile_nch, scratch, st);
-    // persistent: up to 6 × 4 warps per SM (80 regs), fewer when views run concurrently; dynamic item claiming
+    // persistent: up to 6 × 4 warps per SM (80 regs), fewer when views run concurrently; static items
     const int blocks = sm_count() * persistent_ctas(6, concurrency);
     record_event(ev_begin, st);
     k_moments<<<blocks, kMomentsThreads, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), qslot, items, n_items,
-                                                  counter,
                                                   reinterpret_cast<const float4*>(coef4), coefa, acc2d);
     record_event(ev_end, st);
   }
