@@ -36,6 +36,12 @@
  *      images [3][H][W] fp32 (CHW, row-major).
  *  - Decisions (visibility, tile rectangle, pair contribution, α clamp) follow the fp32 spec of
  *    DESIGN.md §3 op-by-op, so they are bit-identical to the CPU oracle's.
+ *
+ * Entry points: a1 oit_project_cull; a2 oit_bin_tiles; a3 oit_composite_fwd(_ex), a3+a4 fused
+ * oit_composite_fwd_loss; a4 oit_loss_grad; a5/a6 oit_composite_bwd(_ex), the per-pixel ablation
+ * oit_composite_bwd_perpixel; a7 oit_select_views, oit_score_subsample; a8 oit_update_active_set;
+ * NEXT-1 oit_active_set_delta, oit_reconcile_cache; NEXT-2 oit_adam_step; NEXT-3
+ * oit_loss_dssim; plus the *_workspace_bytes queries, oit_num_tiles, oit_status_string.
  */
 #ifndef OIT_H
 #define OIT_H
