@@ -66,7 +66,7 @@ def parse():
     ap.add_argument("--splats", type=int, default=300_000)
     ap.add_argument("--res", type=int, default=800)
     ap.add_argument("--sub-rate", type=float, default=0.05, help="refresh subsample rate S/V")
-    ap.add_argument("--streams", type=int, default=16, help="training views processed concurrently (one stream each)")
+    ap.add_argument("--streams", type=int, default=12, help="training views processed concurrently (one stream each)")
     ap.add_argument("--targets", choices=["u8", "f32"], default="u8",
                     help="training-image format: 8-bit (the datasets' PNGs, OIT_TARGET_U8) or fp32")
     ap.add_argument("--no-sweep", action="store_true")
