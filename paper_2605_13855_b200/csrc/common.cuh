@@ -222,6 +222,19 @@ __device__ __forceinline__ unsigned quadrant_mask(const DevCam& cam, int tile, c
   return m;
 }
 
+// e if power ∈ [lo, 0] (the step 13 contribution test: power <= 0 && power >= lo; NaN fails both),
+// else 0 — written as two predicated compares and one select (the C form compiles to two selects).
+__device__ __forceinline__ float select_contrib(float e, float power, float lo) {
+  float r;
+  asm("{\n\t.reg .pred p, q;\n\t"
+      "setp.le.f32 q, %1, 0f00000000;\n\t"
+      "setp.ge.and.f32 p, %1, %2, q;\n\t"
+      "selp.f32 %0, %3, 0f00000000, p;\n\t}"
+      : "=f"(r)
+      : "f"(power), "f"(lo), "f"(e));
+  return r;
+}
+
 // DESIGN.md §3 step 13 (the per-pixel power; exact op order, no contraction beyond the two fmas).
 __device__ __forceinline__ float spec_power(float nA, float nB, float nC, float dx, float dy) {
   float by = __fmul_rn(nB, dy);

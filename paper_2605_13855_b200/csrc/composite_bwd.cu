@@ -114,12 +114,15 @@ __device__ __forceinline__ void moments_window(Moments& m, const float* __restri
     for (int px = pxe; px <= px1; px += 2) {
       const f2_t pw2 = fma2(dx2, fma2(nA2, dx2, by2), cy2);
       const float pl = f2lo(pw2), ph = f2hi(pw2);
-      const bool cl = pl <= 0.0f && pl >= lo, ch = ph <= 0.0f && ph >= lo;
       const f2_t arg2 = fma2(nkx2, dx2, fma2(pw2, l2e, ra2));
       const float el = ex2_approx(f2lo(arg2)), eh = ex2_approx(f2hi(arg2));
-      float al = cl ? el : 0.0f, ah = ch ? eh : 0.0f;
+      float al, ah;
       bool kl = false, kh = false;
-      if (kClamp) {
+      if (!kClamp) {  // α = e if power ∈ [lo, 0] else 0: two compares and one select per pixel
+        al = select_contrib(el, pl, lo);
+        ah = select_contrib(eh, ph, lo);
+      } else {
+        const bool cl = pl <= 0.0f && pl >= lo, ch = ph <= 0.0f && ph >= lo;
         kl = pl >= thr_hi;
         kh = ph >= thr_hi;
         al = cl ? (kl ? 0.99f : el) : 0.0f;
