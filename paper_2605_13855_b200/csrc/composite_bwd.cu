@@ -110,7 +110,7 @@ __device__ __forceinline__ void moments_window(Moments& m, const float* __restri
     const float* row = s_u + (py - qy0) * 8 - qx0;
     f2_t dx2 = sub2(f2((float)(tx0 + pxe), (float)(tx0 + pxe + 1)), mx2);
     const f2_t two2 = f2s(2.0f);
-#pragma unroll 2
+#pragma unroll 4
     for (int px = pxe; px <= px1; px += 2) {
       const f2_t pw2 = fma2(dx2, fma2(nA2, dx2, by2), cy2);
       const float pl = f2lo(pw2), ph = f2hi(pw2);
