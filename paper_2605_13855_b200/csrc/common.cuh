@@ -197,27 +197,36 @@ __device__ __forceinline__ bool spec_tile_keep(int tx, int ty, int W, int H, flo
 
 // Work partitioning below the tile (not a spec decision): the step-12b test on an 8×8 quadrant's
 // pixel-centre rectangle; conservative, so a quadrant holding a contributing pixel is never dropped.
-__device__ __forceinline__ bool rect_keep(float ax0, float ax1, float ay0, float ay1, float nA, float nB, float nC,
-                                          float thr_lo) {
-  if (ax0 <= 0.0f && 0.0f <= ax1 && ay0 <= 0.0f && 0.0f <= ay1) return true;
-  float m = spec_edge_max(ax0, ay0, ay1, nA, nB, nC);
-  m = fmaxf(m, spec_edge_max(ax1, ay0, ay1, nA, nB, nC));
-  m = fmaxf(m, spec_edge_max(ay0, ax0, ax1, nC, nB, nA));
-  m = fmaxf(m, spec_edge_max(ay1, ax0, ax1, nC, nB, nA));
-  return m >= __fmul_rn(thr_lo, 1.0009765625f);
+// The same max over one edge with the argmax −q/(2R) taken through a precomputed reciprocal
+// (inv2R = 1/(2R)): the value at a point within an ulp of the argmax differs from the max only at
+// second order (the concave quadratic is flat there), far inside the 2^-10 margin — conservative
+// for work partitioning (never for spec decisions).
+__device__ __forceinline__ float edge_max_rcp(float a, float b0, float b1, float P, float Qc, float R, float inv2R) {
+  const float q = Qc * a;
+  const float t = fminf(fmaxf(-q * inv2R, b0), b1);
+  return fmaf(t, fmaf(R, t, q), (P * a) * a);
 }
 
 __device__ __forceinline__ unsigned quadrant_mask(const DevCam& cam, int tile, const float4& q0, const float4& q1) {
   const int tx0 = (tile % cam.TX) * kTile, ty0 = (tile / cam.TX) * kTile;
+  const float nA = q0.z, nB = q0.w, nC = q1.x, lo = q1.y * 1.0009765625f;
+  const float inv2A = 1.0f / (2.0f * nA), inv2C = 1.0f / (2.0f * nC);
   unsigned m = 0;
 #pragma unroll
   for (int q = 0; q < 4; q++) {
     const int X0 = tx0 + 8 * (q & 1), Y0 = ty0 + 8 * (q >> 1);
     if (X0 >= cam.W || Y0 >= cam.H) continue;
     const int X1 = min(X0 + 7, cam.W - 1), Y1 = min(Y0 + 7, cam.H - 1);
-    if (rect_keep(__fsub_rn((float)X0, q0.x), __fsub_rn((float)X1, q0.x), __fsub_rn((float)Y0, q0.y),
-                  __fsub_rn((float)Y1, q0.y), q0.z, q0.w, q1.x, q1.y))
-      m |= 1u << q;
+    const float ax0 = (float)X0 - q0.x, ax1 = (float)X1 - q0.x, ay0 = (float)Y0 - q0.y, ay1 = (float)Y1 - q0.y;
+    bool keep = ax0 <= 0.0f && 0.0f <= ax1 && ay0 <= 0.0f && 0.0f <= ay1;
+    if (!keep) {
+      float e = edge_max_rcp(ax0, ay0, ay1, nA, nB, nC, inv2C);
+      e = fmaxf(e, edge_max_rcp(ax1, ay0, ay1, nA, nB, nC, inv2C));
+      e = fmaxf(e, edge_max_rcp(ay0, ax0, ax1, nC, nB, nA, inv2A));
+      e = fmaxf(e, edge_max_rcp(ay1, ax0, ax1, nC, nB, nA, inv2A));
+      keep = e >= lo;
+    }
+    if (keep) m |= 1u << q;
   }
   return m;
 }
