@@ -134,14 +134,24 @@ __global__ void __launch_bounds__(256) k_quad_bin(DevCam cam, const float4* __re
                                                   int32_t* __restrict__ qlen, int32_t* __restrict__ qslot) {
   const int n_tiles = cam.TX * cam.TY;
   const int n = (int)min((int64_t)offs[n_tiles], capacity);
-  const int stride = gridDim.x * blockDim.x;
-  for (int j0 = blockIdx.x * blockDim.x; j0 < n; j0 += stride) {  // warp-uniform trip count
-    const int j = j0 + threadIdx.x;
-    const bool live = j < n;
+  // each warp takes a contiguous range of pairs, 32 at a time; the tile of its first pair comes
+  // from one binary search, after which each lane steps the warp's tile cursor forward (tile lists
+  // are long, so mostly zero or one step)
+  const int lane = threadIdx.x & 31;
+  const int n_warps = (gridDim.x * blockDim.x) >> 5, gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int per = (((n + n_warps - 1) / n_warps) + 31) & ~31;
+  const int jb = gw * per, je = min(n, jb + per);
+  int tc = jb < je ? tile_of_pair(offs, n_tiles, jb) : 0;  // warp-uniform
+  for (int j0 = jb; j0 < je; j0 += 32) {                  // warp-uniform trip count
+    const int j = j0 + lane;
+    const bool live = j < je;
+    int t = tc;
+    if (live)
+      while (__ldg(offs + t + 1) <= j) t++;
+    tc = __shfl_sync(0xffffffffu, t, 31);  // the cursor for the next 32 pairs
     unsigned m = 0;
-    int t = 0, slot = 0, base = 0, L = 0;
+    int slot = 0, base = 0, L = 0;
     if (live) {
-      t = tile_of_pair(offs, n_tiles, j);
       slot = pair_slot[j];
       const float4* r = rec + (size_t)slot * kRec4;
       m = quadrant_mask(cam, t, r[0], r[1]);
