@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(256) k_moments_pixel(DevCam cam, const float4*
 // gradients, the h/v rows are updated while streaming the coefficients, and the direction's
 // gradient is reduced to 3 floats. Phase 2 (geometry): μ', conic → Σ' → (Σ, J) → (q, s, μ).
 // Ordering the phases keeps the SH and the 3×3 geometry state from being live together.
-__global__ void __launch_bounds__(128, 3) k_epilogue(DevCam cam, const float4* __restrict__ rows,
+__global__ void __launch_bounds__(128, 4) k_epilogue(DevCam cam, const float4* __restrict__ rows,
                                                   const float* __restrict__ sigma_p, const int32_t* __restrict__ idx,
                                                   int32_t n_slots, const float4* __restrict__ rec,
                                                   const float4* __restrict__ acc2d, float scale,
