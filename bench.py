@@ -253,9 +253,10 @@ def event_ms(a, b):
 
 
 def scan_kernels(n):
+    """k_scan_blocks alone for n <= 4096 (it writes the total), else + k_scan_sums + k_scan_add."""
     if n <= 0:
         return 0
-    return 2 + (1 if (n + 4095) // 4096 > 1 else 0)
+    return 1 if (n + 4095) // 4096 == 1 else 3
 
 
 class Workload:

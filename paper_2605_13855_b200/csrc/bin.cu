@@ -119,8 +119,8 @@ void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_sl
   if (n_slots > 0)
     k_bin_expand<false><<<blocks, 128, 0, st>>>(r4, tiles_per_slot, n_slots, cam.TX, cam.W, cam.H, counts, pair_slot, capacity,
                                                 tile_offsets, n_tiles, d_n_pairs, d_max_pairs);
-  launch_exclusive_scan(counts, tile_offsets, n_tiles, tmp, st);
-  cudaMemcpyAsync(counts, tile_offsets, sizeof(int32_t) * n_tiles, cudaMemcpyDeviceToDevice, st);
+  // tile_offsets = exclusive scan of the histogram; the counts become the scatter cursors
+  launch_exclusive_scan(counts, tile_offsets, n_tiles, tmp, st, counts);
   k_bin_expand<true><<<blocks, 128, 0, st>>>(r4, tiles_per_slot, n_slots, cam.TX, cam.W, cam.H, counts, pair_slot, capacity,
                                              tile_offsets, n_tiles, d_n_pairs, d_max_pairs);
 }

@@ -15,7 +15,8 @@ void launch_project(const DevCam& cam, const float* rows, const float* sigma, co
 
 // scan.cu — exclusive scan of n int32 counts; out[n] = total. tmp: scan_tmp_bytes(n).
 size_t scan_tmp_bytes(int64_t n);
-void launch_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, void* tmp, cudaStream_t st);
+void launch_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, void* tmp, cudaStream_t st,
+                           int32_t* out2 = nullptr);
 
 // bin.cu — a2
 size_t bin_ws_bytes(int32_t n_tiles);

@@ -37,8 +37,11 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* s_warp, int* tot
   return s_warp[wid] + inc - v;
 }
 
+// With one block (n <= 4096) it finishes the scan itself: out[n] = total, and the prefixes also go
+// to out2 (nullable; e.g. the binning cursors), saving the block-sum pass and a copy.
 __global__ void __launch_bounds__(kScanThreads) k_scan_blocks(const int32_t* __restrict__ in, int32_t* __restrict__ out,
-                                                              int64_t n, int32_t* __restrict__ block_sums) {
+                                                              int64_t n, int32_t* __restrict__ block_sums,
+                                                              int32_t* __restrict__ out2) {
   __shared__ int s_warp[32];
   __shared__ int s_total;
   int64_t base = (int64_t)blockIdx.x * kScanBlock + (int64_t)threadIdx.x * kScanItems;
@@ -52,10 +55,16 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_blocks(const int32_t* __r
   int pre = block_exclusive_scan(sum, s_warp, &s_total);
 #pragma unroll
   for (int i = 0; i < kScanItems; i++) {
-    if (base + i < n) out[base + i] = pre;
+    if (base + i < n) {
+      out[base + i] = pre;
+      if (out2) out2[base + i] = pre;
+    }
     pre += v[i];
   }
-  if (threadIdx.x == 0) block_sums[blockIdx.x] = s_total;
+  if (threadIdx.x == 0) {
+    block_sums[blockIdx.x] = s_total;
+    if (gridDim.x == 1) out[n] = s_total;
+  }
 }
 
 // Scans the block sums in place (nb <= 4096) and writes the grand total to out[n].
@@ -94,16 +103,18 @@ size_t scan_tmp_bytes(int64_t n) {
   return align_up((size_t)(nb > 0 ? nb : 1) * sizeof(int32_t));
 }
 
-void launch_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, void* tmp, cudaStream_t st) {
+void launch_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, void* tmp, cudaStream_t st, int32_t* out2) {
   if (n <= 0) {
     cudaMemsetAsync(out, 0, sizeof(int32_t), st);
     return;
   }
   int64_t nb = (n + kScanBlock - 1) / kScanBlock;  // <= 4096 (checked by callers)
   int32_t* sums = static_cast<int32_t*>(tmp);
-  k_scan_blocks<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, sums);
+  k_scan_blocks<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, sums, nb == 1 ? out2 : nullptr);
+  if (nb == 1) return;
   k_scan_sums<<<1, kScanThreads, 0, st>>>(sums, (int)nb, out, n);
-  if (nb > 1) k_scan_add<<<(unsigned)nb, kScanThreads, 0, st>>>(out, n, sums);
+  k_scan_add<<<(unsigned)nb, kScanThreads, 0, st>>>(out, n, sums);
+  if (out2) cudaMemcpyAsync(out2, out, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st);
 }
 
 }  // namespace oit
