@@ -159,8 +159,9 @@ int oit_composite_fwd_ex(const oit_camera* cam, const float* rec, const int32_t*
  * oit_loss_grad) against target [3][H][W] and writes the backward coefficients (K, u, s, a) straight
  * into bwd_ws — the workspace (of oit_bwd_workspace_bytes(cam, n_slots, pair_capacity) bytes) the
  * following oit_composite_bwd_ex call on the same stream receives with target = NULL,
- * dL_dimage = NULL and loss = OIT_COEF_IN_WS. No pixel-state round trip; state (nullable) is still
- * written if given. ws: oit_fwd_workspace_bytes scratch. D-SSIM (loss 2) is not pixel-local: use
+ * dL_dimage = NULL and loss = OIT_COEF_IN_WS, over the SAME records and pair lists. No pixel-state
+ * round trip; state (nullable) is still written if given. Without a state, coefficients are
+ * written only for tiles that hold pairs (the only ones that backward reads). ws: oit_fwd_workspace_bytes scratch. D-SSIM (loss 2) is not pixel-local: use
  * oit_composite_bwd_ex with a target for it. */
 #define OIT_COEF_IN_WS 0x200 /* oit_composite_bwd_ex: the coefficients are already in ws */
 int oit_composite_fwd_loss(const oit_camera* cam, const float* rec, const int32_t* pair_slot,

@@ -141,6 +141,7 @@ int oit_composite_fwd_loss(const oit_camera* cam, const float* rec, const int32_
   fl.loss = l;
   fl.coef4 = reinterpret_cast<float4*>(cv.take<float>((size_t)nt * kTilePx * 4));
   fl.coefa = cv.take<float>((size_t)nt * kTilePx);
+  fl.listed_tiles_only = true;
   launch_composite_fwd(dev_cam(cam, bg_host), rec, pair_slot, tile_offsets, pair_capacity, base, nullptr, nullptr,
                        state, nullptr, S(stream), nullptr, ws, concurrency, fl);
   return launch_status();

@@ -359,7 +359,11 @@ void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pa
     float* partial = cv.take<float>((size_t)max_items * 5 * kTilePx);
     cudaMemsetAsync(done, 0, sizeof(int32_t) * n_tiles, st);
     cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
-    launch_build_items(tile_offsets, nullptr, n_tiles, capacity, chunk_len, 1, items, n_items, tile_nch, scratch, st);
+    // every tile gets an item (its state/image is written even without pairs), except in the fused
+    // training forward, whose only output are the coefficients of the tiles the backward reads
+    const int empty_items = (fl.target && fl.listed_tiles_only && !state && !image) ? 0 : 1;
+    launch_build_items(tile_offsets, nullptr, n_tiles, capacity, chunk_len, empty_items, items, n_items, tile_nch,
+                       scratch, st);
     // persistent grid: as many 64-thread CTAs per SM as the instantiation's registers let reside
     // (16-18), fewer when views run concurrently; items are claimed dynamically
 #define OIT_FWD2(B, K, L)                                                                                   \

@@ -33,6 +33,9 @@ struct FwdLoss {
   int32_t loss = 0;
   float4* coef4 = nullptr;
   float* coefa = nullptr;
+  // the following backward runs over the same pair lists, so it reads the coefficients of tiles
+  // that hold pairs only: tiles without pairs get no work item (nothing read or written for them)
+  bool listed_tiles_only = false;
 };
 void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pair_slot,
                           const int32_t* tile_offsets, int64_t capacity, const float* base, const uint8_t* route,

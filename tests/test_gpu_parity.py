@@ -423,8 +423,10 @@ def test_c2_full_size_bench_configuration_parity():
     t8 = synth.target_image_u8(cam, 32)
     rows, sigma = _t(sc.rows), _t(np.array([sc.sigma], np.float32))
     p = _pipe(cam, len(act), cap=1 << 22)
-    st = p.forward_loss(rows, sigma, _t(act), sc.bg, _t(t8), "l2", base=_t(plain_to_tile_major(cache, W, H)),
-                        state=True, concurrency=16)
+    base = _t(plain_to_tile_major(cache, W, H))
+    st = p.forward_loss(rows, sigma, _t(act), sc.bg, _t(t8), "l2", base=base, state=True, concurrency=16).clone()
+    # the gradient through the exact bench path: no state, coefficients of the listed tiles only
+    assert p.forward_loss(rows, sigma, _t(act), sc.bg, _t(t8), "l2", base=base, state=False, concurrency=16) is None
     grad = torch.zeros((len(act), 80), dtype=torch.float32, device=DEV)
     dsig = torch.zeros(1, dtype=torch.float32, device=DEV)
     p.backward(rows, sigma, _t(act), sc.bg, None, None, grad, dsig, coef_ready=True, concurrency=16)
@@ -719,19 +721,21 @@ def test_forward_loss_fusion_equals_separate_calls(loss, u8):
     cache = st0.clone()
     n = int(act.numel())
     out = []
-    for fused in (False, True):
+    for mode in ("separate", "fused+state", "fused"):   # "fused": the bench's path (listed tiles only)
         grad = torch.zeros((n, 80), dtype=torch.float32, device=DEV)
         ds = torch.zeros(1, dtype=torch.float32, device=DEV)
-        if fused:
-            st = p.forward_loss(rows, sigma, act, sc.bg, tgt, loss, base=cache, state=True, concurrency=4)
+        if mode != "separate":
+            st = p.forward_loss(rows, sigma, act, sc.bg, tgt, loss, base=cache, state=mode == "fused+state",
+                                concurrency=4)
             p.backward(rows, sigma, act, sc.bg, None, None, grad, ds, coef_ready=True, concurrency=4)
         else:
             _, st = p.forward(rows, sigma, act, sc.bg, base=cache, image=False)
             p.backward(rows, sigma, act, sc.bg, st, None, grad, ds, target=tgt, loss=loss)
-        out.append((st.cpu().numpy().copy(), grad.cpu().numpy(), ds.item()))
+        out.append((None if st is None else st.cpu().numpy().copy(), grad.cpu().numpy(), ds.item()))
     assert np.allclose(out[1][0], out[0][0], rtol=1e-5, atol=1e-7)
-    assert np.abs(out[1][1] - out[0][1]).max() <= 1e-5 * np.abs(out[0][1]).max()
-    assert abs(out[1][2] - out[0][2]) <= 1e-5 * abs(out[0][2]) + 1e-12
+    for k in (1, 2):
+        assert np.abs(out[k][1] - out[0][1]).max() <= 1e-5 * np.abs(out[0][1]).max()
+        assert abs(out[k][2] - out[0][2]) <= 1e-5 * abs(out[0][2]) + 1e-12
     assert np.abs(out[0][1]).max() > 0
     # and against the oracle (loss gradient of the oracle's image pushed through its backward)
     full = O.render(sc.rows, sc.sigma, np.arange(sc.n), cam, sc.bg)
@@ -740,8 +744,8 @@ def test_forward_loss_fusion_equals_separate_calls(loss, u8):
     gimg = O.loss_grad(full["image"], t64, loss)
     a = np.flatnonzero(mask).astype(np.int32)
     gr, _, _, bnd = O.backward_bound(sc.rows, sc.sigma, a, cam, sc.bg, full["state"], gimg)
-    ok, bad = grad_close(out[1][1], gr, bnd, atol=1e-6 / (3 * cam["width"] * cam["height"]))
-    assert ok, describe_bad(out[1][1], gr, bad, bnd)
+    ok, bad = grad_close(out[2][1], gr, bnd, atol=1e-6 / (3 * cam["width"] * cam["height"]))
+    assert ok, describe_bad(out[2][1], gr, bad, bnd)
 
 
 # ------------------------------------------------------------------ NEXT-1 reconcile ------
