@@ -20,6 +20,7 @@ constexpr int kFwdThreads = 64;    // 4 pixels per thread (one tile row: columns
 // slots per work item: 128 balances the persistent grid (alone on the GPU: 84 vs 124 µs per C2
 // view at 256; 64 is no faster); the workspace is sized for chunks down to kFwdChunkMin
 constexpr int kFwdChunk = 128;
+constexpr int kFwdChunkShared = 256;
 constexpr int kFwdChunkMin = 64;
 
 __device__ __forceinline__ void accum_px(float power, float thr_hi, float arg, const float4& q2, float& P0, float& P1,
@@ -347,7 +348,11 @@ void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pa
   const float4* r4 = reinterpret_cast<const float4*>(rec);
   auto* cnt = reinterpret_cast<unsigned long long*>(counters);
   if (!route) {
-    const int chunk_len = kFwdChunk;
+    // alone on the GPU, 128-slot chunks balance the persistent grid; with views running concurrently
+    // the per-item costs (claim, base load, split-tile merge) matter more than one kernel's balance
+    // (C2 ρ 0.2, 12 streams: chunk 64/128/192/256/384/512 → 4115/4218/4256/4275/4287/4313 Mpix/s,
+    // but ρ 0.05 peaks at 256)
+    const int chunk_len = concurrency > 1 ? kFwdChunkShared : kFwdChunk;
     const int64_t max_items = capacity / chunk_len + n_tiles + 1;
     Carve cv(ws);
     int4* items = cv.take<int4>(max_items);
