@@ -98,6 +98,7 @@ __device__ __forceinline__ void moments_window(Moments& m, const float* __restri
   const f2_t mx2 = f2s(mx), nA2 = f2s(nA), nkx2 = f2s(-kx), l2e = f2s(kLog2e), one2 = f2s(1.0f);
   const f2_t cR2 = f2s(cR), cG2 = f2s(cG), cB2 = f2s(cB), w2 = f2s(w);
   f2_t U0 = f2s(0.f), U1 = f2s(0.f), U2 = f2s(0.f), NS = f2s(0.f);  // packed (even, odd pixel) partial sums; NS = −S
+  f2_t Rdxx = f2s(0.f);  // Σ d dx² needs no dy: accumulated over the whole window
   for (int py = py0; py <= py1; py++) {
     const float dy = __fsub_rn((float)(ty0 + py), my);
     const bool ract = valid && fabsf(dy) <= ey;
@@ -106,7 +107,7 @@ __device__ __forceinline__ void moments_window(Moments& m, const float* __restri
     const f2_t cy2 = f2s(__fmul_rn(__fmul_rn(nC, dy), dy));
     const f2_t ra2 = f2s(fmaf(-ky, dy, log2o));
     const float lo = ract ? thr_lo : 1.0f;  // folds the row test into the pixel test
-    f2_t Rd = f2s(0.f), Rdx = f2s(0.f), Rdxx = f2s(0.f);
+    f2_t Rd = f2s(0.f), Rdx = f2s(0.f);
     const float* row = s_u + (py - qy0) * 8 - qx0;
     f2_t dx2 = sub2(f2((float)(tx0 + pxe), (float)(tx0 + pxe + 1)), mx2);
     const f2_t two2 = f2s(2.0f);
@@ -149,14 +150,14 @@ __device__ __forceinline__ void moments_window(Moments& m, const float* __restri
       fma2_acc(Rdxx, t, dx2);
       add2_acc(dx2, two2);  // next pair: dx + 2 (exact: small integers minus the same mx)
     }
-    const float rd = f2lo(Rd) + f2hi(Rd), rdx = f2lo(Rdx) + f2hi(Rdx), rdxx = f2lo(Rdxx) + f2hi(Rdxx);
+    const float rd = f2lo(Rd) + f2hi(Rd), rdx = f2lo(Rdx) + f2hi(Rdx);
     m.Od += rd;
     m.M1 += rdx;
     m.M2 = fmaf(dy, rd, m.M2);
-    m.XX += rdxx;
     m.XY = fmaf(dy, rdx, m.XY);
     m.YY = fmaf(dy * dy, rd, m.YY);
   }
+  m.XX += f2lo(Rdxx) + f2hi(Rdxx);
   m.U0 += f2lo(U0) + f2hi(U0);
   m.U1 += f2lo(U1) + f2hi(U1);
   m.U2 += f2lo(U2) + f2hi(U2);
