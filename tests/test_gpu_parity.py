@@ -748,6 +748,40 @@ def test_forward_loss_fusion_equals_separate_calls(loss, u8):
     assert ok, describe_bad(out[2][1], gr, bad, bnd)
 
 
+def test_forward_loss_with_no_active_slots():
+    """Empty active set through the fused training path (no pairs: no work item at all) and the
+    score with nothing active (a synthetic cache alone is the pixel state): no error, zero
+    gradients for the empty set, and the score equals the oracle's."""
+    sc = SCENES[1]
+    cam = sc.cams[0]
+    rows, sigma = _t(sc.rows), _t(np.array([sc.sigma], np.float32))
+    p = _pipe(cam, sc.n)
+    empty = torch.empty(0, dtype=torch.int32, device=DEV)
+    tgt = _t(synth.target_image_u8(cam, 3))
+    assert p.forward_loss(rows, sigma, empty, sc.bg, tgt, "l1") is None
+    grad = torch.zeros((1, 80), dtype=torch.float32, device=DEV)
+    ds = torch.zeros(1, dtype=torch.float32, device=DEV)
+    p.backward(rows, sigma, empty, sc.bg, None, None, grad, ds, coef_ready=True)
+    torch.cuda.synchronize()
+    assert float(grad.abs().sum()) == 0.0 and float(ds.item()) == 0.0
+    L = _L()
+    idx = np.arange(sc.n, dtype=np.int32)
+    t32 = synth.target_image(cam, 4)
+    cap = 1 << 20
+    ws = torch.empty(L.oit_score_workspace_bytes(cam, 0, sc.n, cap), dtype=torch.uint8, device=DEV)
+    sg = torch.zeros((sc.n, 80), dtype=torch.float32, device=DEV)
+    sds = torch.zeros(1, dtype=torch.float32, device=DEV)
+    mp = torch.zeros(1, dtype=torch.int64, device=DEV)
+    W, H = cam["width"], cam["height"]
+    cache = synth.pixel_state(cam, 5)   # everything frozen: the cache alone is the pixel state
+    L.oit_score_subsample(rows, sigma, [cam], [_t(t32)], [_t(plain_to_tile_major(cache, W, H))], empty, _t(idx), [0],
+                          "l2", sc.bg, sg, sds, cap, mp, ws)
+    ref, dsref, bnd = O.score_subsample(sc.rows, sc.sigma, [cam], [t32], [cache], np.zeros(0, np.int32), idx, [0],
+                                        sc.bg, "l2", with_bound=True)
+    ok, bad = grad_close(sg.cpu().numpy(), ref, bnd, atol=1e-6 / (3 * cam["width"] * cam["height"]))
+    assert ok, describe_bad(sg.cpu().numpy(), ref, bad, bnd)
+
+
 # ------------------------------------------------------------------ NEXT-1 reconcile ------
 def _state_close(got, ref, rtol=2e-4, frac=1e-5):
     """Pixel-state bar (as test_composite_fwd_parity) plus a per-channel floor for the P̄/Q̄
