@@ -11,14 +11,19 @@
 // legal: partial (P, Q, T) of the chunks combine as P = ΣP_k, Q = ΣQ_k, T = ΠT_k, done in chunk
 // order by the last CTA to finish the tile (deterministic). Each thread owns 4 pixels of one row
 // (x, x+4, x+8, x+12), which shares the record loads and the row terms of the spec test across
-// the 4 pixels and gives four independent dependency chains. k_fwd (one CTA per tile) serves the BAU route path.
+// the 4 pixels and gives four independent dependency chains. The persistent grid and the chunk
+// length follow the caller's concurrency hint (views in flight on other streams). With kLoss the
+// epilogue applies the pixel-local loss and writes the backward coefficients (a4 fused); then
+// tiles without pairs can be left out entirely (their coefficients are never read).
+// k_fwd (one CTA per tile) serves the BAU route path.
 #include "kernels.h"
 
 namespace oit {
 
 constexpr int kFwdThreads = 64;    // 4 pixels per thread (one tile row: columns c, c+4, c+8, c+12)
-// slots per work item: 128 balances the persistent grid (alone on the GPU: 84 vs 124 µs per C2
-// view at 256; 64 is no faster); the workspace is sized for chunks down to kFwdChunkMin
+// slots per work item: alone on the GPU 128 balances the persistent grid (84 vs 124 µs per C2 view
+// at 256; 64 is no faster); with concurrent views 256 (per-item costs dominate); the workspace is
+// sized for chunks down to kFwdChunkMin
 constexpr int kFwdChunk = 128;
 constexpr int kFwdChunkShared = 256;
 constexpr int kFwdChunkMin = 64;
