@@ -91,10 +91,17 @@ def parse():
 _REF = {}
 
 
-def _ref_init(seed_views, n_splats, res, rho, kind):
+def _ref_init(seed_views, n_splats, res, rho, kind, crop=1):
     import oracle as O
     from paper_2605_13855_b200 import synth
     sc = synth.scene_c2(n=n_splats, n_views=seed_views, res=res)
+    if crop > 1:   # a res/crop × res/crop window of every view, view v taking window v mod crop², so
+        w = res // crop   # that the workers together cover every part of the image (a bounded sample)
+        for v, c in enumerate(sc.cams):
+            q = v % (crop * crop)
+            c["width"] = c["height"] = w
+            c["cx"] -= (q % crop) * w
+            c["cy"] -= (q // crop) * w
     mask = synth.active_mask(sc, rho, kind)
     _REF.update(O=O, synth=synth, sc=sc, act=np.flatnonzero(mask).astype(np.int32),
                 ina=np.flatnonzero(~mask).astype(np.int32), caches={}, targets={})
@@ -125,13 +132,14 @@ class OracleRunner:
     Worker k prepares (untimed) and then repeatedly processes view k; a step's time is the slowest
     worker's compute time for its view (the views run concurrently)."""
 
-    def __init__(self, args, n_views_total):
+    def __init__(self, args, n_views_total, crop=1):
         self.cores = os.cpu_count() or 1
         self.views = list(range(min(self.cores, n_views_total)))
         ctx = mp.get_context("spawn")
         self.pool = ctx.Pool(len(self.views), initializer=_ref_init,
-                             initargs=(n_views_total, args.splats, args.res, args.rho, args.kind))
-        self.px_per_view = args.res * args.res
+                             initargs=(n_views_total, args.splats, args.res, args.rho, args.kind, crop))
+        self.crop = crop
+        self.px_per_view = (args.res // crop) ** 2
 
     def step(self):
         return max(self.pool.map(_ref_prepare_and_step, self.views, chunksize=1))
@@ -147,8 +155,8 @@ def _ref_prepare_and_step(v):
     return _ref_step(v)
 
 
-def cpu_leg(args, n_views_total, steps, warmup):
-    r = OracleRunner(args, n_views_total)
+def cpu_leg(args, n_views_total, steps, warmup, crop=1):
+    r = OracleRunner(args, n_views_total, crop)
     try:
         # the first pass also prepares each view's cache (untimed: _ref_step times only its own work)
         for _ in range(max(1, warmup)):
@@ -160,15 +168,21 @@ def cpu_leg(args, n_views_total, steps, warmup):
     px = len(r.views) * r.px_per_view
     return dict(value=px / mean / 1e6, unit=UNIT, cores=r.cores, kind="oracle", ms_per_step=mean * 1e3,
                 sample=f"{len(r.views)} training views (one per host core, independent processes) of the same "
-                       f"workload, each: oracle render of the active set over its pre-render cache + L1 gradient "
-                       f"+ backward (single-threaded C, fp64)")
+                       f"workload" + (f", each cropped to one {args.res // crop}x{args.res // crop} window (view v: "
+                                      f"window v mod {crop * crop}, so the workers cover every part of the image)"
+                                      if crop > 1 else "") +
+                       ", each: oracle render of the active set over its pre-render cache + L1 gradient "
+                       "+ backward (single-threaded C, fp64)")
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    res = cpu_leg(args, args.views, max(1, args.steps), max(0, args.warmup))
+    # K + W steps of one view per core would take ~12 s each at full size: the reference arm samples
+    # a quarter window of every view (the four windows spread over the workers) so that the whole
+    # run stays within a few minutes
+    res = cpu_leg(args, args.views, max(1, args.steps), max(0, args.warmup), crop=2)
     line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
