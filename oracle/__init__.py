@@ -117,6 +117,18 @@ def project_value(rows64, sigma, idx, cam) -> dict:
                 color=out[:, 5:8], w=out[:, 8], tz=out[:, 9], o=out[:, 10])
 
 
+def branch_flags(rows64, sigma, idx, cam) -> dict:
+    """Which piecewise branch of the value path each slot sits on (test bookkeeping for the FD pins
+    of the clamp branches): tan-fov clamp in J (R13, Eq. 6), colour clamp per channel
+    (R7, Eq. 4), v(r) <= 0 (R4, Eq. 1), d >= σ (Eq. 1)."""
+    rows64, idx = _f64(rows64), _i32(idx)
+    out = np.zeros((len(idx), 7), np.int32)
+    lib().orc_branch_flags(_p(rows64), C.c_double(sigma), _p(idx), C.c_int32(len(idx)),
+                           C.byref(camera(cam)), _p(out))
+    out = out.astype(bool)
+    return dict(clampx=out[:, 0], clampy=out[:, 1], color=out[:, 2:5], vneg=out[:, 5], ramp0=out[:, 6])
+
+
 def n_tiles(cam) -> tuple:
     return (int(cam["width"]) + 15) // 16, (int(cam["height"]) + 15) // 16
 
@@ -194,20 +206,27 @@ def backward(rows32, sigma, idx, cam, bg, state, dL_dC, mode: str = "rect", rows
     return grad, float(dsig[0]), dcov
 
 
-def backward_bound(rows32, sigma, idx, cam, bg, state, dL_dC, mode: str = "rect"):
+def backward_bound(rows32, sigma, idx, cam, bg, state, dL_dC, mode: str = "rect", full: bool = False):
     """``backward`` plus, per splat and row field, the forward-error scale of the gradient:
     Σ_k |∂row/∂G2_k|·Σ_pairs|term_k| (the 2D-gradient terms' magnitudes before cancellation,
     through |chain Jacobian|). Test bookkeeping for the fp32 tolerance (R31), not part
-    of the method. Returns (grad, dsigma, dcov, bound)."""
+    of the method. Returns (grad, dsigma, dcov, bound), or with ``full`` a dict that adds the same
+    scale for dΣ (``bound_cov`` [n,6]) and dσ (``bound_sigma``)."""
     rows32, idx = _f32(rows32), _i32(idx)
     rows64 = _f64(rows32)
     grad = np.zeros((len(idx), ROW))
     bound = np.zeros((len(idx), ROW))
     dcov = np.zeros((len(idx), 6))
     dsig = np.zeros(1)
+    bcov = np.zeros((len(idx), 6))
+    bsig = np.zeros(1)
     lib().orc_backward_bound(_p(rows32), _p(rows64), C.c_double(sigma), _p(idx), C.c_int32(len(idx)),
                              C.byref(camera(cam)), _p(_f64(bg)), _p(_f64(state)), _p(_f64(dL_dC)),
-                             C.c_int32(0 if mode == "brute" else 1), _p(grad), _p(dsig), _p(dcov), _p(bound))
+                             C.c_int32(0 if mode == "brute" else 1), _p(grad), _p(dsig), _p(dcov), _p(bound),
+                             _p(bcov), _p(bsig))
+    if full:
+        return dict(grad=grad, dsigma=float(dsig[0]), dcov=dcov, bound=bound, bound_cov=bcov,
+                    bound_sigma=float(bsig[0]))
     return grad, float(dsig[0]), dcov, bound
 
 
@@ -260,18 +279,22 @@ def score_subsample(rows32, sigma, cams, targets, caches, active_idx, score_idx,
     """Subsampled gradient score (Alg. 1 l.8-12; §4.1): for each subsampled
     view j, the full-𝒢 pixel state is the cached frozen-set accumulators ⊕ the active set
     (R16); L_j's gradient (R20, R24) is back-propagated to the scored splats; the mean over
-    the S views is returned (R19) as (score_grad [n_score,80], dsigma[, bound])."""
+    the S views is returned (R19) as (score_grad [n_score,80], dsigma[, bound[, bound_sigma]])
+    (``with_bound="full"`` adds the dσ error scale)."""
     acc = np.zeros((len(score_idx), ROW))
     bnd = np.zeros((len(score_idx), ROW))
-    dsig = 0.0
+    dsig = bsig = 0.0
     for j in views:
         cam = cams[j]
         fwd = render(rows32, sigma, active_idx, cam, bg, base=caches[j], mode=mode)
         g = loss_dssim(fwd["image"], targets[j], 0.2)[1] if loss == "dssim" else loss_grad(fwd["image"], targets[j], loss)
-        gr, ds, _, b = backward_bound(rows32, sigma, score_idx, cam, bg, fwd["state"], g, mode=mode)
-        acc += gr
-        bnd += b
-        dsig += ds
+        r = backward_bound(rows32, sigma, score_idx, cam, bg, fwd["state"], g, mode=mode, full=True)
+        acc += r["grad"]
+        bnd += r["bound"]
+        dsig += r["dsigma"]
+        bsig += r["bound_sigma"]
+    if with_bound == "full":
+        return acc / len(views), dsig / len(views), bnd / len(views), bsig / len(views)
     if with_bound:
         return acc / len(views), dsig / len(views), bnd / len(views)
     return acc / len(views), dsig / len(views)

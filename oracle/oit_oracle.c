@@ -399,6 +399,23 @@ void orc_project_value(const double* rows, double sigma, const int32_t* idx, int
     }
 }
 
+/* Which piecewise branch of the value path each slot sits on (test bookkeeping for the
+ * finite-difference pins of the clamp branches): out[k][7] = clampx, clampy (tan-fov clamp in J,
+ * R13 / Eq. 6), craw_ch <= 0 for ch = 0..2 (colour clamp, R7 / Eq. 4),
+ * vraw <= 0 (v⁺ guard, R4 / Eq. 1), ramp_raw <= 0 (d >= σ, Eq. 1). */
+void orc_branch_flags(const double* rows, double sigma, const int32_t* idx, int32_t n_slots,
+                      const orc_camera* cam, int32_t* out7) {
+    for (int32_t k = 0; k < n_slots; k++) {
+        orc_val v;
+        orc_value_project(rows + (size_t)idx[k] * ROW, sigma, cam, &v);
+        int32_t* o = out7 + (size_t)k * 7;
+        o[0] = v.clampx; o[1] = v.clampy;
+        for (int ch = 0; ch < 3; ch++) o[2 + ch] = !(v.craw[ch] > 0);
+        o[5] = !(v.vraw > 0);
+        o[6] = !(v.ramp_raw > 0);
+    }
+}
+
 /* Brute force, for the binning pins: out[k][t] = 1 iff some pixel of tile t passes the step-13
  * contribution test for slot k (independent of the rectangle and of the tile test). */
 void orc_tile_contrib(const float* rows, const int32_t* idx, int32_t n_slots, const orc_camera* cam, uint8_t* out) {
@@ -698,13 +715,13 @@ static void chain_to_params(const double* row, double sigma, const orc_camera* c
 void orc_backward_bound(const float* rows_dec, const double* rows_val, double sigma, const int32_t* idx,
                         int32_t n_slots, const orc_camera* cam, const double* bg, const double* state,
                         const double* dL_dC, int32_t mode, double* grad, double* dsigma, double* dcov,
-                        double* bound);
+                        double* bound, double* bound_cov, double* bound_sigma);
 
 void orc_backward(const float* rows_dec, const double* rows_val, double sigma, const int32_t* idx,
                   int32_t n_slots, const orc_camera* cam, const double* bg, const double* state,
                   const double* dL_dC, int32_t mode, double* grad, double* dsigma, double* dcov) {
     orc_backward_bound(rows_dec, rows_val, sigma, idx, n_slots, cam, bg, state, dL_dC, mode, grad, dsigma,
-                       dcov, NULL);
+                       dcov, NULL, NULL, NULL);
 }
 
 /* Same as orc_backward; if bound != NULL it also receives, per splat and row field, a
@@ -712,11 +729,12 @@ void orc_backward(const float* rows_dec, const double* rows_val, double sigma, c
  * i.e. the magnitude of the per-pair terms each 2D gradient component G2_k sums (before any
  * cancellation), pushed through the absolute value of the splat's chain-rule Jacobian, which is
  * obtained column by column by applying the (linear) chain to unit 2D gradients. A floating-point
- * evaluation that rounds each term with relative error u has an error of order u·bound. */
+ * evaluation that rounds each term with relative error u has an error of order u·bound. bound_cov
+ * [n][6] and *bound_sigma (+=, nullable) are the same scale for dΣ and dσ. */
 void orc_backward_bound(const float* rows_dec, const double* rows_val, double sigma, const int32_t* idx,
                         int32_t n_slots, const orc_camera* cam, const double* bg, const double* state,
                         const double* dL_dC, int32_t mode, double* grad, double* dsigma, double* dcov,
-                        double* bound) {
+                        double* bound, double* bound_cov, double* bound_sigma) {
     int Wd = cam->width, H = cam->height;
     size_t np = (size_t)Wd * H;
     for (int32_t k = 0; k < n_slots; k++) {
@@ -795,10 +813,13 @@ void orc_backward_bound(const float* rows_dec, const double* rows_val, double si
                 memset(&e, 0, sizeof(e));
                 double* ec[10] = {&e.gc[0], &e.gc[1], &e.gc[2], &e.gw, &e.go, &e.gA, &e.gB, &e.gC, &e.gmx, &e.gmy};
                 *ec[c] = 1.0;
-                double col[ROW], ds = 0;
+                double col[ROW], ds = 0, ccov[6] = {0, 0, 0, 0, 0, 0};
                 memset(col, 0, sizeof(col));
-                chain_to_params(row, sigma, cam, &v, &e, col, &ds, NULL);
+                chain_to_params(row, sigma, cam, &v, &e, col, &ds, ccov);
                 for (int f = 0; f < ROW; f++) bound[(size_t)k * ROW + f] += fabs(col[f]) * *comp[c];
+                if (bound_cov)
+                    for (int f = 0; f < 6; f++) bound_cov[(size_t)k * 6 + f] += fabs(ccov[f]) * *comp[c];
+                if (bound_sigma) *bound_sigma += fabs(ds) * *comp[c];
             }
         }
     }

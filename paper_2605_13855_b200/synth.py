@@ -199,6 +199,61 @@ def scene_degenerate(seed: int = 5) -> Scene:
     return Scene("degenerate", np.stack(rows).astype(np.float32), base.sigma, base.cams, base.bg, dict(seed=seed))
 
 
+BRANCH_KINDS = ("fov", "color", "vneg", "ramp")
+
+
+def scene_branch(kind: str, seed: int = 0, n: int = 10) -> Scene:
+    """Tiny scenes whose splats sit on the piecewise branches of the value path, for the
+    finite-difference pins and the GPU parity of those branches. One 16×16 camera at the origin
+    with the identity rotation (camera space = world space, f = 12, c = (8, 8)), so every position
+    below is directly camera-space; μ_z ~ U[2.5, 4].
+
+    * ``fov``: 6 of the n splats at |t_x/t_z| (or |t_y/t_z|) ∈ [1.08, 1.5]·1.3·tan(fov/2) — the J
+      clamp of R13 active — with s ~ U[0.6, 1.0] so the α = 1/255 ellipse still reaches the image;
+    * ``color``: 6 splats with one or two colour channels' DC ~ U[-3.5, -2.2] (SH + 0.5 < 0: R7 clamp);
+    * ``vneg``: 5 splats with v DC ~ U[-6, -3] (v(r) < 0: w = 0 through R4, still in T per R11);
+    * ``ramp``: σ fixed at 3.2; 3 splats at d ∈ σ·[1.01, 1.3] (d ≥ σ: w = 0), 4 at d ∈ σ·[0.98, 0.999]
+      (within 2% below σ), the rest nearer.
+    The other splats are ordinary (in-frustum, positive colour and weight)."""
+    assert kind in BRANCH_KINDS
+    g = rng(7700 + 97 * BRANCH_KINDS.index(kind) + seed)
+    width = height = 16
+    f = 12.0
+    cam = dict(width=width, height=height, fx=f, fy=f, cx=8.0, cy=8.0, R=np.eye(3, dtype=np.float32).reshape(9),
+               t=np.zeros(3, np.float32), center=np.zeros(3, np.float32), znear=0.2)
+    rows = np.zeros((n, ROW), np.float32)
+    z = g.uniform(2.5, 4.0, n)
+    u = g.uniform(-0.45, 0.45, (n, 2))                 # in-frustum t_x/t_z, t_y/t_z
+    s = np.exp(g.normal(math.log(0.25), 0.3, (n, 3)))
+    _appearance(g, n, rows)
+    rows[:, O] = g.uniform(0.3, 0.95, n).astype(np.float32)
+    sigma = 4.75
+    if kind == "fov":
+        lim = 1.3 * (0.5 * width / f)
+        for k in range(6):
+            ax = k % 2                                  # x for even k, y for odd k
+            sign = 1.0 if (k // 2) % 2 == 0 else -1.0
+            u[k, ax] = sign * lim * g.uniform(1.08, 1.5)
+            s[k] = g.uniform(0.6, 1.0, 3)
+    elif kind == "color":
+        for k in range(6):
+            chans = [k % 3] if k < 3 else [k % 3, (k + 1) % 3]
+            for ch in chans:
+                rows[k, H + ch] = g.uniform(-3.5, -2.2)
+    elif kind == "vneg":
+        rows[:5, V] = g.uniform(-6.0, -3.0, 5)
+    else:  # ramp
+        sigma = 3.2
+        z[:3] = sigma * g.uniform(1.01, 1.3, 3)
+        z[3:7] = sigma * g.uniform(0.98, 0.999, 4)
+        z[7:] = sigma * g.uniform(0.7, 0.9, n - 7)
+    rows[:, MU] = (u[:, 0] * z).astype(np.float32)
+    rows[:, MU + 1] = (u[:, 1] * z).astype(np.float32)
+    rows[:, MU + 2] = z.astype(np.float32)
+    rows[:, S:S + 3] = s.astype(np.float32)
+    return Scene(f"branch-{kind}", rows, sigma, [cam], np.array([0.1, 0.2, 0.3]), dict(seed=seed, kind=kind))
+
+
 def active_mask(scene: Scene, rho: float, kind: str = "clustered", seed: int = 11) -> np.ndarray:
     """Forced active set of fraction ρ: 'uniform' (Bernoulli(ρ)) or 'clustered' (μ_x in the top ρ
     quantile — the paper's "small objects … large number of iterations")."""

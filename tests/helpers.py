@@ -50,6 +50,56 @@ def strict_fraction(got, ref, rtol=1e-4, atol=1e-6):
     return float((np.abs(got - ref) <= rtol * np.abs(ref) + atol).mean())
 
 
+def assert_grad_bar(got, ref, bound, atol=1e-6, name="grad", min_strict=0.99, rtol=1e-4, kappa=0.1, extra=None):
+    """The gradient parity assertion of every GPU test (R31, "how the bar is applied").
+
+    Primary check — the north-star bar elementwise: |Δ| ≤ 1e-4·|ref| + atol.
+    An element may miss it only if
+      (a) its sum is cancellation-dominated: κ·B ≥ |ref| (the oracle's forward-error scale B —
+          Σ|per-pair terms| through |chain Jacobian| — is at least 10× the cancelled result), and
+      (b) it meets R31: |Δ| ≤ 1e-4·(|ref| + κ·B) + atol;
+    and the fraction of elements meeting the primary bar must be ≥ ``min_strict``. ``extra``
+    (optional, per element) is a propagated INPUT tolerance (e.g. the D-SSIM dL/dC bar pushed through
+    the backward): an element within |Δ| ≤ 1e-4·(|ref| + κ·B) + extra + atol also passes.
+    Prints (and with OIT_PARITY_LOG appends as JSON) the element count, the strict misses, the
+    worst strict miss (|Δ| over the primary bar) and the largest |Δ|/B."""
+    import json
+    import os
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    B = np.zeros_like(ref) if bound is None else np.broadcast_to(np.asarray(bound, np.float64), ref.shape)
+    d = np.abs(got - ref)
+    strict_lim = rtol * np.abs(ref) + atol
+    strict_ok = d <= strict_lim
+    miss = ~strict_ok
+    cancel = kappa * B >= np.abs(ref)
+    r31_ok = d <= rtol * (np.abs(ref) + kappa * B) + atol
+    n = int(ref.size)
+    n_miss = int(miss.sum())
+    frac = 1.0 - n_miss / max(n, 1)
+    worst = float((d / strict_lim).max()) if n else 0.0
+    with np.errstate(divide="ignore", invalid="ignore"):
+        rb = np.where(B > 0, d / np.where(B > 0, B, 1.0), 0.0)
+    stats = dict(name=name, test=os.environ.get("PYTEST_CURRENT_TEST", "").split(" ")[0], n=n,
+                 strict_misses=n_miss, strict_fraction=frac, worst_strict_ratio=worst,
+                 max_err_over_B=float(rb.max()) if n else 0.0)
+    ok_alt = cancel & r31_ok
+    if extra is not None:
+        E = np.broadcast_to(np.asarray(extra, np.float64), ref.shape)
+        in_tol = d <= rtol * (np.abs(ref) + kappa * B) + E + atol
+        stats["input_tolerance_misses"] = int((miss & ~ok_alt & in_tol).sum())
+        ok_alt = ok_alt | in_tol
+    bad = miss & ~ok_alt
+    print("grad bar", json.dumps(stats))
+    log = os.environ.get("OIT_PARITY_LOG")
+    if log:
+        with open(log, "a") as f:
+            f.write(json.dumps(stats) + "\n")
+    assert not bad.any(), f"{name}: " + describe_bad(got, ref, bad, B)
+    assert frac >= min_strict, (name, stats)
+    return stats
+
+
 def decode_rect(rec):
     """rec [n][16] fp32 → (x0, y0, x1, y1) int arrays from the packed uint32 bits of q3.x/q3.y."""
     r = np.ascontiguousarray(rec, np.float32)

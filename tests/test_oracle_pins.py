@@ -399,6 +399,90 @@ def test_backward_matches_central_finite_differences(seed):
     assert checked > 100
 
 
+def _fd_check_scene(rows, sigma, cam, bg, gimg, h=1e-5):
+    """Central FD (fp64, decision sets frozen at θ: rows32 decides, rows64 carries the values) of
+    L = Σ g·C for every row field of every splat and for σ. Returns (grad, fd [n,80], dsig, fd_sig)."""
+    n = rows.shape[0]
+    idx = np.arange(n)
+    base = O.render(rows, sigma, idx, cam, bg, mode="brute")
+    grad, dsig, _ = O.backward(rows, sigma, idx, cam, bg, base["state"], gimg, mode="brute")
+
+    def loss(r64, sg):
+        return float((O.render(rows, sg, idx, cam, bg, mode="brute", rows64=r64)["image"] * gimg).sum())
+
+    r64 = rows.astype(np.float64)
+    fd = np.zeros_like(grad)
+    for i in range(n):
+        for f in FD_FIELDS:
+            rp, rm = r64.copy(), r64.copy()
+            step = h * max(1.0, abs(r64[i, f]))
+            rp[i, f] += step
+            rm[i, f] -= step
+            fd[i, f] = (loss(rp, sigma) - loss(rm, sigma)) / (2 * step)
+    fd_sig = (loss(r64, sigma + h) - loss(r64, sigma - h)) / (2 * h)
+    return grad, fd, dsig, fd_sig
+
+
+def _fd_ok(fd, an):
+    tol = 1e-7 if abs(an) < 1e-3 else 1e-4 * abs(an)
+    return abs(fd - an) <= max(tol, 1e-7)
+
+
+@pytest.mark.parametrize("kind", synth.BRANCH_KINDS)
+def test_clamp_branches_match_central_finite_differences(kind):
+    """FD pins of every piecewise branch of the chain (oracle ``chain_to_params``), which the
+    random FD scenes above never reach: the tan-fov clamp inside J with ∂J/∂t masked where clamped
+    (R13, Eq. 6), the colour clamp max(0, SH + 0.5) (R7, Eq. 4), v(r) ≤ 0 (the
+    v⁺ guard, R4, Eq. 1) and the ramp at d ≥ σ and within 2% below σ (Eq. 1). Per branch:
+    ≥ 20 nonzero (splat, field) gradients of splats on the branch agree with central FD at 1e-4
+    relative, every field and σ included; the gradients the branch masks are exactly 0 (and the FD
+    agrees)."""
+    hits = 0
+    masked = 0
+    near_sigma = 0
+    for seed in range(5):
+        sc = synth.scene_branch(kind, seed=seed)
+        cam, bg, sigma = sc.cams[0], sc.bg, sc.sigma
+        n = sc.n
+        idx = np.arange(n)
+        gimg = synth.rng(4321 + seed).uniform(-1, 1, (3, cam["height"], cam["width"]))
+        grad, fd, dsig, fd_sig = _fd_check_scene(sc.rows, sigma, cam, bg, gimg)
+        for i in range(n):
+            for f in FD_FIELDS:
+                assert _fd_ok(fd[i, f], grad[i, f]), (kind, seed, i, f, fd[i, f], grad[i, f])
+        assert abs(fd_sig - dsig) <= max(1e-4 * abs(dsig), 1e-7), (kind, seed, fd_sig, dsig)
+        fl = O.branch_flags(sc.rows.astype(np.float64), sigma, idx, cam)
+        if kind == "fov":
+            on = fl["clampx"] | fl["clampy"]
+        elif kind == "color":
+            on = fl["color"].any(axis=1)
+            for i in np.flatnonzero(on):       # a clamped channel's h gradient is exactly 0
+                for ch in np.flatnonzero(fl["color"][i]):
+                    cols = [28 + 3 * j + ch for j in range(16)]
+                    assert np.all(grad[i, cols] == 0.0) and np.all(np.abs(fd[i, cols]) <= 1e-7)
+                    masked += len(cols)
+        elif kind == "vneg":
+            on = fl["vneg"]
+            for i in np.flatnonzero(on):       # v⁺ = 0: no weight-SH gradient
+                assert np.all(grad[i, 12:28] == 0.0) and np.all(np.abs(fd[i, 12:28]) <= 1e-7)
+                masked += 16
+        else:
+            on = fl["ramp0"]
+            for i in np.flatnonzero(on):       # d ≥ σ: w = 0, no weight-SH gradient
+                assert np.all(grad[i, 12:28] == 0.0) and np.all(np.abs(fd[i, 12:28]) <= 1e-7)
+                masked += 16
+            tz = O.project_value(sc.rows.astype(np.float64), sigma, idx, cam)["tz"]
+            near_sigma += int(((tz < sigma) & (tz > 0.98 * sigma) & (np.abs(grad).max(axis=1) > 1e-6)).sum())
+        assert on.sum() >= 3, (kind, seed, int(on.sum()))
+        for i in np.flatnonzero(on):
+            hits += int((np.abs(grad[i, FD_FIELDS]) > 1e-6).sum())
+    assert hits >= 20, (kind, hits)
+    if kind in ("color", "vneg", "ramp"):
+        assert masked >= 20, (kind, masked)
+    if kind == "ramp":
+        assert near_sigma >= 5, near_sigma
+
+
 def test_backward_zero_when_q_zero_pixels_only_T_term():
     """R10: a pixel with Q = 0 gives no colour/weight gradient (∂C/∂c = ∂C/∂w = 0)."""
     cam = axis_cam()
