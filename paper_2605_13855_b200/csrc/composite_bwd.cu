@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(256) k_moments_pixel(DevCam cam, const float4*
 // gradients, the h/v rows are updated while streaming the coefficients, and the direction's
 // gradient is reduced to 3 floats. Phase 2 (geometry): μ', conic → Σ' → (Σ, J) → (q, s, μ).
 // Ordering the phases keeps the SH and the 3×3 geometry state from being live together.
-__global__ void __launch_bounds__(128, 4) k_epilogue(DevCam cam, const float4* __restrict__ rows,
+__global__ void __launch_bounds__(128, 3) k_epilogue(DevCam cam, const float4* __restrict__ rows,
                                                   const float* __restrict__ sigma_p, const int32_t* __restrict__ idx,
                                                   int32_t n_slots, const float4* __restrict__ rec,
                                                   const float4* __restrict__ acc2d, float scale,
@@ -411,35 +411,44 @@ __global__ void __launch_bounds__(128, 4) k_epilogue(DevCam cam, const float4* _
         gmu2 = (gr2 - rz * rdot) * idn;
       }
       // =============================== phase 2: geometry (Eq. 2, 5, 6) =====================
+      // In fp64: the chain conic → Σ' → (Σ, J) → (q, s, μ) sums large terms of opposite sign
+      // (e.g. ∂L/∂s_j = Σ_i ∂L/∂M_ij R_ij), which in fp32 can lose the small result entirely when the
+      // 2D moments themselves are accurate; a few hundred DFMA per slot, negligible next to the
+      // row traffic of this latency/HBM-bound kernel.
       const float4 q0 = rec[(size_t)k * kRec4 + 0];
       const float4 q1 = rec[(size_t)k * kRec4 + 1];
       const float4 q4 = rec[(size_t)k * kRec4 + 4];
-      const float nA = q0.z, nB = q0.w, nC = q1.x;
+      const double nA = q0.z, nB = q0.w, nC = q1.x;
       const float4 rb = r[1], rc = r[2];
-      const float W[3][3] = {{cam.R[0], cam.R[1], cam.R[2]}, {cam.R[3], cam.R[4], cam.R[5]}, {cam.R[6], cam.R[7], cam.R[8]}};
-      float t[3];
+      double W[3][3];
 #pragma unroll
-      for (int i = 0; i < 3; i++) t[i] = W[i][0] * mu0 + W[i][1] * mu1 + W[i][2] * mu2 + cam.t[i];
-      const float tz = t[2], itz = 1.0f / tz, itz2 = itz * itz;
-      const float limx = 1.3f * (0.5f * (float)cam.W / cam.fx), limy = 1.3f * (0.5f * (float)cam.H / cam.fy);
-      const float ux = t[0] * itz, uy = t[1] * itz;
+      for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) W[i][j] = (double)cam.R[3 * i + j];
+      double t[3];
+      cam_point_fp64(cam, mu0, mu1, mu2, t);
+      const double fx = cam.fx, fy = cam.fy;
+      const double tz = t[2], itz = 1.0 / tz, itz2 = itz * itz;
+      const double limx = 1.3 * (0.5 * (double)cam.W / fx), limy = 1.3 * (0.5 * (double)cam.H / fy);
+      const double ux = t[0] * itz, uy = t[1] * itz;
       const bool clx = ux > limx || ux < -limx, cly = uy > limy || uy < -limy;
-      const float uxc = fminf(limx, fmaxf(-limx, ux)), uyc = fminf(limy, fmaxf(-limy, uy));
-      const float J00 = cam.fx * itz, J02 = -cam.fx * uxc * itz, J11 = cam.fy * itz, J12 = -cam.fy * uyc * itz;
-      float T[2][3];
+      const double uxc = fmin(limx, fmax(-limx, ux)), uyc = fmin(limy, fmax(-limy, uy));
+      const double J00 = fx * itz, J02 = -fx * uxc * itz, J11 = fy * itz, J12 = -fy * uyc * itz;
+      double T[2][3];
 #pragma unroll
       for (int j = 0; j < 3; j++) {
         T[0][j] = J00 * W[0][j] + J02 * W[2][j];
         T[1][j] = J11 * W[1][j] + J12 * W[2][j];
       }
-      const float qn = sqrtf(rb.x * rb.x + rb.y * rb.y + rb.z * rb.z + rb.w * rb.w), iqn = 1.0f / qn;
-      const float qw = rb.x * iqn, qx = rb.y * iqn, qy = rb.z * iqn, qz = rb.w * iqn;
-      float Rq[3][3];
-      Rq[0][0] = 1.f - 2.f * (qy * qy + qz * qz); Rq[0][1] = 2.f * (qx * qy - qw * qz); Rq[0][2] = 2.f * (qx * qz + qw * qy);
-      Rq[1][0] = 2.f * (qx * qy + qw * qz); Rq[1][1] = 1.f - 2.f * (qx * qx + qz * qz); Rq[1][2] = 2.f * (qy * qz - qw * qx);
-      Rq[2][0] = 2.f * (qx * qz - qw * qy); Rq[2][1] = 2.f * (qy * qz + qw * qx); Rq[2][2] = 1.f - 2.f * (qx * qx + qy * qy);
-      const float s[3] = {rc.x, rc.y, rc.z};
-      float M[3][3], Sg[3][3];
+      const double q0w = rb.x, q0x = rb.y, q0y = rb.z, q0z = rb.w;
+      const double qn = sqrt(q0w * q0w + q0x * q0x + q0y * q0y + q0z * q0z), iqn = 1.0 / qn;
+      const double qw = q0w * iqn, qx = q0x * iqn, qy = q0y * iqn, qz = q0z * iqn;
+      double Rq[3][3];
+      Rq[0][0] = 1.0 - 2.0 * (qy * qy + qz * qz); Rq[0][1] = 2.0 * (qx * qy - qw * qz); Rq[0][2] = 2.0 * (qx * qz + qw * qy);
+      Rq[1][0] = 2.0 * (qx * qy + qw * qz); Rq[1][1] = 1.0 - 2.0 * (qx * qx + qz * qz); Rq[1][2] = 2.0 * (qy * qz - qw * qx);
+      Rq[2][0] = 2.0 * (qx * qz - qw * qy); Rq[2][1] = 2.0 * (qy * qz + qw * qx); Rq[2][2] = 1.0 - 2.0 * (qx * qx + qy * qy);
+      const double s[3] = {rc.x, rc.y, rc.z};
+      double M[3][3], Sg[3][3];
 #pragma unroll
       for (int i = 0; i < 3; i++)
 #pragma unroll
@@ -450,22 +459,22 @@ __global__ void __launch_bounds__(128, 4) k_epilogue(DevCam cam, const float4* _
         for (int j = 0; j < 3; j++) Sg[i][j] = M[i][0] * M[j][0] + M[i][1] * M[j][1] + M[i][2] * M[j][2];
       // the moments were accumulated with the spec offsets dx = x - μ'_spec; the true offsets are
       // dx - δx (δ = μ'_fp64 - μ'_spec, rec q4.zw): re-centre the moments exactly
-      const float dmx = q4.z, dmy = q4.w;
-      const float Od = m1.x, M1s = m1.y, M2s = m1.z;
-      const float M1 = M1s - dmx * Od, M2 = M2s - dmy * Od;
-      const float XX = m1.w - 2.f * dmx * M1s + dmx * dmx * Od;
-      const float XY = m2.x - dmy * M1s - dmx * M2s + dmx * dmy * Od;
-      const float YY = m2.y - 2.f * dmy * M2s + dmy * dmy * Od;
-      const float go = Od / op;
-      const float gmx = -(2.f * nA * M1 + nB * M2), gmy = -(nB * M1 + 2.f * nC * M2);
+      const double dmx = q4.z, dmy = q4.w;
+      const double Od = m1.x, M1s = m1.y, M2s = m1.z;
+      const double M1 = M1s - dmx * Od, M2 = M2s - dmy * Od;
+      const double XX = m1.w - 2.0 * dmx * M1s + dmx * dmx * Od;
+      const double XY = m2.x - dmy * M1s - dmx * M2s + dmx * dmy * Od;
+      const double YY = m2.y - 2.0 * dmy * M2s + dmy * dmy * Od;
+      const float go = (float)(Od / (double)op);
+      const double gmx = -(2.0 * nA * M1 + nB * M2), gmy = -(nB * M1 + 2.0 * nC * M2);
       // conic K = [[-2nA, -nB], [-nB, -2nC]]; dL/dK = -½[[XX, XY], [XY, YY]]; dL/dΣ' = -K dL/dK K
-      const float K00 = -2.f * nA, K01 = -nB, K11 = -2.f * nC;
-      const float A00 = 0.5f * (K00 * XX + K01 * XY), A01 = 0.5f * (K00 * XY + K01 * YY);
-      const float A10 = 0.5f * (K01 * XX + K11 * XY), A11 = 0.5f * (K01 * XY + K11 * YY);
-      const float G00 = A00 * K00 + A01 * K01, G01 = A00 * K01 + A01 * K11, G11 = A10 * K01 + A11 * K11;
+      const double K00 = -2.0 * nA, K01 = -nB, K11 = -2.0 * nC;
+      const double A00 = 0.5 * (K00 * XX + K01 * XY), A01 = 0.5 * (K00 * XY + K01 * YY);
+      const double A10 = 0.5 * (K01 * XX + K11 * XY), A11 = 0.5 * (K01 * XY + K11 * YY);
+      const double G00 = A00 * K00 + A01 * K01, G01 = A00 * K01 + A01 * K11, G11 = A10 * K01 + A11 * K11;
       // Σ' = T Σ Tᵀ + 0.3 I: dL/dΣ = Tᵀ G T, dL/dT = 2 G T Σ
-      const float G[2][2] = {{G00, G01}, {G01, G11}};
-      float gS[3][3], GT[2][3], gT[2][3];
+      const double G[2][2] = {{G00, G01}, {G01, G11}};
+      double gS[3][3], GT[2][3], gT[2][3];
 #pragma unroll
       for (int p = 0; p < 2; p++)
 #pragma unroll
@@ -477,68 +486,69 @@ __global__ void __launch_bounds__(128, 4) k_epilogue(DevCam cam, const float4* _
 #pragma unroll
       for (int p = 0; p < 2; p++)
 #pragma unroll
-        for (int j = 0; j < 3; j++) gT[p][j] = 2.f * (GT[p][0] * Sg[0][j] + GT[p][1] * Sg[1][j] + GT[p][2] * Sg[2][j]);
+        for (int j = 0; j < 3; j++) gT[p][j] = 2.0 * (GT[p][0] * Sg[0][j] + GT[p][1] * Sg[1][j] + GT[p][2] * Sg[2][j]);
       // T = J W -> J
-      const float gJ00 = gT[0][0] * W[0][0] + gT[0][1] * W[0][1] + gT[0][2] * W[0][2];
-      const float gJ02 = gT[0][0] * W[2][0] + gT[0][1] * W[2][1] + gT[0][2] * W[2][2];
-      const float gJ11 = gT[1][0] * W[1][0] + gT[1][1] * W[1][1] + gT[1][2] * W[1][2];
-      const float gJ12 = gT[1][0] * W[2][0] + gT[1][1] * W[2][1] + gT[1][2] * W[2][2];
-      float gt[3] = {0.f, 0.f, gtz_w};
-      gt[2] += -(cam.fx * gJ00 + cam.fy * gJ11) * itz2 + (gJ02 * cam.fx * uxc + gJ12 * cam.fy * uyc) * itz2;
-      if (!clx) {
-        gt[0] += -gJ02 * cam.fx * itz2;
-        gt[2] += gJ02 * cam.fx * t[0] * itz2 * itz;
+      const double gJ00 = gT[0][0] * W[0][0] + gT[0][1] * W[0][1] + gT[0][2] * W[0][2];
+      const double gJ02 = gT[0][0] * W[2][0] + gT[0][1] * W[2][1] + gT[0][2] * W[2][2];
+      const double gJ11 = gT[1][0] * W[1][0] + gT[1][1] * W[1][1] + gT[1][2] * W[1][2];
+      const double gJ12 = gT[1][0] * W[2][0] + gT[1][1] * W[2][1] + gT[1][2] * W[2][2];
+      double gt[3] = {0.0, 0.0, (double)gtz_w};
+      gt[2] += -(fx * gJ00 + fy * gJ11) * itz2 + (gJ02 * fx * uxc + gJ12 * fy * uyc) * itz2;
+      if (!clx) {  // ∂J02/∂t is masked where the tan-fov clamp holds u_x fixed (R13)
+        gt[0] += -gJ02 * fx * itz2;
+        gt[2] += gJ02 * fx * t[0] * itz2 * itz;
       }
       if (!cly) {
-        gt[1] += -gJ12 * cam.fy * itz2;
-        gt[2] += gJ12 * cam.fy * t[1] * itz2 * itz;
+        gt[1] += -gJ12 * fy * itz2;
+        gt[2] += gJ12 * fy * t[1] * itz2 * itz;
       }
       // μ' -> t
-      gt[0] += gmx * cam.fx * itz;
-      gt[1] += gmy * cam.fy * itz;
-      gt[2] -= (gmx * cam.fx * t[0] + gmy * cam.fy * t[1]) * itz2;
-      gmu0 += W[0][0] * gt[0] + W[1][0] * gt[1] + W[2][0] * gt[2];
-      gmu1 += W[0][1] * gt[0] + W[1][1] * gt[1] + W[2][1] * gt[2];
-      gmu2 += W[0][2] * gt[0] + W[1][2] * gt[1] + W[2][2] * gt[2];
+      gt[0] += gmx * fx * itz;
+      gt[1] += gmy * fy * itz;
+      gt[2] -= (gmx * fx * t[0] + gmy * fy * t[1]) * itz2;
+      const double gm0 = gmu0 + W[0][0] * gt[0] + W[1][0] * gt[1] + W[2][0] * gt[2];
+      const double gm1 = gmu1 + W[0][1] * gt[0] + W[1][1] * gt[1] + W[2][1] * gt[2];
+      const double gm2 = gmu2 + W[0][2] * gt[0] + W[1][2] * gt[1] + W[2][2] * gt[2];
       // Σ = M Mᵀ -> M -> (s, R)
-      float gM[3][3];
+      double gM[3][3];
 #pragma unroll
       for (int i = 0; i < 3; i++)
 #pragma unroll
         for (int j = 0; j < 3; j++)
-          gM[i][j] = 2.f * (gS[i][0] * M[0][j] + gS[i][1] * M[1][j] + gS[i][2] * M[2][j]);
-      float gs[3];
+          gM[i][j] = 2.0 * (gS[i][0] * M[0][j] + gS[i][1] * M[1][j] + gS[i][2] * M[2][j]);
+      double gs[3];
 #pragma unroll
       for (int j = 0; j < 3; j++) gs[j] = gM[0][j] * Rq[0][j] + gM[1][j] * Rq[1][j] + gM[2][j] * Rq[2][j];
-      float gR[3][3];
+      double gR[3][3];
 #pragma unroll
       for (int i = 0; i < 3; i++)
 #pragma unroll
         for (int j = 0; j < 3; j++) gR[i][j] = gM[i][j] * s[j];
-      float gq[4];
-      gq[0] = 2.f * (-qz * gR[0][1] + qy * gR[0][2] + qz * gR[1][0] - qx * gR[1][2] - qy * gR[2][0] + qx * gR[2][1]);
-      gq[1] = 2.f * (qy * gR[0][1] + qz * gR[0][2] + qy * gR[1][0] - 2.f * qx * gR[1][1] - qw * gR[1][2] +
-                     qz * gR[2][0] + qw * gR[2][1] - 2.f * qx * gR[2][2]);
-      gq[2] = 2.f * (-2.f * qy * gR[0][0] + qx * gR[0][1] + qw * gR[0][2] + qx * gR[1][0] + qz * gR[1][2] -
-                     qw * gR[2][0] + qz * gR[2][1] - 2.f * qy * gR[2][2]);
-      gq[3] = 2.f * (-2.f * qz * gR[0][0] - qw * gR[0][1] + qx * gR[0][2] + qw * gR[1][0] - 2.f * qz * gR[1][1] +
+      double gq[4];
+      gq[0] = 2.0 * (-qz * gR[0][1] + qy * gR[0][2] + qz * gR[1][0] - qx * gR[1][2] - qy * gR[2][0] + qx * gR[2][1]);
+      gq[1] = 2.0 * (qy * gR[0][1] + qz * gR[0][2] + qy * gR[1][0] - 2.0 * qx * gR[1][1] - qw * gR[1][2] +
+                     qz * gR[2][0] + qw * gR[2][1] - 2.0 * qx * gR[2][2]);
+      gq[2] = 2.0 * (-2.0 * qy * gR[0][0] + qx * gR[0][1] + qw * gR[0][2] + qx * gR[1][0] + qz * gR[1][2] -
+                     qw * gR[2][0] + qz * gR[2][1] - 2.0 * qy * gR[2][2]);
+      gq[3] = 2.0 * (-2.0 * qz * gR[0][0] - qw * gR[0][1] + qx * gR[0][2] + qw * gR[1][0] - 2.0 * qz * gR[1][1] +
                      qy * gR[1][2] + qx * gR[2][0] + qy * gR[2][1]);
-      const float qdot = qw * gq[0] + qx * gq[1] + qy * gq[2] + qz * gq[3];
+      const double qdot = qw * gq[0] + qx * gq[1] + qy * gq[2] + qz * gq[3];
       // ---- accumulate into the gradient row (+=, scaled) with vector atomics: concurrent views
       // (one stream each) may accumulate into the same rows ----
       float* g = reinterpret_cast<float*>(gr);
-      red_add_v4(g, scale * gmu0, scale * gmu1, scale * gmu2, scale * go);
-      red_add_v4(g + 4, scale * (gq[0] - qw * qdot) * iqn, scale * (gq[1] - qx * qdot) * iqn,
-                 scale * (gq[2] - qy * qdot) * iqn, scale * (gq[3] - qz * qdot) * iqn);
-      red_add_v4(g + 8, scale * gs[0], scale * gs[1], scale * gs[2], 0.f);
+      const double sc = scale;
+      red_add_v4(g, (float)(sc * gm0), (float)(sc * gm1), (float)(sc * gm2), scale * go);
+      red_add_v4(g + 4, (float)(sc * (gq[0] - qw * qdot) * iqn), (float)(sc * (gq[1] - qx * qdot) * iqn),
+                 (float)(sc * (gq[2] - qy * qdot) * iqn), (float)(sc * (gq[3] - qz * qdot) * iqn));
+      red_add_v4(g + 8, (float)(sc * gs[0]), (float)(sc * gs[1]), (float)(sc * gs[2]), 0.f);
       if (dL_dcov) {
         float* dc = dL_dcov + (size_t)k * 6;
-        atomicAdd(dc + 0, scale * gS[0][0]);
-        atomicAdd(dc + 1, scale * (gS[0][1] + gS[1][0]));
-        atomicAdd(dc + 2, scale * (gS[0][2] + gS[2][0]));
-        atomicAdd(dc + 3, scale * gS[1][1]);
-        atomicAdd(dc + 4, scale * (gS[1][2] + gS[2][1]));
-        atomicAdd(dc + 5, scale * gS[2][2]);
+        atomicAdd(dc + 0, (float)(sc * gS[0][0]));
+        atomicAdd(dc + 1, (float)(sc * (gS[0][1] + gS[1][0])));
+        atomicAdd(dc + 2, (float)(sc * (gS[0][2] + gS[2][0])));
+        atomicAdd(dc + 3, (float)(sc * gS[1][1]));
+        atomicAdd(dc + 4, (float)(sc * (gS[1][2] + gS[2][1])));
+        atomicAdd(dc + 5, (float)(sc * gS[2][2]));
       }
     }
   }
