@@ -35,11 +35,17 @@ METRIC = "fwd+bwd OIT render Mpix/s and splat-pixel evals/s vs active-set fracti
 UNIT = "Mpix/s"
 WORKLOAD = "C2 NeRF-synthetic-shaped: 300k splats, 100 views 800x800 per GPU, rho=0.2 clustered"
 
-# Algorithmic FP32 work per splat-pixel evaluation (FMA = 2 flops, MUFU = 1):
-# the per-pixel spec test costs F_TEST, a contributing pair adds F_CONTRIB.
+# Algorithmic FP32 work per tile-granular splat-pixel evaluation, as SURVEY.md §8(d) defines it
+# (FP32 instructions): the forward costs ≈18 per contributing and ≈9 per skipped
+# evaluation, the backward ≈36 per contributing and ≈10 per skipped one. Peak = 148 SMs × 128
+# FP32 lanes × 1965 MHz = 37.2 T instr/s (B200_PROFILING.md unit counts).
+FWD_I_SKIP, FWD_I_CONTRIB = 9, 18
+BWD_I_SKIP, BWD_I_CONTRIB = 10, 36
+FP32_PEAK_TINSTR = 148 * 128 * 1.965e9 / 1e12       # 37.2
+# the same work in FLOPs (FMA = 2, MUFU = 1), kept for comparison with round 1's accounting
 FWD_F_TEST, FWD_F_CONTRIB = 9, 17
 BWD_F_TEST, BWD_F_CONTRIB = 9, 32
-FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: 148 SMs × 128 FP32 lanes × FMA × 1965 MHz
+FP32_PEAK_TFLOPS = 2 * FP32_PEAK_TINSTR             # 74.4
 
 
 def _hbm_peak():
@@ -1063,16 +1069,34 @@ def build_line(args, world, res, results):
     value = mpix_per_s(res, world)
     evals = world * 256 * res["pairs"]
     f_c = res["contrib"] / max(res["tile_evals"], 1)
-    # roofline of the dominant kernel (fwd composite or bwd moments, both FP32-ALU bound)
-    fwd_flops = res["tile_evals"] * FWD_F_TEST + res["contrib"] * FWD_F_CONTRIB
-    bwd_flops = res["tile_evals"] * BWD_F_TEST + res["contrib"] * BWD_F_CONTRIB
+    # roofline of the dominant kernel (fwd composite or bwd moments, both FP32-ALU bound), in the
+    # FP32-instruction accounting of SURVEY §8(d)
+    contrib, skipped = res["contrib"], res["tile_evals"] - res["contrib"]
+    fwd_instr = contrib * FWD_I_CONTRIB + skipped * FWD_I_SKIP
+    bwd_instr = contrib * BWD_I_CONTRIB + skipped * BWD_I_SKIP
+    fwd_flops = res["tile_evals"] * FWD_F_TEST + contrib * FWD_F_CONTRIB
+    bwd_flops = res["tile_evals"] * BWD_F_TEST + contrib * BWD_F_CONTRIB
+    per_kernel = {}
+    for name, instr, flops_, kms_ in (("k_fwd_items", fwd_instr, fwd_flops, res["ser_fwd_ms"]),
+                                      ("k_moments", bwd_instr, bwd_flops, res["ser_bwd_ms"])):
+        a = instr / (kms_ * 1e-3) / 1e12
+        per_kernel[name] = {"algorithmic_instr_per_step": instr, "kernel_ms_per_step": kms_, "achieved": a,
+                            "frac": a / FP32_PEAK_TINSTR, "flops_per_step": flops_,
+                            "frac_flop_accounting": flops_ / (kms_ * 1e-3) / 1e12 / FP32_PEAK_TFLOPS}
     if res["ser_bwd_ms"] >= res["ser_fwd_ms"]:
-        kern, flops, kms, tkey = "k_moments (oit_composite_bwd a5)", bwd_flops, res["ser_bwd_ms"], "k_moments"
+        kern, tkey = "k_moments (oit_composite_bwd a5)", "k_moments"
+        pk = per_kernel["k_moments"]
     else:
-        kern, flops, kms = "k_fwd_items (oit_composite_fwd_loss a3+a4)", fwd_flops, res["ser_fwd_ms"]
+        kern = "k_fwd_items (oit_composite_fwd_loss a3+a4)"
         tkey = "k_fwd_items<1, 0, 2>" if args.targets == "u8" else "k_fwd_items<1, 0, 1>"
+        pk = per_kernel["k_fwd_items"]
     traffic, traffic_src = _ncu_traffic(tkey)
-    achieved = flops / (kms * 1e-3) / 1e12
+    achieved = pk["achieved"]
+    # step level: the whole timed step's tile-granular evaluations against the fwd+bwd FP32 ceiling
+    # at the measured f_c (37.2e12 / (54·f_c + 19·(1 − f_c)) evaluations/s)
+    fc = contrib / max(res["tile_evals"], 1)
+    ceiling = FP32_PEAK_TINSTR * 1e12 / ((FWD_I_CONTRIB + BWD_I_CONTRIB) * fc + (FWD_I_SKIP + BWD_I_SKIP) * (1 - fc))
+    step_evals_per_s = world * res["tile_evals"] / (res["ms"] * 1e-3)
     sweep = {}
     for rho, r in sorted(results.items(), reverse=True):
         sweep[str(rho)] = {"mpix_per_s": mpix_per_s(r, world), "ms_per_step": r["ms"],
@@ -1102,14 +1126,24 @@ def build_line(args, world, res, results):
                                        "step runs views on several streams concurrently",
                                "concurrent_fwd_composite": res["fwd_ms"], "concurrent_bwd_moments": res["bwd_ms"]},
         "segments_ms": {"train_views": res["train_ms"], "refresh": res["refresh_ms"]},
-        "roofline": {"kernel": kern, "bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
-                     "algorithmic_flops_per_step": flops, "kernel_ms_per_step": kms,
-                     "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
+        "roofline": {"kernel": kern, "bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TINSTR,
+                     "unit": "T FP32 instr/s", "frac": achieved / FP32_PEAK_TINSTR, "traffic": traffic,
+                     "algorithmic_instr_per_step": pk["algorithmic_instr_per_step"],
+                     "kernel_ms_per_step": pk["kernel_ms_per_step"],
+                     "instr_per_eval": {"fwd": [FWD_I_CONTRIB, FWD_I_SKIP], "bwd": [BWD_I_CONTRIB, BWD_I_SKIP],
+                                        "note": "[contributing, skipped] FP32 instructions per tile-granular "
+                                                "evaluation, SURVEY §8(d); evaluations and contributing pairs are "
+                                                "counted on the GPU (oit_composite_fwd_ex counters)"},
+                     "per_kernel": per_kernel,
+                     "step": {"evals_per_s": step_evals_per_s, "ceiling_evals_per_s": ceiling,
+                              "frac": step_evals_per_s / ceiling, "f_c": fc},
                      "timing": "the step's training views replayed on ONE stream (between L2 flushes), the kernel "
-                               "with its full-GPU persistent grid (concurrency 1); the timed step launches it "
-                               f"with concurrency = {args.streams} (smaller grids, views sharing the SMs)",
+                               "with its full-GPU persistent grid (concurrency 1), CUDA events on the launching "
+                               f"stream; the timed step launches it with concurrency = {args.streams} (smaller "
+                               "grids, views sharing the SMs)",
                      "traffic_source": traffic_src,
-                     "peak_source": "148 SMs x 128 FP32 lanes x 2 (FMA) x 1965 MHz (B200_PROFILING.md unit counts)"},
+                     "peak_source": "148 SMs x 128 FP32 lanes x 1965 MHz = 37.2 T instr/s (B200_PROFILING.md unit "
+                                    "counts; MEASURED_PEAKS.json has no FP32 entry)"},
         "clocks": res["clocks"], "gpu_launches": res["launches"] * args.steps,
         "sweep": sweep,
     }

@@ -109,13 +109,16 @@ int oit_project_cull(const oit_scene* scene, const oit_camera* cam, const int32_
 /* ---------------------------------------------------------------------------------------
  * a2  oit_bin_tiles — Alg. 2 l.3-6 (CreateTiles, DuplicateWithKeys, SortByKeys "only by tile
  * ID", IdentifyTileRanges). One (tile, slot) pair per tile of each slot's
- * rectangle that passes the exact tile–ellipse test (DESIGN.md §3 step 12b), grouped by tile: pair_slot[tile_offsets[t] .. tile_offsets[t+1]) lists the slots
- * covering tile t. No depth key; the order inside a tile is unspecified (R15).
+ * rectangle that passes the exact tile–ellipse test (DESIGN.md §3 step 12b), grouped by tile:
+ * pair_slot[tile_offsets[t] .. tile_offsets[t+1]) lists the slots covering tile t in ascending
+ * slot order (no depth key; the stable counting sort's order, R15), so the lists — and the
+ * forward's summation order — are bit-identical run to run and to the oracle's.
  * tile_offsets has n_tiles+1 entries; *d_n_pairs (device int64) receives the total pair count
  * (if it exceeds pair_capacity, pair_slot holds only a prefix and the caller must re-call).
- * Scratch: ws of oit_bin_workspace_bytes(cam) bytes.
+ * Scratch: ws of oit_bin_workspace_bytes(cam, pair_capacity) bytes (≈ 4·pair_capacity + 8·n_tiles;
+ * 0 for a null camera or a negative capacity).
  * --------------------------------------------------------------------------------------- */
-size_t oit_bin_workspace_bytes(const oit_camera* cam);
+size_t oit_bin_workspace_bytes(const oit_camera* cam, int64_t pair_capacity);
 int oit_bin_tiles(const oit_camera* cam, const float* rec, const int32_t* tiles_per_slot,
                   int32_t n_slots, int32_t* pair_slot, int64_t pair_capacity,
                   int32_t* tile_offsets, int64_t* d_n_pairs, void* ws, size_t ws_bytes,

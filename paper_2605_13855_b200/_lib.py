@@ -82,7 +82,7 @@ def lib() -> C.CDLL:
             "oit_status_string": (C.c_char_p, [C.c_int]),
             "oit_num_tiles": (i32, [cam_p]),
             "oit_project_cull": (C.c_int, [scene_p, cam_p, vp, i32, vp, vp, vp]),
-            "oit_bin_workspace_bytes": (sz, [cam_p]),
+            "oit_bin_workspace_bytes": (sz, [cam_p, i64]),
             "oit_bin_tiles": (C.c_int, [cam_p, vp, vp, i32, vp, i64, vp, vp, vp, sz, vp]),
             "oit_fwd_workspace_bytes": (sz, [cam_p, i64]),
             "oit_composite_fwd": (C.c_int, [cam_p, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
@@ -169,8 +169,8 @@ def oit_project_cull(rows, sigma, cam, idx, rec, tiles_per_slot, stream=None):
                                   _ptr(tiles_per_slot), _stream(stream)), "oit_project_cull")
 
 
-def oit_bin_workspace_bytes(cam) -> int:
-    return int(lib().oit_bin_workspace_bytes(C.byref(camera(cam))))
+def oit_bin_workspace_bytes(cam, pair_capacity: int) -> int:
+    return int(lib().oit_bin_workspace_bytes(C.byref(camera(cam)), int(pair_capacity)))
 
 
 def oit_bin_tiles(cam, rec, tiles_per_slot, n_slots, pair_slot, tile_offsets, n_pairs, ws, stream=None):

@@ -45,6 +45,8 @@ inline cudaStream_t S(oit_stream_t s) { return reinterpret_cast<cudaStream_t>(s)
 
 // nb of scan blocks supported by the 3-phase scan (4096 blocks of 4096 elements)
 constexpr int64_t kMaxScan = 4096LL * 4096LL;
+// pair positions are int32 on the device, and the backward's quadrant lists index 4·capacity
+constexpr int64_t kMaxPairs = 0x7fffffffLL / 4;
 
 }  // namespace
 
@@ -75,9 +77,9 @@ int oit_project_cull(const oit_scene* scene, const oit_camera* cam, const int32_
   return launch_status();
 }
 
-size_t oit_bin_workspace_bytes(const oit_camera* cam) {
-  if (!cam) return 0;
-  return bin_ws_bytes(oit_num_tiles(cam));
+size_t oit_bin_workspace_bytes(const oit_camera* cam, int64_t pair_capacity) {
+  if (!cam || pair_capacity < 0) return 0;
+  return bin_ws_bytes(oit_num_tiles(cam), pair_capacity);
 }
 
 int oit_bin_tiles(const oit_camera* cam, const float* rec, const int32_t* tiles_per_slot, int32_t n_slots,
@@ -87,7 +89,8 @@ int oit_bin_tiles(const oit_camera* cam, const float* rec, const int32_t* tiles_
   if (n_slots > 0 && (!rec || !tiles_per_slot)) return OIT_EINVAL;
   if (pair_capacity > 0 && !pair_slot) return OIT_EINVAL;
   if (!shape_ok(cam) || oit_num_tiles(cam) > kMaxScan) return OIT_ESHAPE;
-  if (ws_bytes < oit_bin_workspace_bytes(cam)) return OIT_ECAPACITY;
+  if (pair_capacity > kMaxPairs) return OIT_ESHAPE;
+  if (ws_bytes < oit_bin_workspace_bytes(cam, pair_capacity)) return OIT_ECAPACITY;
   launch_bin(dev_cam(cam), rec, tiles_per_slot, n_slots, pair_slot, pair_capacity, tile_offsets, d_n_pairs, nullptr,
              ws, S(stream));
   return launch_status();
@@ -114,6 +117,7 @@ int oit_composite_fwd_ex(const oit_camera* cam, const float* rec, const int32_t*
   if (route && !base_out) return OIT_EINVAL;
   if (!route && !ws) return OIT_EINVAL;
   if (!shape_ok(cam)) return OIT_ESHAPE;
+  if (pair_capacity > kMaxPairs) return OIT_ESHAPE;
   if (!route && ws_bytes < oit_fwd_workspace_bytes(cam, pair_capacity)) return OIT_ECAPACITY;
   launch_composite_fwd(dev_cam(cam, bg_host), rec, pair_slot, tile_offsets, pair_capacity, base, route, image, state,
                        base_out, S(stream), d_counters, ws, concurrency);
@@ -130,6 +134,7 @@ int oit_composite_fwd_loss(const oit_camera* cam, const float* rec, const int32_
   if (l != 0 && l != 1) return OIT_EINVAL;
   if (pair_capacity > 0 && (!rec || !pair_slot)) return OIT_EINVAL;
   if (!shape_ok(cam)) return OIT_ESHAPE;
+  if (pair_capacity > kMaxPairs) return OIT_ESHAPE;
   if (ws_bytes < oit_fwd_workspace_bytes(cam, pair_capacity) ||
       bwd_ws_bytes < oit_bwd_workspace_bytes(cam, n_slots, pair_capacity))
     return OIT_ECAPACITY;
@@ -226,6 +231,7 @@ int oit_composite_bwd_ex(const oit_scene* scene, const oit_camera* cam, const in
   if (n_slots > 0 && (!idx || !rec || !grad)) return OIT_EINVAL;
   if (pair_capacity > 0 && !pair_slot) return OIT_EINVAL;
   if (!shape_ok(cam) || n_slots > scene->n || oit_num_tiles(cam) > kMaxScan) return OIT_ESHAPE;
+  if (pair_capacity > kMaxPairs) return OIT_ESHAPE;
   if (ws_bytes < oit_bwd_workspace_bytes(cam, n_slots, pair_capacity)) return OIT_ECAPACITY;
   const int32_t nt = oit_num_tiles(cam);
   DevCam dc = dev_cam(cam, bg_host);
@@ -254,6 +260,7 @@ int oit_composite_bwd_perpixel(const oit_scene* scene, const oit_camera* cam, co
   if (n_slots > 0 && (!idx || !rec || !grad)) return OIT_EINVAL;
   if (pair_capacity > 0 && !pair_slot) return OIT_EINVAL;
   if (!shape_ok(cam) || n_slots > scene->n || oit_num_tiles(cam) > kMaxScan) return OIT_ESHAPE;
+  if (pair_capacity > kMaxPairs) return OIT_ESHAPE;
   if (ws_bytes < oit_bwd_workspace_bytes(cam, n_slots, pair_capacity)) return OIT_ECAPACITY;
   const int32_t nt = oit_num_tiles(cam);
   DevCam dc = dev_cam(cam, bg_host);
@@ -300,7 +307,7 @@ static ScoreWs score_layout(void* ws, const oit_camera* cam, int32_t n_active, i
   w.state = cv.take<float>((size_t)nt * kTilePx * 5);
   w.coef4 = cv.take<float>((size_t)nt * kTilePx * 4);
   w.coefa = cv.take<float>((size_t)nt * kTilePx);
-  w.bin_ws = cv.take<char>(bin_ws_bytes(nt));
+  w.bin_ws = cv.take<char>(bin_ws_bytes(nt, cap));
   w.fwd_ws = cv.take<char>(fwd_ws_bytes(nt, cap));
   w.bwd_ws = cv.take<char>(bwd_ws_bytes(nt, n_score, cap));
   w.dssim_ws = cv.take<char>(dssim_bytes(cam));
@@ -326,6 +333,7 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
     return OIT_EINVAL;
   if ((n_active > 0 && !active_idx) || (n_score > 0 && (!score_idx || !score_grad))) return OIT_EINVAL;
   if (n_active > scene->n || n_score > scene->n) return OIT_ESHAPE;
+  if (pair_capacity > kMaxPairs) return OIT_ESHAPE;
   for (int s = 0; s < n_sub; s++) {
     int j = views_host[s];
     if (j < 0 || j >= n_views || !targets_host[j] || !cam_ok(&cams_host[j])) return OIT_EINVAL;
@@ -443,7 +451,7 @@ static size_t reconcile_layout(void* ws, const oit_camera* cam, int32_t n, int64
   *tps = cv.take<int32_t>((size_t)n + 1);
   *pairs = cv.take<int32_t>((size_t)cap + 1);
   *offs = cv.take<int32_t>((size_t)nt + 1);
-  *bin_ws = cv.take<char>(bin_ws_bytes(nt));
+  *bin_ws = cv.take<char>(bin_ws_bytes(nt, cap));
   return cv.off;
 }
 
@@ -460,6 +468,7 @@ int oit_reconcile_cache(const oit_scene* scene, const oit_camera* cam, const int
   if (n_fold < 0 || n_unfold < 0 || pair_capacity < 0) return OIT_EINVAL;
   if ((n_fold > 0 && !fold_idx) || (n_unfold > 0 && !unfold_idx)) return OIT_EINVAL;
   if (!shape_ok(cam) || n_fold + n_unfold > 2 * scene->n || oit_num_tiles(cam) > kMaxScan) return OIT_ESHAPE;
+  if (pair_capacity > kMaxPairs) return OIT_ESHAPE;
   const int32_t n = n_fold + n_unfold;
   if (ws_bytes < oit_reconcile_workspace_bytes(cam, n, pair_capacity)) return OIT_ECAPACITY;
   int32_t *idx, *tps, *pairs, *offs;

@@ -19,7 +19,7 @@ void launch_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, void* tmp
                            int32_t* out2 = nullptr);
 
 // bin.cu — a2
-size_t bin_ws_bytes(int32_t n_tiles);
+size_t bin_ws_bytes(int32_t n_tiles, int64_t capacity);
 void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_slot, int32_t n_slots,
                 int32_t* pair_slot, int64_t capacity, int32_t* tile_offsets, int64_t* d_n_pairs,
                 int64_t* d_max_pairs, void* ws, cudaStream_t st);

@@ -31,7 +31,18 @@ def test_json_line_has_the_contract_keys(monkeypatch):
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert k in r, k
     assert r["frac"] == pytest.approx(r["achieved"] / r["peak"])
-    assert r["bound"] == "alu" and r["unit"] == "TFLOP/s"
+    assert r["bound"] == "alu" and r["unit"] == "T FP32 instr/s"
+    # the §8(d) accounting, recomputable from the line: instructions = contributing·18 + skipped·9
+    # (fwd), contributing·36 + skipped·10 (bwd); the dominant kernel is the slower one
+    c, sk = res["contrib"], res["tile_evals"] - res["contrib"]
+    fwd = r["per_kernel"]["k_fwd_items"]
+    assert fwd["algorithmic_instr_per_step"] == c * 18 + sk * 9
+    assert fwd["frac"] == pytest.approx((c * 18 + sk * 9) / (res["ser_fwd_ms"] * 1e-3) / 37.2e12, rel=1e-3)
+    assert r["per_kernel"]["k_moments"]["algorithmic_instr_per_step"] == c * 36 + sk * 10
+    assert r["achieved"] == pytest.approx(fwd["achieved"])     # ser_fwd_ms > ser_bwd_ms here
+    fc = c / res["tile_evals"]
+    assert r["step"]["ceiling_evals_per_s"] == pytest.approx(37.2e12 / (54 * fc + 19 * (1 - fc)), rel=1e-3)
+    assert r["step"]["frac"] == pytest.approx(res["tile_evals"] / 16e-3 / r["step"]["ceiling_evals_per_s"])
     e = line["e2e"]
     assert e["unit"] == "Mpix/s" and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert e["value"] == pytest.approx(100 * 800 * 800 / 19e-3 / 1e6)
