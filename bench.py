@@ -479,22 +479,24 @@ class Workload:
                                     self.counts[2:3], self.upd_ws)
 
     def kernel_launches(self):
-        """Our kernels launched by one step (per the launch structure of each C-ABI call)."""
+        """Our kernels launched by one step (per the launch structure of each C-ABI call; checked
+        against the ncu launch list of the bench command in profiles/)."""
         nt = self.n_tiles
         nw = (self.n + 31) // 32
         a, s = self.n_act, self.n_ina
         proj = lambda n: 1 if n > 0 else 0  # noqa: E731
-        binn = lambda n: (1 if n > 0 else 0) + scan_kernels(nt) + 1  # noqa: E731
-        fwd = 2                                            # fused item builder, k_fwd_items
-        # coef | quadrant count, scan, quadrant scatter, fused item builder, moments, epilogue
-        bwd = lambda n: 1 + ((5 + scan_kernels(4 * nt)) if n > 0 else 0)  # noqa: E731
-        lossk = 3 if self.loss == "dssim" else 0   # resolve + 2 SSIM stencil passes (L1/L2: fused in k_coef)
+        # k_bin_expand<0> (n > 0), the tile scan, k_bin_expand<1>, k_tile_sort (n > 0)
+        binn = lambda n: (2 if n > 0 else 0) + scan_kernels(nt) + 1  # noqa: E731
+        fwd = 3                                            # item histogram + emission, k_fwd_items
+        # k_quad_bin, item histogram + emission, k_moments, k_epilogue (none for an empty slot list)
+        bwd = lambda n: 5 if n > 0 else 0  # noqa: E731
+        lossk = 4 if self.loss == "dssim" else 0   # resolve + 2 SSIM stencil passes + k_coef
         # training views with L1/L2: a4 fused into the forward's epilogue (no k_coef launch)
-        train = self.V * (proj(a) + binn(a) + fwd + bwd(a) - (1 if self.loss in ("l1", "l2") else 0) + lossk)
-        refresh = 1
+        train = self.V * (proj(a) + binn(a) + fwd + bwd(a) + lossk)
+        refresh = 1                                        # k_fps
         if s > 0:
-            refresh += self.S * (proj(a) + binn(a) + fwd + 1 + lossk + proj(s) + binn(s) + (bwd(s) - 1))
-            refresh += 1 + 1 + 3 * scan_kernels(nw) + 1
+            refresh += self.S * (proj(a) + binn(a) + fwd + lossk + proj(s) + binn(s) + bwd(s))
+            refresh += 1 + 1 + 3 * scan_kernels(nw) + 1    # k_update_bits, k_popc3, 3 scans, k_emit3
         return train + refresh
 
 

@@ -39,7 +39,8 @@
  *
  * Entry points: a1 oit_project_cull; a2 oit_bin_tiles; a3 oit_composite_fwd(_ex), a3+a4 fused
  * oit_composite_fwd_loss; a4 oit_loss_grad; a5/a6 oit_composite_bwd(_ex), the per-pixel ablation
- * oit_composite_bwd_perpixel; a7 oit_select_views, oit_score_subsample; a8 oit_update_active_set;
+ * oit_composite_bwd_perpixel; a7 oit_select_views, oit_score_subsample; a8 oit_update_active_set
+ * (= oit_score_activeness + oit_apply_activeness, the halves the sharded refresh calls);
  * NEXT-1 oit_active_set_delta, oit_reconcile_cache; NEXT-2 oit_adam_step; NEXT-3
  * oit_loss_dssim; plus the *_workspace_bytes queries, oit_num_tiles, oit_status_string.
  */
@@ -300,6 +301,27 @@ int oit_update_active_set(const float* score_grad, const int32_t* score_idx, int
                           uint32_t* active_bits, int32_t* active_idx, int32_t* d_n_active,
                           int32_t* newly_frozen, int32_t* d_n_frozen, int32_t* newly_active,
                           int32_t* d_n_activated, void* ws, size_t ws_bytes, oit_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * a8 split in two halves for the view-sharded refresh (reduce-scatter the score
+ * rows by row range, threshold locally, all-gather the membership bits, recompact everywhere).
+ * oit_update_active_set(…) ≡ oit_score_activeness(…) then oit_apply_activeness(…), bit for bit.
+ *
+ * oit_score_activeness: Eq. 8 with the ∃ reading (R18) per score row, by the fp32 update spec of
+ * bit j of row_bits [⌈n_rows/32⌉] (out; bits past n_rows are 0) ⟺ some per-attribute
+ * L2 norm of score_grad[j] (μ, q, s, o, h, v) exceeds eps_host (same order). n_rows may be 0.
+ *
+ * oit_apply_activeness: applies the row bits of rows 0 … n_score−1 to the splats score_idx[j]
+ * (distinct) in mode FRESH / MONOTONE (R21), then recompacts as oit_update_active_set (same
+ * outputs, same workspace: oit_update_workspace_bytes(n_total)).
+ * Errors as oit_update_active_set.
+ * --------------------------------------------------------------------------------------- */
+int oit_score_activeness(const float* score_grad, int32_t n_rows, const float eps_host[6], uint32_t* row_bits,
+                         oit_stream_t stream);
+int oit_apply_activeness(const uint32_t* row_bits, const int32_t* score_idx, int32_t n_score, int32_t mode,
+                         int32_t n_total, uint32_t* active_bits, int32_t* active_idx, int32_t* d_n_active,
+                         int32_t* newly_frozen, int32_t* d_n_frozen, int32_t* newly_active,
+                         int32_t* d_n_activated, void* ws, size_t ws_bytes, oit_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------
  * NEXT-1  lazy pre-render reconciliation (§4.1: "delay the update of the pre-rendered image

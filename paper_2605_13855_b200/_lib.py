@@ -110,6 +110,8 @@ def lib() -> C.CDLL:
             "oit_loss_dssim": (C.c_int, [cam_p, vp, vp, C.c_float, vp, vp, vp, sz, vp]),
             "oit_adam_step": (C.c_int, [vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.POINTER(AdamCfg), vp]),
             "oit_update_active_set": (C.c_int, [vp, vp, i32, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+            "oit_score_activeness": (C.c_int, [vp, i32, vp, vp, vp]),
+            "oit_apply_activeness": (C.c_int, [vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -124,7 +126,8 @@ EXPORTED = ["oit_status_string", "oit_num_tiles", "oit_project_cull", "oit_bin_w
             "oit_select_views", "oit_score_workspace_bytes", "oit_score_subsample", "oit_update_workspace_bytes",
             "oit_update_active_set", "oit_delta_workspace_bytes", "oit_active_set_delta",
             "oit_reconcile_workspace_bytes", "oit_reconcile_cache", "oit_adam_step",
-            "oit_dssim_workspace_bytes", "oit_loss_dssim", "oit_composite_bwd_perpixel"]
+            "oit_dssim_workspace_bytes", "oit_loss_dssim", "oit_composite_bwd_perpixel", "oit_score_activeness",
+            "oit_apply_activeness"]
 
 
 # ------------------------------------------------------------------ marshalling helpers ---
@@ -287,6 +290,24 @@ def oit_update_active_set(score_grad, score_idx, eps, mode: str, n_total: int, a
                                        _ptr(active_idx), _ptr(n_active), _ptr(newly_frozen), _ptr(n_frozen),
                                        _ptr(newly_active), _ptr(n_activated), _ptr(ws), int(ws.numel()),
                                        _stream(stream)), "oit_update_active_set")
+
+
+def oit_score_activeness(score_grad, n_rows: int, eps, row_bits, stream=None):
+    """a8, first half: Eq. 8 per score row → row bitmask [⌈n_rows/32⌉] (int32/uint32 tensor)."""
+    e = (C.c_float * 6)(*[float(x) for x in eps])
+    _check(lib().oit_score_activeness(_ptr(score_grad), int(n_rows), e, _ptr(row_bits), _stream(stream)),
+           "oit_score_activeness")
+
+
+def oit_apply_activeness(row_bits, score_idx, mode: str, n_total: int, active_bits, active_idx, n_active,
+                         newly_frozen=None, n_frozen=None, newly_active=None, n_activated=None, ws=None,
+                         stream=None):
+    """a8, second half: the row bits applied to the splats score_idx, then recompaction."""
+    _check(lib().oit_apply_activeness(_ptr(row_bits), _ptr(score_idx), int(score_idx.numel()),
+                                      1 if mode == "monotone" else 0, int(n_total), _ptr(active_bits),
+                                      _ptr(active_idx), _ptr(n_active), _ptr(newly_frozen), _ptr(n_frozen),
+                                      _ptr(newly_active), _ptr(n_activated), _ptr(ws), int(ws.numel()),
+                                      _stream(stream)), "oit_apply_activeness")
 
 
 def oit_delta_workspace_bytes(n_total: int) -> int:

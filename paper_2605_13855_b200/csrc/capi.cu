@@ -388,7 +388,31 @@ int oit_update_active_set(const float* score_grad, const int32_t* score_idx, int
   if ((newly_frozen && !d_n_frozen) || (newly_active && !d_n_activated)) return OIT_EINVAL;
   if (n_score > n_total || ((int64_t)n_total + 31) / 32 > kMaxScan) return OIT_ESHAPE;
   if (ws_bytes < oit_update_workspace_bytes(n_total)) return OIT_ECAPACITY;
-  launch_update(score_grad, score_idx, n_score, eps_host, mode, n_total, active_bits, active_idx, d_n_active,
+  launch_update(score_grad, nullptr, score_idx, n_score, eps_host, mode, n_total, active_bits, active_idx, d_n_active,
+                newly_frozen, d_n_frozen, newly_active, d_n_activated, ws, S(stream));
+  return launch_status();
+}
+
+int oit_score_activeness(const float* score_grad, int32_t n_rows, const float eps_host[6], uint32_t* row_bits,
+                         oit_stream_t stream) {
+  if (!eps_host || n_rows < 0) return OIT_EINVAL;
+  if (n_rows > 0 && (!score_grad || !row_bits)) return OIT_EINVAL;
+  launch_row_activeness(score_grad, n_rows, eps_host, row_bits, S(stream));
+  return launch_status();
+}
+
+int oit_apply_activeness(const uint32_t* row_bits, const int32_t* score_idx, int32_t n_score, int32_t mode,
+                         int32_t n_total, uint32_t* active_bits, int32_t* active_idx, int32_t* d_n_active,
+                         int32_t* newly_frozen, int32_t* d_n_frozen, int32_t* newly_active, int32_t* d_n_activated,
+                         void* ws, size_t ws_bytes, oit_stream_t stream) {
+  if ((mode != 0 && mode != 1) || n_total < 0 || n_score < 0 || !d_n_active || !ws) return OIT_EINVAL;
+  if (n_total > 0 && (!active_bits || !active_idx)) return OIT_EINVAL;
+  if (n_score > 0 && (!row_bits || !score_idx)) return OIT_EINVAL;
+  if ((newly_frozen && !d_n_frozen) || (newly_active && !d_n_activated)) return OIT_EINVAL;
+  if (n_score > n_total || ((int64_t)n_total + 31) / 32 > kMaxScan) return OIT_ESHAPE;
+  if (ws_bytes < oit_update_workspace_bytes(n_total)) return OIT_ECAPACITY;
+  const float no_eps[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  launch_update(nullptr, row_bits, score_idx, n_score, no_eps, mode, n_total, active_bits, active_idx, d_n_active,
                 newly_frozen, d_n_frozen, newly_active, d_n_activated, ws, S(stream));
   return launch_status();
 }

@@ -378,7 +378,7 @@ void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pa
     // (16-18), fewer when views run concurrently; items are claimed dynamically
 #define OIT_FWD2(B, K, L)                                                                                   \
   do {                                                                                                      \
-    static const int occ = resident_ctas(k_fwd_items<B, K, L>, kFwdThreads);                                \
+    const int occ = resident_ctas<k_fwd_items<B, K, L>>(kFwdThreads);                                       \
     k_fwd_items<B, K, L><<<sm_count() * persistent_ctas(occ, concurrency), kFwdThreads, 0, st>>>(           \
         cam, r4, pair_slot, tile_offsets, capacity, items, n_items, counter, tile_nch, done, partial, base,  \
         image, state, cnt, chunk_len, fl);                                                                  \

@@ -7,7 +7,7 @@
 // the light ones fill the tail. Items of one tile are contiguous, so chunk k of the tile whose
 // first item is f sits at f + k. An item is int4 (tile, chunk, first pair, end pair), so a consumer
 // reaches its pair range with one load. Two grid-wide kernels: a bucket histogram, then the
-// emission (fused into one launch with a grid barrier when the grid is co-resident).
+// emission.
 #include "kernels.h"
 
 namespace oit {
@@ -178,62 +178,6 @@ void launch_quad_bin(const DevCam& cam, const float* rec, const int32_t* pair_sl
 }
 
 
-// Fused variant for small tile counts (grid ≤ SM count, hence co-resident): the histogram, a
-// software grid barrier and the emission in one launch. g[66] is the barrier counter.
-__global__ void __launch_bounds__(256) k_items_fused(const int32_t* __restrict__ offs, const int32_t* __restrict__ qlen,
-                                                     int n_tiles, int64_t capacity,
-                                                     int chunk, int empty_items, int32_t* __restrict__ g,
-                                                     int4* __restrict__ items, int32_t* __restrict__ n_items,
-                                                     int32_t* __restrict__ tile_nch) {
-  __shared__ int s_cnt[kNB];
-  __shared__ int s_off[kNB];
-  if (threadIdx.x < kNB) s_cnt[threadIdx.x] = 0;
-  __syncthreads();
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  int nch = 0, b = 0, js = 0, je = 0;
-  if (t < n_tiles) {
-    tile_len(offs, qlen, t, capacity, chunk, empty_items, nch, b, js, je);
-    if (tile_nch) tile_nch[t] = nch;
-    if (nch) atomicAdd(&s_cnt[b], nch);
-  }
-  __syncthreads();
-  if (threadIdx.x < kNB && s_cnt[threadIdx.x]) atomicAdd(g + threadIdx.x, s_cnt[threadIdx.x]);
-  // grid barrier (all blocks are resident: gridDim.x ≤ number of SMs)
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    atomicAdd(g + 2 * kNB, 1);
-    while (atomicAdd(g + 2 * kNB, 0) < (int)gridDim.x) {
-    }
-    int off = 0;
-    for (int bb = kNB - 1; bb >= 0; bb--) {  // descending: longest lists first
-      s_off[bb] = off;
-      off += atomicAdd(g + bb, 0);
-    }
-    if (blockIdx.x == 0) *n_items = off;
-  }
-  __syncthreads();
-  if (nch) {
-    const int lane = threadIdx.x & 31;
-    const unsigned peers = __match_any_sync(__activemask(), b);
-    const int leader = __ffs(peers) - 1;
-    int before = 0, total = 0;
-    unsigned m = peers;
-    while (m) {
-      const int src = __ffs(m) - 1;
-      m &= m - 1;
-      const int v = __shfl_sync(peers, nch, src);
-      if (src < lane) before += v;
-      total += v;
-    }
-    int base = 0;
-    if (lane == leader) base = atomicAdd(g + kNB + b, total);
-    base = __shfl_sync(peers, base, leader);
-    const int pos = s_off[b] + base + before;
-    for (int c = 0; c < nch; c++) items[pos + c] = make_int4(t, c, js + c * chunk, min(je, js + (c + 1) * chunk));
-  }
-}
-
 size_t items_bytes(int32_t n_tiles, int64_t capacity, int chunk) {
   const int64_t max_items = capacity / chunk + n_tiles + 1;
   return align_up((size_t)max_items * sizeof(int4)) + align_up(16) + align_up((size_t)(n_tiles + 1) * 4) +
@@ -246,11 +190,8 @@ void launch_build_items(const int32_t* tile_offsets, const int32_t* qlen, int n_
                         int empty_items, int4* items, int32_t* n_items, int32_t* tile_nch, int32_t* g, cudaStream_t st) {
   const int blocks = (n_tiles + 255) / 256;
   cudaMemsetAsync(g, 0, (2 * kNB + 2) * sizeof(int32_t), st);
-  if (blocks <= sm_count()) {
-    k_items_fused<<<blocks, 256, 0, st>>>(tile_offsets, qlen, n_tiles, capacity, chunk, empty_items, g, items, n_items,
-                                          tile_nch);
-    return;
-  }
+  // two grid-wide kernels, no software grid barrier: co-residency of a grid is not guaranteed
+  // while other streams' persistent kernels hold the SMs
   k_items_hist<<<blocks, 256, 0, st>>>(tile_offsets, qlen, n_tiles, capacity, chunk, empty_items, g);
   k_items_emit<<<blocks, 256, 0, st>>>(tile_offsets, qlen, n_tiles, capacity, chunk, empty_items, g, items, n_items,
                                        tile_nch);

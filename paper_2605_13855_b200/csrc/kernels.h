@@ -1,6 +1,7 @@
 // kernels.h — internal launchers of liboit (host side). The C-ABI in capi.cu validates
 // arguments, carves workspaces and calls these; every launcher is asynchronous on `st`.
 #pragma once
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -41,14 +42,39 @@ void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pa
                           const int32_t* tile_offsets, int64_t capacity, const float* base, const uint8_t* route,
                           float* image, float* state, float* base_out, cudaStream_t st, int64_t* counters, void* ws,
                           int concurrency = 1, FwdLoss fl = FwdLoss());
-// Persistent-grid CTAs per SM for `full` (the kernel's resident maximum) when `concurrency` calls
-// run at once on different streams: about 2·full/concurrency, at least 2, at most full.
-template <class Kernel>
-inline int resident_ctas(Kernel kernel, int threads) {  // CTAs of `kernel` one SM holds (≥ 1)
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, 0) != cudaSuccess || n < 1) n = 1;
+// Launch-shape facts of the current device (SM count; CTAs of a kernel one SM holds), looked up
+// once per device id: hardware constants, not state — a multi-device process gets each device's
+// own value, and concurrent first calls only race to store the same number.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+inline int sm_count() {
+  static std::atomic<int> cache[kMaxDevices];
+  const int dev = current_device();
+  int n = (dev >= 0 && dev < kMaxDevices) ? cache[dev].load(std::memory_order_relaxed) : 0;
+  if (n == 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    if (dev >= 0 && dev < kMaxDevices) cache[dev].store(n, std::memory_order_relaxed);
+  }
   return n;
 }
+// CTAs of kernel K (at `threads` per CTA, no dynamic smem) one SM of the current device holds (≥ 1).
+template <auto K>
+inline int resident_ctas(int threads) {
+  static std::atomic<int> cache[kMaxDevices];
+  const int dev = current_device();
+  int n = (dev >= 0 && dev < kMaxDevices) ? cache[dev].load(std::memory_order_relaxed) : 0;
+  if (n == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, K, threads, 0) != cudaSuccess || n < 1) n = 1;
+    if (dev >= 0 && dev < kMaxDevices) cache[dev].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
+// Persistent-grid CTAs per SM for `full` (the kernel's resident maximum) when `concurrency` calls
+// run at once on different streams: about 2·full/concurrency, at least 2, at most full.
 inline int persistent_ctas(int full, int concurrency) {
   const int c = concurrency < 1 ? 1 : concurrency;
   int k = (2 * full + c - 1) / c;
@@ -66,17 +92,6 @@ void launch_build_items(const int32_t* tile_offsets, const int32_t* qlen, int n_
 // within a list unspecified), tq[capacity] and qcount[4·n_tiles] scratch, tmp = scan_tmp_bytes(4·n_tiles)
 void launch_quad_bin(const DevCam& cam, const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
                      int64_t capacity, int32_t* qlen, int32_t* qslot, cudaStream_t st);
-
-inline int sm_count() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
 
 // composite_bwd.cu — a4 coefficients, a5 moments, a6 epilogue
 size_t bwd_ws_bytes(int32_t n_tiles, int32_t n_slots, int64_t capacity);
@@ -122,10 +137,12 @@ void launch_adam(const float* grad, const int32_t* active_idx, int32_t n_cap, co
                  const float lr[8], float beta1, float beta2, float eps, cudaStream_t st);
 void launch_delta(const uint32_t* old_bits, const uint32_t* bits, int32_t n_total, int32_t* fold, int32_t* d_n_fold,
                   int32_t* unfold, int32_t* d_n_unfold, void* ws, cudaStream_t st);
-void launch_update(const float* score_grad, const int32_t* score_idx, int32_t n_score, const float eps[6],
-                   int32_t mode, int32_t n_total, uint32_t* bits, int32_t* active_idx, int32_t* d_n_active,
-                   int32_t* frozen, int32_t* d_n_frozen, int32_t* activated, int32_t* d_n_activated, void* ws,
-                   cudaStream_t st);
+void launch_row_activeness(const float* score_grad, int32_t n_rows, const float eps[6], uint32_t* row_bits,
+                           cudaStream_t st);
+void launch_update(const float* score_grad, const uint32_t* row_bits, const int32_t* score_idx, int32_t n_score,
+                   const float eps[6], int32_t mode, int32_t n_total, uint32_t* bits, int32_t* active_idx,
+                   int32_t* d_n_active, int32_t* frozen, int32_t* d_n_frozen, int32_t* activated,
+                   int32_t* d_n_activated, void* ws, cudaStream_t st);
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 

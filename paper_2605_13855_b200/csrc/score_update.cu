@@ -124,12 +124,7 @@ __device__ __forceinline__ float group_norm(const float* g, int lo, int n) {
   return __fsqrt_rn(ss);
 }
 
-__global__ void __launch_bounds__(256) k_update_bits(const float4* __restrict__ score_grad,
-                                                     const int32_t* __restrict__ score_idx, int32_t n_score,
-                                                     Eps6 eps, int32_t mode, const uint32_t* __restrict__ old_bits,
-                                                     uint32_t* __restrict__ bits) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n_score) return;
+__device__ __forceinline__ bool row_active(const float4* __restrict__ score_grad, int j, const Eps6& eps) {
   float g[80];
 #pragma unroll
   for (int q = 0; q < 20; q++) {
@@ -142,6 +137,41 @@ __global__ void __launch_bounds__(256) k_update_bits(const float4* __restrict__ 
   act |= group_norm(g, kO, 1) > eps.e[3];
   act |= group_norm(g, kH, 48) > eps.e[4];
   act |= group_norm(g, kV, 16) > eps.e[5];
+  return act;
+}
+
+// Eq. 8 per score row → row bitmask (one ballot per warp of 32 consecutive rows; no atomics).
+__global__ void __launch_bounds__(256) k_row_activeness(const float4* __restrict__ score_grad, int32_t n_rows,
+                                                        Eps6 eps, uint32_t* __restrict__ row_bits) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool act = j < n_rows && row_active(score_grad, j, eps);
+  const unsigned word = __ballot_sync(0xffffffffu, act);
+  if ((threadIdx.x & 31) == 0 && j < ((n_rows + 31) & ~31)) row_bits[j >> 5] = word;
+}
+
+// The row bits applied to the scored splats' membership bits (FRESH / MONOTONE).
+__global__ void __launch_bounds__(256) k_apply_bits(const uint32_t* __restrict__ row_bits,
+                                                    const int32_t* __restrict__ score_idx, int32_t n_score,
+                                                    int32_t mode, const uint32_t* __restrict__ old_bits,
+                                                    uint32_t* __restrict__ bits) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_score) return;
+  const bool act = (row_bits[j >> 5] >> (j & 31)) & 1u;
+  const int i = score_idx[j];
+  const uint32_t m = 1u << (i & 31);
+  const bool oldb = (old_bits[i >> 5] & m) != 0u;
+  const bool nb = mode == 1 ? (oldb && act) : act;
+  if (nb) atomicOr(bits + (i >> 5), m);
+  else atomicAnd(bits + (i >> 5), ~m);
+}
+
+__global__ void __launch_bounds__(256) k_update_bits(const float4* __restrict__ score_grad,
+                                                     const int32_t* __restrict__ score_idx, int32_t n_score,
+                                                     Eps6 eps, int32_t mode, const uint32_t* __restrict__ old_bits,
+                                                     uint32_t* __restrict__ bits) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_score) return;
+  const bool act = row_active(score_grad, j, eps);
   int i = score_idx[j];
   uint32_t m = 1u << (i & 31);
   bool oldb = (old_bits[i >> 5] & m) != 0u;
@@ -218,10 +248,20 @@ size_t update_ws_bytes(int32_t n_total) {
   return align_up(nw * 4) + 3 * align_up(nw * 4) + 3 * align_up((nw + 1) * 4) + scan_tmp_bytes(nw);
 }
 
-void launch_update(const float* score_grad, const int32_t* score_idx, int32_t n_score, const float eps[6],
-                   int32_t mode, int32_t n_total, uint32_t* bits, int32_t* active_idx, int32_t* d_n_active,
-                   int32_t* frozen, int32_t* d_n_frozen, int32_t* activated, int32_t* d_n_activated, void* ws,
-                   cudaStream_t st) {
+void launch_row_activeness(const float* score_grad, int32_t n_rows, const float eps[6], uint32_t* row_bits,
+                           cudaStream_t st) {
+  if (n_rows <= 0) return;
+  Eps6 e;
+  for (int a = 0; a < 6; a++) e.e[a] = eps[a];
+  k_row_activeness<<<(n_rows + 255) / 256, 256, 0, st>>>(reinterpret_cast<const float4*>(score_grad), n_rows, e,
+                                                          row_bits);
+}
+
+// score_grad != nullptr: Eq. 8 on the rows (fused); else row_bits carries the rows' activeness.
+void launch_update(const float* score_grad, const uint32_t* row_bits, const int32_t* score_idx, int32_t n_score,
+                   const float eps[6], int32_t mode, int32_t n_total, uint32_t* bits, int32_t* active_idx,
+                   int32_t* d_n_active, int32_t* frozen, int32_t* d_n_frozen, int32_t* activated,
+                   int32_t* d_n_activated, void* ws, cudaStream_t st) {
   const int nw = (n_total + 31) / 32;
   Carve cv(ws);
   uint32_t* old_bits = cv.take<uint32_t>(nw);
@@ -233,11 +273,16 @@ void launch_update(const float* score_grad, const int32_t* score_idx, int32_t n_
   int32_t* on = cv.take<int32_t>(nw + 1);
   void* tmp = cv.take<char>(scan_tmp_bytes(nw));
   if (nw > 0) cudaMemcpyAsync(old_bits, bits, sizeof(uint32_t) * nw, cudaMemcpyDeviceToDevice, st);
-  Eps6 e;
-  for (int a = 0; a < 6; a++) e.e[a] = eps[a];
-  if (n_score > 0)
-    k_update_bits<<<(n_score + 255) / 256, 256, 0, st>>>(reinterpret_cast<const float4*>(score_grad), score_idx,
-                                                          n_score, e, mode, old_bits, bits);
+  if (n_score > 0) {
+    if (score_grad) {
+      Eps6 e;
+      for (int a = 0; a < 6; a++) e.e[a] = eps[a];
+      k_update_bits<<<(n_score + 255) / 256, 256, 0, st>>>(reinterpret_cast<const float4*>(score_grad), score_idx,
+                                                            n_score, e, mode, old_bits, bits);
+    } else {
+      k_apply_bits<<<(n_score + 255) / 256, 256, 0, st>>>(row_bits, score_idx, n_score, mode, old_bits, bits);
+    }
+  }
   const int wb = (nw + 255) / 256;
   if (nw > 0) k_popc3<<<wb, 256, 0, st>>>(old_bits, bits, nw, n_total, ca, cf, cn);
   launch_exclusive_scan(ca, oa, nw, tmp, st);

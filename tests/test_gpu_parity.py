@@ -361,6 +361,26 @@ def test_update_active_set_bitexact(mode):
     assert np.array_equal(fro[:c[1]].cpu().numpy(), ref_fro)
     assert np.array_equal(new[:c[2]].cpu().numpy(), ref_new)
     assert 0 < len(ref_act) < n
+    # the two halves the sharded refresh calls (Eq. 8 per row → row bits; apply + recompact) give
+    # the same bits, lists and counts; with the rows split over 3 "ranks" and the bits concatenated
+    from paper_2605_13855_b200 import dist as D
+    for world in (1, 3):
+        chunk = D.score_rows_per_rank(len(score_idx), world)
+        rows = np.zeros((chunk * world, 80), np.float32)
+        rows[:len(score_idx)] = sgrad
+        rb = torch.zeros(chunk // 32 * world, dtype=torch.int32, device=DEV)
+        for r in range(world):
+            valid = max(0, min(chunk, len(score_idx) - r * chunk))
+            L.oit_score_activeness(_t(rows[r * chunk:(r + 1) * chunk]), valid, eps, rb[r * chunk // 32:(r + 1) * chunk // 32])
+        bits2 = _t(bits0.view(np.int32))
+        cnt2 = torch.zeros(3, dtype=torch.int32, device=DEV)
+        L.oit_apply_activeness(rb, _t(score_idx), mode, n, bits2, act, cnt2[0:1], fro, cnt2[1:2], new, cnt2[2:3], ws)
+        c2 = cnt2.cpu().numpy()
+        assert np.array_equal(bits2.cpu().numpy().view(np.uint32), ref_bits)
+        assert np.array_equal(c2, c)
+        assert np.array_equal(act[:c2[0]].cpu().numpy(), ref_act)
+        assert np.array_equal(fro[:c2[1]].cpu().numpy(), ref_fro)
+        assert np.array_equal(new[:c2[2]].cpu().numpy(), ref_new)
 
 
 # ------------------------------------------------------------------ edge cases ------------

@@ -15,7 +15,7 @@ echo "launch list rc=$?"
 KS=("$@")
 if [ ${#KS[@]} -eq 0 ]; then
   KS=('k_fwd_items<\(bool\)1, \(bool\)0, \(int\)2>' 'oit::k_moments\(' 'oit::k_epilogue' 'oit::k_project'
-      'k_bin_expand<\(bool\)1>' 'oit::k_quad_bin' 'oit::k_items_fused')
+      'k_bin_expand<\(bool\)1>' 'oit::k_quad_bin' 'oit::k_items_emit' 'oit::k_tile_sort')
 fi
 i=0
 for k in "${KS[@]}"; do
