@@ -9,6 +9,8 @@
 //   4. k_tile_sort:         each tile's segment is put in ascending slot order (R15: the stable
 //                           counting sort's order, which makes the lists — and hence the forward's
 //                           fp32 summation order — identical run to run and to the oracle's).
+//                           Skipped (sorted = false) for lists only the backward reads: its moments
+//                           are order-free per (splat, tile) and are summed with atomics anyway.
 // Integer-only, latency/atomic-bound: ≈ 4 B written + 2 atomics per pair, then one smem sort
 // per tile (4 B read + 4 B written per pair).
 #include <algorithm>
@@ -108,24 +110,28 @@ __global__ void __launch_bounds__(128) k_bin_expand(const float4* __restrict__ r
 
 // ------------------------------------------------------------------ per-tile slot sort ----
 // The scatter leaves each tile's segment as an arbitrary interleaving of ascending runs (one per
-// warp step); the segment's values are distinct slot indices in [0, n_slots). A persistent grid
-// restores ascending order:
-//  * warp phase — tiles of L ≤ 256 entries: one warp, a bitonic network held in REGISTERS
-//    (element i = r·32 + lane in register r of lane `lane`: partners at distance j < 32 are
-//    exchanged with shuffles, j ≥ 32 are register pairs of the same lane; padded with INT_MAX
-//    to 32·E, E ≤ 8) — no barrier, and the unrolled network stays small for the i-cache;
-//  * CTA phase — longer tiles: a counting sort over a bitmap of the slot range kept in shared
-//    memory (one bit per slot of the window): set the segment's bits, scan the popcounts of the
-//    words between the segment's min and max (each thread owns a contiguous run of words), and
-//    each thread writes its words' set bits in order at its prefix — O(L + range/32) per tile,
-//    no comparison network. The bitmap is cleared as it is read, so it stays zero between tiles.
-//    With n_slots ≤ kSortBits the window is the whole slot range and the sort is in place; larger
-//    ranges take windows of kSortBits slots over [min, max], reading the segment from a copy in
-//    `tmp` (same offsets) while the output is written in place.
-constexpr int kSortThreads = 256;
-constexpr int kSortWarpMax = 256;                              // warp phase: E ≤ 8 registers per lane
-constexpr int kSortWords = 4096;                               // bitmap words (16 KB)
-constexpr int kSortBits = kSortWords * 32;                     // slots per window (131,072)
+// warp step); the segment's values are distinct slot indices in [0, n_slots). k_tile_sort restores
+// ascending order with one CTA per tile (every tile sorts independently, so a long list never
+// queues behind others; the many empty tiles exit at once):
+//  * short lists, warp 0 alone: a bitonic network held in REGISTERS (element i = r·32 + lane in
+//    register r: partners at distance j < 32 exchanged with shuffles, j ≥ 32 register pairs of the
+//    same lane; padded with INT_MAX) for L ≤ 64 — and up to 256 when the slot range is large —, or
+//    a counting sort over a bitmap of the ≤ 2^16-slot range for 64 < L ≤ 128;
+//  * longer: the counting sort by the whole CTA over a bitmap of the slot range (≤ 45 KB, windows
+//    beyond), so a long list's chain is split 4 ways.
+// Bitmap counting sort: set the segment's bits (windowed over [min, max] of the segment when the
+// slot range exceeds one window), every thread sums the popcounts of its consecutive bitmap words,
+// one scan gives each thread its output position, and each thread writes its words' set bits in
+// order — O(L/threads + range/(32·threads)) per thread, no comparison network. The words of the
+// range are dealt out evenly (`per` consecutive words per thread), thread t's i-th word at physical
+// i·threads + t, so the ordered sweeps are bank-conflict free; the bitmap is cleared as it is read.
+// With several windows the segment is read from a copy in `tmp` (same offsets) while the output is
+// written in place.
+constexpr int kSortWarps = 4;
+constexpr int kSortThreads = 32 * kSortWarps;
+constexpr int kSortNetMax = 64;                                // bitonic up to E = 2 registers per lane
+constexpr int kSortWarpMax = 128;                              // longer lists: the whole CTA
+constexpr int kSortWords = 2048;                               // bitmap words per CTA (8 KB): 2^16 slots
 
 // Ascending bitonic sort of the warp's 32·E register-resident elements (i = r·32 + lane).
 template <int E>
@@ -177,128 +183,171 @@ __device__ __forceinline__ void seg_range(const int32_t* offs, int t, int64_t ca
   L = (int)(e - b);
 }
 
-// Block-wide min and max (all threads get both); red: 2·(threads/32) ints of scratch.
-__device__ __forceinline__ void block_min_max(int& mn, int& mx, int* red) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+// A sorting group: one warp (NT = 32) or the whole CTA (NT = kSortThreads); `red` is CTA scratch.
+template <int NT>
+struct SortGroup {
+  int r;  // rank in the group
+  int* red;
+  __device__ __forceinline__ void sync() const {
+    if (NT == 32) __syncwarp(); else __syncthreads();
   }
-  if (lane == 0) { red[wid] = mn; red[kSortThreads / 32 + wid] = mx; }
-  __syncthreads();
-  mn = red[0];
-  mx = red[kSortThreads / 32];
+  __device__ __forceinline__ int max_all(int v) const {
 #pragma unroll
-  for (int w = 1; w < kSortThreads / 32; w++) {
-    mn = min(mn, red[w]);
-    mx = max(mx, red[kSortThreads / 32 + w]);
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (NT == 32) return v;
+    __syncthreads();
+    if ((r & 31) == 0) red[r >> 5] = v;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < NT / 32; w++) v = max(v, red[w]);
+    return v;
+  }
+  // exclusive prefix of v over the group, and the total
+  __device__ __forceinline__ int scan(int v, int& total) const {
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if ((r & 31) >= o) inc += y;
+    }
+    if (NT == 32) {
+      total = __shfl_sync(0xffffffffu, inc, 31);
+      return inc - v;
+    }
+    __syncthreads();
+    if ((r & 31) == 31) red[r >> 5] = inc;
+    __syncthreads();
+    int pre = 0;
+    total = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; w++) {
+      if (w < (r >> 5)) pre += red[w];
+      total += red[w];
+    }
+    return pre + inc - v;
+  }
+};
+
+// Bitmap layout: thread t owns the `per` consecutive logical words t·per … t·per+per−1 (fixed for
+// a window); logical word t·per + i sits at physical i·NT + t.
+template <int NT>
+__device__ __forceinline__ int bm_phys(int w, int per) {
+  const int t = w / per;
+  return (w - t * per) * NT + t;
+}
+
+// Apply f(i, seg[i]) to the elements i ≡ r (mod NT), eight loads in flight per thread (long lists
+// are read from L2: the loads, not the bitmap, set the time).
+template <int NT, class F>
+__device__ __forceinline__ void for_each_batched(const int32_t* seg, int L, int r, F f) {
+  for (int i0 = r; i0 < L; i0 += 8 * NT) {
+    int v[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] = i0 + NT * k < L ? seg[i0 + NT * k] : -1;
+#pragma unroll
+    for (int k = 0; k < 8; k++)
+      if (v[k] >= 0) f(i0 + NT * k, v[k]);
   }
 }
 
-// Emit the set bits of bitmap words [wlo, whi] (window origin w0) in ascending order to
-// out[done …], clearing the words; returns the number of bits emitted. Block-wide.
-__device__ __forceinline__ int bitmap_emit(unsigned* bm, int wlo, int whi, int64_t w0, int done, int32_t* out,
-                                           int* red) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int nwords = whi - wlo + 1;
-  const int per = (nwords + kSortThreads - 1) / kSortThreads;
-  const int q0 = wlo + tid * per, q1 = min(q0 + per, whi + 1);
-  int tot = 0;
-  for (int q = q0; q < q1; q++) tot += __popc(bm[q]);
-  int inc = tot;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += y;
-  }
-  __syncthreads();  // red is reused
-  if (lane == 31) red[wid] = inc;
-  __syncthreads();
-  int pos = done + inc - tot, all = 0;
-#pragma unroll
-  for (int w = 0; w < kSortThreads / 32; w++) {
-    if (w < wid) pos += red[w];
-    all += red[w];
-  }
-  for (int q = q0; q < q1; q++) {
-    unsigned m = bm[q];
+// Emit the set bits of logical bitmap words [0, nw) (window origin w0) in ascending order to
+// seg[done …], clearing them; returns the number emitted.
+template <int NT>
+__device__ __forceinline__ int bitmap_emit(const SortGroup<NT>& g, unsigned* bm, int per, int nw, int w0, int done,
+                                           int32_t* seg) {
+  const int q0 = g.r * per, n = max(0, min(per, nw - q0));
+  int cnt = 0;
+  for (int i = 0; i < n; i++) cnt += __popc(bm[i * NT + g.r]);
+  int total;
+  int pos = done + g.scan(cnt, total);
+  for (int i = 0; i < n; i++) {
+    unsigned m = bm[i * NT + g.r];
     if (!m) continue;
-    bm[q] = 0u;
-    const int64_t base = w0 + 32 * (int64_t)q;
+    bm[i * NT + g.r] = 0u;
+    const int base = w0 + 32 * (q0 + i);
     while (m) {
       const int bit = __ffs(m) - 1;
       m &= m - 1;
-      out[pos++] = (int)(base + bit);
+      seg[pos++] = base + bit;
     }
   }
-  return all;
+  return total;
+}
+
+// Counting sort of one segment through the group's bitmap of kBits slots (zero on entry and exit).
+template <int NT>
+__device__ __forceinline__ void bitmap_sort(const SortGroup<NT>& g, unsigned* bm, int kBits, int32_t* seg,
+                                            int32_t* tmp_seg, int L, int n_slots) {
+  if (n_slots <= kBits) {  // one window [0, n_slots): a single read of the segment
+    const int per = ((n_slots + 31) / 32 + NT - 1) / NT;
+    int mx = 0;
+    for_each_batched<NT>(seg, L, g.r, [&](int, int x) {
+      atomicOr(bm + bm_phys<NT>(x >> 5, per), 1u << (x & 31));
+      mx = max(mx, x);
+    });
+    mx = g.max_all(mx);  // (its barrier also orders the bit sets before the sweep)
+    g.sync();
+    bitmap_emit<NT>(g, bm, per, (mx >> 5) + 1, 0, 0, seg);
+    g.sync();
+    return;
+  }
+  int mn = 0x7fffffff, mx = -1;
+  for_each_batched<NT>(seg, L, g.r, [&](int i, int x) {  // range of the segment, and a copy to read from
+    mn = min(mn, x);
+    mx = max(mx, x);
+    tmp_seg[i] = x;
+  });
+  mn = -g.max_all(-mn);
+  mx = g.max_all(mx);
+  g.sync();
+  int done = 0;
+  for (int w0 = mn; w0 <= mx; w0 += kBits) {
+    const int nw = (min(mx - w0, kBits - 1) >> 5) + 1;
+    const int per = (nw + NT - 1) / NT;
+    for_each_batched<NT>(tmp_seg, L, g.r, [&](int, int x) {
+      const int d = x - w0;
+      if (d >= 0 && d < kBits) atomicOr(bm + bm_phys<NT>(d >> 5, per), 1u << (d & 31));
+    });
+    g.sync();
+    done += bitmap_emit<NT>(g, bm, per, nw, w0, done, seg);
+    g.sync();
+  }
 }
 
 __global__ void __launch_bounds__(kSortThreads) k_tile_sort(const int32_t* __restrict__ offs, int n_tiles,
-                                                            int64_t capacity, int32_t n_slots,
+                                                            int64_t capacity, int32_t n_slots, int bm_words,
                                                             int32_t* __restrict__ pair_slot,
                                                             int32_t* __restrict__ tmp) {
-  __shared__ unsigned bm[kSortWords];
-  __shared__ int red[2 * (kSortThreads / 32)];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  // ---- warp phase: L ≤ 256 ----
-  const int gw = blockIdx.x * (kSortThreads / 32) + wid, nw = gridDim.x * (kSortThreads / 32);
-  for (int t = gw; t < n_tiles; t += nw) {
-    int64_t b;
-    int L;
-    seg_range(offs, t, capacity, b, L);
-    if (L <= 1 || L > kSortWarpMax) continue;
-    int32_t* seg = pair_slot + b;
-    if (L <= 32) warp_sort_segment<1>(seg, L, lane);
-    else if (L <= 64) warp_sort_segment<2>(seg, L, lane);
-    else if (L <= 128) warp_sort_segment<4>(seg, L, lane);
-    else warp_sort_segment<8>(seg, L, lane);
+  extern __shared__ unsigned bm[];  // bm_words words (≥ kSortWords)
+  __shared__ int red[kSortWarps];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int t = blockIdx.x;  // one CTA per tile: the decisions below are CTA-uniform
+  int64_t b;
+  int L;
+  seg_range(offs, t, capacity, b, L);
+  int32_t* seg = pair_slot + b;
+  // short lists: warp 0 alone — a bitonic network in registers, or (slot range ≤ one warp
+  // bitmap) the warp's bitmap counting sort, whichever is cheaper for the list length
+  const bool small_range = n_slots <= 32 * kSortWords;
+  if (L <= (small_range ? kSortNetMax : 2 * kSortWarpMax)) {
+    if (tid < 32) {
+      if (L > 1 && L <= 32) warp_sort_segment<1>(seg, L, lane);
+      else if (L > 32 && L <= 64) warp_sort_segment<2>(seg, L, lane);
+      else if (L > 64 && L <= 128) warp_sort_segment<4>(seg, L, lane);
+      else if (L > 128) warp_sort_segment<8>(seg, L, lane);
+    }
+    return;
   }
-  // ---- CTA phase: L > 256, bitmap counting sort ----
-  for (int i = tid; i < kSortWords; i += kSortThreads) bm[i] = 0u;
+  if (small_range && L <= kSortWarpMax) {
+    if (tid >= 32) return;
+    for (int i = lane; i < kSortWords; i += 32) bm[i] = 0u;
+    __syncwarp();
+    bitmap_sort<32>(SortGroup<32>{lane, red}, bm, 32 * kSortWords, seg, tmp + b, L, n_slots);
+    return;
+  }
+  for (int i = tid; i < bm_words; i += kSortThreads) bm[i] = 0u;
   __syncthreads();
-  const bool one_window = n_slots <= kSortBits;
-  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-    int64_t b;
-    int L;
-    seg_range(offs, t, capacity, b, L);
-    if (L <= kSortWarpMax) continue;  // CTA-uniform
-    int32_t* seg = pair_slot + b;
-    int mn = 0x7fffffff, mx = -1;
-    if (one_window) {
-      for (int i = tid; i < L; i += kSortThreads) {
-        const int x = seg[i];
-        atomicOr(bm + (x >> 5), 1u << (x & 31));
-        mn = min(mn, x);
-        mx = max(mx, x);
-      }
-      block_min_max(mn, mx, red);  // (its barrier also orders the atomics before the scan)
-      bitmap_emit(bm, mn >> 5, mx >> 5, 0, 0, seg, red);
-      __syncthreads();             // the bitmap is clear again; red is free
-      continue;
-    }
-    int32_t* src = tmp + b;
-    for (int i = tid; i < L; i += kSortThreads) {
-      const int x = seg[i];
-      src[i] = x;
-      mn = min(mn, x);
-      mx = max(mx, x);
-    }
-    block_min_max(mn, mx, red);
-    int done = 0;
-    for (int64_t w0 = mn; w0 <= mx; w0 += kSortBits) {
-      __syncthreads();
-      for (int i = tid; i < L; i += kSortThreads) {
-        const int64_t d = (int64_t)src[i] - w0;
-        if (d >= 0 && d < kSortBits) atomicOr(bm + (d >> 5), 1u << (d & 31));
-      }
-      __syncthreads();
-      const int64_t top = min((int64_t)mx - w0, (int64_t)kSortBits - 1);
-      done += bitmap_emit(bm, 0, (int)(top >> 5), w0, done, seg, red);
-    }
-    __syncthreads();
-  }
+  bitmap_sort<kSortThreads>(SortGroup<kSortThreads>{tid, red}, bm, 32 * bm_words, seg, tmp + b, L, n_slots);
 }
 
 size_t bin_ws_bytes(int32_t n_tiles, int64_t capacity) {
@@ -308,7 +357,7 @@ size_t bin_ws_bytes(int32_t n_tiles, int64_t capacity) {
 
 void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_slot, int32_t n_slots,
                 int32_t* pair_slot, int64_t capacity, int32_t* tile_offsets, int64_t* d_n_pairs,
-                int64_t* d_max_pairs, void* ws, cudaStream_t st) {
+                int64_t* d_max_pairs, void* ws, cudaStream_t st, bool sorted) {
   int n_tiles = cam.TX * cam.TY;
   Carve cv(ws);
   int32_t* counts = cv.take<int32_t>(n_tiles + 1);
@@ -325,10 +374,12 @@ void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_sl
   launch_exclusive_scan(counts, tile_offsets, n_tiles, tmp, st, counts);
   k_bin_expand<true><<<blocks, 128, 0, st>>>(r4, tiles_per_slot, n_slots, cam.TX, cam.W, cam.H, counts, pair_slot, capacity,
                                              tile_offsets, n_tiles, d_n_pairs, d_max_pairs);
-  if (n_slots > 0 && capacity > 0) {
-    // persistent: a warp per ~2 tiles, at most 4 CTAs per SM (views run concurrently)
-    const int ctas = std::max(1, std::min((n_tiles + 15) / 16, sm_count() * 4));
-    k_tile_sort<<<ctas, kSortThreads, 0, st>>>(tile_offsets, n_tiles, capacity, n_slots, pair_slot, sort_tmp);
+  if (sorted && n_slots > 0 && capacity > 0) {
+    // one CTA per tile (most exit at once: empty or short lists); the bitmap covers the slot range
+    // in one window up to 368,640 slots (45 KB: dynamic + static stay under the 48 KB default), windows beyond
+    const int words = std::min(std::max(kSortWords, (n_slots + 31) / 32 + 127) / 128 * 128, 11520);
+    k_tile_sort<<<n_tiles, kSortThreads, sizeof(unsigned) * words, st>>>(tile_offsets, n_tiles, capacity, n_slots,
+                                                                         words, pair_slot, sort_tmp);
   }
 }
 

@@ -368,7 +368,9 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
     }
     // back-propagate L_j to the scored splats (R20)
     launch_project(dc, scene->rows, scene->sigma, score_idx, n_score, w.rec_s, w.tps_s, st);
-    launch_bin(dc, w.rec_s, w.tps_s, n_score, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st);
+    // (the scored lists feed the backward only: no per-tile slot sort, see bin.cu)
+    launch_bin(dc, w.rec_s, w.tps_s, n_score, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st,
+               false);
     launch_composite_bwd(dc, scene->rows, scene->sigma, score_idx, n_score, w.rec_s, w.pairs, w.offs, pair_capacity,
                          w.coef4, w.coefa, scale, score_grad, dL_dsigma, nullptr, w.bwd_ws, st, nullptr, nullptr, 0,
                          concurrency);

@@ -23,7 +23,7 @@ void launch_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, void* tmp
 size_t bin_ws_bytes(int32_t n_tiles, int64_t capacity);
 void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_slot, int32_t n_slots,
                 int32_t* pair_slot, int64_t capacity, int32_t* tile_offsets, int64_t* d_n_pairs,
-                int64_t* d_max_pairs, void* ws, cudaStream_t st);
+                int64_t* d_max_pairs, void* ws, cudaStream_t st, bool sorted = true);
 
 // composite_fwd.cu — a3
 // Fused a4 for training views (pixel-local L1/L2 loss): target fp32 or uint8 [3][H][W]; the

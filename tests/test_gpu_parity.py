@@ -125,11 +125,14 @@ def _long_list_scene(n_total, stride, res=48):
     return rows, sc, cam
 
 
-@pytest.mark.parametrize("n_total,stride", [(200, 1), (800, 1), (3000, 1), (40000, 5), (600000, 50)])
+@pytest.mark.parametrize("n_total,stride", [(3000, 60), (8000, 80), (200000, 2000), (200, 1), (800, 1), (3000, 1),
+                                            (40000, 5), (600000, 50), (200000, 1000)])
 def test_bin_tiles_long_lists_sorted(n_total, stride):
-    """Tile lists of 200, 800, 3000 and 8000 entries (bitmap, one window) and 12000 (bitmap, three
-    windows over a 600k slot range) come out bit-identical to the oracle's ascending lists; short
-    lists (≤ 32, the warp network) are covered by every scene of test_bin_tiles_bitexact."""
+    """Every path of the per-tile sort comes out bit-identical to the oracle's ascending lists: 50
+    entries (warp network, two registers), 100 (≤ 2^16 slots: warp bitmap; a 200k slot range: warp
+    network, four registers), 200 over a 200k range (warp network, eight registers), 200 / 800 / 3000
+    / 8000 (CTA bitmap, one window), 12000 over a 600k range (CTA bitmap, two windows); lists of ≤ 32
+    (one register) are covered by every scene of test_bin_tiles_bitexact."""
     rows, sc, cam = _long_list_scene(n_total, stride)
     idx = np.arange(n_total, dtype=np.int32)
     p = _pipe(cam, n_total, cap=1 << 20)
