@@ -3,14 +3,19 @@
 
 Workload (BASELINE.json configs[1], "NeRF-synthetic-shaped object"): 300k splats, 100 views of
 800×800 per GPU, headline active fraction ρ = 0.2 (clustered mask); the sweep adds ρ = 1.0 and 0.05.
-One STEP = one refresh period of Alg. 1 at I = 100 iterations: the 100 training views
-each go through a1 project → a2 bin → a3 composite over the view's pre-render cache → a4 L1 loss
-gradient → a5/a6 backward (grad rows +=), then the refresh: a7 FPS view subsample (S = 5% of the
-views) + gradient score of the inactive splats, and a8 the active-set update (into a scratch
-bitmask, so the forced ρ is kept across steps). For N > 1 (torchrun), each rank owns its own 100
-views (weak scaling) and the compacted gradient rows (a9) and score rows are combined with an
-NCCL all-reduce. Inputs are synthetic (paper_2605_13855_b200.synth), larger than L2 per step, and
-L2 is flushed between timed steps.
+One STEP = one batch of 100 training views against one parameter state (R28: gradients summed, one
+optimizer step) followed by one refresh (Alg. 1): the 100 views each go through a1
+project → a2 bin → a3 composite over the view's pre-render cache → a4 L1 loss gradient → a5/a6
+backward (grad rows +=), then one masked Adam step on the compacted rows (NEXT-2), then the
+refresh: a7 FPS view subsample (S = 5% of the views) + gradient score of the inactive splats, and a8
+the active-set update (into a scratch bitmask, so the forced ρ is kept across steps; the caches
+therefore need no reconciliation inside the step — NEXT-1 is timed separately). The parameter rows
+and σ are restored between timed steps (outside the timed region) so every step sees the same
+workload. For N > 1 (torchrun), each rank owns its own 100 views (weak scaling); the gradient rows
++ dσ are one NCCL all-reduce (a9), the score rows are reduce-scattered by row range and the Eq. 8
+bits all-gathered. configs[4] (C5) adds the view-sharded step with strong scaling:
+3M splats, 64 views per step split over the ranks. Inputs are synthetic
+(paper_2605_13855_b200.synth), larger than L2 per step, and L2 is flushed between timed steps.
 
 --impl reference times the CPU oracle (oracle/, test infrastructure) on the same workload: each
 step renders + back-propagates one training view per host core (independent processes).
@@ -87,6 +92,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-c3", action="store_true", help="skip the configs[2] (C3, 3M splats) measurement")
     ap.add_argument("--no-c4", action="store_true", help="skip the configs[3] (C4 score sweep) measurement")
+    ap.add_argument("--no-c5", action="store_true", help="skip the configs[4] (C5 view-sharded step) measurement")
+    ap.add_argument("--c5-rhos", type=float, nargs="+", default=[0.1, 1.0], help="C5 active fractions")
     ap.add_argument("--profile-once", action="store_true", help="run one eager step (for ncu) and exit")
     return ap.parse_args()
 
@@ -276,6 +283,10 @@ def event_ms(a, b):
     return ms.value
 
 
+def torch_logit(torch, o):
+    return torch.logit(o.clamp(1e-6, 1.0 - 1e-6))
+
+
 def scan_kernels(n):
     """k_scan_blocks alone for n <= 4096 (it writes the total), else + k_scan_sums + k_scan_add."""
     if n <= 0:
@@ -355,9 +366,11 @@ class Workload:
         self.contrib, self.tile_evals = int(c[0]), int(c[1])
         assert max_pairs <= cap, "pair capacity overflow"
         self.max_pairs_train = max_pairs
-        # ---- buffers of the step ----
-        self.grad = torch.zeros((max(self.n_act, 1), 80), dtype=torch.float32, device=dev)
-        self.dsig = torch.zeros(1, dtype=torch.float32, device=dev)
+        # ---- buffers of the step: the a9 exchange buffer (gradient rows ⊕ dσ, one all-reduce) ----
+        from paper_2605_13855_b200 import dist as D
+        self.gbuf = D.GradBuffer(max(self.n_act, 1), device=dev)
+        self.grad, self.dsig = self.gbuf.rows, self.gbuf.dsigma
+        self._setup_adam()
         self.with_refresh = with_refresh
         self._setup_refresh(args, synth, mask, cams, cap) if with_refresh else None
         # events around the two hot kernels of every training view (external nodes in the graph)
@@ -369,6 +382,40 @@ class Workload:
             pair[0].record()                      # torch creates the CUDA event lazily on first record
             pair[1].record()
         torch.cuda.synchronize()
+
+    def _setup_adam(self):
+        """NEXT-2 optimizer state for all N splats (untimed setup): latent = the physical rows
+        through the inverse 3DGS activations (logit o, log s; μ, q, v, h as is), zero moments; σ's
+        state (log σ, m, v, t). The rows/σ at the start of every timed step are these."""
+        torch, dev = self.torch, self.dev
+        lat = self.rows.clone()
+        lat[:, 3] = torch_logit(torch, self.rows[:, 3])
+        lat[:, 8:11] = torch.log(self.rows[:, 8:11])
+        self.lat, self.m, self.v = lat, torch.zeros_like(lat), torch.zeros_like(lat)
+        self.astep = torch.zeros(self.n, dtype=torch.int32, device=dev)
+        self.sig_state = torch.tensor([math.log(float(self.sigma.item())), 0.0, 0.0, 0.0], dtype=torch.float32,
+                                      device=dev)
+        self.sig_state0 = self.sig_state.clone()
+        self.rows0, self.sigma0 = self.rows.clone(), self.sigma.clone()
+        self.adam_cfg = self.L.adam_cfg()
+
+    def adam(self):
+        """One masked Adam step on the (combined) compacted gradient rows: the active splats' latent
+        and physical rows and σ move; frozen splats are untouched."""
+        self.L.oit_adam_step(self.grad, self.act, self.lat, self.m, self.v, self.astep, self.rows, self.adam_cfg,
+                             dsigma=self.dsig, sigma_state=self.sig_state, sigma=self.sigma)
+
+    def restore_params(self):
+        """Outside the timed region: back to the initial rows/σ/optimizer state (same work each step)."""
+        self.rows.copy_(self.rows0)
+        self.sigma.copy_(self.sigma0)
+        self.lat[:, :] = self.rows0
+        self.lat[:, 3] = torch_logit(self.torch, self.rows0[:, 3])
+        self.lat[:, 8:11] = self.torch.log(self.rows0[:, 8:11])
+        self.m.zero_()
+        self.v.zero_()
+        self.astep.zero_()
+        self.sig_state.copy_(self.sig_state0)
 
     def _setup_refresh(self, args, synth, mask, cams, cap):
         torch, L, dev = self.torch, self.L, self.dev
@@ -382,7 +429,11 @@ class Workload:
         nsc = max(1, min(self.S, self.n_streams))
         self.score_ws = [torch.empty(max(L.oit_score_workspace_bytes(cams[0], self.n_act, self.n_ina, cap), 256),
                                      dtype=torch.uint8, device=dev) for _ in range(nsc)]
-        self.score_grad = torch.zeros((max(self.n_ina, 1), 80), dtype=torch.float32, device=dev)
+        from paper_2605_13855_b200 import dist as D
+        # padded to the sharded refresh's row ranges (rows beyond n_ina stay zero)
+        self.score_rows = torch.zeros((D.score_buffer_rows(self.n_ina, self.world), 80), dtype=torch.float32,
+                                      device=dev)
+        self.score_grad = self.score_rows[:max(self.n_ina, 1)]
         self.score_dsig = torch.zeros(1, dtype=torch.float32, device=dev)
         self.max_pairs = torch.zeros(1, dtype=torch.int64, device=dev)
         self.bits0 = torch.from_numpy(synth.bits_from_mask(mask).view(np.int32)).to(dev)
@@ -410,8 +461,7 @@ class Workload:
         torch, L = self.torch, self.L
         ns = self.n_streams if n_streams is None else n_streams
         main = torch.cuda.current_stream()
-        self.grad.zero_()
-        self.dsig.zero_()
+        self.gbuf.zero_()
         if host_targets is not None:
             self.copy_stream.wait_stream(main)
             with torch.cuda.stream(self.copy_stream):
@@ -473,7 +523,15 @@ class Workload:
     def update(self):
         L = self.L
         self.bits.copy_(self.bits0)
-        if self.n_ina > 0:
+        if self.n_ina > 0 and self.world > 1:
+            # reduce-scatter of the score rows by row range, Eq. 8 on this rank's
+            # range, all-gather of the row bits, recompaction on every rank
+            from paper_2605_13855_b200 import dist as D
+            D.sharded_refresh_update(self.score_rows, self.ina, self.eps, "fresh", self.n, self.bits, self.act_out,
+                                     self.counts[0:1], self.upd_ws, newly_frozen=self.fro_out,
+                                     n_frozen=self.counts[1:2], newly_active=self.new_out,
+                                     n_activated=self.counts[2:3])
+        elif self.n_ina > 0:
             L.oit_update_active_set(self.score_grad, self.ina, self.eps, "fresh", self.n, self.bits, self.act_out,
                                     self.counts[0:1], self.fro_out, self.counts[1:2], self.new_out,
                                     self.counts[2:3], self.upd_ws)
@@ -492,11 +550,15 @@ class Workload:
         bwd = lambda n: 5 if n > 0 else 0  # noqa: E731
         lossk = 4 if self.loss == "dssim" else 0   # resolve + 2 SSIM stencil passes + k_coef
         # training views with L1/L2: a4 fused into the forward's epilogue (no k_coef launch)
-        train = self.V * (proj(a) + binn(a) + fwd + bwd(a) + lossk)
+        train = self.V * (proj(a) + binn(a) + fwd + bwd(a) + lossk) + 1   # + k_adam
         refresh = 1                                        # k_fps
         if s > 0:
-            refresh += self.S * (proj(a) + binn(a) + fwd + lossk + proj(s) + binn(s) + bwd(s))
-            refresh += 1 + 1 + 3 * scan_kernels(nw) + 1    # k_update_bits, k_popc3, 3 scans, k_emit3
+            # (the scored set's lists feed the backward only: no k_tile_sort)
+            refresh += self.S * (proj(a) + binn(a) + fwd + lossk + proj(s) + binn(s) - 1 + bwd(s))
+            if self.world > 1:   # k_row_activeness + k_apply_bits, k_popc3, 3 scans, k_emit3
+                refresh += 1 + 1 + 1 + 3 * scan_kernels(nw) + 1
+            else:                # k_update_bits, k_popc3, 3 scans, k_emit3
+                refresh += 1 + 1 + 3 * scan_kernels(nw) + 1
         return train + refresh
 
 
@@ -541,15 +603,19 @@ def run_ours(args):
     del wl
     torch.cuda.empty_cache()
     extra = {}
-    if world == 1:
-        flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-        if not args.no_c3:
-            extra["c3_mip360_shaped"] = time_c3(args, torch, L, synth, flush)
-            torch.cuda.empty_cache()
-        if not args.no_c4:
-            extra["c4_score_sweep"] = time_c4(args, torch, L, synth, flush)
-            torch.cuda.empty_cache()
-        del flush
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    sc3 = synth.scene_c3(n_views=200) if (not args.no_c5 or (world == 1 and not args.no_c3)) else None
+    if world == 1 and not args.no_c3:
+        extra["c3_mip360_shaped"] = time_c3(args, torch, L, synth, flush, sc3)
+        torch.cuda.empty_cache()
+    if not args.no_c5:
+        extra["c5_view_sharded_step"] = time_c5(args, torch, dist, L, synth, sc3, world, rank, flush)
+        torch.cuda.empty_cache()
+    del sc3
+    if world == 1 and not args.no_c4:
+        extra["c4_score_sweep"] = time_c4(args, torch, L, synth, flush)
+        torch.cuda.empty_cache()
+    del flush
     if rank == 0:
         line = build_line(args, world, res, results)
         line.update(extra)
@@ -571,18 +637,15 @@ def time_workload(args, torch, dist, wl, world, headline_run):
 
     from paper_2605_13855_b200 import dist as D
 
-    def comm():   # a9: NCCL all-reduce of the compacted gradient rows + dσ
+    def comm():   # a9: ONE NCCL all-reduce of the GradBuffer (compacted gradient rows ⊕ dσ)
         if allred:
-            D.combine_gradients(wl.grad, wl.dsig)
-
-    def comm2():  # refresh: global mean of the per-rank score rows
-        if allred and wl.n_ina > 0:
-            D.combine_scores(wl.score_grad, wl.S * world, wl.S)
+            D.combine_gradients(wl.gbuf)
 
     use_graph = not args.no_graph
     # warm-up eagerly once (also initialises lazy state inside the library)
-    wl.train_views(); comm(); wl.refresh(); comm2(); wl.update()
+    wl.train_views(); comm(); wl.adam(); wl.refresh(); wl.update()
     torch.cuda.synchronize()
+    wl.restore_params()
     graphs = []
     if use_graph:
         s = torch.cuda.Stream()
@@ -591,12 +654,15 @@ def time_workload(args, torch, dist, wl, world, headline_run):
             def whole():
                 wl.ev_seg[0].record()
                 wl.train_views()
+                wl.adam()
                 wl.ev_seg[1].record()
                 wl.refresh()
                 wl.update()
                 wl.ev_seg[2].record()
 
-            for fn in ([wl.train_views, wl.refresh, wl.update] if allred else [whole]):
+            # N > 1: the collectives (a9 all-reduce; the refresh's reduce-scatter / all-gather inside
+            # update()) run eagerly between the graphs
+            for fn in ([wl.train_views, wl.adam, wl.refresh] if allred else [whole]):
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=s):
                     fn()
@@ -607,14 +673,15 @@ def time_workload(args, torch, dist, wl, world, headline_run):
     def step():
         if use_graph:
             if allred:
-                graphs[0].replay(); comm(); graphs[1].replay(); comm2(); graphs[2].replay()
+                graphs[0].replay(); comm(); graphs[1].replay(); graphs[2].replay(); wl.update()
             else:
                 graphs[0].replay()
         else:
-            wl.train_views(); comm(); wl.refresh(); comm2(); wl.update()
+            wl.train_views(); comm(); wl.adam(); wl.refresh(); wl.update()
 
     for _ in range(args.warmup):
         step()
+        wl.restore_params()
     torch.cuda.synchronize()
     if allred:
         dist.barrier()
@@ -623,6 +690,7 @@ def time_workload(args, torch, dist, wl, world, headline_run):
     sampler = ClockSampler(torch.cuda.current_device())
     with sampler:
         for _ in range(args.steps):
+            wl.restore_params()                # same parameters every step (outside the timed region)
             flush.zero_()                      # L2 flush outside the timed region
             torch.cuda.synchronize()
             if allred:
@@ -638,6 +706,7 @@ def time_workload(args, torch, dist, wl, world, headline_run):
             bwd_ms.append(sum(event_ms(a, b) for a, b in wl.ev_bwd))
             if use_graph and not allred:
                 seg_ms.append((event_ms(wl.ev_seg[0], wl.ev_seg[1]), event_ms(wl.ev_seg[1], wl.ev_seg[2])))
+    wl.restore_params()                        # the legs below start from the initial parameters
     ms = float(np.mean(times))
     if allred:
         t = torch.tensor([ms], dtype=torch.float64, device=wl.dev)
@@ -714,13 +783,14 @@ def _graph_time(torch, fn, flush, warmup, steps):
     return float(np.mean(times))
 
 
-def time_c3(args, torch, L, synth, flush, n_views=16):
+def time_c3(args, torch, L, synth, flush, sc, n_views=16):
     """configs[2] (Mip-NeRF360-shaped: 3M splats, 1600×1064, ρ = 0.1): training views a1-a6 over
-    their frozen-set caches, 16 streams in one CUDA graph (no refresh), clustered and uniform masks."""
-    sc = synth.scene_c3(n_views=n_views)
+    their frozen-set caches, 16 streams in one CUDA graph (no refresh), clustered and uniform masks.
+    The 16 views are every 12th camera of the 200-view C3 rig."""
+    cams = sc.cams[::12][:n_views]
     out = {"views": n_views, "splats": sc.n, "res": [1600, 1064], "rho": 0.1}
     for kind in ("clustered", "uniform"):
-        wl = Workload(args, torch, L, synth, 0.1, sc.cams, 0, 1, scene=sc, cap=1 << 22, cache_cap=1 << 25,
+        wl = Workload(args, torch, L, synth, 0.1, cams, 0, 1, scene=sc, cap=1 << 22, cache_cap=1 << 25,
                       with_refresh=False, kind=kind)
         ms = _graph_time(torch, wl.train_views, flush, args.warmup, args.steps)
         px = n_views * wl.H * wl.W
@@ -729,6 +799,89 @@ def time_c3(args, torch, L, synth, flush, n_views=16):
                      "pairs_per_view": sum(wl.pairs_act) / n_views, "n_active": wl.n_act,
                      "f_c": wl.contrib / max(wl.tile_evals, 1)}
         del wl
+        torch.cuda.empty_cache()
+    return out
+
+
+def time_c5(args, torch, dist, L, synth, sc, world, rank, flush, n_step_views=64):
+    """configs[4] (C5): the view-sharded training step with STRONG scaling — the
+    C3 scene (3M splats, 1600×1064), 64 views per step in all, split over the ranks (64/G each) and
+    drawn from the rank's own contiguous shard of the 200-view rig (static view → rank map, so each
+    rank's caches never move); per rank a1-a6 over its views (concurrent streams, one CUDA graph),
+    then a9 = ONE all-reduce of the GradBuffer (compacted rows ⊕ dσ; NCCL over NVLink at N > 1), then
+    one masked Adam step (NEXT-2, identical on every rank). Step time = max over ranks; value = all
+    64 views' pixels / step time. The parameters are restored between steps (outside the timing)."""
+    from paper_2605_13855_b200 import dist as D
+    shard = list(D.shard_views(len(sc.cams), rank, world))
+    per = len(D.shard_views(n_step_views, rank, world))
+    cams = [sc.cams[shard[i * len(shard) // per]] for i in range(per)]   # stratified over the own shard
+    out = {"views_per_step": n_step_views, "views_per_rank": per, "splats": sc.n, "res": [1600, 1064],
+           "scaling": "strong", "mask": "clustered", "rig_views": len(sc.cams)}
+    allred = world > 1
+    for rho in args.c5_rhos:
+        big = rho >= 0.5
+        wl = Workload(args, torch, L, synth, rho, cams, rank, world, scene=sc, cap=(1 << 25) if big else (1 << 22),
+                      cache_cap=1 << 25, with_refresh=False, kind="clustered")
+        ev_c = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+        def comm():
+            if allred:
+                ev_c[0].record()
+                D.combine_gradients(wl.gbuf)
+                ev_c[1].record()
+
+        wl.train_views(); comm(); wl.adam()
+        torch.cuda.synchronize()
+        wl.restore_params()
+        graphs = []
+        if not args.no_graph:
+            s_ = torch.cuda.Stream()
+            s_.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s_):
+                for fn in (wl.train_views, wl.adam):
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=s_):
+                        fn()
+                    graphs.append(g)
+            torch.cuda.current_stream().wait_stream(s_)
+            torch.cuda.synchronize()
+
+        def step():
+            if graphs:
+                graphs[0].replay(); comm(); graphs[1].replay()
+            else:
+                wl.train_views(); comm(); wl.adam()
+
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        times, comm_ms = [], []
+        for i in range(args.warmup + args.steps):
+            wl.restore_params()
+            flush.zero_()
+            torch.cuda.synchronize()
+            if allred:
+                dist.barrier()
+            t0.record()
+            step()
+            t1.record()
+            torch.cuda.synchronize()
+            if allred:
+                dist.barrier()
+            if i >= args.warmup:
+                times.append(t0.elapsed_time(t1))
+                if allred:
+                    comm_ms.append(ev_c[0].elapsed_time(ev_c[1]))
+        ms = float(np.mean(times))
+        cm = float(np.mean(comm_ms)) if comm_ms else 0.0
+        if allred:
+            t = torch.tensor([ms, cm], dtype=torch.float64, device=wl.dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms, cm = float(t[0].item()), float(t[1].item())
+        px = n_step_views * wl.H * wl.W
+        out[str(rho)] = {"ms_per_step": ms, "mpix_per_s": px / (ms * 1e-3) / 1e6, "n_active": wl.n_act,
+                         "allreduce_bytes": int(wl.gbuf.flat.numel() * 4), "allreduce_ms": cm,
+                         "pairs_per_view": sum(wl.pairs_act) / max(per, 1),
+                         "f_c": wl.contrib / max(wl.tile_evals, 1)}
+        del wl, graphs
         torch.cuda.empty_cache()
     return out
 
@@ -988,7 +1141,8 @@ def time_e2e(args, torch, dist, wl, step, flush, allred):
     the parameter rows (before anything else) and of every training image (on a copy stream, in
     view order; each view waits only for its own image, so the copies overlap the compute of the
     earlier views), and device → host reads of the gradient rows and the refreshed bitmask — all
-    inside the timed region (one CUDA graph per step, copies included)."""
+    inside the timed region (one CUDA graph per step, copies included). The device state the copies
+    do not cover (σ, optimizer moments) is restored between steps, outside the timed region."""
     rows_h = wl.rows.cpu().pin_memory()
     targets_h = wl.targets.cpu().pin_memory()
     grad_h = torch.empty_like(wl.grad, device="cpu").pin_memory()
@@ -1002,6 +1156,7 @@ def time_e2e(args, torch, dist, wl, step, flush, allred):
         wl.train_views(host_targets=host_views)
         if allred:
             return
+        wl.adam()
         wl.refresh()
         wl.update()
         grad_h.copy_(wl.grad, non_blocking=True)
@@ -1022,6 +1177,7 @@ def time_e2e(args, torch, dist, wl, step, flush, allred):
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     times = []
     for i in range(args.warmup + args.steps):
+        wl.restore_params()
         flush.zero_()
         torch.cuda.synchronize()
         if allred:
@@ -1041,6 +1197,7 @@ def time_e2e(args, torch, dist, wl, step, flush, allred):
         torch.cuda.synchronize()
         if i >= args.warmup:
             times.append(t0.elapsed_time(t1))
+    wl.restore_params()
     ms = float(np.mean(times))
     if allred:
         t = torch.tensor([ms], dtype=torch.float64, device=wl.dev)
@@ -1114,8 +1271,10 @@ def build_line(args, world, res, results):
         "data": "synthetic (seeded; paper_2605_13855_b200.synth)",
         "config": {"workload": WORKLOAD, "splats": args.splats, "views_per_gpu": res["V"], "res": [res["W"], res["H"]],
                    "rho": res["rho"], "mask": args.kind, "n_active": res["n_act"], "refresh_views_S": res["S"],
-                   "step": "I=100 iterations (one view each, fwd+bwd) + one refresh (a7 score over the inactive "
-                           "set on S views, a8 update)",
+                   "step": "one batch of the rank's 100 training views against one parameter state (R28: "
+                           "fwd+bwd each, gradients summed; a9 all-reduce at N>1) + one masked Adam step + one "
+                           "refresh (a7 FPS + score of the inactive set on S views, a8 update into a scratch "
+                           "bitmask); parameters restored between timed steps",
                    "l2": "flushed between timed steps (256 MB write)", "graph": not args.no_graph,
                    "streams": args.streams, "loss": args.loss,
                    "targets": ("uint8 [3][H][W] 8-bit training images (OIT_TARGET_U8)" if args.targets == "u8"

@@ -611,6 +611,24 @@ def test_c4_score_full_size_parity_sampled():
     got = sg.cpu().numpy()[sample]
     assert_grad_bar(got, ref, bnd, atol=1e-6 / (3 * W * H), name="score")
     assert np.abs(ref).max() > 0
+    # a7 → a8 chain (SURVEY §8(c) Update pin): GPU score rows → GPU Eq. 8 against the oracle's score
+    # rows → the oracle's Eq. 8, with ε at the median norm of each attribute (a real decision); rows
+    # may differ only where the norm lies within 1e-4 relative of ε
+    groups = [(0, 3), (4, 8), (8, 11), (3, 4), (28, 76), (12, 28)]   # μ, q, s, o, h, v
+    norms = np.stack([np.sqrt((ref[:, a:b].astype(np.float64) ** 2).sum(1)) for a, b in groups], 1)
+    eps = np.median(norms, axis=0).astype(np.float32)
+    n_s = len(sample)
+    rb = torch.zeros((n_s + 31) // 32, dtype=torch.int32, device=DEV)
+    L.oit_score_activeness(_t(np.ascontiguousarray(got)), n_s, eps, rb)
+    gpu_act = synth.mask_from_bits(rb.cpu().numpy().view(np.uint32), n_s)
+    bits_o, _, _, _ = O.update_active(ref.astype(np.float32), np.arange(n_s, dtype=np.int32), eps, "fresh", n_s,
+                                      np.zeros((n_s + 31) // 32, np.uint32))
+    ora_act = synth.mask_from_bits(bits_o, n_s)
+    flips = np.flatnonzero(gpu_act != ora_act)
+    near = (np.abs(norms - eps[None, :].astype(np.float64)) / eps[None, :] < 1e-4).any(axis=1)
+    print(f"C4 a7->a8 chain: {len(flips)} membership flips of {n_s} sampled rows, {int(near.sum())} within 1e-4·ε")
+    assert 0.1 < ora_act.mean() < 0.99
+    assert np.all(near[flips]), flips[~near[flips]][:10]
 
 
 # ------------------------------------------------------------------ concurrency ----------
