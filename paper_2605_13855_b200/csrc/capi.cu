@@ -284,9 +284,10 @@ int oit_select_views(const float* centers, int32_t n_views, int32_t n_sub, uint6
   return launch_status();
 }
 
-// Score workspace: per-view buffers reused across the subsampled views.
+// Score workspace: per-view buffers reused across the subsampled views; the scored set's records
+// and moments are kept for a group of kMvViews views (one multi-view epilogue per group).
 struct ScoreWs {
-  float *rec_a, *rec_s, *state, *coef4, *coefa;
+  float *rec_a, *rec_s[kMvViews], *acc_s[kMvViews], *state, *coef4, *coefa;
   int32_t *tps_a, *tps_s, *pairs, *offs;
   int64_t* npairs;
   void *bin_ws, *bwd_ws, *fwd_ws, *dssim_ws;
@@ -298,7 +299,10 @@ static ScoreWs score_layout(void* ws, const oit_camera* cam, int32_t n_active, i
   Carve cv(ws);
   ScoreWs w;
   w.rec_a = cv.take<float>(((size_t)n_active + 1) * kRec4 * 4);
-  w.rec_s = cv.take<float>(((size_t)n_score + 1) * kRec4 * 4);
+  for (int g = 0; g < kMvViews; g++) {
+    w.rec_s[g] = cv.take<float>(((size_t)n_score + 1) * kRec4 * 4);
+    w.acc_s[g] = cv.take<float>(((size_t)n_score + 1) * 12);
+  }
   w.tps_a = cv.take<int32_t>((size_t)n_active + 1);
   w.tps_s = cv.take<int32_t>((size_t)n_score + 1);
   w.pairs = cv.take<int32_t>((size_t)cap + 1);
@@ -343,6 +347,8 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
   if (ws_bytes < oit_score_workspace_bytes(&cams_host[0], n_active, n_score, pair_capacity)) return OIT_ECAPACITY;
   ScoreWs w = score_layout(ws, &cams_host[0], n_active, n_score, pair_capacity);
   cudaStream_t st = S(stream);
+  DevCam group_cams[kMvViews];
+  int in_group = 0;
   for (int s = 0; s < n_sub; s++) {
     const int j = views_host[s];
     DevCam dc = dev_cam(&cams_host[j], bg_host);
@@ -366,14 +372,22 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
                            nullptr, w.fwd_ws, concurrency);
       coef_from_target(dc, &cams_host[j], w.state, targets_host[j], loss, w.coef4, w.coefa, w.dssim_ws, st);
     }
-    // back-propagate L_j to the scored splats (R20)
-    launch_project(dc, scene->rows, scene->sigma, score_idx, n_score, w.rec_s, w.tps_s, st);
+    // back-propagate L_j to the scored splats (R20): the moments of this view; the chain to the
+    // rows runs once per group of kMvViews views (the rows are read-modify-written once per group)
+    float* rec_s = w.rec_s[in_group];
+    launch_project(dc, scene->rows, scene->sigma, score_idx, n_score, rec_s, w.tps_s, st);
     // (the scored lists feed the backward only: no per-tile slot sort, see bin.cu)
-    launch_bin(dc, w.rec_s, w.tps_s, n_score, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st,
+    launch_bin(dc, rec_s, w.tps_s, n_score, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st,
                false);
-    launch_composite_bwd(dc, scene->rows, scene->sigma, score_idx, n_score, w.rec_s, w.pairs, w.offs, pair_capacity,
+    launch_composite_bwd(dc, scene->rows, scene->sigma, score_idx, n_score, rec_s, w.pairs, w.offs, pair_capacity,
                          w.coef4, w.coefa, scale, score_grad, dL_dsigma, nullptr, w.bwd_ws, st, nullptr, nullptr, 0,
-                         concurrency);
+                         concurrency, w.acc_s[in_group]);
+    group_cams[in_group++] = dc;
+    if (in_group == kMvViews || s == n_sub - 1) {
+      launch_epilogue_mv(group_cams, w.rec_s, w.acc_s, in_group, scene->rows, scene->sigma, score_idx, n_score, scale,
+                         score_grad, dL_dsigma, st);
+      in_group = 0;
+    }
   }
   return launch_status();
 }

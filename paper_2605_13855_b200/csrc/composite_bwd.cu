@@ -324,9 +324,234 @@ __global__ void __launch_bounds__(256) k_moments_pixel(DevCam cam, const float4*
 
 // ------------------------------------------------------------------------ a6 epilogue ----
 // One thread per slot. Phase 1 (appearance): view direction, SH colour/weight and their
-// gradients, the h/v rows are updated while streaming the coefficients, and the direction's
-// gradient is reduced to 3 floats. Phase 2 (geometry): μ', conic → Σ' → (Σ, J) → (q, s, μ).
-// Ordering the phases keeps the SH and the 3×3 geometry state from being live together.
+// gradients, the h/v gradient float4s are handed to the sink while streaming the coefficients,
+// and the direction's gradient is reduced to 3 floats. Phase 2 (geometry): μ', conic → Σ' →
+// (Σ, J) → (q, s, μ). Ordering the phases keeps the SH and the 3×3 geometry state from being live
+// together. `r`: the slot's parameter row; q0, q1, q4: its record of this view; m0-m2: its moments
+// of this view. Returns the slot's (unscaled) dL/dσ. The sink receives the scaled row gradient:
+// hv(f4, ...) for the row float4s 3..18 (v, h), geo(...) for μ, o, q, s, cov(...) for dΣ.
+template <class Sink>
+__device__ __forceinline__ float epilogue_chain(const DevCam& cam, const float4* __restrict__ r, float sigma,
+                                                const float4& q0, const float4& q1, const float4& q4,
+                                                const float4& m0, const float4& m1, const float4& m2, float scale,
+                                                Sink& sink) {
+  float gsig = 0.f;
+  const float4 ra = r[0];
+  const float mu0 = ra.x, mu1 = ra.y, mu2 = ra.z, op = ra.w;
+  float gmu0, gmu1, gmu2, gtz_w = 0.f;
+  // =============================== phase 1: appearance (Eq. 4 colour, Eq. 1 weight) ====
+  {
+    const float dvx = mu0 - cam.center[0], dvy = mu1 - cam.center[1], dvz = mu2 - cam.center[2];
+    const float dn = sqrtf(dvx * dvx + dvy * dvy + dvz * dvz), idn = 1.0f / dn;
+    const float rx = dvx * idn, ry = dvy * idn, rz = dvz * idn;
+    float Y[16];
+    sh_basis(rx, ry, rz, Y);
+    float vraw = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const float4 vv = r[3 + q];
+      vraw += vv.x * Y[4 * q] + vv.y * Y[4 * q + 1] + vv.z * Y[4 * q + 2] + vv.w * Y[4 * q + 3];
+    }
+    float craw[3] = {0.5f, 0.5f, 0.5f};
+#pragma unroll
+    for (int q = 0; q < 12; q++) {
+      const float4 hh = r[7 + q];
+      const float e[4] = {hh.x, hh.y, hh.z, hh.w};
+#pragma unroll
+      for (int u = 0; u < 4; u++) craw[(4 * q + u) % 3] += e[u] * Y[(4 * q + u) / 3];
+    }
+    const double ramp_d = ((double)sigma - depth_fp64(cam, mu0, mu1, mu2)) / (double)sigma;  // see ramp_fp64
+    const float ramp = ramp_d > 0.0 ? (float)ramp_d : 0.f, vplus = fmaxf(vraw, 0.f), w = ramp * vplus;
+    const float col0 = fmaxf(craw[0], 0.f), col1 = fmaxf(craw[1], 0.f), col2 = fmaxf(craw[2], 0.f);
+    // dL/dc = w U, dL/dw = U·c − S
+    const float gw = m0.x * col0 + m0.y * col1 + m0.z * col2 - m0.w;
+    const float gch[3] = {craw[0] > 0.f ? w * m0.x : 0.f, craw[1] > 0.f ? w * m0.y : 0.f,
+                          craw[2] > 0.f ? w * m0.z : 0.f};
+    const float gvp = vraw > 0.f ? gw * ramp : 0.f;  // dL/dv⁺ through the max(0, ·) of R4
+    if (ramp_d > 0.0) {
+      const float gramp = gw * vplus;
+      gtz_w = -gramp / sigma;                                   // ∂w/∂d = −v⁺/σ
+      gsig = gramp * (float)((double)sigma - ramp_d * (double)sigma) / (sigma * sigma);  // ∂w/∂σ = v⁺ d/σ²
+    }
+    // h, v rows: dL/dh_j,ch = gc_ch Y_j, dL/dv_j = gv⁺ Y_j; direction: Σ_j cf_j ∇Y_j
+    float cf[16];
+    const float sv = scale * gvp;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const float4 vv = r[3 + q];
+      cf[4 * q] = gvp * vv.x; cf[4 * q + 1] = gvp * vv.y; cf[4 * q + 2] = gvp * vv.z; cf[4 * q + 3] = gvp * vv.w;
+      sink.hv(3 + q, sv * Y[4 * q], sv * Y[4 * q + 1], sv * Y[4 * q + 2], sv * Y[4 * q + 3]);
+    }
+    const float sh3[3] = {scale * gch[0], scale * gch[1], scale * gch[2]};
+#pragma unroll
+    for (int q = 0; q < 12; q++) {
+      const float4 hh = r[7 + q];
+      const float e[4] = {hh.x, hh.y, hh.z, hh.w};
+#pragma unroll
+      for (int u = 0; u < 4; u++) cf[(4 * q + u) / 3] = fmaf(gch[(4 * q + u) % 3], e[u], cf[(4 * q + u) / 3]);
+      sink.hv(7 + q, sh3[(4 * q) % 3] * Y[(4 * q) / 3], sh3[(4 * q + 1) % 3] * Y[(4 * q + 1) / 3],
+              sh3[(4 * q + 2) % 3] * Y[(4 * q + 2) / 3], sh3[(4 * q + 3) % 3] * Y[(4 * q + 3) / 3]);
+    }
+    float gr0, gr1, gr2;
+    sh_vjp(rx, ry, rz, cf, gr0, gr1, gr2);
+    const float rdot = rx * gr0 + ry * gr1 + rz * gr2;  // r = (μ − f)/‖μ − f‖ → μ
+    gmu0 = (gr0 - rx * rdot) * idn;
+    gmu1 = (gr1 - ry * rdot) * idn;
+    gmu2 = (gr2 - rz * rdot) * idn;
+  }
+  // =============================== phase 2: geometry (Eq. 2, 5, 6) =====================
+  // In fp64: the chain conic → Σ' → (Σ, J) → (q, s, μ) sums large terms of opposite sign
+  // (e.g. ∂L/∂s_j = Σ_i ∂L/∂M_ij R_ij), which in fp32 can lose the small result entirely when the
+  // 2D moments themselves are accurate; a few hundred DFMA per slot, negligible next to the
+  // row traffic of this latency/HBM-bound kernel.
+  const double nA = q0.z, nB = q0.w, nC = q1.x;
+  const float4 rb = r[1], rc = r[2];
+  double W[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int j = 0; j < 3; j++) W[i][j] = (double)cam.R[3 * i + j];
+  double t[3];
+  cam_point_fp64(cam, mu0, mu1, mu2, t);
+  const double fx = cam.fx, fy = cam.fy;
+  const double tz = t[2], itz = 1.0 / tz, itz2 = itz * itz;
+  const double limx = 1.3 * (0.5 * (double)cam.W / fx), limy = 1.3 * (0.5 * (double)cam.H / fy);
+  const double ux = t[0] * itz, uy = t[1] * itz;
+  const bool clx = ux > limx || ux < -limx, cly = uy > limy || uy < -limy;
+  const double uxc = fmin(limx, fmax(-limx, ux)), uyc = fmin(limy, fmax(-limy, uy));
+  const double J00 = fx * itz, J02 = -fx * uxc * itz, J11 = fy * itz, J12 = -fy * uyc * itz;
+  double T[2][3];
+#pragma unroll
+  for (int j = 0; j < 3; j++) {
+    T[0][j] = J00 * W[0][j] + J02 * W[2][j];
+    T[1][j] = J11 * W[1][j] + J12 * W[2][j];
+  }
+  const double q0w = rb.x, q0x = rb.y, q0y = rb.z, q0z = rb.w;
+  const double qn = sqrt(q0w * q0w + q0x * q0x + q0y * q0y + q0z * q0z), iqn = 1.0 / qn;
+  const double qw = q0w * iqn, qx = q0x * iqn, qy = q0y * iqn, qz = q0z * iqn;
+  double Rq[3][3];
+  Rq[0][0] = 1.0 - 2.0 * (qy * qy + qz * qz); Rq[0][1] = 2.0 * (qx * qy - qw * qz); Rq[0][2] = 2.0 * (qx * qz + qw * qy);
+  Rq[1][0] = 2.0 * (qx * qy + qw * qz); Rq[1][1] = 1.0 - 2.0 * (qx * qx + qz * qz); Rq[1][2] = 2.0 * (qy * qz - qw * qx);
+  Rq[2][0] = 2.0 * (qx * qz - qw * qy); Rq[2][1] = 2.0 * (qy * qz + qw * qx); Rq[2][2] = 1.0 - 2.0 * (qx * qx + qy * qy);
+  const double s[3] = {rc.x, rc.y, rc.z};
+  double M[3][3], Sg[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int j = 0; j < 3; j++) M[i][j] = Rq[i][j] * s[j];
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int j = 0; j < 3; j++) Sg[i][j] = M[i][0] * M[j][0] + M[i][1] * M[j][1] + M[i][2] * M[j][2];
+  // the moments were accumulated with the spec offsets dx = x - μ'_spec; the true offsets are
+  // dx - δx (δ = μ'_fp64 - μ'_spec, rec q4.zw): re-centre the moments exactly
+  const double dmx = q4.z, dmy = q4.w;
+  const double Od = m1.x, M1s = m1.y, M2s = m1.z;
+  const double M1 = M1s - dmx * Od, M2 = M2s - dmy * Od;
+  const double XX = m1.w - 2.0 * dmx * M1s + dmx * dmx * Od;
+  const double XY = m2.x - dmy * M1s - dmx * M2s + dmx * dmy * Od;
+  const double YY = m2.y - 2.0 * dmy * M2s + dmy * dmy * Od;
+  const float go = (float)(Od / (double)op);
+  const double gmx = -(2.0 * nA * M1 + nB * M2), gmy = -(nB * M1 + 2.0 * nC * M2);
+  // conic K = [[-2nA, -nB], [-nB, -2nC]]; dL/dK = -½[[XX, XY], [XY, YY]]; dL/dΣ' = -K dL/dK K
+  const double K00 = -2.0 * nA, K01 = -nB, K11 = -2.0 * nC;
+  const double A00 = 0.5 * (K00 * XX + K01 * XY), A01 = 0.5 * (K00 * XY + K01 * YY);
+  const double A10 = 0.5 * (K01 * XX + K11 * XY), A11 = 0.5 * (K01 * XY + K11 * YY);
+  const double G00 = A00 * K00 + A01 * K01, G01 = A00 * K01 + A01 * K11, G11 = A10 * K01 + A11 * K11;
+  // Σ' = T Σ Tᵀ + 0.3 I: dL/dΣ = Tᵀ G T, dL/dT = 2 G T Σ
+  const double G[2][2] = {{G00, G01}, {G01, G11}};
+  double gS[3][3], GT[2][3], gT[2][3];
+#pragma unroll
+  for (int p = 0; p < 2; p++)
+#pragma unroll
+    for (int j = 0; j < 3; j++) GT[p][j] = G[p][0] * T[0][j] + G[p][1] * T[1][j];
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int j = 0; j < 3; j++) gS[i][j] = T[0][i] * GT[0][j] + T[1][i] * GT[1][j];
+#pragma unroll
+  for (int p = 0; p < 2; p++)
+#pragma unroll
+    for (int j = 0; j < 3; j++) gT[p][j] = 2.0 * (GT[p][0] * Sg[0][j] + GT[p][1] * Sg[1][j] + GT[p][2] * Sg[2][j]);
+  // T = J W -> J
+  const double gJ00 = gT[0][0] * W[0][0] + gT[0][1] * W[0][1] + gT[0][2] * W[0][2];
+  const double gJ02 = gT[0][0] * W[2][0] + gT[0][1] * W[2][1] + gT[0][2] * W[2][2];
+  const double gJ11 = gT[1][0] * W[1][0] + gT[1][1] * W[1][1] + gT[1][2] * W[1][2];
+  const double gJ12 = gT[1][0] * W[2][0] + gT[1][1] * W[2][1] + gT[1][2] * W[2][2];
+  double gt[3] = {0.0, 0.0, (double)gtz_w};
+  gt[2] += -(fx * gJ00 + fy * gJ11) * itz2 + (gJ02 * fx * uxc + gJ12 * fy * uyc) * itz2;
+  if (!clx) {  // ∂J02/∂t is masked where the tan-fov clamp holds u_x fixed (R13)
+    gt[0] += -gJ02 * fx * itz2;
+    gt[2] += gJ02 * fx * t[0] * itz2 * itz;
+  }
+  if (!cly) {
+    gt[1] += -gJ12 * fy * itz2;
+    gt[2] += gJ12 * fy * t[1] * itz2 * itz;
+  }
+  // μ' -> t
+  gt[0] += gmx * fx * itz;
+  gt[1] += gmy * fy * itz;
+  gt[2] -= (gmx * fx * t[0] + gmy * fy * t[1]) * itz2;
+  const double gm0 = gmu0 + W[0][0] * gt[0] + W[1][0] * gt[1] + W[2][0] * gt[2];
+  const double gm1 = gmu1 + W[0][1] * gt[0] + W[1][1] * gt[1] + W[2][1] * gt[2];
+  const double gm2 = gmu2 + W[0][2] * gt[0] + W[1][2] * gt[1] + W[2][2] * gt[2];
+  // Σ = M Mᵀ -> M -> (s, R)
+  double gM[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int j = 0; j < 3; j++)
+      gM[i][j] = 2.0 * (gS[i][0] * M[0][j] + gS[i][1] * M[1][j] + gS[i][2] * M[2][j]);
+  double gs[3];
+#pragma unroll
+  for (int j = 0; j < 3; j++) gs[j] = gM[0][j] * Rq[0][j] + gM[1][j] * Rq[1][j] + gM[2][j] * Rq[2][j];
+  double gR[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int j = 0; j < 3; j++) gR[i][j] = gM[i][j] * s[j];
+  double gq[4];
+  gq[0] = 2.0 * (-qz * gR[0][1] + qy * gR[0][2] + qz * gR[1][0] - qx * gR[1][2] - qy * gR[2][0] + qx * gR[2][1]);
+  gq[1] = 2.0 * (qy * gR[0][1] + qz * gR[0][2] + qy * gR[1][0] - 2.0 * qx * gR[1][1] - qw * gR[1][2] +
+                 qz * gR[2][0] + qw * gR[2][1] - 2.0 * qx * gR[2][2]);
+  gq[2] = 2.0 * (-2.0 * qy * gR[0][0] + qx * gR[0][1] + qw * gR[0][2] + qx * gR[1][0] + qz * gR[1][2] -
+                 qw * gR[2][0] + qz * gR[2][1] - 2.0 * qy * gR[2][2]);
+  gq[3] = 2.0 * (-2.0 * qz * gR[0][0] - qw * gR[0][1] + qx * gR[0][2] + qw * gR[1][0] - 2.0 * qz * gR[1][1] +
+                 qy * gR[1][2] + qx * gR[2][0] + qy * gR[2][1]);
+  const double qdot = qw * gq[0] + qx * gq[1] + qy * gq[2] + qz * gq[3];
+  // ---- the row's μ, o, q, s gradient (+ the packed dΣ), scaled ----
+  const double sc = scale;
+  sink.geo((float)(sc * gm0), (float)(sc * gm1), (float)(sc * gm2), scale * go,
+           (float)(sc * (gq[0] - qw * qdot) * iqn), (float)(sc * (gq[1] - qx * qdot) * iqn),
+           (float)(sc * (gq[2] - qy * qdot) * iqn), (float)(sc * (gq[3] - qz * qdot) * iqn), (float)(sc * gs[0]),
+           (float)(sc * gs[1]), (float)(sc * gs[2]));
+  sink.cov((float)(sc * gS[0][0]), (float)(sc * (gS[0][1] + gS[1][0])), (float)(sc * (gS[0][2] + gS[2][0])),
+           (float)(sc * gS[1][1]), (float)(sc * (gS[1][2] + gS[2][1])), (float)(sc * gS[2][2]));
+  return gsig;
+}
+
+struct AtomicRowSink {  // the row's gradient accumulated in place with vector atomics
+  float* g;
+  float* dcov;
+  __device__ __forceinline__ void hv(int f4, float a, float b, float c, float d) { red_add_v4(g + 4 * f4, a, b, c, d); }
+  __device__ __forceinline__ void geo(float m0, float m1, float m2, float o, float q0, float q1, float q2, float q3,
+                                      float s0, float s1, float s2) {
+    red_add_v4(g, m0, m1, m2, o);
+    red_add_v4(g + 4, q0, q1, q2, q3);
+    red_add_v4(g + 8, s0, s1, s2, 0.f);
+  }
+  __device__ __forceinline__ void cov(float a, float b, float c, float d, float e, float f) {
+    if (!dcov) return;
+    atomicAdd(dcov + 0, a); atomicAdd(dcov + 1, b); atomicAdd(dcov + 2, c);
+    atomicAdd(dcov + 3, d); atomicAdd(dcov + 4, e); atomicAdd(dcov + 5, f);
+  }
+};
+
+__device__ __forceinline__ bool epilogue_needed(const float4& q3, const float4& m0, const float4& m1) {
+  const bool vis = __float_as_uint(q3.x) != 0u || __float_as_uint(q3.y) != 0u;
+  return vis && (m0.x != 0.f || m0.y != 0.f || m0.z != 0.f || m0.w != 0.f || m1.x != 0.f);
+}
+
 __global__ void __launch_bounds__(128, 3) k_epilogue(DevCam cam, const float4* __restrict__ rows,
                                                   const float* __restrict__ sigma_p, const int32_t* __restrict__ idx,
                                                   int32_t n_slots, const float4* __restrict__ rec,
@@ -337,222 +562,91 @@ __global__ void __launch_bounds__(128, 3) k_epilogue(DevCam cam, const float4* _
   float gsig = 0.f;
   if (k < n_slots) {
     const float4 q3 = rec[(size_t)k * kRec4 + 3];
-    const bool vis = __float_as_uint(q3.x) != 0u || __float_as_uint(q3.y) != 0u;
     const float4 m0 = acc2d[(size_t)k * 3 + 0];  // U0 U1 U2 S
     const float4 m1 = acc2d[(size_t)k * 3 + 1];  // Od M1 M2 XX
     const float4 m2 = acc2d[(size_t)k * 3 + 2];  // XY YY
-    if (vis && (m0.x != 0.f || m0.y != 0.f || m0.z != 0.f || m0.w != 0.f || m1.x != 0.f)) {
-      const float4* r = rows + (size_t)idx[k] * kRow4;
-      float4* gr = grad + (size_t)k * kRow4;
-      const float4 ra = r[0];
-      const float mu0 = ra.x, mu1 = ra.y, mu2 = ra.z, op = ra.w;
-      float gmu0, gmu1, gmu2, gtz_w = 0.f;
-      // =============================== phase 1: appearance (Eq. 4 colour, Eq. 1 weight) ====
-      {
-        const float dvx = mu0 - cam.center[0], dvy = mu1 - cam.center[1], dvz = mu2 - cam.center[2];
-        const float dn = sqrtf(dvx * dvx + dvy * dvy + dvz * dvz), idn = 1.0f / dn;
-        const float rx = dvx * idn, ry = dvy * idn, rz = dvz * idn;
-        float Y[16];
-        sh_basis(rx, ry, rz, Y);
-        float vraw = 0.f;
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          const float4 vv = r[3 + q];
-          vraw += vv.x * Y[4 * q] + vv.y * Y[4 * q + 1] + vv.z * Y[4 * q + 2] + vv.w * Y[4 * q + 3];
-        }
-        float craw[3] = {0.5f, 0.5f, 0.5f};
-#pragma unroll
-        for (int q = 0; q < 12; q++) {
-          const float4 hh = r[7 + q];
-          const float e[4] = {hh.x, hh.y, hh.z, hh.w};
-#pragma unroll
-          for (int u = 0; u < 4; u++) craw[(4 * q + u) % 3] += e[u] * Y[(4 * q + u) / 3];
-        }
-        const float sigma = *sigma_p;
-        const double ramp_d = ((double)sigma - depth_fp64(cam, mu0, mu1, mu2)) / (double)sigma;  // see ramp_fp64
-        const float ramp = ramp_d > 0.0 ? (float)ramp_d : 0.f, vplus = fmaxf(vraw, 0.f), w = ramp * vplus;
-        const float col0 = fmaxf(craw[0], 0.f), col1 = fmaxf(craw[1], 0.f), col2 = fmaxf(craw[2], 0.f);
-        // dL/dc = w U, dL/dw = U·c − S
-        const float gw = m0.x * col0 + m0.y * col1 + m0.z * col2 - m0.w;
-        const float gch[3] = {craw[0] > 0.f ? w * m0.x : 0.f, craw[1] > 0.f ? w * m0.y : 0.f,
-                              craw[2] > 0.f ? w * m0.z : 0.f};
-        const float gvp = vraw > 0.f ? gw * ramp : 0.f;  // dL/dv⁺ through the max(0, ·) of R4
-        if (ramp_d > 0.0) {
-          const float gramp = gw * vplus;
-          gtz_w = -gramp / sigma;                                   // ∂w/∂d = −v⁺/σ
-          gsig = gramp * (float)((double)sigma - ramp_d * (double)sigma) / (sigma * sigma);  // ∂w/∂σ = v⁺ d/σ²
-        }
-        // h, v rows: dL/dh_j,ch = gc_ch Y_j, dL/dv_j = gv⁺ Y_j; direction: Σ_j cf_j ∇Y_j
-        float cf[16];
-        const float sv = scale * gvp;
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          const float4 vv = r[3 + q];
-          cf[4 * q] = gvp * vv.x; cf[4 * q + 1] = gvp * vv.y; cf[4 * q + 2] = gvp * vv.z; cf[4 * q + 3] = gvp * vv.w;
-          red_add_v4(reinterpret_cast<float*>(gr + 3 + q), sv * Y[4 * q], sv * Y[4 * q + 1], sv * Y[4 * q + 2],
-                     sv * Y[4 * q + 3]);
-        }
-        const float sh3[3] = {scale * gch[0], scale * gch[1], scale * gch[2]};
-#pragma unroll
-        for (int q = 0; q < 12; q++) {
-          const float4 hh = r[7 + q];
-          const float e[4] = {hh.x, hh.y, hh.z, hh.w};
-#pragma unroll
-          for (int u = 0; u < 4; u++) cf[(4 * q + u) / 3] = fmaf(gch[(4 * q + u) % 3], e[u], cf[(4 * q + u) / 3]);
-          red_add_v4(reinterpret_cast<float*>(gr + 7 + q), sh3[(4 * q) % 3] * Y[(4 * q) / 3],
-                     sh3[(4 * q + 1) % 3] * Y[(4 * q + 1) / 3], sh3[(4 * q + 2) % 3] * Y[(4 * q + 2) / 3],
-                     sh3[(4 * q + 3) % 3] * Y[(4 * q + 3) / 3]);
-        }
-        float gr0, gr1, gr2;
-        sh_vjp(rx, ry, rz, cf, gr0, gr1, gr2);
-        const float rdot = rx * gr0 + ry * gr1 + rz * gr2;  // r = (μ − f)/‖μ − f‖ → μ
-        gmu0 = (gr0 - rx * rdot) * idn;
-        gmu1 = (gr1 - ry * rdot) * idn;
-        gmu2 = (gr2 - rz * rdot) * idn;
-      }
-      // =============================== phase 2: geometry (Eq. 2, 5, 6) =====================
-      // In fp64: the chain conic → Σ' → (Σ, J) → (q, s, μ) sums large terms of opposite sign
-      // (e.g. ∂L/∂s_j = Σ_i ∂L/∂M_ij R_ij), which in fp32 can lose the small result entirely when the
-      // 2D moments themselves are accurate; a few hundred DFMA per slot, negligible next to the
-      // row traffic of this latency/HBM-bound kernel.
-      const float4 q0 = rec[(size_t)k * kRec4 + 0];
-      const float4 q1 = rec[(size_t)k * kRec4 + 1];
-      const float4 q4 = rec[(size_t)k * kRec4 + 4];
-      const double nA = q0.z, nB = q0.w, nC = q1.x;
-      const float4 rb = r[1], rc = r[2];
-      double W[3][3];
-#pragma unroll
-      for (int i = 0; i < 3; i++)
-#pragma unroll
-        for (int j = 0; j < 3; j++) W[i][j] = (double)cam.R[3 * i + j];
-      double t[3];
-      cam_point_fp64(cam, mu0, mu1, mu2, t);
-      const double fx = cam.fx, fy = cam.fy;
-      const double tz = t[2], itz = 1.0 / tz, itz2 = itz * itz;
-      const double limx = 1.3 * (0.5 * (double)cam.W / fx), limy = 1.3 * (0.5 * (double)cam.H / fy);
-      const double ux = t[0] * itz, uy = t[1] * itz;
-      const bool clx = ux > limx || ux < -limx, cly = uy > limy || uy < -limy;
-      const double uxc = fmin(limx, fmax(-limx, ux)), uyc = fmin(limy, fmax(-limy, uy));
-      const double J00 = fx * itz, J02 = -fx * uxc * itz, J11 = fy * itz, J12 = -fy * uyc * itz;
-      double T[2][3];
-#pragma unroll
-      for (int j = 0; j < 3; j++) {
-        T[0][j] = J00 * W[0][j] + J02 * W[2][j];
-        T[1][j] = J11 * W[1][j] + J12 * W[2][j];
-      }
-      const double q0w = rb.x, q0x = rb.y, q0y = rb.z, q0z = rb.w;
-      const double qn = sqrt(q0w * q0w + q0x * q0x + q0y * q0y + q0z * q0z), iqn = 1.0 / qn;
-      const double qw = q0w * iqn, qx = q0x * iqn, qy = q0y * iqn, qz = q0z * iqn;
-      double Rq[3][3];
-      Rq[0][0] = 1.0 - 2.0 * (qy * qy + qz * qz); Rq[0][1] = 2.0 * (qx * qy - qw * qz); Rq[0][2] = 2.0 * (qx * qz + qw * qy);
-      Rq[1][0] = 2.0 * (qx * qy + qw * qz); Rq[1][1] = 1.0 - 2.0 * (qx * qx + qz * qz); Rq[1][2] = 2.0 * (qy * qz - qw * qx);
-      Rq[2][0] = 2.0 * (qx * qz - qw * qy); Rq[2][1] = 2.0 * (qy * qz + qw * qx); Rq[2][2] = 1.0 - 2.0 * (qx * qx + qy * qy);
-      const double s[3] = {rc.x, rc.y, rc.z};
-      double M[3][3], Sg[3][3];
-#pragma unroll
-      for (int i = 0; i < 3; i++)
-#pragma unroll
-        for (int j = 0; j < 3; j++) M[i][j] = Rq[i][j] * s[j];
-#pragma unroll
-      for (int i = 0; i < 3; i++)
-#pragma unroll
-        for (int j = 0; j < 3; j++) Sg[i][j] = M[i][0] * M[j][0] + M[i][1] * M[j][1] + M[i][2] * M[j][2];
-      // the moments were accumulated with the spec offsets dx = x - μ'_spec; the true offsets are
-      // dx - δx (δ = μ'_fp64 - μ'_spec, rec q4.zw): re-centre the moments exactly
-      const double dmx = q4.z, dmy = q4.w;
-      const double Od = m1.x, M1s = m1.y, M2s = m1.z;
-      const double M1 = M1s - dmx * Od, M2 = M2s - dmy * Od;
-      const double XX = m1.w - 2.0 * dmx * M1s + dmx * dmx * Od;
-      const double XY = m2.x - dmy * M1s - dmx * M2s + dmx * dmy * Od;
-      const double YY = m2.y - 2.0 * dmy * M2s + dmy * dmy * Od;
-      const float go = (float)(Od / (double)op);
-      const double gmx = -(2.0 * nA * M1 + nB * M2), gmy = -(nB * M1 + 2.0 * nC * M2);
-      // conic K = [[-2nA, -nB], [-nB, -2nC]]; dL/dK = -½[[XX, XY], [XY, YY]]; dL/dΣ' = -K dL/dK K
-      const double K00 = -2.0 * nA, K01 = -nB, K11 = -2.0 * nC;
-      const double A00 = 0.5 * (K00 * XX + K01 * XY), A01 = 0.5 * (K00 * XY + K01 * YY);
-      const double A10 = 0.5 * (K01 * XX + K11 * XY), A11 = 0.5 * (K01 * XY + K11 * YY);
-      const double G00 = A00 * K00 + A01 * K01, G01 = A00 * K01 + A01 * K11, G11 = A10 * K01 + A11 * K11;
-      // Σ' = T Σ Tᵀ + 0.3 I: dL/dΣ = Tᵀ G T, dL/dT = 2 G T Σ
-      const double G[2][2] = {{G00, G01}, {G01, G11}};
-      double gS[3][3], GT[2][3], gT[2][3];
-#pragma unroll
-      for (int p = 0; p < 2; p++)
-#pragma unroll
-        for (int j = 0; j < 3; j++) GT[p][j] = G[p][0] * T[0][j] + G[p][1] * T[1][j];
-#pragma unroll
-      for (int i = 0; i < 3; i++)
-#pragma unroll
-        for (int j = 0; j < 3; j++) gS[i][j] = T[0][i] * GT[0][j] + T[1][i] * GT[1][j];
-#pragma unroll
-      for (int p = 0; p < 2; p++)
-#pragma unroll
-        for (int j = 0; j < 3; j++) gT[p][j] = 2.0 * (GT[p][0] * Sg[0][j] + GT[p][1] * Sg[1][j] + GT[p][2] * Sg[2][j]);
-      // T = J W -> J
-      const double gJ00 = gT[0][0] * W[0][0] + gT[0][1] * W[0][1] + gT[0][2] * W[0][2];
-      const double gJ02 = gT[0][0] * W[2][0] + gT[0][1] * W[2][1] + gT[0][2] * W[2][2];
-      const double gJ11 = gT[1][0] * W[1][0] + gT[1][1] * W[1][1] + gT[1][2] * W[1][2];
-      const double gJ12 = gT[1][0] * W[2][0] + gT[1][1] * W[2][1] + gT[1][2] * W[2][2];
-      double gt[3] = {0.0, 0.0, (double)gtz_w};
-      gt[2] += -(fx * gJ00 + fy * gJ11) * itz2 + (gJ02 * fx * uxc + gJ12 * fy * uyc) * itz2;
-      if (!clx) {  // ∂J02/∂t is masked where the tan-fov clamp holds u_x fixed (R13)
-        gt[0] += -gJ02 * fx * itz2;
-        gt[2] += gJ02 * fx * t[0] * itz2 * itz;
-      }
-      if (!cly) {
-        gt[1] += -gJ12 * fy * itz2;
-        gt[2] += gJ12 * fy * t[1] * itz2 * itz;
-      }
-      // μ' -> t
-      gt[0] += gmx * fx * itz;
-      gt[1] += gmy * fy * itz;
-      gt[2] -= (gmx * fx * t[0] + gmy * fy * t[1]) * itz2;
-      const double gm0 = gmu0 + W[0][0] * gt[0] + W[1][0] * gt[1] + W[2][0] * gt[2];
-      const double gm1 = gmu1 + W[0][1] * gt[0] + W[1][1] * gt[1] + W[2][1] * gt[2];
-      const double gm2 = gmu2 + W[0][2] * gt[0] + W[1][2] * gt[1] + W[2][2] * gt[2];
-      // Σ = M Mᵀ -> M -> (s, R)
-      double gM[3][3];
-#pragma unroll
-      for (int i = 0; i < 3; i++)
-#pragma unroll
-        for (int j = 0; j < 3; j++)
-          gM[i][j] = 2.0 * (gS[i][0] * M[0][j] + gS[i][1] * M[1][j] + gS[i][2] * M[2][j]);
-      double gs[3];
-#pragma unroll
-      for (int j = 0; j < 3; j++) gs[j] = gM[0][j] * Rq[0][j] + gM[1][j] * Rq[1][j] + gM[2][j] * Rq[2][j];
-      double gR[3][3];
-#pragma unroll
-      for (int i = 0; i < 3; i++)
-#pragma unroll
-        for (int j = 0; j < 3; j++) gR[i][j] = gM[i][j] * s[j];
-      double gq[4];
-      gq[0] = 2.0 * (-qz * gR[0][1] + qy * gR[0][2] + qz * gR[1][0] - qx * gR[1][2] - qy * gR[2][0] + qx * gR[2][1]);
-      gq[1] = 2.0 * (qy * gR[0][1] + qz * gR[0][2] + qy * gR[1][0] - 2.0 * qx * gR[1][1] - qw * gR[1][2] +
-                     qz * gR[2][0] + qw * gR[2][1] - 2.0 * qx * gR[2][2]);
-      gq[2] = 2.0 * (-2.0 * qy * gR[0][0] + qx * gR[0][1] + qw * gR[0][2] + qx * gR[1][0] + qz * gR[1][2] -
-                     qw * gR[2][0] + qz * gR[2][1] - 2.0 * qy * gR[2][2]);
-      gq[3] = 2.0 * (-2.0 * qz * gR[0][0] - qw * gR[0][1] + qx * gR[0][2] + qw * gR[1][0] - 2.0 * qz * gR[1][1] +
-                     qy * gR[1][2] + qx * gR[2][0] + qy * gR[2][1]);
-      const double qdot = qw * gq[0] + qx * gq[1] + qy * gq[2] + qz * gq[3];
-      // ---- accumulate into the gradient row (+=, scaled) with vector atomics: concurrent views
-      // (one stream each) may accumulate into the same rows ----
-      float* g = reinterpret_cast<float*>(gr);
-      const double sc = scale;
-      red_add_v4(g, (float)(sc * gm0), (float)(sc * gm1), (float)(sc * gm2), scale * go);
-      red_add_v4(g + 4, (float)(sc * (gq[0] - qw * qdot) * iqn), (float)(sc * (gq[1] - qx * qdot) * iqn),
-                 (float)(sc * (gq[2] - qy * qdot) * iqn), (float)(sc * (gq[3] - qz * qdot) * iqn));
-      red_add_v4(g + 8, (float)(sc * gs[0]), (float)(sc * gs[1]), (float)(sc * gs[2]), 0.f);
-      if (dL_dcov) {
-        float* dc = dL_dcov + (size_t)k * 6;
-        atomicAdd(dc + 0, (float)(sc * gS[0][0]));
-        atomicAdd(dc + 1, (float)(sc * (gS[0][1] + gS[1][0])));
-        atomicAdd(dc + 2, (float)(sc * (gS[0][2] + gS[2][0])));
-        atomicAdd(dc + 3, (float)(sc * gS[1][1]));
-        atomicAdd(dc + 4, (float)(sc * (gS[1][2] + gS[2][1])));
-        atomicAdd(dc + 5, (float)(sc * gS[2][2]));
-      }
+    if (epilogue_needed(q3, m0, m1)) {
+      AtomicRowSink sink{reinterpret_cast<float*>(grad + (size_t)k * kRow4), dL_dcov ? dL_dcov + (size_t)k * 6 : nullptr};
+      gsig = epilogue_chain(cam, rows + (size_t)idx[k] * kRow4, *sigma_p, rec[(size_t)k * kRec4 + 0],
+                            rec[(size_t)k * kRec4 + 1], rec[(size_t)k * kRec4 + 4], m0, m1, m2, scale, sink);
     }
   }
   // σ: warp reduce, one atomic per warp
+  gsig = warp_sum(gsig * scale);
+  if ((threadIdx.x & 31) == 0 && gsig != 0.f) atomicAdd(dL_dsigma, gsig);
+}
+
+// Multi-view epilogue (the score, a7): the chains of up to kMvViews views of a slot summed in
+// registers / shared memory, then ONE vector-atomic update of the slot's row — the row is read
+// once per group of views instead of once per view, and its 320-B read-modify-write happens once
+// (S × 640 B → 640 B of RMW per scored splat and group). Slots culled or without contribution in
+// a view skip that view; slots idle in every view of the group touch nothing.
+constexpr int kMvThreads = 128;
+struct MvCams {
+  DevCam cam[kMvViews];
+  const float4* rec[kMvViews];
+  const float4* acc[kMvViews];
+};
+
+struct SmemRowSink {  // per-thread accumulators in shared memory (stride kMvThreads): the chain's
+  float4* hvs;        // registers stay the single-view epilogue's; v/h: the row float4s 3..18
+  float* geos;        // μ (3), o, q (4), s (3)
+  __device__ __forceinline__ void hv(int f4, float x, float y, float z, float w) {
+    float4& t = hvs[(f4 - 3) * kMvThreads];
+    t.x += x; t.y += y; t.z += z; t.w += w;
+  }
+  __device__ __forceinline__ void geo(float m0, float m1, float m2, float o, float q0, float q1, float q2, float q3,
+                                      float s0, float s1, float s2) {
+    const float v[11] = {m0, m1, m2, o, q0, q1, q2, q3, s0, s1, s2};
+#pragma unroll
+    for (int i = 0; i < 11; i++) geos[i * kMvThreads] += v[i];
+  }
+  __device__ __forceinline__ void cov(float, float, float, float, float, float) {}
+};
+
+__global__ void __launch_bounds__(kMvThreads, 2) k_epilogue_mv(MvCams mv, int n_views, const float4* __restrict__ rows,
+                                                             const float* __restrict__ sigma_p,
+                                                             const int32_t* __restrict__ idx, int32_t n_slots,
+                                                             float scale, float4* __restrict__ grad,
+                                                             float* __restrict__ dL_dsigma) {
+  __shared__ float4 s_hv[16 * kMvThreads];
+  __shared__ float s_geo[11 * kMvThreads];
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  float gsig = 0.f;
+  if (k < n_slots) {
+    SmemRowSink sink{s_hv + threadIdx.x, s_geo + threadIdx.x};
+#pragma unroll
+    for (int q = 0; q < 16; q++) sink.hvs[q * kMvThreads] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < 11; q++) sink.geos[q * kMvThreads] = 0.f;
+    bool any = false;
+    const float4* r = rows + (size_t)idx[k] * kRow4;
+    const float sigma = *sigma_p;
+    // unrolled over the group's views: each chain reads its camera from the kernel parameters
+    // (constant-bank operands, as in the single-view epilogue) instead of holding it in registers
+#pragma unroll
+    for (int v = 0; v < kMvViews; v++) {
+      if (v >= n_views) break;
+      const float4* rc = mv.rec[v] + (size_t)k * kRec4;
+      const float4* ac = mv.acc[v] + (size_t)k * 3;
+      const float4 q3 = rc[3], m0 = ac[0], m1 = ac[1];
+      if (!epilogue_needed(q3, m0, m1)) continue;
+      any = true;
+      gsig += epilogue_chain(mv.cam[v], r, sigma, rc[0], rc[1], rc[4], m0, m1, ac[2], scale, sink);
+    }
+    if (any) {
+      float* g = reinterpret_cast<float*>(grad + (size_t)k * kRow4);
+      const float* a = sink.geos;
+      red_add_v4(g, a[0], a[kMvThreads], a[2 * kMvThreads], a[3 * kMvThreads]);
+      red_add_v4(g + 4, a[4 * kMvThreads], a[5 * kMvThreads], a[6 * kMvThreads], a[7 * kMvThreads]);
+      red_add_v4(g + 8, a[8 * kMvThreads], a[9 * kMvThreads], a[10 * kMvThreads], 0.f);
+#pragma unroll
+      for (int q = 0; q < 16; q++) {
+        const float4 t = sink.hvs[q * kMvThreads];
+        red_add_v4(g + 12 + 4 * q, t.x, t.y, t.z, t.w);
+      }
+    }
+  }
   gsig = warp_sum(gsig * scale);
   if ((threadIdx.x & 31) == 0 && gsig != 0.f) atomicAdd(dL_dsigma, gsig);
 }
@@ -587,7 +681,7 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
                           int32_t n_slots, const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
                           int64_t capacity, const float* coef4, const float* coefa, float scale, float* grad,
                           float* dL_dsigma, float* dL_dcov, void* ws, cudaStream_t st, cudaEvent_t ev_begin,
-                          cudaEvent_t ev_end, int variant, int concurrency) {
+                          cudaEvent_t ev_end, int variant, int concurrency, float* acc_out) {
   if (n_slots <= 0) {
     record_event(ev_begin, st);
     record_event(ev_end, st);
@@ -598,6 +692,7 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
   const int64_t max_items = qcap / 32 + 4 * n_tiles + 1;
   Carve cv(ws);
   float* acc2d = cv.take<float>((size_t)n_slots * 12);
+  if (acc_out) acc2d = acc_out;  // moments only: the caller runs the (multi-view) epilogue
   int4* items = cv.take<int4>(max_items);
   int32_t* n_items = cv.take<int32_t>(4);
   int32_t* tile_nch = cv.take<int32_t>(4 * n_tiles + 1);
@@ -622,10 +717,27 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
                                                   reinterpret_cast<const float4*>(coef4), coefa, acc2d);
     record_event(ev_end, st);
   }
+  if (acc_out) return;
   k_epilogue<<<(n_slots + 127) / 128, 128, 0, st>>>(cam, reinterpret_cast<const float4*>(rows), sigma, idx, n_slots,
                                                     reinterpret_cast<const float4*>(rec),
                                                     reinterpret_cast<const float4*>(acc2d), scale,
                                                     reinterpret_cast<float4*>(grad), dL_dsigma, dL_dcov);
+}
+
+void launch_epilogue_mv(const DevCam* cams, const float* const* recs, const float* const* accs, int n_views,
+                        const float* rows, const float* sigma, const int32_t* idx, int32_t n_slots, float scale,
+                        float* grad, float* dL_dsigma, cudaStream_t st) {
+  if (n_slots <= 0 || n_views <= 0) return;
+  MvCams mv;
+  for (int v = 0; v < kMvViews; v++) {
+    const int u = v < n_views ? v : 0;
+    mv.cam[v] = cams[u];
+    mv.rec[v] = reinterpret_cast<const float4*>(recs[u]);
+    mv.acc[v] = reinterpret_cast<const float4*>(accs[u]);
+  }
+  k_epilogue_mv<<<(n_slots + kMvThreads - 1) / kMvThreads, kMvThreads, 0, st>>>(
+      mv, n_views, reinterpret_cast<const float4*>(rows), sigma, idx, n_slots, scale, reinterpret_cast<float4*>(grad),
+      dL_dsigma);
 }
 
 }  // namespace oit

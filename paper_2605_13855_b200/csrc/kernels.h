@@ -104,7 +104,14 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
                           int64_t capacity, const float* coef4, const float* coefa, float scale, float* grad,
                           float* dL_dsigma, float* dL_dcov, void* ws, cudaStream_t st,
                           cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr, int variant = 0,
-                          int concurrency = 1);
+                          int concurrency = 1, float* acc_out = nullptr);
+// acc_out (nullable): moments only, into acc_out [n_slots][12] (zeroed here); no epilogue. The
+// multi-view epilogue (score): the chains of n_views ≤ kMvViews views (records recs[v], moments
+// accs[v] of the same n_slots slots) summed per slot, one row update each.
+constexpr int kMvViews = 4;
+void launch_epilogue_mv(const DevCam* cams, const float* const* recs, const float* const* accs, int n_views,
+                        const float* rows, const float* sigma, const int32_t* idx, int32_t n_slots, float scale,
+                        float* grad, float* dL_dsigma, cudaStream_t st);
 
 // Record an event on a stream, as an external event node when the stream is being captured.
 inline void record_event(cudaEvent_t ev, cudaStream_t st) {
