@@ -62,8 +62,9 @@ __global__ void __launch_bounds__(kFwdThreads, kLoss ? 16 : 1) k_fwd_items(
     int32_t* __restrict__ done, float* __restrict__ partial, const float* __restrict__ base,
     float* __restrict__ image, float* __restrict__ state, unsigned long long* __restrict__ counters, int chunk_len,
     FwdLoss fl) {
-  __shared__ float4 s_q0[kFwdThreads], s_q1[kFwdThreads], s_q2[kFwdThreads];
-  __shared__ float2 s_k[kFwdThreads];
+  // staged records, one 64-B entry each (q0, q1, q2, (kx, ky, -, -)): one shared-memory pointer
+  // walks all four fields (a single uniform increment per record in the loop)
+  __shared__ float4 s_rec[kFwdThreads][4];
   __shared__ int s_item, s_last;
   const int tid = threadIdx.x;
   const int n_tiles = cam.TX * cam.TY;
@@ -105,16 +106,16 @@ __global__ void __launch_bounds__(kFwdThreads, kLoss ? 16 : 1) k_fwd_items(
       const int n = min(kFwdThreads, end - b);
       if (tid < n) {
         const float4* r = rec + (size_t)pair_slot[b + tid] * kRec4;
-        s_q0[tid] = r[0];
-        s_q1[tid] = r[1];
-        s_q2[tid] = r[2];
-        s_k[tid] = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(r + 3) + 2);
+        s_rec[tid][0] = r[0];
+        s_rec[tid][1] = r[1];
+        s_rec[tid][2] = r[2];
+        s_rec[tid][3] = r[3];  // (rect_x, rect_y, kx, ky): the loop reads .zw
       }
       __syncthreads();
 #pragma unroll 1
       for (int i = 0; i < n; i++) {
-        const float4 q0 = s_q0[i];  // mx my nA nB
-        const float4 q1 = s_q1[i];  // nC thr_lo thr_hi log2o
+        const float4 q0 = s_rec[i][0];  // mx my nA nB
+        const float4 q1 = s_rec[i][1];  // nC thr_lo thr_hi log2o
         // spec test (DESIGN.md §3 step 13) on the pixel pairs (x, x+4), (x+8, x+12): the packed
         // sub/fma are per element the scalar __fsub_rn/__fmaf_rn, so the decisions are unchanged
         const float dy = __fsub_rn(fy, q0.y);
@@ -124,11 +125,13 @@ __global__ void __launch_bounds__(kFwdThreads, kLoss ? 16 : 1) k_fwd_items(
         const f2_t dxA = sub2(fxA, mx2), dxB = sub2(fxB, mx2);
         const f2_t pwA = fma2(dxA, fma2(nA2, dxA, by2), cy2), pwB = fma2(dxB, fma2(nA2, dxB, by2), cy2);
         const float pw0 = f2lo(pwA), pw1 = f2hi(pwA), pw2 = f2lo(pwB), pw3 = f2hi(pwB);
-        const bool c0 = pw0 <= 0.0f && pw0 >= q1.y, c1 = pw1 <= 0.0f && pw1 >= q1.y;
-        const bool c2 = pw2 <= 0.0f && pw2 >= q1.y, c3 = pw3 <= 0.0f && pw3 >= q1.y;
-        if (__any_sync(0xffffffffu, c0 || c1 || c2 || c3)) {  // warp-uniform; α = 0 for the others
-          const float4 q2 = s_q2[i];  // cR cG cB w
-          const float2 kk = s_k[i];   // sub-ulp μ' correction of the exponent (value path)
+        // warp skip test, conservative: no pixel of the warp reaches thr_lo (power ≤ 0 is decided
+        // exactly below, per pixel)
+        if (__any_sync(0xffffffffu, fmaxf(fmaxf(pw0, pw1), fmaxf(pw2, pw3)) >= q1.y)) {
+          const bool c0 = pw0 <= 0.0f && pw0 >= q1.y, c1 = pw1 <= 0.0f && pw1 >= q1.y;
+          const bool c2 = pw2 <= 0.0f && pw2 >= q1.y, c3 = pw3 <= 0.0f && pw3 >= q1.y;
+          const float4 q2 = s_rec[i][2];  // cR cG cB w
+          const float2 kk = *reinterpret_cast<const float2*>(&s_rec[i][3].z);  // sub-ulp μ' correction (value path)
           const f2_t base2 = f2s(fmaf(-kk.y, dy, q1.w)), nkx2 = f2s(-kk.x), l2e = f2s(kLog2e);
           const f2_t argA = fma2(nkx2, dxA, fma2(pwA, l2e, base2));
           const f2_t argB = fma2(nkx2, dxB, fma2(pwB, l2e, base2));
