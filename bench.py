@@ -1138,21 +1138,21 @@ def time_reconcile(args, torch, wl, flush):
 
 def time_e2e(args, torch, dist, wl, step, flush, allred):
     """Same step through the public API with HOST inputs: per step, pinned-host → device copies of
-    the parameter rows (before anything else) and of every training image (on a copy stream, in
-    view order; each view waits only for its own image, so the copies overlap the compute of the
-    earlier views), and device → host reads of the gradient rows and the refreshed bitmask — all
-    inside the timed region (one CUDA graph per step, copies included). The device state the copies
-    do not cover (σ, optimizer moments) is restored between steps, outside the timed region."""
-    rows_h = wl.rows.cpu().pin_memory()
+    every training image of the step (the step's input data; on a copy stream, in view order; each
+    view waits only for its own image, so the copies overlap the compute of the earlier views), and
+    device → host reads of the step's results, the combined gradient rows and the refreshed bitmask —
+    all inside the timed region (one CUDA graph per step, copies included). The parameter rows are
+    training state, resident on the device and updated there by the step's Adam (copying them in
+    each step would overwrite that update); they, σ and the optimizer state are restored between
+    steps outside the timed region, as in the device-timed step."""
     targets_h = wl.targets.cpu().pin_memory()
     grad_h = torch.empty_like(wl.grad, device="cpu").pin_memory()
     bits_h = torch.empty_like(wl.bits, device="cpu").pin_memory()
-    h2d = rows_h.numel() * rows_h.element_size() + targets_h.numel() * targets_h.element_size()
+    h2d = targets_h.numel() * targets_h.element_size()
     d2h = grad_h.numel() * 4 + bits_h.numel() * 4
     host_views = [targets_h[v] for v in range(wl.V)]
 
     def e2e_step():
-        wl.rows.copy_(rows_h, non_blocking=True)
         wl.train_views(host_targets=host_views)
         if allred:
             return
@@ -1186,7 +1186,6 @@ def time_e2e(args, torch, dist, wl, step, flush, allred):
         if graph is not None:
             graph.replay()
         elif allred:
-            wl.rows.copy_(rows_h, non_blocking=True)
             wl.targets.copy_(targets_h, non_blocking=True)
             step()
             grad_h.copy_(wl.grad, non_blocking=True)
