@@ -148,8 +148,8 @@ int oit_composite_fwd(const oit_camera* cam, const float* rec, const int32_t* pa
 /* Same as oit_composite_fwd, with `concurrency` as in oit_composite_bwd_ex (≥ 1; sizes the
  * persistent grid for that many concurrent calls); d_counters (nullable, device int64[2], accumulated +=) receives
  * [0] the number of contributing (splat, pixel) pairs (α ≥ 1/255, inside the image) and [1] the
- * splat-pixel evaluations the kernel performs (64 per (splat, 8×8 quadrant) pair after the
- * quadrant sub-binning; the metric's tile-granular count is 256 × *d_n_pairs of the bin).
+ * tile-granular splat-pixel evaluations (256 per (splat, tile) pair of the lists, = 256 ×
+ * *d_n_pairs of the bin; the metric's evaluation count).
  * Counting adds one reduction per work item; the plain call skips it. */
 int oit_composite_fwd_ex(const oit_camera* cam, const float* rec, const int32_t* pair_slot,
                          const int32_t* tile_offsets, int64_t pair_capacity, const float bg_host[3],
@@ -173,6 +173,19 @@ int oit_composite_fwd_loss(const oit_camera* cam, const float* rec, const int32_
                            const float* base, const void* target, int32_t loss, float* state, void* ws,
                            size_t ws_bytes, void* bwd_ws, size_t bwd_ws_bytes, int32_t n_slots,
                            int32_t concurrency, oit_stream_t stream);
+
+/* Same, with ev (nullable): two cudaEvent_t recorded on `stream` right before and right after the
+ * a3 composite kernel itself (the work-list builder kernels that precede it are outside), so
+ * callers can time the hot loop alone (also inside CUDA-graph capture, as external event nodes). */
+typedef struct {
+  void* kernel_begin; /* cudaEvent_t or NULL */
+  void* kernel_end;   /* cudaEvent_t or NULL */
+} oit_kernel_events;
+int oit_composite_fwd_loss_ex(const oit_camera* cam, const float* rec, const int32_t* pair_slot,
+                              const int32_t* tile_offsets, int64_t pair_capacity, const float bg_host[3],
+                              const float* base, const void* target, int32_t loss, float* state, void* ws,
+                              size_t ws_bytes, void* bwd_ws, size_t bwd_ws_bytes, int32_t n_slots,
+                              const oit_kernel_events* ev, int32_t concurrency, oit_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------
  * a4  oit_loss_grad — pixel loss gradient dL/dC of L = mean_{3HW} |C - I| (loss 0, sign(0)=0)

@@ -34,6 +34,10 @@ class BwdEvents(C.Structure):
     _fields_ = [("moments_begin", C.c_void_p), ("moments_end", C.c_void_p)]
 
 
+class KernelEvents(C.Structure):
+    _fields_ = [("kernel_begin", C.c_void_p), ("kernel_end", C.c_void_p)]
+
+
 class Scene(C.Structure):
     _fields_ = [("n", C.c_int32), ("rows", C.c_void_p), ("sigma", C.c_void_p)]
 
@@ -122,7 +126,8 @@ def lib() -> C.CDLL:
 
 
 EXPORTED = ["oit_status_string", "oit_num_tiles", "oit_project_cull", "oit_bin_workspace_bytes", "oit_bin_tiles",
-            "oit_fwd_workspace_bytes", "oit_composite_fwd", "oit_composite_fwd_ex", "oit_composite_fwd_loss", "oit_loss_grad", "oit_bwd_workspace_bytes", "oit_composite_bwd", "oit_composite_bwd_ex",
+            "oit_fwd_workspace_bytes", "oit_composite_fwd", "oit_composite_fwd_ex", "oit_composite_fwd_loss",
+            "oit_composite_fwd_loss_ex", "oit_loss_grad", "oit_bwd_workspace_bytes", "oit_composite_bwd", "oit_composite_bwd_ex",
             "oit_select_views", "oit_score_workspace_bytes", "oit_score_subsample", "oit_update_workspace_bytes",
             "oit_update_active_set", "oit_delta_workspace_bytes", "oit_active_set_delta",
             "oit_reconcile_workspace_bytes", "oit_reconcile_cache", "oit_adam_step",
@@ -201,15 +206,20 @@ def oit_composite_fwd(cam, rec, pair_slot, tile_offsets, bg, ws, base=None, rout
 
 
 def oit_composite_fwd_loss(cam, rec, pair_slot, tile_offsets, bg, ws, bwd_ws, n_slots: int, target, loss: str,
-                           base=None, state=None, stream=None, concurrency: int = 1):
+                           base=None, state=None, stream=None, concurrency: int = 1, events=None):
     """a3 + a4 fused (training view): the forward whose epilogue applies the L1/L2 loss against
     target (fp32 or uint8) and writes the backward coefficients into bwd_ws; follow with
-    oit_composite_bwd(..., coef_ready=True) on the same bwd_ws."""
-    _check(lib().oit_composite_fwd_loss(C.byref(camera(cam)), _ptr(rec), _ptr(pair_slot), _ptr(tile_offsets),
-                                        int(pair_slot.numel()), _f3(bg), _ptr(base), _ptr(target),
-                                        _loss_flags(loss, [target]), _ptr(state), _ptr(ws), int(ws.numel()),
-                                        _ptr(bwd_ws), int(bwd_ws.numel()), int(n_slots), int(concurrency),
-                                        _stream(stream)), "oit_composite_fwd_loss")
+    oit_composite_bwd(..., coef_ready=True) on the same bwd_ws. events: optional (begin, end)
+    torch.cuda.Event pair recorded around the composite kernel alone (oit_composite_fwd_loss_ex)."""
+    args = (C.byref(camera(cam)), _ptr(rec), _ptr(pair_slot), _ptr(tile_offsets), int(pair_slot.numel()), _f3(bg),
+            _ptr(base), _ptr(target), _loss_flags(loss, [target]), _ptr(state), _ptr(ws), int(ws.numel()),
+            _ptr(bwd_ws), int(bwd_ws.numel()), int(n_slots))
+    if events is None:
+        _check(lib().oit_composite_fwd_loss(*args, int(concurrency), _stream(stream)), "oit_composite_fwd_loss")
+    else:
+        ev = C.byref(KernelEvents(C.c_void_p(events[0].cuda_event), C.c_void_p(events[1].cuda_event)))
+        _check(lib().oit_composite_fwd_loss_ex(*args, ev, int(concurrency), _stream(stream)),
+               "oit_composite_fwd_loss_ex")
 
 
 def oit_loss_grad(cam, image, target, loss: str, dL_dimage, stream=None):

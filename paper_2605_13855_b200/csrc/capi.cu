@@ -124,10 +124,11 @@ int oit_composite_fwd_ex(const oit_camera* cam, const float* rec, const int32_t*
   return launch_status();
 }
 
-int oit_composite_fwd_loss(const oit_camera* cam, const float* rec, const int32_t* pair_slot,
+int oit_composite_fwd_loss_ex(const oit_camera* cam, const float* rec, const int32_t* pair_slot,
                            const int32_t* tile_offsets, int64_t pair_capacity, const float bg_host[3], const float* base,
                            const void* target, int32_t loss, float* state, void* ws, size_t ws_bytes, void* bwd_ws,
-                           size_t bwd_ws_bytes, int32_t n_slots, int32_t concurrency, oit_stream_t stream) {
+                           size_t bwd_ws_bytes, int32_t n_slots, const oit_kernel_events* ev,
+                           int32_t concurrency, oit_stream_t stream) {
   if (!cam_ok(cam) || !tile_offsets || !bg_host || pair_capacity < 0 || !target || !ws || !bwd_ws || n_slots < 0)
     return OIT_EINVAL;
   const int32_t l = loss & ~OIT_TARGET_U8;
@@ -148,8 +149,18 @@ int oit_composite_fwd_loss(const oit_camera* cam, const float* rec, const int32_
   fl.coefa = cv.take<float>((size_t)nt * kTilePx);
   fl.listed_tiles_only = true;
   launch_composite_fwd(dev_cam(cam, bg_host), rec, pair_slot, tile_offsets, pair_capacity, base, nullptr, nullptr,
-                       state, nullptr, S(stream), nullptr, ws, concurrency, fl);
+                       state, nullptr, S(stream), nullptr, ws, concurrency, fl,
+                       ev ? static_cast<cudaEvent_t>(ev->kernel_begin) : nullptr,
+                       ev ? static_cast<cudaEvent_t>(ev->kernel_end) : nullptr);
   return launch_status();
+}
+
+int oit_composite_fwd_loss(const oit_camera* cam, const float* rec, const int32_t* pair_slot,
+                           const int32_t* tile_offsets, int64_t pair_capacity, const float bg_host[3], const float* base,
+                           const void* target, int32_t loss, float* state, void* ws, size_t ws_bytes, void* bwd_ws,
+                           size_t bwd_ws_bytes, int32_t n_slots, int32_t concurrency, oit_stream_t stream) {
+  return oit_composite_fwd_loss_ex(cam, rec, pair_slot, tile_offsets, pair_capacity, bg_host, base, target, loss, state,
+                                   ws, ws_bytes, bwd_ws, bwd_ws_bytes, n_slots, nullptr, concurrency, stream);
 }
 
 int oit_loss_grad(const oit_camera* cam, const float* image, const float* target, int32_t loss, float* dL_dimage,

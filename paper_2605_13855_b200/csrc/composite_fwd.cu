@@ -351,7 +351,7 @@ size_t fwd_ws_bytes(int32_t n_tiles, int64_t capacity) {
 void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pair_slot,
                           const int32_t* tile_offsets, int64_t capacity, const float* base, const uint8_t* route,
                           float* image, float* state, float* base_out, cudaStream_t st, int64_t* counters, void* ws,
-                          int concurrency, FwdLoss fl) {
+                          int concurrency, FwdLoss fl, cudaEvent_t ev_begin, cudaEvent_t ev_end) {
   const int n_tiles = cam.TX * cam.TY;
   const float4* r4 = reinterpret_cast<const float4*>(rec);
   auto* cnt = reinterpret_cast<unsigned long long*>(counters);
@@ -382,9 +382,11 @@ void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pa
 #define OIT_FWD2(B, K, L)                                                                                   \
   do {                                                                                                      \
     const int occ = resident_ctas<k_fwd_items<B, K, L>>(kFwdThreads);                                       \
+    record_event(ev_begin, st);                                                                             \
     k_fwd_items<B, K, L><<<sm_count() * persistent_ctas(occ, concurrency), kFwdThreads, 0, st>>>(           \
         cam, r4, pair_slot, tile_offsets, capacity, items, n_items, counter, tile_nch, done, partial, base,  \
         image, state, cnt, chunk_len, fl);                                                                  \
+    record_event(ev_end, st);                                                                               \
   } while (0)
     if (fl.target) {
       const bool u8 = fl.target_u8;

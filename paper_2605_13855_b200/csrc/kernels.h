@@ -41,7 +41,8 @@ struct FwdLoss {
 void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pair_slot,
                           const int32_t* tile_offsets, int64_t capacity, const float* base, const uint8_t* route,
                           float* image, float* state, float* base_out, cudaStream_t st, int64_t* counters, void* ws,
-                          int concurrency = 1, FwdLoss fl = FwdLoss());
+                          int concurrency = 1, FwdLoss fl = FwdLoss(), cudaEvent_t ev_begin = nullptr,
+                          cudaEvent_t ev_end = nullptr);
 // Launch-shape facts of the current device (SM count; CTAs of a kernel one SM holds), looked up
 // once per device id: hardware constants, not state — a multi-device process gets each device's
 // own value, and concurrent first calls only race to store the same number.

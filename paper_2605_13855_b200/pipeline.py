@@ -68,13 +68,10 @@ class ViewPipeline:
         coefficients into this pipeline's backward workspace; follow with backward(...,
         coef_ready=True). Returns the state buffer if state=True (else None, not written)."""
         rec = self.project_bin(rows, sigma, idx, stream)
-        if events is not None:
-            events[0].record()
+        # events (optional): recorded by the library around the composite kernel alone
         L.oit_composite_fwd_loss(self.cam, rec, self.pairs, self.offs, bg, self.fwd_ws, self.bwd_ws, self.max_slots,
                                  target, loss, base=base, state=self.state if state else None, stream=stream,
-                                 concurrency=concurrency)
-        if events is not None:
-            events[1].record()
+                                 concurrency=concurrency, events=events)
         return self.state if state else None
 
     def backward(self, rows, sigma, idx, bg, state, dL_dimage, grad, dL_dsigma, dL_dcov=None, scale=1.0,
