@@ -55,7 +55,7 @@ __device__ __forceinline__ void store_px(const Px& a, float* dst, size_t plane, 
 // kLoss (a4 fused into the epilogue, training views): 0 none; 1 / 2 — the L1/L2 loss against an
 // fp32 / 8-bit target, the backward coefficients (coef4, coefa) written instead of a state round trip.
 template <bool kBase, bool kCount, int kLoss = 0>
-__global__ void __launch_bounds__(kFwdThreads, kLoss ? 16 : 1) k_fwd_items(
+__global__ void __launch_bounds__(kFwdThreads, kLoss ? 18 : 1) k_fwd_items(
     DevCam cam, const float4* __restrict__ rec, const int32_t* __restrict__ pair_slot,
     const int32_t* __restrict__ offs, int64_t capacity, const int4* __restrict__ items,
     const int32_t* __restrict__ n_items_p, int32_t* __restrict__ counter, const int32_t* __restrict__ tile_nch,
