@@ -429,6 +429,8 @@ class Workload:
         nsc = max(1, min(self.S, self.n_streams))
         self.score_ws = [torch.empty(max(L.oit_score_workspace_bytes(cams[0], self.n_act, self.n_ina, cap), 256),
                                      dtype=torch.uint8, device=dev) for _ in range(nsc)]
+        # the refresh's own streams: it runs concurrently with the training views (R35)
+        self.score_streams = [torch.cuda.Stream() for _ in range(nsc)]
         from paper_2605_13855_b200 import dist as D
         # padded to the sharded refresh's row ranges (rows beyond n_ina stay zero)
         self.score_rows = torch.zeros((D.score_buffer_rows(self.n_ina, self.world), 80), dtype=torch.float32,
@@ -453,7 +455,12 @@ class Workload:
         t = self.targets[v]
         return t.float() / 255.0 if t.dtype == self.torch.uint8 else t.contiguous()
 
-    def train_views(self, n_streams=None, host_targets=None):
+    def refresh_parts(self):
+        if not self.with_refresh or self.n_ina <= 0:
+            return 0
+        return sum(1 for k in range(len(self.score_ws)) if self.views_host[k::len(self.score_ws)])
+
+    def train_views(self, n_streams=None, host_targets=None, extra_concurrency=0):
         """a1-a6 over every training view (Alg. 1 l.3-6, one view per iteration); views are dealt
         round-robin to n_streams streams (fork/join on the current stream). host_targets (e2e):
         pinned-host training images, copied in view order on a copy stream; each view's loss
@@ -483,21 +490,25 @@ class Workload:
                     # a3 + a4 fused: the forward's epilogue applies the pixel-local loss and writes the
                     # backward coefficients into the backward workspace (no pixel-state round trip)
                     p.forward_loss(self.rows, self.sigma, self.act, self.bg, self.targets[v], self.loss,
-                                   base=self.caches[v], events=self.ev_fwd[v], concurrency=ns)
+                                   base=self.caches[v], events=self.ev_fwd[v], concurrency=ns + extra_concurrency)
                     p.backward(self.rows, self.sigma, self.act, self.bg, None, None, self.grad, self.dsig,
-                               events=self.ev_bwd[v], coef_ready=True, concurrency=ns)
+                               events=self.ev_bwd[v], coef_ready=True, concurrency=ns + extra_concurrency)
                 else:   # D-SSIM is not pixel-local: state → resolve → SSIM stencils → coefficients
                     _, st = p.forward(self.rows, self.sigma, self.act, self.bg, base=self.caches[v], image=False,
-                                      events=self.ev_fwd[v], concurrency=ns)
+                                      events=self.ev_fwd[v], concurrency=ns + extra_concurrency)
                     p.backward(self.rows, self.sigma, self.act, self.bg, st, None, self.grad, self.dsig,
-                               events=self.ev_bwd[v], target=self.targets[v], loss=self.loss, concurrency=ns)
+                               events=self.ev_bwd[v], target=self.targets[v], loss=self.loss,
+                               concurrency=ns + extra_concurrency)
         for st_ in self.streams[:ns]:
             main.wait_stream(st_)
         if host_targets is not None:
             main.wait_stream(self.copy_stream)
 
-    def refresh(self):
-        """a7 (FPS + subsampled score of the inactive splats) and a8 (Eq. 8 update)."""
+    def refresh(self, join=True, extra_concurrency=0):
+        """a7 (FPS + subsampled score of the inactive splats) on the refresh's own streams, forked
+        from the current stream; join=False leaves them running (refresh_join() later), so the
+        score overlaps the training views (R35: the period's refresh scores the parameters the
+        period's batch uses, the update applies to the next period)."""
         L = self.L
         torch = self.torch
         L.oit_select_views(self.centers, self.S, 2605, 0, self.views_dev)
@@ -507,18 +518,35 @@ class Workload:
             # the S subsampled views are scored concurrently (disjoint subsets, scale 1/S each)
             main = torch.cuda.current_stream()
             parts = [self.views_host[k::len(self.score_ws)] for k in range(len(self.score_ws))]
+            conc = sum(1 for q in parts if q) + extra_concurrency
             for k, part in enumerate(parts):
                 if not part:
                     continue
-                self.streams[k].wait_stream(main)
-                with torch.cuda.stream(self.streams[k]):
+                self.score_streams[k].wait_stream(main)
+                with torch.cuda.stream(self.score_streams[k]):
                     L.oit_score_subsample(self.rows, self.sigma, self.cams, self.targets_list, self.caches_list,
                                           self.act, self.ina, part, self.loss, self.bg, self.score_grad, self.score_dsig,
                                           self.score_cap, self.max_pairs, self.score_ws[k], scale=1.0 / self.S,
-                                          concurrency=sum(1 for q in parts if q))
-            for k, part in enumerate(parts):
-                if part:
-                    main.wait_stream(self.streams[k])
+                                          concurrency=conc)
+            if join:
+                self.refresh_join()
+
+    def refresh_join(self):
+        if self.n_ina <= 0:
+            return
+        main = self.torch.cuda.current_stream()
+        for k in range(len(self.score_ws)):
+            if self.views_host[k::len(self.score_ws)]:
+                main.wait_stream(self.score_streams[k])
+
+    def train_and_refresh(self, host_targets=None):
+        """The step's a1-a6 over the 100 views and the refresh's a7, concurrently (R35)."""
+        nr = self.refresh_parts()
+        if self.with_refresh:
+            self.refresh(join=False, extra_concurrency=self.n_streams)
+        self.train_views(host_targets=host_targets, extra_concurrency=nr)
+        if self.with_refresh:
+            self.refresh_join()
 
     def update(self):
         L = self.L
@@ -643,7 +671,7 @@ def time_workload(args, torch, dist, wl, world, headline_run):
 
     use_graph = not args.no_graph
     # warm-up eagerly once (also initialises lazy state inside the library)
-    wl.train_views(); comm(); wl.adam(); wl.refresh(); wl.update()
+    wl.train_and_refresh(); comm(); wl.adam(); wl.update()
     torch.cuda.synchronize()
     wl.restore_params()
     graphs = []
@@ -653,16 +681,15 @@ def time_workload(args, torch, dist, wl, world, headline_run):
         with torch.cuda.stream(s):
             def whole():
                 wl.ev_seg[0].record()
-                wl.train_views()
-                wl.adam()
+                wl.train_and_refresh()
                 wl.ev_seg[1].record()
-                wl.refresh()
+                wl.adam()
                 wl.update()
                 wl.ev_seg[2].record()
 
             # N > 1: the collectives (a9 all-reduce; the refresh's reduce-scatter / all-gather inside
             # update()) run eagerly between the graphs
-            for fn in ([wl.train_views, wl.adam, wl.refresh] if allred else [whole]):
+            for fn in ([wl.train_and_refresh, wl.adam] if allred else [whole]):
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=s):
                     fn()
@@ -673,11 +700,11 @@ def time_workload(args, torch, dist, wl, world, headline_run):
     def step():
         if use_graph:
             if allred:
-                graphs[0].replay(); comm(); graphs[1].replay(); graphs[2].replay(); wl.update()
+                graphs[0].replay(); comm(); graphs[1].replay(); wl.update()
             else:
                 graphs[0].replay()
         else:
-            wl.train_views(); comm(); wl.adam(); wl.refresh(); wl.update()
+            wl.train_and_refresh(); comm(); wl.adam(); wl.update()
 
     for _ in range(args.warmup):
         step()
@@ -741,8 +768,11 @@ def time_workload(args, torch, dist, wl, world, headline_run):
                pairs=int(sum(wl.pairs_act)), contrib=wl.contrib, tile_evals=wl.tile_evals, V=wl.V, H=wl.H, W=wl.W,
                n_act=wl.n_act, n_ina=wl.n_ina, S=wl.S, launches=wl.kernel_launches(), rho=wl.rho,
                max_score_pairs=int(wl.max_pairs.item()),
-               train_ms=float(np.mean([a for a, _ in seg_ms])) if seg_ms else None,
-               refresh_ms=float(np.mean([b for _, b in seg_ms])) if seg_ms else None)
+               train_refresh_ms=float(np.mean([a for a, _ in seg_ms])) if seg_ms else None,
+               adam_update_ms=float(np.mean([b for _, b in seg_ms])) if seg_ms else None)
+    if headline_run and wl.with_refresh and wl.n_ina > 0 and use_graph:
+        # the refresh (a7) alone, for the record (inside the step it overlaps the training views)
+        res["refresh_alone_ms"] = _graph_time(torch, wl.refresh, flush, args.warmup, args.steps)
     if headline_run and not args.no_e2e:
         res["e2e"] = time_e2e(args, torch, dist, wl, step, flush, allred)
     if headline_run and not args.no_reconcile and wl.n_ina > 0:
@@ -1153,11 +1183,10 @@ def time_e2e(args, torch, dist, wl, step, flush, allred):
     host_views = [targets_h[v] for v in range(wl.V)]
 
     def e2e_step():
-        wl.train_views(host_targets=host_views)
+        wl.train_and_refresh(host_targets=host_views)
         if allred:
             return
         wl.adam()
-        wl.refresh()
         wl.update()
         grad_h.copy_(wl.grad, non_blocking=True)
         bits_h.copy_(wl.bits, non_blocking=True)
@@ -1260,7 +1289,7 @@ def build_line(args, world, res, results):
         sweep[str(rho)] = {"mpix_per_s": mpix_per_s(r, world), "ms_per_step": r["ms"],
                            "evals_per_s": world * 256 * r["pairs"] / (r["ms"] * 1e-3),
                            "fwd_kernel_ms": r["fwd_ms"], "bwd_moments_ms": r["bwd_ms"], "n_active": r["n_act"],
-                           "train_ms": r["train_ms"], "refresh_ms": r["refresh_ms"],
+                           "train_and_refresh_ms": r["train_refresh_ms"], "adam_and_update_ms": r["adam_update_ms"],
                            "pairs_per_view": r["pairs"] / r["V"],
                            "f_c": r["contrib"] / max(r["tile_evals"], 1),
                            "f_c_tile_granular": r["contrib"] / max(256 * r["pairs"], 1)}
@@ -1271,9 +1300,10 @@ def build_line(args, world, res, results):
         "config": {"workload": WORKLOAD, "splats": args.splats, "views_per_gpu": res["V"], "res": [res["W"], res["H"]],
                    "rho": res["rho"], "mask": args.kind, "n_active": res["n_act"], "refresh_views_S": res["S"],
                    "step": "one batch of the rank's 100 training views against one parameter state (R28: "
-                           "fwd+bwd each, gradients summed; a9 all-reduce at N>1) + one masked Adam step + one "
-                           "refresh (a7 FPS + score of the inactive set on S views, a8 update into a scratch "
-                           "bitmask); parameters restored between timed steps",
+                           "fwd+bwd each, gradients summed; a9 all-reduce at N>1) and, concurrently, the "
+                           "period's refresh on the same parameters (R35: a7 FPS + score of the inactive set on "
+                           "S views), then one masked Adam step and a8 (Eq. 8 update into a scratch bitmask); "
+                           "parameters restored between timed steps",
                    "l2": "flushed between timed steps (256 MB write)", "graph": not args.no_graph,
                    "streams": args.streams, "loss": args.loss,
                    "targets": ("uint8 [3][H][W] 8-bit training images (OIT_TARGET_U8)" if args.targets == "u8"
@@ -1285,7 +1315,8 @@ def build_line(args, world, res, results):
                                "note": "sum over the step's training views, single-stream roofline pass; the timed "
                                        "step runs views on several streams concurrently",
                                "concurrent_fwd_composite": res["fwd_ms"], "concurrent_bwd_moments": res["bwd_ms"]},
-        "segments_ms": {"train_views": res["train_ms"], "refresh": res["refresh_ms"]},
+        "segments_ms": {"train_views_and_refresh_overlapped": res["train_refresh_ms"],
+                        "adam_and_update": res["adam_update_ms"], "refresh_alone": res.get("refresh_alone_ms")},
         "roofline": {"kernel": kern, "bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TINSTR,
                      "unit": "T FP32 instr/s", "frac": achieved / FP32_PEAK_TINSTR, "traffic": traffic,
                      "algorithmic_instr_per_step": pk["algorithmic_instr_per_step"],

@@ -11,7 +11,7 @@ def _res(ms=16.0, V=100, W=800, H=800):
     return dict(ms=ms, fwd_ms=20.0, bwd_ms=15.0, clocks={"sm_mhz": 1965.0, "sm_max_mhz": 1965, "reasons": []},
                 ser_fwd_ms=7.7, ser_bwd_ms=7.0, pairs=28_500_000, contrib=2_110_000_000, tile_evals=7_300_000_000,
                 V=V, H=H, W=W, n_act=60_000, n_ina=240_000, S=5, launches=1600, rho=0.2, max_score_pairs=1,
-                train_ms=13.5, refresh_ms=2.5,
+                train_refresh_ms=13.5, adam_update_ms=0.1,
                 e2e=dict(ms=19.0, h2d=288_000_000, d2h=19_237_500))
 
 
