@@ -306,8 +306,11 @@ def test_select_views_bitexact(V, S, seed, refresh):
     assert np.array_equal(out.cpu().numpy(), O.fps(centers, S, seed, refresh))
 
 
-@pytest.mark.parametrize("loss", ["l1", "l2", "dssim"])
-def test_score_subsample_parity(loss):
+@pytest.mark.parametrize("loss,views", [("l1", [0, 3, 5]), ("l2", [0, 3, 5]), ("dssim", [0, 3, 5]),
+                                        ("l2", [0, 1, 2, 3, 4, 5]), ("l1", [4, 1, 5, 0, 2])])
+def test_score_subsample_parity(loss, views):
+    """The score of the inactive splats over the subsampled views (mean of R19) against the oracle;
+    5 and 6 views in one call span two groups of the multi-view epilogue (4 + 1, 4 + 2)."""
     L = _L()
     sc = synth.scene_c2(n=8000, n_views=6, res=96)
     mask = synth.active_mask(sc, 0.25, "clustered")
@@ -319,7 +322,6 @@ def test_score_subsample_parity(loss):
         img = O.render(sc.rows, sc.sigma, np.arange(sc.n), c, sc.bg)["image"]
         off = synth.rng(300 + k).uniform(0.01, 0.1, img.shape) * np.where(synth.rng(400 + k).random(img.shape) < 0.5, -1, 1)
         targets.append((img + off).astype(np.float32))
-    views = [0, 3, 5]
     ref, dsref, bnd, bsig = O.score_subsample(sc.rows, sc.sigma, sc.cams, targets, caches_o, act, ina, views, sc.bg,
                                               loss, with_bound="full")
     W, H = sc.cams[0]["width"], sc.cams[0]["height"]
