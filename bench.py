@@ -78,6 +78,7 @@ def parse():
     ap.add_argument("--res", type=int, default=800)
     ap.add_argument("--sub-rate", type=float, default=0.05, help="refresh subsample rate S/V")
     ap.add_argument("--streams", type=int, default=12, help="training views processed concurrently (one stream each)")
+    ap.add_argument("--score-streams", type=int, default=0, help="refresh streams (0: one per subsampled view)")
     ap.add_argument("--targets", choices=["u8", "f32"], default="u8",
                     help="training-image format: 8-bit (the datasets' PNGs, OIT_TARGET_U8) or fp32")
     ap.add_argument("--no-sweep", action="store_true")
@@ -426,7 +427,9 @@ class Workload:
         L.oit_select_views(self.centers, self.S, 2605, 0, self.views_dev)
         self.views_host = [int(x) for x in self.views_dev.cpu().numpy()]   # same refresh index each step
         self.score_cap = cap
-        nsc = max(1, min(self.S, self.n_streams))
+        # the refresh's streams: S views split over them (each call chains its views in groups of the
+        # multi-view epilogue); default: one stream per view up to the training stream count
+        nsc = max(1, min(self.S, args.score_streams if args.score_streams > 0 else self.n_streams))
         self.score_ws = [torch.empty(max(L.oit_score_workspace_bytes(cams[0], self.n_act, self.n_ina, cap), 256),
                                      dtype=torch.uint8, device=dev) for _ in range(nsc)]
         # the refresh's own streams: it runs concurrently with the training views (R35)
