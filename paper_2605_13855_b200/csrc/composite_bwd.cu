@@ -711,7 +711,7 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
     launch_quad_bin(cam, rec, pair_slot, tile_offsets, capacity, qlen, qslot, st);
     launch_build_items(tile_offsets, qlen, 4 * n_tiles, capacity, 32, 0, items, n_items, tile_nch, scratch, st);
     // persistent: up to 6 × 4 warps per SM (80 regs), fewer when views run concurrently; static items
-    const int blocks = sm_count() * persistent_ctas(6, concurrency);
+    const int blocks = sm_count() * persistent_ctas(resident_ctas<k_moments>(kMomentsThreads), concurrency);
     record_event(ev_begin, st);
     k_moments<<<blocks, kMomentsThreads, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), qslot, items, n_items,
                                                   reinterpret_cast<const float4*>(coef4), coefa, acc2d);
