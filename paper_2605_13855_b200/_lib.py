@@ -93,6 +93,8 @@ def lib() -> C.CDLL:
             "oit_composite_fwd_ex": (C.c_int, [cam_p, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, sz, i32, vp]),
             "oit_composite_fwd_loss": (C.c_int, [cam_p, vp, vp, vp, i64, vp, vp, vp, i32, vp, vp, sz, vp, sz, i32, i32,
                                                  vp]),
+            "oit_composite_fwd_loss_ex": (C.c_int, [cam_p, vp, vp, vp, i64, vp, vp, vp, i32, vp, vp, sz, vp, sz, i32,
+                                                    C.POINTER(KernelEvents), i32, vp]),
             "oit_loss_grad": (C.c_int, [cam_p, vp, vp, i32, vp, vp]),
             "oit_bwd_workspace_bytes": (sz, [cam_p, i32, i64]),
             "oit_composite_bwd": (C.c_int, [scene_p, cam_p, vp, i32, vp, vp, vp, i64, vp, vp, vp, f32, vp, vp,
@@ -117,6 +119,9 @@ def lib() -> C.CDLL:
             "oit_score_activeness": (C.c_int, [vp, i32, vp, vp, vp]),
             "oit_apply_activeness": (C.c_int, [vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         }
+        missing = [n for n in EXPORTED if n not in sig]
+        if missing:  # every entry point the binding calls is called through a declared prototype
+            raise OitError(f"no ctypes prototype for {missing}")
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
             fn.restype = res
