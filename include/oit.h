@@ -116,10 +116,14 @@ int oit_project_cull(const oit_scene* scene, const oit_camera* cam, const int32_
  * forward's summation order — are bit-identical run to run and to the oracle's.
  * tile_offsets has n_tiles+1 entries; *d_n_pairs (device int64) receives the total pair count
  * (if it exceeds pair_capacity, pair_slot holds only a prefix and the caller must re-call).
- * Scratch: ws of oit_bin_workspace_bytes(cam, pair_capacity) bytes (≈ 4·pair_capacity + 8·n_tiles;
- * 0 for a null camera or a negative capacity).
+ * Scratch: ws of at least oit_bin_workspace_bytes(cam, pair_capacity) bytes (≈ 4·pair_capacity +
+ * 8·n_tiles; 0 for a null camera or a negative capacity): a histogram, a scatter and a per-tile
+ * slot sort. With oit_bin_workspace_bytes_ex(cam, n_slots, pair_capacity) bytes (the former plus
+ * n_tiles·⌈n_slots/32⌉·4 B when that bitmap is ≤ 24 MB) the call bins small views through a
+ * (tile × slot) bitmap instead: one expansion and an ordered emission. Both give the same lists.
  * --------------------------------------------------------------------------------------- */
 size_t oit_bin_workspace_bytes(const oit_camera* cam, int64_t pair_capacity);
+size_t oit_bin_workspace_bytes_ex(const oit_camera* cam, int32_t n_slots, int64_t pair_capacity);
 int oit_bin_tiles(const oit_camera* cam, const float* rec, const int32_t* tiles_per_slot,
                   int32_t n_slots, int32_t* pair_slot, int64_t pair_capacity,
                   int32_t* tile_offsets, int64_t* d_n_pairs, void* ws, size_t ws_bytes,

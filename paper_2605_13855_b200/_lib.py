@@ -87,6 +87,7 @@ def lib() -> C.CDLL:
             "oit_num_tiles": (i32, [cam_p]),
             "oit_project_cull": (C.c_int, [scene_p, cam_p, vp, i32, vp, vp, vp]),
             "oit_bin_workspace_bytes": (sz, [cam_p, i64]),
+            "oit_bin_workspace_bytes_ex": (sz, [cam_p, i32, i64]),
             "oit_bin_tiles": (C.c_int, [cam_p, vp, vp, i32, vp, i64, vp, vp, vp, sz, vp]),
             "oit_fwd_workspace_bytes": (sz, [cam_p, i64]),
             "oit_composite_fwd": (C.c_int, [cam_p, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
@@ -130,7 +131,8 @@ def lib() -> C.CDLL:
     return _lib
 
 
-EXPORTED = ["oit_status_string", "oit_num_tiles", "oit_project_cull", "oit_bin_workspace_bytes", "oit_bin_tiles",
+EXPORTED = ["oit_status_string", "oit_num_tiles", "oit_project_cull", "oit_bin_workspace_bytes",
+            "oit_bin_workspace_bytes_ex", "oit_bin_tiles",
             "oit_fwd_workspace_bytes", "oit_composite_fwd", "oit_composite_fwd_ex", "oit_composite_fwd_loss",
             "oit_composite_fwd_loss_ex", "oit_loss_grad", "oit_bwd_workspace_bytes", "oit_composite_bwd", "oit_composite_bwd_ex",
             "oit_select_views", "oit_score_workspace_bytes", "oit_score_subsample", "oit_update_workspace_bytes",
@@ -182,8 +184,11 @@ def oit_project_cull(rows, sigma, cam, idx, rec, tiles_per_slot, stream=None):
                                   _ptr(tiles_per_slot), _stream(stream)), "oit_project_cull")
 
 
-def oit_bin_workspace_bytes(cam, pair_capacity: int) -> int:
-    return int(lib().oit_bin_workspace_bytes(C.byref(camera(cam)), int(pair_capacity)))
+def oit_bin_workspace_bytes(cam, pair_capacity: int, n_slots=None) -> int:
+    """Scratch of oit_bin_tiles; with n_slots, enough for the bitmap path on views that small."""
+    if n_slots is None:
+        return int(lib().oit_bin_workspace_bytes(C.byref(camera(cam)), int(pair_capacity)))
+    return int(lib().oit_bin_workspace_bytes_ex(C.byref(camera(cam)), int(n_slots), int(pair_capacity)))
 
 
 def oit_bin_tiles(cam, rec, tiles_per_slot, n_slots, pair_slot, tile_offsets, n_pairs, ws, stream=None):

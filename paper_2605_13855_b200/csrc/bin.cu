@@ -33,17 +33,20 @@ __device__ __forceinline__ void rect_of(const float4* rec, int k, int& x0, int& 
 // kScatter = false: histogram (counts[tile] += n); true: cursor claims and pair_slot writes.
 constexpr int kSlotsPerWarp = 8;
 
-template <bool kScatter>
+// kBitmap (the bitmap path, launch_bin): instead of counting, set bit `slot` of tile t's row in
+// bm[t · bm_words …] (a reduction, no return value; ordering comes from the row itself).
+template <bool kScatter, bool kBitmap = false>
 __global__ void __launch_bounds__(128) k_bin_expand(const float4* __restrict__ rec, const int32_t* __restrict__ tps,
                                                     int32_t n_slots, int TX, int W, int H, int32_t* __restrict__ cnt,
                                                     int32_t* __restrict__ pair_slot, int64_t capacity,
                                                     const int32_t* __restrict__ offsets, int n_tiles,
-                                                    int64_t* __restrict__ d_n_pairs, int64_t* __restrict__ d_max) {
+                                                    int64_t* __restrict__ d_n_pairs, int64_t* __restrict__ d_max,
+                                                    unsigned* __restrict__ bm = nullptr, int bm_words = 0) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  if (kScatter && gw == 0 && lane == 0) {
+  if (kScatter && !kBitmap && gw == 0 && lane == 0) {
     const int64_t n = offsets[n_tiles];
     *d_n_pairs = n;
     if (d_max) atomicMax(reinterpret_cast<unsigned long long*>(d_max), (unsigned long long)n);
@@ -90,6 +93,13 @@ __global__ void __launch_bounds__(128) k_bin_expand(const float4* __restrict__ r
       const float onC = __shfl_sync(FULL, nC, owner), olo = __shfl_sync(FULL, thr_lo, owner);
       const int ty = oy0 + local / ow, tx = ox0 + local % ow;
       // candidate tiles of the rectangle are kept by the exact tile test (DESIGN.md §3 step 12b)
+      if (kBitmap) {
+        if (j < total && spec_tile_keep(tx, ty, W, H, omx, omy, onA, onB, onC, olo)) {
+          const int slot = base + owner;
+          atomicOr(bm + (size_t)(ty * TX + tx) * bm_words + (slot >> 5), 1u << (slot & 31));
+        }
+        continue;
+      }
       if (j < total && spec_tile_keep(tx, ty, W, H, omx, omy, onA, onB, onC, olo)) {
         const int tile = ty * TX + tx;
         const unsigned peers = __match_any_sync(__activemask(), tile);
@@ -350,23 +360,129 @@ __global__ void __launch_bounds__(kSortThreads) k_tile_sort(const int32_t* __res
   bitmap_sort<kSortThreads>(SortGroup<kSortThreads>{tid, red}, bm, 32 * bm_words, seg, tmp + b, L, n_slots);
 }
 
+// ------------------------------------------------------------------ bitmap path ----------
+// For views whose (tile × slot) bitmap is small (n_tiles · ⌈n_slots/32⌉ words ≤ kBitmapMaxWords,
+// e.g. the C2 training views: 2,500 tiles × 60k slots = 18.75 MB), the pairs are binned through
+// that bitmap instead of a histogram + scatter + per-tile sort: ONE expansion sets bit `slot` of
+// tile t's row (atomicOr), a warp per tile counts its row (popcounts), the tile offsets are the
+// exclusive scan of the counts, and a CTA per tile writes its row's set bits in ascending order —
+// the stable counting sort's order (R15) by construction, one expansion instead of two.
+constexpr size_t kBitmapMaxWords = (size_t)6 << 20;  // 24 MB
+
+__host__ __device__ inline int bitmap_row_words(int32_t n_slots) { return (((n_slots + 31) / 32) + 3) & ~3; }
+
+__global__ void __launch_bounds__(256) k_bitmap_count(const unsigned* __restrict__ bm, int bm_words, int n_tiles,
+                                                      int32_t* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (t >= n_tiles) return;
+  const uint4* row = reinterpret_cast<const uint4*>(bm + (size_t)t * bm_words);
+  int c = 0;
+  for (int i = lane; i < bm_words / 4; i += 32) {
+    const uint4 v = __ldcg(row + i);
+    c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) counts[t] = c;
+}
+
+// One CTA per tile (the tile's count is known here: empty tiles exit at once); thread i owns the
+// consecutive uint4 groups [i·per, i·per + per) of the row: popcounts, a CTA scan for the thread's
+// first position, then its set bits in ascending order.
+constexpr int kEmitThreads = 128;
+__global__ void __launch_bounds__(kEmitThreads) k_bitmap_emit(const unsigned* __restrict__ bm, int bm_words,
+                                                              int n_tiles, const int32_t* __restrict__ offsets,
+                                                              int64_t capacity, int32_t* __restrict__ pair_slot,
+                                                              int64_t* __restrict__ d_n_pairs,
+                                                              int64_t* __restrict__ d_max) {
+  __shared__ int s_w[kEmitThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int t = blockIdx.x;
+  if (t == 0 && tid == 0) {
+    const int64_t n = offsets[n_tiles];
+    *d_n_pairs = n;
+    if (d_max) atomicMax(reinterpret_cast<unsigned long long*>(d_max), (unsigned long long)n);
+  }
+  const int b = offsets[t];
+  if (offsets[t + 1] == b) return;  // CTA-uniform
+  const uint4* row = reinterpret_cast<const uint4*>(bm + (size_t)t * bm_words);
+  const int n4 = bm_words / 4, per = (n4 + kEmitThreads - 1) / kEmitThreads;
+  const int g0 = tid * per, g1 = min(g0 + per, n4);
+  int c = 0;
+  for (int g = g0; g < g1; g++) {
+    const uint4 v = __ldcg(row + g);
+    c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+  }
+  int inc = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_w[wid] = inc;
+  __syncthreads();
+  int pre = 0;
+#pragma unroll
+  for (int w = 0; w < kEmitThreads / 32; w++)
+    if (w < wid) pre += s_w[w];
+  int64_t pos = (int64_t)b + pre + inc - c;
+  for (int g = g0; g < g1; g++) {
+    const uint4 v = __ldcg(row + g);
+    const unsigned w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      unsigned m = w4[q];
+      const int s0 = 32 * (4 * g + q);
+      while (m) {
+        const int bit = __ffs(m) - 1;
+        m &= m - 1;
+        if (pos < capacity) pair_slot[pos] = s0 + bit;
+        pos++;
+      }
+    }
+  }
+}
+
 size_t bin_ws_bytes(int32_t n_tiles, int64_t capacity) {
   return align_up((size_t)(n_tiles + 1) * sizeof(int32_t)) + scan_tmp_bytes(n_tiles) +
          align_up((size_t)(capacity > 0 ? capacity : 1) * sizeof(int32_t));
 }
 
+size_t bin_bitmap_bytes(int32_t n_tiles, int32_t n_slots) {
+  if (n_slots <= 0) return 0;
+  const size_t words = (size_t)n_tiles * bitmap_row_words(n_slots);
+  return words <= kBitmapMaxWords ? align_up(words * sizeof(unsigned)) : 0;
+}
+
 void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_slot, int32_t n_slots,
                 int32_t* pair_slot, int64_t capacity, int32_t* tile_offsets, int64_t* d_n_pairs,
-                int64_t* d_max_pairs, void* ws, cudaStream_t st, bool sorted) {
+                int64_t* d_max_pairs, void* ws, cudaStream_t st, bool sorted, size_t ws_bytes) {
   int n_tiles = cam.TX * cam.TY;
   Carve cv(ws);
   int32_t* counts = cv.take<int32_t>(n_tiles + 1);
   void* tmp = cv.take<char>(scan_tmp_bytes(n_tiles));
   int32_t* sort_tmp = cv.take<int32_t>(capacity > 0 ? capacity : 1);
-  cudaMemsetAsync(counts, 0, sizeof(int32_t) * n_tiles, st);
   const float4* r4 = reinterpret_cast<const float4*>(rec);
   const int warps = n_slots > 0 ? (n_slots + kSlotsPerWarp - 1) / kSlotsPerWarp : 1;
   const int blocks = (warps + 3) / 4;
+  const size_t bmb = bin_bitmap_bytes(n_tiles, n_slots);
+  if (sorted && bmb > 0 && ws_bytes >= cv.off + bmb) {
+    // bitmap path (small views): one expansion, ordered emission
+    unsigned* bm = cv.take<unsigned>(bmb / sizeof(unsigned));
+    const int bw = bitmap_row_words(n_slots);
+    cudaMemsetAsync(bm, 0, bmb, st);
+    k_bin_expand<true, true><<<blocks, 128, 0, st>>>(r4, tiles_per_slot, n_slots, cam.TX, cam.W, cam.H, counts,
+                                                     pair_slot, capacity, tile_offsets, n_tiles, d_n_pairs,
+                                                     d_max_pairs, bm, bw);
+    const int tblocks = (n_tiles * 32 + 255) / 256;
+    k_bitmap_count<<<tblocks, 256, 0, st>>>(bm, bw, n_tiles, counts);
+    launch_exclusive_scan(counts, tile_offsets, n_tiles, tmp, st);
+    k_bitmap_emit<<<n_tiles, kEmitThreads, 0, st>>>(bm, bw, n_tiles, tile_offsets, capacity, pair_slot, d_n_pairs,
+                                                     d_max_pairs);
+    return;
+  }
+  cudaMemsetAsync(counts, 0, sizeof(int32_t) * n_tiles, st);
   if (n_slots > 0)
     k_bin_expand<false><<<blocks, 128, 0, st>>>(r4, tiles_per_slot, n_slots, cam.TX, cam.W, cam.H, counts, pair_slot, capacity,
                                                 tile_offsets, n_tiles, d_n_pairs, d_max_pairs);

@@ -82,6 +82,12 @@ size_t oit_bin_workspace_bytes(const oit_camera* cam, int64_t pair_capacity) {
   return bin_ws_bytes(oit_num_tiles(cam), pair_capacity);
 }
 
+size_t oit_bin_workspace_bytes_ex(const oit_camera* cam, int32_t n_slots, int64_t pair_capacity) {
+  if (!cam || pair_capacity < 0 || n_slots < 0) return 0;
+  const int32_t nt = oit_num_tiles(cam);
+  return bin_ws_bytes(nt, pair_capacity) + bin_bitmap_bytes(nt, n_slots);
+}
+
 int oit_bin_tiles(const oit_camera* cam, const float* rec, const int32_t* tiles_per_slot, int32_t n_slots,
                   int32_t* pair_slot, int64_t pair_capacity, int32_t* tile_offsets, int64_t* d_n_pairs, void* ws,
                   size_t ws_bytes, oit_stream_t stream) {
@@ -92,7 +98,7 @@ int oit_bin_tiles(const oit_camera* cam, const float* rec, const int32_t* tiles_
   if (pair_capacity > kMaxPairs) return OIT_ESHAPE;
   if (ws_bytes < oit_bin_workspace_bytes(cam, pair_capacity)) return OIT_ECAPACITY;
   launch_bin(dev_cam(cam), rec, tiles_per_slot, n_slots, pair_slot, pair_capacity, tile_offsets, d_n_pairs, nullptr,
-             ws, S(stream));
+             ws, S(stream), true, ws_bytes);
   return launch_status();
 }
 

@@ -20,10 +20,14 @@ void launch_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, void* tmp
                            int32_t* out2 = nullptr);
 
 // bin.cu — a2
+// bin_ws_bytes: the histogram + scatter + per-tile sort path (any size); bin_bitmap_bytes: the extra
+// scratch of the bitmap path (0 if the view's bitmap is too large for it). launch_bin takes the
+// bitmap path when sorted lists are asked for and ws_bytes covers both.
 size_t bin_ws_bytes(int32_t n_tiles, int64_t capacity);
+size_t bin_bitmap_bytes(int32_t n_tiles, int32_t n_slots);
 void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_slot, int32_t n_slots,
                 int32_t* pair_slot, int64_t capacity, int32_t* tile_offsets, int64_t* d_n_pairs,
-                int64_t* d_max_pairs, void* ws, cudaStream_t st, bool sorted = true);
+                int64_t* d_max_pairs, void* ws, cudaStream_t st, bool sorted = true, size_t ws_bytes = 0);
 
 // composite_fwd.cu — a3
 // Fused a4 for training views (pixel-local L1/L2 loss): target fp32 or uint8 [3][H][W]; the

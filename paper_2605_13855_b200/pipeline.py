@@ -29,7 +29,7 @@ class ViewPipeline:
         self.pairs = torch.empty(max(self.capacity, 1), dtype=torch.int32, device=dev)
         self.offs = torch.empty(self.n_tiles + 1, dtype=torch.int32, device=dev)
         self.n_pairs = torch.zeros(1, dtype=torch.int64, device=dev)
-        self.bin_ws = _ws(L.oit_bin_workspace_bytes(cam, self.capacity), dev)
+        self.bin_ws = _ws(L.oit_bin_workspace_bytes(cam, self.capacity, n_slots=self.max_slots), dev)
         self.fwd_ws = _ws(L.oit_fwd_workspace_bytes(cam, self.capacity), dev)
         self.bwd_ws = _ws(L.oit_bwd_workspace_bytes(cam, self.max_slots, self.capacity), dev)
         self.state = torch.empty((5, self.n_tiles, 256), dtype=torch.float32, device=dev)

@@ -93,6 +93,20 @@ def test_project_cull_empty_and_errors():
 
 
 # ------------------------------------------------------------------ a2 bin_tiles ---------
+def _rebin_sort_path(p, n_slots):
+    """oit_bin_tiles again over the pipeline's records with the MINIMAL workspace (histogram +
+    scatter + per-tile sort path; the pipeline's own workspace takes the bitmap path on small views)."""
+    L = _L()
+    ws = torch.empty(L.oit_bin_workspace_bytes(p.cam, p.capacity), dtype=torch.uint8, device=DEV)
+    pairs = torch.full_like(p.pairs, -1)
+    offs = torch.zeros_like(p.offs)
+    npairs = torch.zeros(1, dtype=torch.int64, device=DEV)
+    L.oit_bin_tiles(p.cam, p.rec, p.tps, n_slots, pairs, offs, npairs, ws)
+    torch.cuda.synchronize()
+    n = int(npairs.item())
+    return pairs[:n].cpu().numpy(), offs.cpu().numpy()
+
+
 def test_bin_tiles_bitexact(scene):
     idx = np.arange(scene.n, dtype=np.int32)
     for cam in scene.cams:
@@ -105,6 +119,9 @@ def test_bin_tiles_bitexact(scene):
         assert n == len(ref_pairs)
         assert np.array_equal(offs, ref_offs)
         assert np.array_equal(pairs, ref_pairs)  # ascending slot order inside each tile (R15)
+        # both binning paths (bitmap with the pipeline's workspace, sort with the minimal one)
+        sp, so = _rebin_sort_path(p, scene.n)
+        assert np.array_equal(so, ref_offs) and np.array_equal(sp, ref_pairs)
 
 
 def _long_list_scene(n_total, stride, res=48):
@@ -143,6 +160,8 @@ def test_bin_tiles_long_lists_sorted(n_total, stride):
     assert np.diff(ref_offs).max() >= n_total // stride - 1
     assert np.array_equal(p.offs.cpu().numpy(), ref_offs)
     assert np.array_equal(p.pairs[:n].cpu().numpy(), ref_pairs)
+    sp, so = _rebin_sort_path(p, n_total)   # the sort path on the same records
+    assert np.array_equal(so, ref_offs) and np.array_equal(sp, ref_pairs)
 
 
 def test_forward_bitwise_reproducible_run_to_run():
