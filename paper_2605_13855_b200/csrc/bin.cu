@@ -467,8 +467,9 @@ void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_sl
   const int warps = n_slots > 0 ? (n_slots + kSlotsPerWarp - 1) / kSlotsPerWarp : 1;
   const int blocks = (warps + 3) / 4;
   const size_t bmb = bin_bitmap_bytes(n_tiles, n_slots);
-  if (sorted && bmb > 0 && ws_bytes >= cv.off + bmb) {
-    // bitmap path (small views): one expansion, ordered emission
+  if (bmb > 0 && ws_bytes >= cv.off + bmb) {
+    // bitmap path (small views): one expansion, ordered emission (also when order is not asked
+    // for: it is the cheaper path wherever its bitmap fits)
     unsigned* bm = cv.take<unsigned>(bmb / sizeof(unsigned));
     const int bw = bitmap_row_words(n_slots);
     cudaMemsetAsync(bm, 0, bmb, st);

@@ -4,6 +4,8 @@
 #include <cstring>
 
 #include "../../include/oit.h"
+#include <algorithm>
+
 #include "kernels.h"
 
 using namespace oit;
@@ -308,6 +310,7 @@ struct ScoreWs {
   int32_t *tps_a, *tps_s, *pairs, *offs;
   int64_t* npairs;
   void *bin_ws, *bwd_ws, *fwd_ws, *dssim_ws;
+  size_t bin_ws_bytes;
   size_t total;
 };
 
@@ -328,7 +331,9 @@ static ScoreWs score_layout(void* ws, const oit_camera* cam, int32_t n_active, i
   w.state = cv.take<float>((size_t)nt * kTilePx * 5);
   w.coef4 = cv.take<float>((size_t)nt * kTilePx * 4);
   w.coefa = cv.take<float>((size_t)nt * kTilePx);
-  w.bin_ws = cv.take<char>(bin_ws_bytes(nt, cap));
+  // (room for the bitmap path of the active set's bin when that view is small, see bin.cu)
+  w.bin_ws_bytes = bin_ws_bytes(nt, cap) + std::max(bin_bitmap_bytes(nt, n_active), bin_bitmap_bytes(nt, n_score));
+  w.bin_ws = cv.take<char>(w.bin_ws_bytes);
   w.fwd_ws = cv.take<char>(fwd_ws_bytes(nt, cap));
   w.bwd_ws = cv.take<char>(bwd_ws_bytes(nt, n_score, cap));
   w.dssim_ws = cv.take<char>(dssim_bytes(cam));
@@ -371,7 +376,8 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
     DevCam dc = dev_cam(&cams_host[j], bg_host);
     // Rasterize(G, I^pre_j): the active set over the view's cache of the frozen set (R16)
     launch_project(dc, scene->rows, scene->sigma, active_idx, n_active, w.rec_a, w.tps_a, st);
-    launch_bin(dc, w.rec_a, w.tps_a, n_active, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st);
+    launch_bin(dc, w.rec_a, w.tps_a, n_active, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st,
+               true, w.bin_ws_bytes);
     const float* cache = caches_host ? caches_host[j] : nullptr;
     if ((loss & ~OIT_TARGET_U8) != 2) {
       // L_j (L1/L2, pixel-local) and the backward coefficients in the forward's epilogue (a3 + a4)
@@ -395,7 +401,7 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
     launch_project(dc, scene->rows, scene->sigma, score_idx, n_score, rec_s, w.tps_s, st);
     // (the scored lists feed the backward only: no per-tile slot sort, see bin.cu)
     launch_bin(dc, rec_s, w.tps_s, n_score, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st,
-               false);
+               false, w.bin_ws_bytes);
     launch_composite_bwd(dc, scene->rows, scene->sigma, score_idx, n_score, rec_s, w.pairs, w.offs, pair_capacity,
                          w.coef4, w.coefa, scale, score_grad, dL_dsigma, nullptr, w.bwd_ws, st, nullptr, nullptr, 0,
                          concurrency, w.acc_s[in_group]);

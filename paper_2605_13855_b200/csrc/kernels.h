@@ -22,7 +22,7 @@ void launch_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, void* tmp
 // bin.cu — a2
 // bin_ws_bytes: the histogram + scatter + per-tile sort path (any size); bin_bitmap_bytes: the extra
 // scratch of the bitmap path (0 if the view's bitmap is too large for it). launch_bin takes the
-// bitmap path when sorted lists are asked for and ws_bytes covers both.
+// bitmap path whenever ws_bytes covers both.
 size_t bin_ws_bytes(int32_t n_tiles, int64_t capacity);
 size_t bin_bitmap_bytes(int32_t n_tiles, int32_t n_slots);
 void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_slot, int32_t n_slots,
