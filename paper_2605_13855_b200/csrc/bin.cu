@@ -361,13 +361,14 @@ __global__ void __launch_bounds__(kSortThreads) k_tile_sort(const int32_t* __res
 }
 
 // ------------------------------------------------------------------ bitmap path ----------
-// For views whose (tile × slot) bitmap is small (n_tiles · ⌈n_slots/32⌉ words ≤ kBitmapMaxWords,
-// e.g. the C2 training views: 2,500 tiles × 60k slots = 18.75 MB), the pairs are binned through
+// For views whose (tile × slot) bitmap fits kBitmapMaxWords (128 MB: e.g. C2 training views, 2,500
+// tiles × 60k slots = 18.75 MB, and up to 300k slots; not C3's 6,700 tiles × 300k), the pairs are
+// binned through
 // that bitmap instead of a histogram + scatter + per-tile sort: ONE expansion sets bit `slot` of
 // tile t's row (atomicOr), a warp per tile counts its row (popcounts), the tile offsets are the
 // exclusive scan of the counts, and a CTA per tile writes its row's set bits in ascending order —
 // the stable counting sort's order (R15) by construction, one expansion instead of two.
-constexpr size_t kBitmapMaxWords = (size_t)6 << 20;  // 24 MB
+constexpr size_t kBitmapMaxWords = (size_t)32 << 20;  // 128 MB
 
 __host__ __device__ inline int bitmap_row_words(int32_t n_slots) { return (((n_slots + 31) / 32) + 3) & ~3; }
 

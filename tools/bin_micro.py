@@ -14,6 +14,9 @@ from paper_2605_13855_b200 import _lib as L  # noqa: E402
 from paper_2605_13855_b200 import synth  # noqa: E402
 from paper_2605_13855_b200.pipeline import ViewPipeline  # noqa: E402
 
+if os.environ.get("OIT_DEV_LIB"):  # A/B against another build of the library (dev only)
+    L.LIB_PATH = os.environ["OIT_DEV_LIB"]
+
 
 def main():
     ap = argparse.ArgumentParser()
