@@ -365,27 +365,44 @@ __global__ void __launch_bounds__(kSortThreads) k_tile_sort(const int32_t* __res
 // tiles × 60k slots = 18.75 MB, and up to 300k slots; not C3's 6,700 tiles × 300k), the pairs are
 // binned through
 // that bitmap instead of a histogram + scatter + per-tile sort: ONE expansion sets bit `slot` of
-// tile t's row (atomicOr), a warp per tile counts its row (popcounts), the tile offsets are the
+// tile t's row (atomicOr), a CTA per tile counts its row (popcounts), the tile offsets are the
 // exclusive scan of the counts, and a CTA per tile writes its row's set bits in ascending order —
 // the stable counting sort's order (R15) by construction, one expansion instead of two.
 constexpr size_t kBitmapMaxWords = (size_t)32 << 20;  // 128 MB
 
 __host__ __device__ inline int bitmap_row_words(int32_t n_slots) { return (((n_slots + 31) / 32) + 3) & ~3; }
 
-__global__ void __launch_bounds__(256) k_bitmap_count(const unsigned* __restrict__ bm, int bm_words, int n_tiles,
-                                                      int32_t* __restrict__ counts) {
-  const int lane = threadIdx.x & 31;
-  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (t >= n_tiles) return;
+// One CTA per tile row: every thread sums the popcounts of its (strided) uint4 groups, loads
+// issued four at a time, then a block reduction.
+constexpr int kCountThreads = 128;
+__global__ void __launch_bounds__(kCountThreads) k_bitmap_count(const unsigned* __restrict__ bm, int bm_words,
+                                                                int n_tiles, int32_t* __restrict__ counts) {
+  __shared__ int s_w[kCountThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int t = blockIdx.x;
   const uint4* row = reinterpret_cast<const uint4*>(bm + (size_t)t * bm_words);
+  const int n4 = bm_words / 4;
   int c = 0;
-  for (int i = lane; i < bm_words / 4; i += 32) {
-    const uint4 v = __ldcg(row + i);
-    c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+  for (int i0 = tid; i0 < n4; i0 += 4 * kCountThreads) {
+    uint4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int i = i0 + k * kCountThreads;
+      v[k] = i < n4 ? __ldcg(row + i) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) c += __popc(v[k].x) + __popc(v[k].y) + __popc(v[k].z) + __popc(v[k].w);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if (lane == 0) counts[t] = c;
+  if (lane == 0) s_w[wid] = c;
+  __syncthreads();
+  if (tid == 0) {
+    int sum = 0;
+#pragma unroll
+    for (int w = 0; w < kCountThreads / 32; w++) sum += s_w[w];
+    counts[t] = sum;
+  }
 }
 
 // One CTA per tile (the tile's count is known here: empty tiles exit at once); thread i owns the
@@ -411,6 +428,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_bitmap_emit(const unsigned* __
   const int n4 = bm_words / 4, per = (n4 + kEmitThreads - 1) / kEmitThreads;
   const int g0 = tid * per, g1 = min(g0 + per, n4);
   int c = 0;
+#pragma unroll 4
   for (int g = g0; g < g1; g++) {
     const uint4 v = __ldcg(row + g);
     c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
@@ -477,8 +495,7 @@ void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_sl
     k_bin_expand<true, true><<<blocks, 128, 0, st>>>(r4, tiles_per_slot, n_slots, cam.TX, cam.W, cam.H, counts,
                                                      pair_slot, capacity, tile_offsets, n_tiles, d_n_pairs,
                                                      d_max_pairs, bm, bw);
-    const int tblocks = (n_tiles * 32 + 255) / 256;
-    k_bitmap_count<<<tblocks, 256, 0, st>>>(bm, bw, n_tiles, counts);
+    k_bitmap_count<<<n_tiles, kCountThreads, 0, st>>>(bm, bw, n_tiles, counts);
     launch_exclusive_scan(counts, tile_offsets, n_tiles, tmp, st);
     k_bitmap_emit<<<n_tiles, kEmitThreads, 0, st>>>(bm, bw, n_tiles, tile_offsets, capacity, pair_slot, d_n_pairs,
                                                      d_max_pairs);
