@@ -95,7 +95,9 @@ def parse():
     ap.add_argument("--no-c4", action="store_true", help="skip the configs[3] (C4 score sweep) measurement")
     ap.add_argument("--no-c5", action="store_true", help="skip the configs[4] (C5 view-sharded step) measurement")
     ap.add_argument("--c5-rhos", type=float, nargs="+", default=[0.1, 1.0], help="C5 active fractions")
-    ap.add_argument("--profile-once", action="store_true", help="run one eager step (for ncu) and exit")
+    ap.add_argument("--profile-once", action="store_true",
+                    help="run one eager step between cudaProfilerStart/Stop (for ncu --profile-from-start off), "
+                         "print the claimed kernel count, exit")
     return ap.parse_args()
 
 
@@ -574,8 +576,12 @@ class Workload:
         nw = (self.n + 31) // 32
         a, s = self.n_act, self.n_ina
         proj = lambda n: 1 if n > 0 else 0  # noqa: E731
-        # k_bin_expand<0> (n > 0), the tile scan, k_bin_expand<1>, k_tile_sort (n > 0)
+        # bitmap path (the view's (tile × slot) bitmap ≤ 128 MB): k_bin_expand<1,1>, k_bitmap_count,
+        # the scan, k_bitmap_emit; otherwise k_bin_expand<0> (n > 0), the scan, k_bin_expand<1>,
+        # k_tile_sort (n > 0, sorted lists only)
+        bitmap = lambda n: n > 0 and nt * ((((n + 31) // 32) + 3) // 4 * 4) <= (32 << 20)  # noqa: E731
         binn = lambda n: (2 if n > 0 else 0) + scan_kernels(nt) + 1  # noqa: E731
+        bin_unsorted = lambda n: binn(n) if bitmap(n) else binn(n) - (1 if n > 0 else 0)  # noqa: E731
         fwd = 3                                            # item histogram + emission, k_fwd_items
         # k_quad_bin, item histogram + emission, k_moments, k_epilogue (none for an empty slot list)
         bwd = lambda n: 5 if n > 0 else 0  # noqa: E731
@@ -584,8 +590,8 @@ class Workload:
         train = self.V * (proj(a) + binn(a) + fwd + bwd(a) + lossk) + 1   # + k_adam
         refresh = 1                                        # k_fps
         if s > 0:
-            # (the scored set's lists feed the backward only: no k_tile_sort)
-            refresh += self.S * (proj(a) + binn(a) + fwd + lossk + proj(s) + binn(s) - 1 + bwd(s))
+            # (the scored set's lists feed the backward only: no k_tile_sort on the histogram path)
+            refresh += self.S * (proj(a) + binn(a) + fwd + lossk + proj(s) + bin_unsorted(s) + bwd(s))
             if self.world > 1:   # k_row_activeness + k_apply_bits, k_popc3, 3 scans, k_emit3
                 refresh += 1 + 1 + 1 + 3 * scan_kernels(nw) + 1
             else:                # k_update_bits, k_popc3, 3 scans, k_emit3
@@ -619,6 +625,19 @@ def run_ours(args):
     all_cams = synth.scene_c2(n=10, n_views=args.views * world, res=args.res).cams
     cams = [all_cams[v] for v in D.views_of_rank(args.views, rank)]   # weak scaling: V views per rank
 
+    if args.profile_once:
+        # one eager step of the headline workload between cudaProfilerStart/Stop (run under
+        # `ncu --profile-from-start off`): the launch list of exactly one step, to check the
+        # gpu_launches claim (kernel_launches) against; prints the claim
+        wl = Workload(args, torch, L, synth, args.rho, cams, rank, world)
+        wl.train_and_refresh(); wl.adam(); wl.update()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        wl.train_and_refresh(); wl.adam(); wl.update()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        print(json.dumps({"kernel_launches_claimed_per_step": wl.kernel_launches()}), flush=True)
+        return 0
     rhos = [args.rho] + ([] if args.no_sweep else [r for r in (1.0, 0.05) if r != args.rho])
     results = {}
     headline = None

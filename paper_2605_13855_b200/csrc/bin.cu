@@ -468,7 +468,16 @@ size_t bin_ws_bytes(int32_t n_tiles, int64_t capacity) {
          align_up((size_t)(capacity > 0 ? capacity : 1) * sizeof(int32_t));
 }
 
+// Scratch the bitmap path needs for calls of up to n_slots slots: the bitmap of n_slots, or (when
+// that exceeds kBitmapMaxWords) the largest bitmap the path accepts, so smaller calls on the same
+// workspace still take it.
 size_t bin_bitmap_bytes(int32_t n_tiles, int32_t n_slots) {
+  if (n_slots <= 0) return 0;
+  const size_t words = std::min((size_t)n_tiles * bitmap_row_words(n_slots), kBitmapMaxWords);
+  return align_up(words * sizeof(unsigned));
+}
+
+static size_t bitmap_bytes_exact(int32_t n_tiles, int32_t n_slots) {
   if (n_slots <= 0) return 0;
   const size_t words = (size_t)n_tiles * bitmap_row_words(n_slots);
   return words <= kBitmapMaxWords ? align_up(words * sizeof(unsigned)) : 0;
@@ -485,7 +494,7 @@ void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_sl
   const float4* r4 = reinterpret_cast<const float4*>(rec);
   const int warps = n_slots > 0 ? (n_slots + kSlotsPerWarp - 1) / kSlotsPerWarp : 1;
   const int blocks = (warps + 3) / 4;
-  const size_t bmb = bin_bitmap_bytes(n_tiles, n_slots);
+  const size_t bmb = bitmap_bytes_exact(n_tiles, n_slots);
   if (bmb > 0 && ws_bytes >= cv.off + bmb) {
     // bitmap path (small views): one expansion, ordered emission (also when order is not asked
     // for: it is the cheaper path wherever its bitmap fits)
