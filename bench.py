@@ -586,8 +586,10 @@ class Workload:
         # k_quad_bin, item histogram + emission, k_moments, k_epilogue (none for an empty slot list)
         bwd = lambda n: 5 if n > 0 else 0  # noqa: E731
         lossk = 4 if self.loss == "dssim" else 0   # resolve + 2 SSIM stencil passes + k_coef
-        # training views with L1/L2: a4 fused into the forward's epilogue (no k_coef launch)
-        train = self.V * (proj(a) + binn(a) + fwd + bwd(a) + lossk) + 1   # + k_adam
+        # training views with L1/L2: a4 fused into the forward's epilogue (no k_coef launch), which
+        # also writes the quadrant lists (no k_quad_bin in the backward)
+        bwd_train = (lambda n: 4 if n > 0 else 0) if self.loss in ("l1", "l2") else bwd  # noqa: E731
+        train = self.V * (proj(a) + binn(a) + fwd + bwd_train(a) + lossk) + 1   # + k_adam
         refresh = 1                                        # k_fps
         if s > 0:
             # (the scored set's lists feed the backward only: no k_tile_sort on the histogram path)

@@ -132,6 +132,8 @@ int oit_composite_fwd_ex(const oit_camera* cam, const float* rec, const int32_t*
   return launch_status();
 }
 
+static size_t dssim_bytes(const oit_camera* cam);
+
 int oit_composite_fwd_loss_ex(const oit_camera* cam, const float* rec, const int32_t* pair_slot,
                            const int32_t* tile_offsets, int64_t pair_capacity, const float bg_host[3], const float* base,
                            const void* target, int32_t loss, float* state, void* ws, size_t ws_bytes, void* bwd_ws,
@@ -148,13 +150,17 @@ int oit_composite_fwd_loss_ex(const oit_camera* cam, const float* rec, const int
       bwd_ws_bytes < oit_bwd_workspace_bytes(cam, n_slots, pair_capacity))
     return OIT_ECAPACITY;
   const int32_t nt = oit_num_tiles(cam);
-  Carve cv(bwd_ws);  // the coefficient region oit_composite_bwd_ex carves first
-  FwdLoss fl;
+  Carve cv(bwd_ws);  // the regions oit_composite_bwd_ex carves: coefficients, D-SSIM scratch, then
+  FwdLoss fl;        // the backward's own workspace, whose quadrant lists the forward writes
   fl.target = target;
   fl.target_u8 = (loss & OIT_TARGET_U8) != 0;
   fl.loss = l;
   fl.coef4 = reinterpret_cast<float4*>(cv.take<float>((size_t)nt * kTilePx * 4));
   fl.coefa = cv.take<float>((size_t)nt * kTilePx);
+  cv.take<char>(dssim_bytes(cam));
+  const BwdWs bl = bwd_ws_layout(cv.base + cv.off, nt, n_slots, pair_capacity);
+  fl.qlen = bl.qlen;
+  fl.qslot = bl.qslot;
   fl.listed_tiles_only = true;
   launch_composite_fwd(dev_cam(cam, bg_host), rec, pair_slot, tile_offsets, pair_capacity, base, nullptr, nullptr,
                        state, nullptr, S(stream), nullptr, ws, concurrency, fl,
@@ -265,7 +271,8 @@ int oit_composite_bwd_ex(const oit_scene* scene, const oit_camera* cam, const in
   launch_composite_bwd(dc, scene->rows, scene->sigma, idx, n_slots, rec, pair_slot, tile_offsets, pair_capacity,
                        coef4, coefa, scale, grad, dL_dsigma, dL_dcov, rest, S(stream),
                        ev ? static_cast<cudaEvent_t>(ev->moments_begin) : nullptr,
-                       ev ? static_cast<cudaEvent_t>(ev->moments_end) : nullptr, 0, concurrency);
+                       ev ? static_cast<cudaEvent_t>(ev->moments_end) : nullptr, 0, concurrency, nullptr,
+                       !target && (loss & OIT_COEF_IN_WS));
   return launch_status();
 }
 

@@ -677,11 +677,29 @@ void launch_u8_to_f32(const uint8_t* src, int64_t n, float* dst, cudaStream_t st
   if (n > 0) k_u8_to_f32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, n, dst);
 }
 
+BwdWs bwd_ws_layout(void* ws, int32_t n_tiles, int32_t n_slots, int64_t capacity) {
+  const int64_t qcap = 4 * capacity;
+  const int64_t max_items = qcap / 32 + 4 * n_tiles + 1;
+  // the regions that do not depend on n_slots first, so a caller that sized the workspace for more
+  // slots than a given call uses (the fused forward's n_slots vs the backward's) sees the same
+  // quadrant lists; the moment rows last
+  Carve cv(ws);
+  BwdWs l;
+  l.items = cv.take<int4>(max_items);
+  l.n_items = cv.take<int32_t>(4);
+  l.tile_nch = cv.take<int32_t>(4 * n_tiles + 1);
+  l.scratch = cv.take<int32_t>(68);
+  l.qlen = cv.take<int32_t>(4 * n_tiles + 1);
+  l.qslot = cv.take<int32_t>(qcap);
+  l.acc2d = cv.take<float>((size_t)n_slots * 12);
+  return l;
+}
+
 void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sigma, const int32_t* idx,
                           int32_t n_slots, const float* rec, const int32_t* pair_slot, const int32_t* tile_offsets,
                           int64_t capacity, const float* coef4, const float* coefa, float scale, float* grad,
                           float* dL_dsigma, float* dL_dcov, void* ws, cudaStream_t st, cudaEvent_t ev_begin,
-                          cudaEvent_t ev_end, int variant, int concurrency, float* acc_out) {
+                          cudaEvent_t ev_end, int variant, int concurrency, float* acc_out, bool quads_ready) {
   if (n_slots <= 0) {
     record_event(ev_begin, st);
     record_event(ev_end, st);
@@ -690,16 +708,16 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
   const int n_tiles = cam.TX * cam.TY;
   const int64_t qcap = 4 * capacity;
   const int64_t max_items = qcap / 32 + 4 * n_tiles + 1;
-  Carve cv(ws);
-  float* acc2d = cv.take<float>((size_t)n_slots * 12);
-  if (acc_out) acc2d = acc_out;  // moments only: the caller runs the (multi-view) epilogue
-  int4* items = cv.take<int4>(max_items);
-  int32_t* n_items = cv.take<int32_t>(4);
-  int32_t* tile_nch = cv.take<int32_t>(4 * n_tiles + 1);
-  int32_t* scratch = cv.take<int32_t>(68);
-  cv.take<int32_t>(4);  // (formerly the item counter; keeps the workspace layout)
-  int32_t* qlen = cv.take<int32_t>(4 * n_tiles + 1);
-  int32_t* qslot = cv.take<int32_t>(qcap);
+  const BwdWs l = bwd_ws_layout(ws, n_tiles, n_slots, capacity);
+  float* acc2d = acc_out ? acc_out : l.acc2d;  // acc_out: moments only, the caller runs the epilogue
+  int4* items = l.items;
+  int32_t* n_items = l.n_items;
+  int32_t* tile_nch = l.tile_nch;
+  int32_t* scratch = l.scratch;
+  int32_t* qlen = l.qlen;
+  int32_t* qslot = l.qslot;
+  (void)max_items;
+  (void)qcap;
   cudaMemsetAsync(acc2d, 0, sizeof(float) * 12 * (size_t)n_slots, st);
   if (variant == 1) {  // NEXT-4 ablation: per-pixel backward over the tile lists
     record_event(ev_begin, st);
@@ -707,8 +725,9 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
                                              capacity, reinterpret_cast<const float4*>(coef4), coefa, acc2d);
     record_event(ev_end, st);
   } else {
-    // quadrant sub-binning of the tile lists, then (quadrant, 32-slot chunk) items
-    launch_quad_bin(cam, rec, pair_slot, tile_offsets, capacity, qlen, qslot, st);
+    // quadrant sub-binning of the tile lists (unless the fused forward already wrote the lists),
+    // then (quadrant, 32-slot chunk) items
+    if (!quads_ready) launch_quad_bin(cam, rec, pair_slot, tile_offsets, capacity, qlen, qslot, st);
     launch_build_items(tile_offsets, qlen, 4 * n_tiles, capacity, 32, 0, items, n_items, tile_nch, scratch, st);
     // persistent: up to 6 × 4 warps per SM (80 regs), fewer when views run concurrently; static items
     const int blocks = sm_count() * persistent_ctas(resident_ctas<k_moments>(kMomentsThreads), concurrency);

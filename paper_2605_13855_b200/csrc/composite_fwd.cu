@@ -66,6 +66,12 @@ __global__ void __launch_bounds__(kFwdThreads, kLoss ? 18 : 1) k_fwd_items(
   // walks all four fields (a single uniform increment per record in the loop)
   __shared__ float4 s_rec[kFwdThreads][4];
   __shared__ int s_item, s_last;
+  // quadrant lists for the following backward (fl.qlen set: the fused training forward): each
+  // staged record's 8×8-quadrant mask and slot, the round's per-warp counts and claimed bases
+  // (double-buffered by round parity)
+  __shared__ uint8_t s_qm[kFwdThreads];
+  __shared__ int s_qslot[kFwdThreads];
+  __shared__ int s_qc[2][kFwdThreads / 32][4], s_qb[2][4];
   const int tid = threadIdx.x;
   const int n_tiles = cam.TX * cam.TY;
   const size_t plane = (size_t)n_tiles * kTilePx;
@@ -102,16 +108,40 @@ __global__ void __launch_bounds__(kFwdThreads, kLoss ? 18 : 1) k_fwd_items(
     f2_t TB = f2(a[2].T, a[3].T);
     const int begin = it.z, end = it.w;  // the chunk's pair range (clipped to capacity by the builder)
     int n_contrib = 0;
-    for (int b = begin; b < end; b += kFwdThreads) {
+    const bool quads = kLoss && fl.qlen != nullptr;
+    int round = 0;
+    for (int b = begin; b < end; b += kFwdThreads, round ^= 1) {
       const int n = min(kFwdThreads, end - b);
+      unsigned qm = 0;
       if (tid < n) {
-        const float4* r = rec + (size_t)pair_slot[b + tid] * kRec4;
-        s_rec[tid][0] = r[0];
-        s_rec[tid][1] = r[1];
+        const int slot = pair_slot[b + tid];
+        const float4* r = rec + (size_t)slot * kRec4;
+        const float4 r0 = r[0], r1 = r[1];
+        s_rec[tid][0] = r0;
+        s_rec[tid][1] = r1;
         s_rec[tid][2] = r[2];
         s_rec[tid][3] = r[3];  // (rect_x, rect_y, kx, ky): the loop reads .zw
+        if (quads) {
+          qm = quadrant_mask(cam, tile, r0, r1);
+          s_qm[tid] = (uint8_t)qm;
+          s_qslot[tid] = slot;
+        }
+      }
+      int qbase = 0;
+      if (quads) {  // this round's quadrant counts; the positions are claimed now, used after the loop
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const unsigned bal = __ballot_sync(0xffffffffu, (qm >> q) & 1u);
+          if ((tid & 31) == 0) s_qc[round][tid >> 5][q] = __popc(bal);
+        }
       }
       __syncthreads();
+      if (quads && tid < 4) {
+        int tot = 0;
+#pragma unroll
+        for (int w = 0; w < kFwdThreads / 32; w++) tot += s_qc[round][w][tid];
+        qbase = tot ? atomicAdd(fl.qlen + 4 * tile + tid, tot) : 0;
+      }
 #pragma unroll 1
       for (int i = 0; i < n; i++) {
         const float4 q0 = s_rec[i][0];  // mx my nA nB
@@ -160,7 +190,25 @@ __global__ void __launch_bounds__(kFwdThreads, kLoss ? 18 : 1) k_fwd_items(
           }
         }
       }
+      if (quads && tid < 4) s_qb[round][tid] = qbase;
       __syncthreads();
+      if (quads) {  // write this round's slots into the tile's quadrant lists (region 4·s + q·L)
+        const unsigned m = tid < n ? s_qm[tid] : 0u;
+        const int64_t s0 = offs[tile];
+        int64_t e0 = offs[tile + 1];
+        if (e0 > capacity) e0 = capacity;
+        const int64_t L = e0 - s0;
+        const unsigned lt = (1u << (tid & 31)) - 1u;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const bool on = (m >> q) & 1u;
+          const unsigned bal = __ballot_sync(0xffffffffu, on);
+          if (on) {
+            const int pos = s_qb[round][q] + ((tid >> 5) ? s_qc[round][0][q] : 0) + __popc(bal & lt);
+            fl.qslot[4 * s0 + q * L + pos] = s_qslot[tid];
+          }
+        }
+      }
     }
     a[0].P0 = f2lo(PA0); a[1].P0 = f2hi(PA0); a[0].P1 = f2lo(PA1); a[1].P1 = f2hi(PA1);
     a[0].P2 = f2lo(PA2); a[1].P2 = f2hi(PA2); a[0].Q = f2lo(QA); a[1].Q = f2hi(QA); a[0].T = f2lo(TA); a[1].T = f2hi(TA);
@@ -371,6 +419,7 @@ void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pa
     int32_t* counter = cv.take<int32_t>(4);
     float* partial = cv.take<float>((size_t)max_items * 5 * kTilePx);
     cudaMemsetAsync(done, 0, sizeof(int32_t) * n_tiles, st);
+    if (fl.target && fl.qlen) cudaMemsetAsync(fl.qlen, 0, sizeof(int32_t) * (4 * (size_t)n_tiles + 1), st);
     cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
     // every tile gets an item (its state/image is written even without pairs), except in the fused
     // training forward, whose only output are the coefficients of the tiles the backward reads

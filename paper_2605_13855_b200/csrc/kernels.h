@@ -41,6 +41,10 @@ struct FwdLoss {
   // the following backward runs over the same pair lists, so it reads the coefficients of tiles
   // that hold pairs only: tiles without pairs get no work item (nothing read or written for them)
   bool listed_tiles_only = false;
+  // quadrant lists of the following backward (nullable): qlen [4·n_tiles] (zeroed by the launcher)
+  // and qslot [4·capacity], laid out as launch_quad_bin's; the backward then skips its sub-binning
+  int32_t* qlen = nullptr;
+  int32_t* qslot = nullptr;
 };
 void launch_composite_fwd(const DevCam& cam, const float* rec, const int32_t* pair_slot,
                           const int32_t* tile_offsets, int64_t capacity, const float* base, const uint8_t* route,
@@ -109,7 +113,15 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
                           int64_t capacity, const float* coef4, const float* coefa, float scale, float* grad,
                           float* dL_dsigma, float* dL_dcov, void* ws, cudaStream_t st,
                           cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr, int variant = 0,
-                          int concurrency = 1, float* acc_out = nullptr);
+                          int concurrency = 1, float* acc_out = nullptr, bool quads_ready = false);
+// The backward workspace after its coefficient region (the pointers launch_composite_bwd uses); the
+// fused training forward writes the quadrant lists (qlen, qslot) into it (quads_ready above).
+struct BwdWs {
+  float* acc2d;
+  int4* items;
+  int32_t *n_items, *tile_nch, *scratch, *qlen, *qslot;
+};
+BwdWs bwd_ws_layout(void* ws, int32_t n_tiles, int32_t n_slots, int64_t capacity);
 // acc_out (nullable): moments only, into acc_out [n_slots][12] (zeroed here); no epilogue. The
 // multi-view epilogue (score): the chains of n_views ≤ kMvViews views (records recs[v], moments
 // accs[v] of the same n_slots slots) summed per slot, one row update each.

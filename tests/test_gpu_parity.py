@@ -842,6 +842,10 @@ def test_forward_loss_fusion_equals_separate_calls(loss, u8):
     n = int(act.numel())
     out = []
     for mode in ("separate", "fused+state", "fused"):   # "fused": the bench's path (listed tiles only)
+        # a fresh pipeline per mode (no lists left in the workspace by another mode), sized for
+        # MORE slots than the call uses, as the bench's first pipeline is
+        p = _pipe(cam, sc.n)
+        p.bwd_ws.fill_(0xFF)
         grad = torch.zeros((n, 80), dtype=torch.float32, device=DEV)
         ds = torch.zeros(1, dtype=torch.float32, device=DEV)
         if mode != "separate":
