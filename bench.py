@@ -579,7 +579,7 @@ class Workload:
         # bitmap path (the view's (tile × slot) bitmap ≤ 128 MB): k_bin_expand<1,1>, k_bitmap_count,
         # the scan, k_bitmap_emit; otherwise k_bin_expand<0> (n > 0), the scan, k_bin_expand<1>,
         # k_tile_sort (n > 0, sorted lists only)
-        bitmap = lambda n: n > 0 and nt * ((((n + 31) // 32) + 3) // 4 * 4) <= (32 << 20)  # noqa: E731
+        bitmap = lambda n: n > 0 and nt <= 4096 and nt * ((((n + 31) // 32) + 3) // 4 * 4) <= (32 << 20)  # noqa: E731
         binn = lambda n: (2 if n > 0 else 0) + scan_kernels(nt) + 1  # noqa: E731
         bin_unsorted = lambda n: binn(n) if bitmap(n) else binn(n) - (1 if n > 0 else 0)  # noqa: E731
         fwd = 3                                            # item histogram + emission, k_fwd_items

@@ -119,7 +119,8 @@ int oit_project_cull(const oit_scene* scene, const oit_camera* cam, const int32_
  * Scratch: ws of at least oit_bin_workspace_bytes(cam, pair_capacity) bytes (≈ 4·pair_capacity +
  * 8·n_tiles; 0 for a null camera or a negative capacity): a histogram, a scatter and a per-tile
  * slot sort. With oit_bin_workspace_bytes_ex(cam, n_slots, pair_capacity) bytes (the former plus
- * n_tiles·⌈n_slots/32⌉·4 B when that bitmap is ≤ 128 MB) the call bins such views through a
+ * n_tiles·⌈n_slots/32⌉·4 B when that bitmap is ≤ 128 MB and the view has ≤ 4096 tiles) the call
+ * bins such views through a
  * (tile × slot) bitmap instead: one expansion and an ordered emission. Both give the same lists.
  * --------------------------------------------------------------------------------------- */
 size_t oit_bin_workspace_bytes(const oit_camera* cam, int64_t pair_capacity);

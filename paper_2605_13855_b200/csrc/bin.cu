@@ -468,17 +468,23 @@ size_t bin_ws_bytes(int32_t n_tiles, int64_t capacity) {
          align_up((size_t)(capacity > 0 ? capacity : 1) * sizeof(int32_t));
 }
 
+// The bitmap path's cost grows with n_tiles per slot (memset + count + emit of n_tiles/32 words per
+// slot), the histogram path's with the pairs: beyond kBitmapMaxTiles tiles per view (C3 / C4:
+// 6,700) the bitmap loses even when it fits (C4's 111k-slot active set: 93 MB, iteration 0.141 →
+// 0.164 ms), so those views take the histogram path.
+constexpr int32_t kBitmapMaxTiles = 4096;
+
 // Scratch the bitmap path needs for calls of up to n_slots slots: the bitmap of n_slots, or (when
 // that exceeds kBitmapMaxWords) the largest bitmap the path accepts, so smaller calls on the same
 // workspace still take it.
 size_t bin_bitmap_bytes(int32_t n_tiles, int32_t n_slots) {
-  if (n_slots <= 0) return 0;
+  if (n_slots <= 0 || n_tiles > kBitmapMaxTiles) return 0;
   const size_t words = std::min((size_t)n_tiles * bitmap_row_words(n_slots), kBitmapMaxWords);
   return align_up(words * sizeof(unsigned));
 }
 
 static size_t bitmap_bytes_exact(int32_t n_tiles, int32_t n_slots) {
-  if (n_slots <= 0) return 0;
+  if (n_slots <= 0 || n_tiles > kBitmapMaxTiles) return 0;
   const size_t words = (size_t)n_tiles * bitmap_row_words(n_slots);
   return words <= kBitmapMaxWords ? align_up(words * sizeof(unsigned)) : 0;
 }
