@@ -210,7 +210,7 @@ __device__ __forceinline__ float edge_max_rcp(float a, float b0, float b1, float
 __device__ __forceinline__ unsigned quadrant_mask(const DevCam& cam, int tile, const float4& q0, const float4& q1) {
   const int tx0 = (tile % cam.TX) * kTile, ty0 = (tile / cam.TX) * kTile;
   const float nA = q0.z, nB = q0.w, nC = q1.x, lo = q1.y * 1.0009765625f;
-  const float inv2A = 1.0f / (2.0f * nA), inv2C = 1.0f / (2.0f * nC);
+  const float inv2A = __frcp_rn(2.0f * nA), inv2C = __frcp_rn(2.0f * nC);  // = 1/x, correctly rounded
   unsigned m = 0;
 #pragma unroll
   for (int q = 0; q < 4; q++) {
