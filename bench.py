@@ -1210,10 +1210,16 @@ def time_e2e(args, torch, dist, wl, step, flush, allred):
         wl.train_and_refresh(host_targets=host_views)
         if allred:
             return
+        # the combined gradient rows are final here: read them back on the copy stream while the
+        # Adam step and the update run (both only read them)
+        main = torch.cuda.current_stream()
+        wl.copy_stream.wait_stream(main)
+        with torch.cuda.stream(wl.copy_stream):
+            grad_h.copy_(wl.grad, non_blocking=True)
         wl.adam()
         wl.update()
-        grad_h.copy_(wl.grad, non_blocking=True)
         bits_h.copy_(wl.bits, non_blocking=True)
+        main.wait_stream(wl.copy_stream)
 
     graph = None
     if not args.no_graph and not allred:
