@@ -1,18 +1,24 @@
 // bin.cu — a2 oit_bin_tiles: CreateTiles / DuplicateWithKeys / SortByKeys ("only by tile ID",
 // P:339) / IdentifyTileRanges (Alg. 2 l.3-6).
 //
-// The key is the tile alone (no depth bits), so the sort degenerates into a counting sort:
-//   1. k_bin_expand<false>: per-tile histogram of the slots' tile rectangles (the rect of a slot
-//                           is read from its record);
-//   2. scan:                tile_offsets = exclusive scan of the histogram (IdentifyTileRanges);
-//   3. k_bin_expand<true>:  every (slot, tile) pair takes the next position of its tile (cursor);
-//   4. k_tile_sort:         each tile's segment is put in ascending slot order (R15: the stable
-//                           counting sort's order, which makes the lists — and hence the forward's
-//                           fp32 summation order — identical run to run and to the oracle's).
-//                           Skipped (sorted = false) for lists only the backward reads: its moments
-//                           are order-free per (splat, tile) and are summed with atomics anyway.
-// Integer-only, latency/atomic-bound: ≈ 4 B written + 2 atomics per pair, then one smem sort
-// per tile (4 B read + 4 B written per pair).
+// The key is the tile alone (no depth bits), so the sort degenerates into a counting sort, and the
+// lists come out in the STABLE counting sort's order — ascending slot inside each tile (R15), which
+// makes the lists, and hence the forward's fp32 summation order, identical run to run and to the
+// oracle's. Two paths give the same lists:
+//  * bitmap path (views of ≤ 4096 tiles whose (tile × slot) bitmap fits 128 MB, when the caller's
+//    workspace has room: oit_bin_workspace_bytes_ex):
+//      k_bin_expand<true, true>: one expansion + exact tile test, bit `slot` of tile t's row set;
+//      k_bitmap_count:           a CTA per tile counts its row;
+//      scan:                     tile_offsets = exclusive scan of the counts;
+//      k_bitmap_emit:            a CTA per tile writes its row's set bits in ascending order;
+//  * histogram path (any size):
+//      k_bin_expand<false>: per-tile histogram of the slots' tile rectangles (exact tile test);
+//      scan:                tile_offsets = exclusive scan of the histogram (IdentifyTileRanges);
+//      k_bin_expand<true>:  every (slot, tile) pair takes the next position of its tile (cursor);
+//      k_tile_sort:         each tile's segment put in ascending slot order; skipped (sorted =
+//                           false) for lists only the backward reads (its moments are order-free per
+//                           (splat, tile) and summed with atomics anyway).
+// Integer-only, latency/atomic-bound.
 #include <algorithm>
 
 #include "kernels.h"
