@@ -41,18 +41,23 @@ constexpr int kSlotsPerWarp = 8;
 
 // kBitmap (the bitmap path, launch_bin): instead of counting, set bit `slot` of tile t's row in
 // bm[t · bm_words …] (a reduction, no return value; ordering comes from the row itself).
-template <bool kScatter, bool kBitmap = false>
+// kQuads (with kScatter; the score's scored set, whose lists only the backward reads): no tile list —
+// each kept (slot, tile) pair goes straight into the 8×8-quadrant lists of its tile (quadrant masks
+// as k_quad_bin's, positions claimed with aggregated atomics on qlen, regions 4·s_t + q·L_t).
+template <bool kScatter, bool kBitmap = false, bool kQuads = false>
 __global__ void __launch_bounds__(128) k_bin_expand(const float4* __restrict__ rec, const int32_t* __restrict__ tps,
                                                     int32_t n_slots, int TX, int W, int H, int32_t* __restrict__ cnt,
                                                     int32_t* __restrict__ pair_slot, int64_t capacity,
                                                     const int32_t* __restrict__ offsets, int n_tiles,
                                                     int64_t* __restrict__ d_n_pairs, int64_t* __restrict__ d_max,
-                                                    unsigned* __restrict__ bm = nullptr, int bm_words = 0) {
+                                                    unsigned* __restrict__ bm = nullptr, int bm_words = 0,
+                                                    int32_t* __restrict__ qlen = nullptr,
+                                                    int32_t* __restrict__ qslot = nullptr) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  if (kScatter && !kBitmap && gw == 0 && lane == 0) {
+  if (kScatter && !kBitmap && gw == 0 && lane == 0) {  // (kQuads too: the total is the scan's)
     const int64_t n = offsets[n_tiles];
     *d_n_pairs = n;
     if (d_max) atomicMax(reinterpret_cast<unsigned long long*>(d_max), (unsigned long long)n);
@@ -99,6 +104,34 @@ __global__ void __launch_bounds__(128) k_bin_expand(const float4* __restrict__ r
       const float onC = __shfl_sync(FULL, nC, owner), olo = __shfl_sync(FULL, thr_lo, owner);
       const int ty = oy0 + local / ow, tx = ox0 + local % ow;
       // candidate tiles of the rectangle are kept by the exact tile test (DESIGN.md §3 step 12b)
+      if (kQuads) {
+        const bool keep = j < total && spec_tile_keep(tx, ty, W, H, omx, omy, onA, onB, onC, olo);
+        const int tile = ty * TX + tx;
+        unsigned m = 0;
+        int64_t s_t = 0, L_t = 0;
+        if (keep) {
+          m = quadrant_mask_at(16 * tx, 16 * ty, W, H, omx, omy, onA, onB, onC, olo);
+          s_t = offsets[tile];
+          int64_t e_t = offsets[tile + 1];
+          if (e_t > capacity) e_t = capacity;
+          if (s_t > e_t) s_t = e_t;
+          L_t = e_t - s_t;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const bool on = (m >> q) & 1u;
+          const unsigned act = __ballot_sync(FULL, on);
+          if (on) {
+            const unsigned peers = __match_any_sync(act, 4 * tile + q);
+            const int leader = __ffs(peers) - 1;
+            int pos = 0;
+            if (lane == leader) pos = atomicAdd(qlen + 4 * tile + q, __popc(peers));
+            pos = __shfl_sync(peers, pos, leader) + __popc(peers & ((1u << lane) - 1u));
+            if (pos < L_t) qslot[4 * s_t + q * L_t + pos] = base + owner;
+          }
+        }
+        continue;
+      }
       if (kBitmap) {
         if (j < total && spec_tile_keep(tx, ty, W, H, omx, omy, onA, onB, onC, olo)) {
           const int slot = base + owner;
@@ -537,6 +570,27 @@ void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_sl
     k_tile_sort<<<n_tiles, kSortThreads, sizeof(unsigned) * words, st>>>(tile_offsets, n_tiles, capacity, n_slots,
                                                                          words, pair_slot, sort_tmp);
   }
+}
+
+void launch_bin_quads(const DevCam& cam, const float* rec, const int32_t* tiles_per_slot, int32_t n_slots,
+                      int64_t capacity, int32_t* tile_offsets, int64_t* d_n_pairs, int64_t* d_max_pairs,
+                      int32_t* qlen, int32_t* qslot, void* ws, cudaStream_t st) {
+  int n_tiles = cam.TX * cam.TY;
+  Carve cv(ws);
+  int32_t* counts = cv.take<int32_t>(n_tiles + 1);
+  void* tmp = cv.take<char>(scan_tmp_bytes(n_tiles));
+  cudaMemsetAsync(counts, 0, sizeof(int32_t) * n_tiles, st);
+  cudaMemsetAsync(qlen, 0, sizeof(int32_t) * (4 * (size_t)n_tiles + 1), st);
+  const float4* r4 = reinterpret_cast<const float4*>(rec);
+  const int warps = n_slots > 0 ? (n_slots + kSlotsPerWarp - 1) / kSlotsPerWarp : 1;
+  const int blocks = (warps + 3) / 4;
+  if (n_slots > 0)
+    k_bin_expand<false><<<blocks, 128, 0, st>>>(r4, tiles_per_slot, n_slots, cam.TX, cam.W, cam.H, counts, nullptr,
+                                                capacity, tile_offsets, n_tiles, d_n_pairs, d_max_pairs);
+  launch_exclusive_scan(counts, tile_offsets, n_tiles, tmp, st);
+  k_bin_expand<true, false, true><<<blocks, 128, 0, st>>>(r4, tiles_per_slot, n_slots, cam.TX, cam.W, cam.H, counts,
+                                                          nullptr, capacity, tile_offsets, n_tiles, d_n_pairs,
+                                                          d_max_pairs, nullptr, 0, qlen, qslot);
 }
 
 }  // namespace oit

@@ -406,12 +406,14 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
     // rows runs once per group of kMvViews views (the rows are read-modify-written once per group)
     float* rec_s = w.rec_s[in_group];
     launch_project(dc, scene->rows, scene->sigma, score_idx, n_score, rec_s, w.tps_s, st);
-    // (the scored lists feed the backward only: no per-tile slot sort, see bin.cu)
-    launch_bin(dc, rec_s, w.tps_s, n_score, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st,
-               false, w.bin_ws_bytes);
+    // (the scored lists feed the backward only: binned straight into its quadrant lists, no tile
+    // list and no separate quadrant sub-binning, see bin.cu)
+    const BwdWs bl = bwd_ws_layout(w.bwd_ws, oit_num_tiles(&cams_host[0]), n_score, pair_capacity);
+    launch_bin_quads(dc, rec_s, w.tps_s, n_score, pair_capacity, w.offs, w.npairs, d_max_pairs, bl.qlen, bl.qslot,
+                     w.bin_ws, st);
     launch_composite_bwd(dc, scene->rows, scene->sigma, score_idx, n_score, rec_s, w.pairs, w.offs, pair_capacity,
                          w.coef4, w.coefa, scale, score_grad, dL_dsigma, nullptr, w.bwd_ws, st, nullptr, nullptr, 0,
-                         concurrency, w.acc_s[in_group]);
+                         concurrency, w.acc_s[in_group], true);
     group_cams[in_group++] = dc;
     if (in_group == kMvViews || s == n_sub - 1) {
       launch_epilogue_mv(group_cams, w.rec_s, w.acc_s, in_group, scene->rows, scene->sigma, score_idx, n_score, scale,

@@ -207,17 +207,18 @@ __device__ __forceinline__ float edge_max_rcp(float a, float b0, float b1, float
   return fmaf(t, fmaf(R, t, q), (P * a) * a);
 }
 
-__device__ __forceinline__ unsigned quadrant_mask(const DevCam& cam, int tile, const float4& q0, const float4& q1) {
-  const int tx0 = (tile % cam.TX) * kTile, ty0 = (tile / cam.TX) * kTile;
-  const float nA = q0.z, nB = q0.w, nC = q1.x, lo = q1.y * 1.0009765625f;
+// tile origin (tx0, ty0) in pixels; mx, my, nA, nB, nC, thr_lo: the record's q0 and q1.x/.y
+__device__ __forceinline__ unsigned quadrant_mask_at(int tx0, int ty0, int W, int H, float mx, float my, float nA,
+                                                     float nB, float nC, float thr_lo) {
+  const float lo = thr_lo * 1.0009765625f;
   const float inv2A = __frcp_rn(2.0f * nA), inv2C = __frcp_rn(2.0f * nC);  // = 1/x, correctly rounded
   unsigned m = 0;
 #pragma unroll
   for (int q = 0; q < 4; q++) {
     const int X0 = tx0 + 8 * (q & 1), Y0 = ty0 + 8 * (q >> 1);
-    if (X0 >= cam.W || Y0 >= cam.H) continue;
-    const int X1 = min(X0 + 7, cam.W - 1), Y1 = min(Y0 + 7, cam.H - 1);
-    const float ax0 = (float)X0 - q0.x, ax1 = (float)X1 - q0.x, ay0 = (float)Y0 - q0.y, ay1 = (float)Y1 - q0.y;
+    if (X0 >= W || Y0 >= H) continue;
+    const int X1 = min(X0 + 7, W - 1), Y1 = min(Y0 + 7, H - 1);
+    const float ax0 = (float)X0 - mx, ax1 = (float)X1 - mx, ay0 = (float)Y0 - my, ay1 = (float)Y1 - my;
     bool keep = ax0 <= 0.0f && 0.0f <= ax1 && ay0 <= 0.0f && 0.0f <= ay1;
     if (!keep) {
       float e = edge_max_rcp(ax0, ay0, ay1, nA, nB, nC, inv2C);
@@ -229,6 +230,11 @@ __device__ __forceinline__ unsigned quadrant_mask(const DevCam& cam, int tile, c
     if (keep) m |= 1u << q;
   }
   return m;
+}
+
+__device__ __forceinline__ unsigned quadrant_mask(const DevCam& cam, int tile, const float4& q0, const float4& q1) {
+  return quadrant_mask_at((tile % cam.TX) * kTile, (tile / cam.TX) * kTile, cam.W, cam.H, q0.x, q0.y, q0.z, q0.w,
+                          q1.x, q1.y);
 }
 
 // e if power ∈ [lo, 0] (the step 13 contribution test: power <= 0 && power >= lo; NaN fails both),

@@ -25,6 +25,12 @@ void launch_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, void* tmp
 // bitmap path whenever ws_bytes covers both.
 size_t bin_ws_bytes(int32_t n_tiles, int64_t capacity);
 size_t bin_bitmap_bytes(int32_t n_tiles, int32_t n_slots);
+// For lists only the backward reads (the score's scored set): the histogram, the tile offsets and
+// the 8×8-quadrant lists (qlen [4·n_tiles+1], qslot [4·capacity], launch_quad_bin's layout) in one
+// scatter, no tile list; ws: bin_ws_bytes. Follow with launch_composite_bwd(…, quads_ready = true).
+void launch_bin_quads(const DevCam& cam, const float* rec, const int32_t* tiles_per_slot, int32_t n_slots,
+                      int64_t capacity, int32_t* tile_offsets, int64_t* d_n_pairs, int64_t* d_max_pairs,
+                      int32_t* qlen, int32_t* qslot, void* ws, cudaStream_t st);
 void launch_bin(const DevCam& cam, const float* rec, const int32_t* tiles_per_slot, int32_t n_slots,
                 int32_t* pair_slot, int64_t capacity, int32_t* tile_offsets, int64_t* d_n_pairs,
                 int64_t* d_max_pairs, void* ws, cudaStream_t st, bool sorted = true, size_t ws_bytes = 0);
