@@ -581,7 +581,6 @@ class Workload:
         # k_tile_sort (n > 0, sorted lists only)
         bitmap = lambda n: n > 0 and nt <= 4096 and nt * ((((n + 31) // 32) + 3) // 4 * 4) <= (32 << 20)  # noqa: E731
         binn = lambda n: (2 if n > 0 else 0) + scan_kernels(nt) + 1  # noqa: E731
-        bin_unsorted = lambda n: binn(n) if bitmap(n) else binn(n) - (1 if n > 0 else 0)  # noqa: E731
         fwd = 3                                            # item histogram + emission, k_fwd_items
         # k_quad_bin, item histogram + emission, k_moments, k_epilogue (none for an empty slot list)
         bwd = lambda n: 5 if n > 0 else 0  # noqa: E731
@@ -592,8 +591,10 @@ class Workload:
         train = self.V * (proj(a) + binn(a) + fwd + bwd_train(a) + lossk) + 1   # + k_adam
         refresh = 1                                        # k_fps
         if s > 0:
-            # (the scored set's lists feed the backward only: no k_tile_sort on the histogram path)
-            refresh += self.S * (proj(a) + binn(a) + fwd + lossk + proj(s) + bin_unsorted(s) + bwd(s))
+            # the scored set is binned straight into the backward's quadrant lists: k_bin_expand<0>,
+            # the scan, the quadrant scatter; its backward has no k_quad_bin
+            bin_q = lambda n: (1 if n > 0 else 0) + scan_kernels(nt) + 1  # noqa: E731
+            refresh += self.S * (proj(a) + binn(a) + fwd + lossk + proj(s) + bin_q(s) + bwd(s) - (1 if s > 0 else 0))
             if self.world > 1:   # k_row_activeness + k_apply_bits, k_popc3, 3 scans, k_emit3
                 refresh += 1 + 1 + 1 + 3 * scan_kernels(nw) + 1
             else:                # k_update_bits, k_popc3, 3 scans, k_emit3
