@@ -261,6 +261,14 @@ __device__ __forceinline__ float spec_power_row(float nA, float dx, float by, fl
   return __fmaf_rn(dx, __fmaf_rn(nA, dx, by), cy);
 }
 
+// gpu-scope release add (the last-arrival pattern of split-tile merges) and acquire fence
+__device__ __forceinline__ int atom_add_release_gpu(int* p, int v) {
+  int r;
+  asm volatile("atom.release.gpu.global.add.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+  return r;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 // ---------------------------------------------------------------- value-path helpers ------
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;

@@ -227,13 +227,18 @@ __global__ void __launch_bounds__(kFwdThreads, kLoss ? 18 : 1) k_fwd_items(
       float* pa = partial + (size_t)item * 5 * kTilePx;
 #pragma unroll
       for (int k = 0; k < 4; k++) store_px(a[k], pa, kTilePx, p0 + 4 * k);
-      __threadfence();
+      // publish: the CTA barrier orders every thread's partial before thread 0's gpu-scope RELEASE
+      // add (cumulative); the last arrival's thread 0 takes an acquire fence and the barrier passes it
+      // on, and the partials are read from L2 (.cg). One release per chunk and one acquire per split
+      // tile — not a sequentially consistent fence per thread, whose L1 invalidation (CCTL.IVALL)
+      // would also drop the record lines of every other CTA on the SM.
       __syncthreads();
-      if (tid == 0) s_last = (atomicAdd(done + tile, 1) == nch - 1);
+      if (tid == 0) s_last = (atom_add_release_gpu(done + tile, 1) == nch - 1);
       __syncthreads();
       write_final = s_last;
       if (write_final) {
-        __threadfence();
+        if (tid == 0) fence_acq_rel_gpu();
+        __syncthreads();
         const int first = item - it.y;  // chunks of a tile are contiguous items
 #pragma unroll
         for (int k = 0; k < 4; k++) {
