@@ -164,7 +164,7 @@ __device__ __forceinline__ void moments_window(Moments& m, const float* __restri
   m.S -= f2lo(NS) + f2hi(NS);
 }
 
-__global__ void __launch_bounds__(kMomentsThreads, 5) k_moments(DevCam cam, const float4* __restrict__ rec,
+__global__ void __launch_bounds__(kMomentsThreads, 6) k_moments(DevCam cam, const float4* __restrict__ rec,
                                                              const int32_t* __restrict__ pair_slot,
                                                              const int4* __restrict__ items,
                                                              const int32_t* __restrict__ n_items_p,
@@ -729,8 +729,9 @@ void launch_composite_bwd(const DevCam& cam, const float* rows, const float* sig
     // then (quadrant, 32-slot chunk) items
     if (!quads_ready) launch_quad_bin(cam, rec, pair_slot, tile_offsets, capacity, qlen, qslot, st);
     launch_build_items(tile_offsets, qlen, 4 * n_tiles, capacity, 32, 0, items, n_items, tile_nch, scratch, st);
-    // persistent: up to 5 × 4 warps per SM (96 regs: alone 4% faster than 6 × 4 at 80 regs, the
-    // step unchanged, profiles/r02f_fwd_qskip_ab.txt), fewer when views run concurrently; static items
+    // persistent: up to 6 × 4 warps per SM (80 regs; 5 × 4 at 96 regs is 4% faster alone but 1.8%
+    // slower on the ρ = 0.05 step, profiles/r02f_fwd_qskip_ab.txt), fewer when views run
+    // concurrently; static items
     const int blocks = sm_count() * persistent_ctas(resident_ctas<k_moments>(kMomentsThreads), concurrency);
     record_event(ev_begin, st);
     k_moments<<<blocks, kMomentsThreads, 0, st>>>(cam, reinterpret_cast<const float4*>(rec), qslot, items, n_items,
