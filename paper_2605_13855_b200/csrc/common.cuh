@@ -261,6 +261,10 @@ __device__ __forceinline__ float spec_power_row(float nA, float dx, float by, fl
   return __fmaf_rn(dx, __fmaf_rn(nA, dx, by), cy);
 }
 
+// L2 prefetch hint (no register, no completion): issued for lines a thread will load later on a
+// dependent path, so the later loads hit L2 instead of waiting a full DRAM round trip
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 // gpu-scope release add (the last-arrival pattern of split-tile merges) and acquire fence
 __device__ __forceinline__ int atom_add_release_gpu(int* p, int v) {
   int r;

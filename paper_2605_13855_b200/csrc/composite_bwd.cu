@@ -561,13 +561,14 @@ __global__ void __launch_bounds__(128, 3) k_epilogue(DevCam cam, const float4* _
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   float gsig = 0.f;
   if (k < n_slots) {
+    const int32_t sid = __ldg(idx + k);  // with the record and moments: one round trip less to the row
     const float4 q3 = rec[(size_t)k * kRec4 + 3];
     const float4 m0 = acc2d[(size_t)k * 3 + 0];  // U0 U1 U2 S
     const float4 m1 = acc2d[(size_t)k * 3 + 1];  // Od M1 M2 XX
     const float4 m2 = acc2d[(size_t)k * 3 + 2];  // XY YY
     if (epilogue_needed(q3, m0, m1)) {
       AtomicRowSink sink{reinterpret_cast<float*>(grad + (size_t)k * kRow4), dL_dcov ? dL_dcov + (size_t)k * 6 : nullptr};
-      gsig = epilogue_chain(cam, rows + (size_t)idx[k] * kRow4, *sigma_p, rec[(size_t)k * kRec4 + 0],
+      gsig = epilogue_chain(cam, rows + (size_t)sid * kRow4, *sigma_p, rec[(size_t)k * kRec4 + 0],
                             rec[(size_t)k * kRec4 + 1], rec[(size_t)k * kRec4 + 4], m0, m1, m2, scale, sink);
     }
   }
@@ -621,6 +622,14 @@ __global__ void __launch_bounds__(kMvThreads, 2) k_epilogue_mv(MvCams mv, int n_
     for (int q = 0; q < 11; q++) sink.geos[q * kMvThreads] = 0.f;
     bool any = false;
     const float4* r = rows + (size_t)idx[k] * kRow4;
+#pragma unroll
+    for (int v = 0; v < kMvViews; v++) {  // the later views' record and moment lines (read in any case)
+      if (v >= n_views) break;
+      if (v > 0) {
+        prefetch_l2(mv.rec[v] + (size_t)k * kRec4);
+        prefetch_l2(mv.acc[v] + (size_t)k * 3);
+      }
+    }
     const float sigma = *sigma_p;
     // unrolled over the group's views: each chain reads its camera from the kernel parameters
     // (constant-bank operands, as in the single-view epilogue) instead of holding it in registers
