@@ -79,6 +79,10 @@ def parse():
     ap.add_argument("--sub-rate", type=float, default=0.05, help="refresh subsample rate S/V")
     ap.add_argument("--streams", type=int, default=12, help="training views processed concurrently (one stream each)")
     ap.add_argument("--score-streams", type=int, default=0, help="refresh streams (0: one per subsampled view)")
+    ap.add_argument("--coef-reuse", action="store_true",
+                    help="the refresh reuses the coefficients of the subsampled views' training forwards instead of "
+                         "rasterising their active set itself (oit_score_subsample_ex; +1.0%% at rho 0.2, -1.1%% at "
+                         "rho 0.05 on one B200, so off by default)")
     ap.add_argument("--targets", choices=["u8", "f32"], default="u8",
                     help="training-image format: 8-bit (the datasets' PNGs, OIT_TARGET_U8) or fp32")
     ap.add_argument("--no-sweep", action="store_true")
@@ -436,6 +440,12 @@ class Workload:
                                      dtype=torch.uint8, device=dev) for _ in range(nsc)]
         # the refresh's own streams: it runs concurrently with the training views (R35)
         self.score_streams = [torch.cuda.Stream() for _ in range(nsc)]
+        # coefficient reuse (L1/L2): the subsampled views' training forwards write every tile's
+        # coefficients into a workspace of their own, which the score reads (oit_score_subsample_ex)
+        self.reuse_coef = self.loss in ("l1", "l2") and args.coef_reuse and self.n_ina > 0
+        picked = sorted(set(self.views_host)) if self.reuse_coef else []
+        self.coef_ws = {j: self.pipe.new_bwd_ws() for j in picked}
+        self.ev_coef = {j: torch.cuda.Event() for j in picked}
         from paper_2605_13855_b200 import dist as D
         # padded to the sharded refresh's row ranges (rows beyond n_ina stay zero)
         self.score_rows = torch.zeros((D.score_buffer_rows(self.n_ina, self.world), 80), dtype=torch.float32,
@@ -465,24 +475,33 @@ class Workload:
             return 0
         return sum(1 for k in range(len(self.score_ws)) if self.views_host[k::len(self.score_ws)])
 
-    def train_views(self, n_streams=None, host_targets=None, extra_concurrency=0):
+    def train_views(self, n_streams=None, host_targets=None, extra_concurrency=0, after_picked=None):
         """a1-a6 over every training view (Alg. 1 l.3-6, one view per iteration); views are dealt
         round-robin to n_streams streams (fork/join on the current stream). host_targets (e2e):
-        pinned-host training images, copied in view order on a copy stream; each view's loss
-        waits only for its own image (copies overlap the compute of earlier views)."""
+        pinned-host training images, copied on a copy stream; each view's loss waits only for its
+        own image (copies overlap the compute of earlier views). after_picked (the refresh with
+        coefficient reuse): the views the refresh scores are enqueued first — their fused forward
+        writes every tile's coefficients into a workspace of their own and records ev_coef — then
+        after_picked() enqueues the refresh (forked before the views, waiting only on ev_coef), then
+        the remaining views."""
         torch, L = self.torch, self.L
         ns = self.n_streams if n_streams is None else n_streams
         main = torch.cuda.current_stream()
         self.gbuf.zero_()
+        picked = list(dict.fromkeys(self.views_host)) if after_picked is not None else []
+        order = picked + [v for v in range(self.V) if v not in set(picked)]
         if host_targets is not None:
             self.copy_stream.wait_stream(main)
             with torch.cuda.stream(self.copy_stream):
-                for v in range(self.V):
+                for v in order:
                     self.targets[v].copy_(host_targets[v], non_blocking=True)
                     self.ev_copy[v].record(self.copy_stream)
         for st_ in self.streams[:ns]:
             st_.wait_stream(main)
-        for v, cam in enumerate(self.cams):
+        for i, v in enumerate(order):
+            if after_picked is not None and i == len(picked):
+                after_picked()
+            cam = self.cams[v]
             k = v % ns
             p = self.pipes[k]
             with torch.cuda.stream(self.streams[k]):
@@ -494,45 +513,58 @@ class Workload:
                 if self.loss in ("l1", "l2"):
                     # a3 + a4 fused: the forward's epilogue applies the pixel-local loss and writes the
                     # backward coefficients into the backward workspace (no pixel-state round trip)
+                    cw = self.coef_ws.get(v) if after_picked is not None else None
                     p.forward_loss(self.rows, self.sigma, self.act, self.bg, self.targets[v], self.loss,
-                                   base=self.caches[v], events=self.ev_fwd[v], concurrency=ns + extra_concurrency)
+                                   base=self.caches[v], events=self.ev_fwd[v], concurrency=ns + extra_concurrency,
+                                   bwd_ws=cw, all_tiles=cw is not None)
+                    if cw is not None:
+                        self.ev_coef[v].record(self.streams[k])
                     p.backward(self.rows, self.sigma, self.act, self.bg, None, None, self.grad, self.dsig,
-                               events=self.ev_bwd[v], coef_ready=True, concurrency=ns + extra_concurrency)
+                               events=self.ev_bwd[v], coef_ready=True, concurrency=ns + extra_concurrency, bwd_ws=cw)
                 else:   # D-SSIM is not pixel-local: state → resolve → SSIM stencils → coefficients
                     _, st = p.forward(self.rows, self.sigma, self.act, self.bg, base=self.caches[v], image=False,
                                       events=self.ev_fwd[v], concurrency=ns + extra_concurrency)
                     p.backward(self.rows, self.sigma, self.act, self.bg, st, None, self.grad, self.dsig,
                                events=self.ev_bwd[v], target=self.targets[v], loss=self.loss,
                                concurrency=ns + extra_concurrency)
+        if after_picked is not None and len(picked) == len(order):
+            after_picked()
         for st_ in self.streams[:ns]:
             main.wait_stream(st_)
         if host_targets is not None:
             main.wait_stream(self.copy_stream)
 
-    def refresh(self, join=True, extra_concurrency=0):
+    def refresh(self, join=True, extra_concurrency=0, fork_from=None, reuse=False):
         """a7 (FPS + subsampled score of the inactive splats) on the refresh's own streams, forked
-        from the current stream; join=False leaves them running (refresh_join() later), so the
-        score overlaps the training views (R35: the period's refresh scores the parameters the
-        period's batch uses, the update applies to the next period)."""
+        from the current stream (or fork_from); join=False leaves them running (refresh_join()
+        later), so the score overlaps the training views (R35: the period's refresh scores the
+        parameters the period's batch uses, the update applies to the next period). reuse: each
+        score stream waits for its views' training forwards (ev_coef) and takes their coefficients
+        instead of rasterising the active set again (oit_score_subsample_ex)."""
         L = self.L
         torch = self.torch
-        L.oit_select_views(self.centers, self.S, 2605, 0, self.views_dev)
-        self.score_grad.zero_()
-        self.score_dsig.zero_()
+        main = torch.cuda.current_stream() if fork_from is None else fork_from
+        with torch.cuda.stream(main):
+            L.oit_select_views(self.centers, self.S, 2605, 0, self.views_dev)
+            self.score_grad.zero_()
+            self.score_dsig.zero_()
         if self.n_ina > 0:
             # the S subsampled views are scored concurrently (disjoint subsets, scale 1/S each)
-            main = torch.cuda.current_stream()
             parts = [self.views_host[k::len(self.score_ws)] for k in range(len(self.score_ws))]
             conc = sum(1 for q in parts if q) + extra_concurrency
             for k, part in enumerate(parts):
                 if not part:
                     continue
                 self.score_streams[k].wait_stream(main)
+                cws = evs = None
+                if reuse:   # the call waits on each view's event only before that view's backward
+                    cws = [self.coef_ws[j] for j in part]
+                    evs = [self.ev_coef[j] for j in part]
                 with torch.cuda.stream(self.score_streams[k]):
                     L.oit_score_subsample(self.rows, self.sigma, self.cams, self.targets_list, self.caches_list,
                                           self.act, self.ina, part, self.loss, self.bg, self.score_grad, self.score_dsig,
                                           self.score_cap, self.max_pairs, self.score_ws[k], scale=1.0 / self.S,
-                                          concurrency=conc)
+                                          concurrency=conc, coef_ws=cws, coef_ready=evs)
             if join:
                 self.refresh_join()
 
@@ -545,8 +577,17 @@ class Workload:
                 main.wait_stream(self.score_streams[k])
 
     def train_and_refresh(self, host_targets=None):
-        """The step's a1-a6 over the 100 views and the refresh's a7, concurrently (R35)."""
+        """The step's a1-a6 over the 100 views and the refresh's a7, concurrently (R35). With
+        coefficient reuse (default for L1/L2) the refresh takes the subsampled views' coefficients
+        from their training forwards — the same parameters, active set, cache and target."""
         nr = self.refresh_parts()
+        if self.with_refresh and self.reuse_coef:
+            main = self.torch.cuda.current_stream()
+            self.train_views(host_targets=host_targets, extra_concurrency=nr,
+                             after_picked=lambda: self.refresh(join=False, extra_concurrency=self.n_streams,
+                                                               fork_from=main, reuse=True))
+            self.refresh_join()
+            return
         if self.with_refresh:
             self.refresh(join=False, extra_concurrency=self.n_streams)
         self.train_views(host_targets=host_targets, extra_concurrency=nr)
@@ -594,7 +635,10 @@ class Workload:
             # the scored set is binned straight into the backward's quadrant lists: k_bin_expand<0>,
             # the scan, the quadrant scatter; its backward has no k_quad_bin
             bin_q = lambda n: (1 if n > 0 else 0) + scan_kernels(nt) + 1  # noqa: E731
-            refresh += self.S * (proj(a) + binn(a) + fwd + lossk + proj(s) + bin_q(s) + bwd(s) - (1 if s > 0 else 0))
+            # (with coefficient reuse the score takes each view's coefficients from its training
+            # forward: no projection, binning or forward of the active set inside the refresh)
+            own = 0 if self.reuse_coef else proj(a) + binn(a) + fwd + lossk
+            refresh += self.S * (own + proj(s) + bin_q(s) + bwd(s) - (1 if s > 0 else 0))
             if self.world > 1:   # k_row_activeness + k_apply_bits, k_popc3, 3 scans, k_emit3
                 refresh += 1 + 1 + 1 + 3 * scan_kernels(nw) + 1
             else:                # k_update_bits, k_popc3, 3 scans, k_emit3

@@ -173,6 +173,9 @@ int oit_composite_fwd_ex(const oit_camera* cam, const float* rec, const int32_t*
  * written only for tiles that hold pairs (the only ones that backward reads). ws: oit_fwd_workspace_bytes scratch. D-SSIM (loss 2) is not pixel-local: use
  * oit_composite_bwd_ex with a target for it. */
 #define OIT_COEF_IN_WS 0x200 /* oit_composite_bwd_ex: the coefficients are already in ws */
+#define OIT_COEF_ALL_TILES 0x400 /* oit_composite_fwd_loss(_ex): coefficients for EVERY tile, also those
+                                    without pairs (their pixels carry the cache's state alone), so that
+                                    oit_score_subsample_ex can back-propagate other splats through them */
 int oit_composite_fwd_loss(const oit_camera* cam, const float* rec, const int32_t* pair_slot,
                            const int32_t* tile_offsets, int64_t pair_capacity, const float bg_host[3],
                            const float* base, const void* target, int32_t loss, float* state, void* ws,
@@ -301,6 +304,27 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
                         const float bg_host[3], float scale, float* score_grad, float* dL_dsigma,
                         int64_t pair_capacity, int64_t* d_max_pairs, void* ws, size_t ws_bytes,
                         int32_t concurrency, oit_stream_t stream);
+
+/* oit_score_subsample_ex: as oit_score_subsample, plus coef_ws_host (nullable HOST array of n_sub
+ * DEVICE pointers, entries nullable): entry s, if given, is a backward workspace into which
+ * oit_composite_fwd_loss(_ex) wrote view views_host[s]'s coefficients with loss | OIT_COEF_ALL_TILES,
+ * for the SAME rows, σ, active set, cache, target and loss as this call (the caller's contract —
+ * e.g. the period's training batch and its refresh on one parameter state, R35). That
+ * view's Rasterize(G, I^pre_j) and loss gradient are then taken from it instead of being recomputed
+ * (no projection, binning or forward of the active set); the workspace is only read. Only the
+ * pixel-local losses (0, 1) have such coefficients: loss 2 with a non-NULL entry is OIT_EINVAL.
+ * coef_ready_host (nullable HOST array of n_sub cudaEvent_t handles, entries nullable): the call's
+ * stream waits on event s (cudaStreamWaitEvent) right before view s first reads coef_ws_host[s] —
+ * after the view's scored splats are projected and binned, which do not need the coefficients — so
+ * a producer on another stream (the view's training forward) overlaps that part of the score. */
+int oit_score_subsample_ex(const oit_scene* scene, const oit_camera* cams_host, int32_t n_views,
+                           const void* const* targets_host, const float* const* caches_host,
+                           const int32_t* active_idx, int32_t n_active, const int32_t* score_idx,
+                           int32_t n_score, const int32_t* views_host, int32_t n_sub, int32_t loss,
+                           const float bg_host[3], float scale, float* score_grad, float* dL_dsigma,
+                           int64_t pair_capacity, int64_t* d_max_pairs, void* ws, size_t ws_bytes,
+                           const void* const* coef_ws_host, void* const* coef_ready_host, int32_t concurrency,
+                           oit_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------
  * a8  oit_update_active_set — Eq. 8 with the text's ∃ reading (R18), Alg. 1 l.13

@@ -62,6 +62,7 @@ class AdamCfg(C.Structure):
 LOSS_CODE = {"l1": 0, "l2": 1, "dssim": 2}   # "dssim" = the 3DGS (1−λ)L1 + λ·D-SSIM, λ = 0.2
 OIT_TARGET_U8 = 0x100                          # loss flag: 8-bit targets (uint8 [3][H][W], value u8/255)
 OIT_COEF_IN_WS = 0x200                         # bwd_ex: coefficients already in ws (oit_composite_fwd_loss)
+OIT_COEF_ALL_TILES = 0x400                     # fwd_loss: coefficients for every tile (reusable by the score)
 
 
 def _loss_flags(loss: str, targets) -> int:
@@ -108,6 +109,8 @@ def lib() -> C.CDLL:
             "oit_score_workspace_bytes": (sz, [cam_p, i32, i32, i64]),
             "oit_score_subsample": (C.c_int, [scene_p, cam_p, i32, vp, vp, vp, i32, vp, i32, vp, i32, i32, vp, f32,
                                               vp, vp, i64, vp, vp, sz, i32, vp]),
+            "oit_score_subsample_ex": (C.c_int, [scene_p, cam_p, i32, vp, vp, vp, i32, vp, i32, vp, i32, i32, vp,
+                                                 f32, vp, vp, i64, vp, vp, sz, vp, vp, i32, vp]),
             "oit_update_workspace_bytes": (sz, [i32]),
             "oit_delta_workspace_bytes": (sz, [i32]),
             "oit_active_set_delta": (C.c_int, [vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]),
@@ -135,7 +138,8 @@ EXPORTED = ["oit_status_string", "oit_num_tiles", "oit_project_cull", "oit_bin_w
             "oit_bin_workspace_bytes_ex", "oit_bin_tiles",
             "oit_fwd_workspace_bytes", "oit_composite_fwd", "oit_composite_fwd_ex", "oit_composite_fwd_loss",
             "oit_composite_fwd_loss_ex", "oit_loss_grad", "oit_bwd_workspace_bytes", "oit_composite_bwd", "oit_composite_bwd_ex",
-            "oit_select_views", "oit_score_workspace_bytes", "oit_score_subsample", "oit_update_workspace_bytes",
+            "oit_select_views", "oit_score_workspace_bytes", "oit_score_subsample", "oit_score_subsample_ex",
+            "oit_update_workspace_bytes",
             "oit_update_active_set", "oit_delta_workspace_bytes", "oit_active_set_delta",
             "oit_reconcile_workspace_bytes", "oit_reconcile_cache", "oit_adam_step",
             "oit_dssim_workspace_bytes", "oit_loss_dssim", "oit_composite_bwd_perpixel", "oit_score_activeness",
@@ -216,13 +220,16 @@ def oit_composite_fwd(cam, rec, pair_slot, tile_offsets, bg, ws, base=None, rout
 
 
 def oit_composite_fwd_loss(cam, rec, pair_slot, tile_offsets, bg, ws, bwd_ws, n_slots: int, target, loss: str,
-                           base=None, state=None, stream=None, concurrency: int = 1, events=None):
+                           base=None, state=None, stream=None, concurrency: int = 1, events=None,
+                           all_tiles: bool = False):
     """a3 + a4 fused (training view): the forward whose epilogue applies the L1/L2 loss against
     target (fp32 or uint8) and writes the backward coefficients into bwd_ws; follow with
     oit_composite_bwd(..., coef_ready=True) on the same bwd_ws. events: optional (begin, end)
-    torch.cuda.Event pair recorded around the composite kernel alone (oit_composite_fwd_loss_ex)."""
+    torch.cuda.Event pair recorded around the composite kernel alone (oit_composite_fwd_loss_ex).
+    all_tiles: coefficients for every tile (OIT_COEF_ALL_TILES), reusable by oit_score_subsample."""
+    flags = _loss_flags(loss, [target]) | (OIT_COEF_ALL_TILES if all_tiles else 0)
     args = (C.byref(camera(cam)), _ptr(rec), _ptr(pair_slot), _ptr(tile_offsets), int(pair_slot.numel()), _f3(bg),
-            _ptr(base), _ptr(target), _loss_flags(loss, [target]), _ptr(state), _ptr(ws), int(ws.numel()),
+            _ptr(base), _ptr(target), flags, _ptr(state), _ptr(ws), int(ws.numel()),
             _ptr(bwd_ws), int(bwd_ws.numel()), int(n_slots))
     if events is None:
         _check(lib().oit_composite_fwd_loss(*args, int(concurrency), _stream(stream)), "oit_composite_fwd_loss")
@@ -279,22 +286,34 @@ def oit_score_workspace_bytes(cam, n_active: int, n_score: int, pair_capacity: i
 
 def oit_score_subsample(rows, sigma, cams, targets, caches, active_idx, score_idx, views, loss: str, bg,
                         score_grad, dL_dsigma, pair_capacity: int, max_pairs, ws, stream=None, scale=None,
-                        concurrency: int = 1):
+                        concurrency: int = 1, coef_ws=None, coef_ready=None):
     """scale: weight of each view's gradient (default 1/len(views): the mean over these views);
-    concurrency: score calls in flight on other streams (grid sizing only)."""
+    concurrency: score calls in flight on other streams (grid sizing only); coef_ws: optional list
+    (one entry per subsampled view, entries may be None) of backward workspaces holding the view's
+    coefficients from oit_composite_fwd_loss(..., all_tiles=True) (oit_score_subsample_ex);
+    coef_ready: optional list of torch.cuda.Event (entries may be None) the call waits on right
+    before it reads the matching coef_ws entry."""
     sc = scene(rows, sigma)
     V = len(cams)
     cam_arr = (Camera * V)(*[camera(c) for c in cams])
     tg = (C.c_void_p * V)(*[(t.data_ptr() if t is not None else None) for t in targets])
     ch = (C.c_void_p * V)(*[(c.data_ptr() if c is not None else None) for c in caches]) if caches is not None else None
     vw = (C.c_int32 * len(views))(*[int(v) for v in views])
-    _check(lib().oit_score_subsample(C.byref(sc), cam_arr, V, tg, ch, _ptr(active_idx), int(active_idx.numel()),
-                                     _ptr(score_idx), int(score_idx.numel()), vw, len(views),
-                                     _loss_flags(loss, targets), _f3(bg),
-                                     C.c_float(1.0 / len(views) if scale is None else scale), _ptr(score_grad),
-                                     _ptr(dL_dsigma),
-                                     int(pair_capacity), _ptr(max_pairs), _ptr(ws), int(ws.numel()),
-                                     int(concurrency), _stream(stream)), "oit_score_subsample")
+    args = (C.byref(sc), cam_arr, V, tg, ch, _ptr(active_idx), int(active_idx.numel()), _ptr(score_idx),
+            int(score_idx.numel()), vw, len(views), _loss_flags(loss, targets), _f3(bg),
+            C.c_float(1.0 / len(views) if scale is None else scale), _ptr(score_grad), _ptr(dL_dsigma),
+            int(pair_capacity), _ptr(max_pairs), _ptr(ws), int(ws.numel()))
+    if coef_ws is None:
+        _check(lib().oit_score_subsample(*args, int(concurrency), _stream(stream)), "oit_score_subsample")
+    else:
+        assert len(coef_ws) == len(views)
+        cw = (C.c_void_p * len(views))(*[(w.data_ptr() if w is not None else None) for w in coef_ws])
+        ev = None
+        if coef_ready is not None:
+            assert len(coef_ready) == len(views)
+            ev = (C.c_void_p * len(views))(*[(e.cuda_event if e is not None else None) for e in coef_ready])
+        _check(lib().oit_score_subsample_ex(*args, cw, ev, int(concurrency), _stream(stream)),
+               "oit_score_subsample_ex")
 
 
 def oit_update_workspace_bytes(n_total: int) -> int:

@@ -141,7 +141,7 @@ int oit_composite_fwd_loss_ex(const oit_camera* cam, const float* rec, const int
                            int32_t concurrency, oit_stream_t stream) {
   if (!cam_ok(cam) || !tile_offsets || !bg_host || pair_capacity < 0 || !target || !ws || !bwd_ws || n_slots < 0)
     return OIT_EINVAL;
-  const int32_t l = loss & ~OIT_TARGET_U8;
+  const int32_t l = loss & ~(OIT_TARGET_U8 | OIT_COEF_ALL_TILES);
   if (l != 0 && l != 1) return OIT_EINVAL;
   if (pair_capacity > 0 && (!rec || !pair_slot)) return OIT_EINVAL;
   if (!shape_ok(cam)) return OIT_ESHAPE;
@@ -161,7 +161,7 @@ int oit_composite_fwd_loss_ex(const oit_camera* cam, const float* rec, const int
   const BwdWs bl = bwd_ws_layout(cv.base + cv.off, nt, n_slots, pair_capacity);
   fl.qlen = bl.qlen;
   fl.qslot = bl.qslot;
-  fl.listed_tiles_only = true;
+  fl.listed_tiles_only = (loss & OIT_COEF_ALL_TILES) == 0;
   launch_composite_fwd(dev_cam(cam, bg_host), rec, pair_slot, tile_offsets, pair_capacity, base, nullptr, nullptr,
                        state, nullptr, S(stream), nullptr, ws, concurrency, fl,
                        ev ? static_cast<cudaEvent_t>(ev->kernel_begin) : nullptr,
@@ -359,6 +359,18 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
                         int32_t n_sub, int32_t loss, const float bg_host[3], float scale, float* score_grad, float* dL_dsigma,
                         int64_t pair_capacity, int64_t* d_max_pairs, void* ws, size_t ws_bytes,
                         int32_t concurrency, oit_stream_t stream) {
+  return oit_score_subsample_ex(scene, cams_host, n_views, targets_host, caches_host, active_idx, n_active, score_idx,
+                                n_score, views_host, n_sub, loss, bg_host, scale, score_grad, dL_dsigma, pair_capacity,
+                                d_max_pairs, ws, ws_bytes, nullptr, nullptr, concurrency, stream);
+}
+
+int oit_score_subsample_ex(const oit_scene* scene, const oit_camera* cams_host, int32_t n_views,
+                           const void* const* targets_host, const float* const* caches_host,
+                           const int32_t* active_idx, int32_t n_active, const int32_t* score_idx, int32_t n_score,
+                           const int32_t* views_host, int32_t n_sub, int32_t loss, const float bg_host[3], float scale,
+                           float* score_grad, float* dL_dsigma, int64_t pair_capacity, int64_t* d_max_pairs, void* ws,
+                           size_t ws_bytes, const void* const* coef_ws_host, void* const* coef_ready_host,
+                           int32_t concurrency, oit_stream_t stream) {
   if (!scene || !scene->rows || !scene->sigma || !cams_host || !targets_host || !views_host || !bg_host ||
       !dL_dsigma || !d_max_pairs || !ws)
     return OIT_EINVAL;
@@ -374,6 +386,9 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
   }
   if (!shape_ok(&cams_host[0]) || oit_num_tiles(&cams_host[0]) > kMaxScan) return OIT_ESHAPE;
   if (ws_bytes < oit_score_workspace_bytes(&cams_host[0], n_active, n_score, pair_capacity)) return OIT_ECAPACITY;
+  if (coef_ws_host && (loss & ~OIT_TARGET_U8) == 2)
+    for (int s = 0; s < n_sub; s++)
+      if (coef_ws_host[s]) return OIT_EINVAL;  // D-SSIM coefficients are not written by the fused forward
   ScoreWs w = score_layout(ws, &cams_host[0], n_active, n_score, pair_capacity);
   cudaStream_t st = S(stream);
   DevCam group_cams[kMvViews];
@@ -381,26 +396,37 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
   for (int s = 0; s < n_sub; s++) {
     const int j = views_host[s];
     DevCam dc = dev_cam(&cams_host[j], bg_host);
-    // Rasterize(G, I^pre_j): the active set over the view's cache of the frozen set (R16)
-    launch_project(dc, scene->rows, scene->sigma, active_idx, n_active, w.rec_a, w.tps_a, st);
-    launch_bin(dc, w.rec_a, w.tps_a, n_active, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st,
-               true, w.bin_ws_bytes);
-    const float* cache = caches_host ? caches_host[j] : nullptr;
-    if ((loss & ~OIT_TARGET_U8) != 2) {
-      // L_j (L1/L2, pixel-local) and the backward coefficients in the forward's epilogue (a3 + a4)
-      FwdLoss fl;
-      fl.target = targets_host[j];
-      fl.target_u8 = (loss & OIT_TARGET_U8) != 0;
-      fl.loss = loss & ~OIT_TARGET_U8;
-      fl.coef4 = reinterpret_cast<float4*>(w.coef4);
-      fl.coefa = w.coefa;
-      launch_composite_fwd(dc, w.rec_a, w.pairs, w.offs, pair_capacity, cache, nullptr, nullptr, nullptr, nullptr, st,
-                           nullptr, w.fwd_ws, concurrency, fl);
+    const float* coef4 = w.coef4;
+    const float* coefa = w.coefa;
+    if (coef_ws_host && coef_ws_host[s]) {
+      // the view's coefficients as oit_composite_fwd_loss wrote them (OIT_COEF_ALL_TILES) into a
+      // backward workspace: its first two regions (the carve of oit_composite_fwd_loss_ex)
+      Carve cv(const_cast<void*>(coef_ws_host[s]));
+      const int32_t nt = oit_num_tiles(&cams_host[0]);
+      coef4 = cv.take<float>((size_t)nt * kTilePx * 4);
+      coefa = cv.take<float>((size_t)nt * kTilePx);
     } else {
-      // D-SSIM is not pixel-local: the state, then resolve → SSIM stencils → coefficients
-      launch_composite_fwd(dc, w.rec_a, w.pairs, w.offs, pair_capacity, cache, nullptr, nullptr, w.state, nullptr, st,
-                           nullptr, w.fwd_ws, concurrency);
-      coef_from_target(dc, &cams_host[j], w.state, targets_host[j], loss, w.coef4, w.coefa, w.dssim_ws, st);
+      // Rasterize(G, I^pre_j): the active set over the view's cache of the frozen set (R16)
+      launch_project(dc, scene->rows, scene->sigma, active_idx, n_active, w.rec_a, w.tps_a, st);
+      launch_bin(dc, w.rec_a, w.tps_a, n_active, w.pairs, pair_capacity, w.offs, w.npairs, d_max_pairs, w.bin_ws, st,
+                 true, w.bin_ws_bytes);
+      const float* cache = caches_host ? caches_host[j] : nullptr;
+      if ((loss & ~OIT_TARGET_U8) != 2) {
+        // L_j (L1/L2, pixel-local) and the backward coefficients in the forward's epilogue (a3 + a4)
+        FwdLoss fl;
+        fl.target = targets_host[j];
+        fl.target_u8 = (loss & OIT_TARGET_U8) != 0;
+        fl.loss = loss & ~OIT_TARGET_U8;
+        fl.coef4 = reinterpret_cast<float4*>(w.coef4);
+        fl.coefa = w.coefa;
+        launch_composite_fwd(dc, w.rec_a, w.pairs, w.offs, pair_capacity, cache, nullptr, nullptr, nullptr, nullptr, st,
+                             nullptr, w.fwd_ws, concurrency, fl);
+      } else {
+        // D-SSIM is not pixel-local: the state, then resolve → SSIM stencils → coefficients
+        launch_composite_fwd(dc, w.rec_a, w.pairs, w.offs, pair_capacity, cache, nullptr, nullptr, w.state, nullptr, st,
+                             nullptr, w.fwd_ws, concurrency);
+        coef_from_target(dc, &cams_host[j], w.state, targets_host[j], loss, w.coef4, w.coefa, w.dssim_ws, st);
+      }
     }
     // back-propagate L_j to the scored splats (R20): the moments of this view; the chain to the
     // rows runs once per group of kMvViews views (the rows are read-modify-written once per group)
@@ -411,8 +437,10 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
     const BwdWs bl = bwd_ws_layout(w.bwd_ws, oit_num_tiles(&cams_host[0]), n_score, pair_capacity);
     launch_bin_quads(dc, rec_s, w.tps_s, n_score, pair_capacity, w.offs, w.npairs, d_max_pairs, bl.qlen, bl.qslot,
                      w.bin_ws, st);
+    if (coef_ws_host && coef_ws_host[s] && coef_ready_host && coef_ready_host[s])
+      cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(coef_ready_host[s]), 0);  // the producer's coefficients
     launch_composite_bwd(dc, scene->rows, scene->sigma, score_idx, n_score, rec_s, w.pairs, w.offs, pair_capacity,
-                         w.coef4, w.coefa, scale, score_grad, dL_dsigma, nullptr, w.bwd_ws, st, nullptr, nullptr, 0,
+                         coef4, coefa, scale, score_grad, dL_dsigma, nullptr, w.bwd_ws, st, nullptr, nullptr, 0,
                          concurrency, w.acc_s[in_group], true);
     group_cams[in_group++] = dc;
     if (in_group == kMvViews || s == n_sub - 1) {

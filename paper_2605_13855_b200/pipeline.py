@@ -62,27 +62,34 @@ class ViewPipeline:
             events[1].record()
         return (self.image if image else None), self.state
 
+    def new_bwd_ws(self):
+        """A backward workspace of this pipeline's shape (e.g. one that keeps a view's coefficients
+        for oit_score_subsample after the pipeline has moved on to other views)."""
+        return _ws(L.oit_bwd_workspace_bytes(self.cam, self.max_slots, self.capacity), self.device)
+
     def forward_loss(self, rows, sigma, idx, bg, target, loss="l1", base=None, state=False, stream=None, events=None,
-                     concurrency=1):
+                     concurrency=1, bwd_ws=None, all_tiles=False):
         """a1-a3 + a4 fused (training view): the forward whose epilogue writes the L1/L2 backward
-        coefficients into this pipeline's backward workspace; follow with backward(...,
-        coef_ready=True). Returns the state buffer if state=True (else None, not written)."""
+        coefficients into this pipeline's backward workspace (or bwd_ws); follow with backward(...,
+        coef_ready=True) on the same workspace. Returns the state buffer if state=True (else None,
+        not written). all_tiles: coefficients for every tile (reusable by oit_score_subsample)."""
         rec = self.project_bin(rows, sigma, idx, stream)
         # events (optional): recorded by the library around the composite kernel alone
-        L.oit_composite_fwd_loss(self.cam, rec, self.pairs, self.offs, bg, self.fwd_ws, self.bwd_ws, self.max_slots,
-                                 target, loss, base=base, state=self.state if state else None, stream=stream,
-                                 concurrency=concurrency, events=events)
+        L.oit_composite_fwd_loss(self.cam, rec, self.pairs, self.offs, bg, self.fwd_ws,
+                                 self.bwd_ws if bwd_ws is None else bwd_ws, self.max_slots, target, loss, base=base,
+                                 state=self.state if state else None, stream=stream, concurrency=concurrency,
+                                 events=events, all_tiles=all_tiles)
         return self.state if state else None
 
     def backward(self, rows, sigma, idx, bg, state, dL_dimage, grad, dL_dsigma, dL_dcov=None, scale=1.0,
                  reuse_bins=True, stream=None, events=None, target=None, loss="l1", per_pixel=False, concurrency=1,
-                 coef_ready=False):
+                 coef_ready=False, bwd_ws=None):
         """a4-a6 for the splats idx (grad rows += ...). With reuse_bins the records/pairs of the
         preceding forward over the same idx are reused."""
         n = int(idx.numel())
         rec = (self.rec[:n] if n > 0 else self.rec) if reuse_bins else self.project_bin(rows, sigma, idx, stream)
         L.oit_composite_bwd(rows, sigma, self.cam, idx, rec, self.pairs, self.offs, bg, state, dL_dimage, grad,
-                            dL_dsigma, self.bwd_ws, dL_dcov=dL_dcov, scale=scale, stream=stream, events=events,
+                            dL_dsigma, self.bwd_ws if bwd_ws is None else bwd_ws, dL_dcov=dL_dcov, scale=scale, stream=stream, events=events,
                             target=target, loss=loss, per_pixel=per_pixel, concurrency=concurrency,
                             coef_ready=coef_ready)
 

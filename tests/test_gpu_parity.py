@@ -359,6 +359,71 @@ def test_score_subsample_parity(loss, views):
     assert_grad_bar([dsig.item()], [dsref], [bsig], atol=1e-6 / (3 * W * H), name="dsigma")
 
 
+@pytest.mark.parametrize("loss", ["l1", "l2"])
+def test_score_reuses_training_coefficients(loss):
+    """oit_score_subsample_ex with the coefficients the training forward of the same views wrote
+    (oit_composite_fwd_loss with OIT_COEF_ALL_TILES, same parameters / active set / cache / target:
+    the period's batch and its refresh, R35) equals the score that rasterises the active set itself
+    and the oracle's score, including views whose tiles have no active pair (the cache alone) and a
+    mix of reused and recomputed views in one call; D-SSIM coefficients cannot be reused (EINVAL)."""
+    L = _L()
+    sc = synth.scene_c2(n=8000, n_views=6, res=96)
+    mask = synth.active_mask(sc, 0.25, "clustered")
+    act, ina = np.flatnonzero(mask).astype(np.int32), np.flatnonzero(~mask).astype(np.int32)
+    caches_o = [O.render(sc.rows, sc.sigma, ina, c, sc.bg)["state"] for c in sc.cams]
+    targets = []
+    for k, c in enumerate(sc.cams):
+        img = O.render(sc.rows, sc.sigma, np.arange(sc.n), c, sc.bg)["image"]
+        off = synth.rng(500 + k).uniform(0.01, 0.1, img.shape) * np.where(synth.rng(600 + k).random(img.shape) < 0.5, -1, 1)
+        targets.append((img + off).astype(np.float32))
+    views = [0, 2, 3, 5]
+    ref, dsref, bnd, bsig = O.score_subsample(sc.rows, sc.sigma, sc.cams, targets, caches_o, act, ina, views, sc.bg,
+                                              loss, with_bound="full")
+    W, H = sc.cams[0]["width"], sc.cams[0]["height"]
+    caches = [_t(plain_to_tile_major(c, W, H).astype(np.float32)) for c in caches_o]
+    tg = [_t(t) for t in targets]
+    rows, sigma, act_t, ina_t = _t(sc.rows), _t(np.array([sc.sigma], np.float32)), _t(act), _t(ina)
+    cap = 1 << 20
+    # the training forwards of the subsampled views, each into a backward workspace of its own
+    p = _pipe(sc.cams[0], sc.n, cap)
+    cws = []
+    for j in views:
+        p.set_camera(sc.cams[j])
+        w = p.new_bwd_ws()
+        p.forward_loss(rows, sigma, act_t, sc.bg, tg[j], loss, base=caches[j], bwd_ws=w, all_tiles=True)
+        cws.append(w)
+    # tiles whose coefficients come from the cache alone are present in these views
+    offs = p.offs.cpu().numpy()
+    assert (np.diff(offs) == 0).any()
+
+    def run(coef_ws):
+        ws = torch.empty(L.oit_score_workspace_bytes(sc.cams[0], len(act), len(ina), cap), dtype=torch.uint8,
+                         device=DEV)
+        sg = torch.zeros((len(ina), 80), dtype=torch.float32, device=DEV)
+        ds = torch.zeros(1, dtype=torch.float32, device=DEV)
+        mp = torch.zeros(1, dtype=torch.int64, device=DEV)
+        L.oit_score_subsample(rows, sigma, sc.cams, tg, caches, act_t, ina_t, views, loss, sc.bg, sg, ds, cap, mp, ws,
+                              coef_ws=coef_ws)
+        torch.cuda.synchronize()
+        return sg.cpu().numpy(), float(ds.item())
+
+    a, da = run(None)
+    b, db = run(cws)
+    c, dc = run([cws[0], None, cws[2], None])
+    for x, dx in ((b, db), (c, dc)):
+        # identical coefficients: the runs differ only by the order of the fp32 atomics
+        assert np.abs(x - a).max() <= 1e-5 * np.abs(a).max() and np.abs(a).max() > 0
+        assert abs(dx - da) <= 1e-5 * abs(da) + 1e-12
+        assert_grad_bar(x, ref, bnd, atol=1e-6 / (3 * W * H), name="score/reused")
+        assert_grad_bar([dx], [dsref], [bsig], atol=1e-6 / (3 * W * H), name="dsigma/reused")
+    ws = torch.empty(L.oit_score_workspace_bytes(sc.cams[0], len(act), len(ina), cap), dtype=torch.uint8, device=DEV)
+    sg = torch.zeros((len(ina), 80), dtype=torch.float32, device=DEV)
+    with pytest.raises(L.OitError):
+        L.oit_score_subsample(rows, sigma, sc.cams, tg, caches, act_t, ina_t, views, "dssim", sc.bg, sg,
+                              torch.zeros(1, device=DEV), cap, torch.zeros(1, dtype=torch.int64, device=DEV), ws,
+                              coef_ws=cws)
+
+
 # ------------------------------------------------------------------ a8 update ------------
 @pytest.mark.parametrize("mode", ["fresh", "monotone"])
 def test_update_active_set_bitexact(mode):
