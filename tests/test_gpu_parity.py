@@ -410,7 +410,29 @@ def test_score_reuses_training_coefficients(loss):
     a, da = run(None)
     b, db = run(cws)
     c, dc = run([cws[0], None, cws[2], None])
-    for x, dx in ((b, db), (c, dc)):
+    # producer on another stream: fresh workspaces written there, the score waits on their events
+    # only right before each view's backward (after its scored set's projection and binning)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    cws2, evs = [], []
+    with torch.cuda.stream(side):
+        for j in views:
+            p.set_camera(sc.cams[j])
+            w = p.new_bwd_ws()
+            w.fill_(0xFF)  # poison: a read before the producer finished would show
+            p.forward_loss(rows, sigma, act_t, sc.bg, tg[j], loss, base=caches[j], bwd_ws=w, all_tiles=True)
+            e = torch.cuda.Event()
+            e.record(side)
+            cws2.append(w)
+            evs.append(e)
+    ws = torch.empty(L.oit_score_workspace_bytes(sc.cams[0], len(act), len(ina), cap), dtype=torch.uint8, device=DEV)
+    sg = torch.zeros((len(ina), 80), dtype=torch.float32, device=DEV)
+    ds = torch.zeros(1, dtype=torch.float32, device=DEV)
+    L.oit_score_subsample(rows, sigma, sc.cams, tg, caches, act_t, ina_t, views, loss, sc.bg, sg, ds, cap,
+                          torch.zeros(1, dtype=torch.int64, device=DEV), ws, coef_ws=cws2, coef_ready=evs)
+    torch.cuda.synchronize()
+    e_, de = sg.cpu().numpy(), float(ds.item())
+    for x, dx in ((b, db), (c, dc), (e_, de)):
         # identical coefficients: the runs differ only by the order of the fp32 atomics
         assert np.abs(x - a).max() <= 1e-5 * np.abs(a).max() and np.abs(a).max() > 0
         assert abs(dx - da) <= 1e-5 * abs(da) + 1e-12
