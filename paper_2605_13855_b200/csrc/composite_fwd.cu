@@ -119,7 +119,8 @@ __global__ void __launch_bounds__(kFwdThreads, kLoss ? 18 : 1) k_fwd_items(
         const float4 r0 = r[0], r1 = r[1];
         s_rec[tid][0] = r0;
         s_rec[tid][1] = r1;
-        s_rec[tid][2] = r[2];
+        const float4 r2 = r[2];  // (cR, cG, cB, w) staged as (cR·w, cG·w, cB·w, w): P += (c·w)·α, Q += w·α
+        s_rec[tid][2] = make_float4(r2.x * r2.w, r2.y * r2.w, r2.z * r2.w, r2.w);
         s_rec[tid][3] = r[3];  // (rect_x, rect_y, kx, ky): the loop reads .zw
         if (quads) {
           qm = quadrant_mask(cam, tile, r0, r1);
@@ -177,10 +178,9 @@ __global__ void __launch_bounds__(kFwdThreads, kLoss ? 18 : 1) k_fwd_items(
             a3 = c3 ? (pw3 >= q1.z ? 0.99f : e3) : 0.0f;
           }
           const f2_t alA = f2(a0, a1), alB = f2(a2, a3), w2 = f2s(q2.w);
-          const f2_t awA = mul2(alA, w2), awB = mul2(alB, w2);
-          const f2_t cR = f2s(q2.x), cG = f2s(q2.y), cB = f2s(q2.z);
-          fma2_acc(PA0, cR, awA); fma2_acc(PA1, cG, awA); fma2_acc(PA2, cB, awA); add2_acc(QA, awA);
-          fma2_acc(PB0, cR, awB); fma2_acc(PB1, cG, awB); fma2_acc(PB2, cB, awB); add2_acc(QB, awB);
+          const f2_t cR = f2s(q2.x), cG = f2s(q2.y), cB = f2s(q2.z);  // colour · weight (staged)
+          fma2_acc(PA0, cR, alA); fma2_acc(PA1, cG, alA); fma2_acc(PA2, cB, alA); fma2_acc(QA, w2, alA);
+          fma2_acc(PB0, cR, alB); fma2_acc(PB1, cG, alB); fma2_acc(PB2, cB, alB); fma2_acc(QB, w2, alB);
           decay2(TA, alA);  // T ← T − αT (one rounding, as fmaf(−α, T, T))
           decay2(TB, alB);
           if (kCount) {
