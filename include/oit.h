@@ -312,7 +312,8 @@ int oit_score_subsample(const oit_scene* scene, const oit_camera* cams_host, int
  * e.g. the period's training batch and its refresh on one parameter state, R35). That
  * view's Rasterize(G, I^pre_j) and loss gradient are then taken from it instead of being recomputed
  * (no projection, binning or forward of the active set); the workspace is only read. Only the
- * pixel-local losses (0, 1) have such coefficients: loss 2 with a non-NULL entry is OIT_EINVAL.
+ * pixel-local losses (0, 1) have such coefficients: loss 2 with a non-NULL entry is OIT_EINVAL, and
+ * so is an entry that is not 16-byte aligned (workspaces are read as float4).
  * coef_ready_host (nullable HOST array of n_sub cudaEvent_t handles, entries nullable): the call's
  * stream waits on event s (cudaStreamWaitEvent) right before view s first reads coef_ws_host[s] —
  * after the view's scored splats are projected and binned, which do not need the coefficients — so

@@ -386,9 +386,12 @@ int oit_score_subsample_ex(const oit_scene* scene, const oit_camera* cams_host, 
   }
   if (!shape_ok(&cams_host[0]) || oit_num_tiles(&cams_host[0]) > kMaxScan) return OIT_ESHAPE;
   if (ws_bytes < oit_score_workspace_bytes(&cams_host[0], n_active, n_score, pair_capacity)) return OIT_ECAPACITY;
-  if (coef_ws_host && (loss & ~OIT_TARGET_U8) == 2)
-    for (int s = 0; s < n_sub; s++)
-      if (coef_ws_host[s]) return OIT_EINVAL;  // D-SSIM coefficients are not written by the fused forward
+  if (coef_ws_host)
+    for (int s = 0; s < n_sub; s++) {
+      if (!coef_ws_host[s]) continue;
+      if ((loss & ~OIT_TARGET_U8) == 2) return OIT_EINVAL;  // D-SSIM coefficients: not written by the fused forward
+      if (reinterpret_cast<uintptr_t>(coef_ws_host[s]) & 15) return OIT_EINVAL;  // read as float4
+    }
   ScoreWs w = score_layout(ws, &cams_host[0], n_active, n_score, pair_capacity);
   cudaStream_t st = S(stream);
   DevCam group_cams[kMvViews];
