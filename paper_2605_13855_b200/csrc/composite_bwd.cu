@@ -95,8 +95,13 @@ __device__ __forceinline__ void moments_window(Moments& m, const float* __restri
                                                float ey) {
   const unsigned FULL = 0xffffffffu;
   const int pxe = px0 & ~1;
-  const f2_t mx2 = f2s(mx), nA2 = f2s(nA), nkx2 = f2s(-kx), l2e = f2s(kLog2e), one2 = f2s(1.0f);
-  const f2_t cR2 = f2s(cR), cG2 = f2s(cG), cB2 = f2s(cB), w2 = f2s(w);
+  const f2_t mx2 = f2s(mx), nA2 = f2s(nA), nkx2 = f2s(-kx), l2e = f2s(kLog2e);
+  // the weight is factored out of d: per pixel d/w = α·(a/(w(1−α)) + u·c − s), and the d-moments are
+  // scaled by w once at the end — one FMUL2 fewer per pixel pair (w(1−α) is one FFMA2, as 1−α was
+  // one FADD2). w = 0 (d ≥ σ or v⁺ = 0: only the T term, R11) runs with w = 2⁻⁶⁴, a power of two, so
+  // the scaling is exact and the w·(u·c − s) term it adds is 2⁻⁶⁴ of a term the true w zeroes.
+  const float wf = fmaxf(w, 5.421010862427522e-20f);  // 2^-64
+  const f2_t cR2 = f2s(cR), cG2 = f2s(cG), cB2 = f2s(cB), w2 = f2s(wf);
   f2_t U0 = f2s(0.f), U1 = f2s(0.f), U2 = f2s(0.f), NS = f2s(0.f);  // packed (even, odd pixel) partial sums; NS = −S
   f2_t Rdxx = f2s(0.f);  // Σ d dx² needs no dy: accumulated over the whole window
   for (int py = py0; py <= py1; py++) {
@@ -135,10 +140,10 @@ __device__ __forceinline__ void moments_window(Moments& m, const float* __restri
       const f2_t uB = *reinterpret_cast<const f2_t*>(row + 128 + px);
       const f2_t ns = *reinterpret_cast<const f2_t*>(row + 192 + px);
       const f2_t ca = *reinterpret_cast<const f2_t*>(row + 256 + px);
-      const f2_t om = sub2(one2, a2);
+      const f2_t om = fma2(f2(-f2lo(a2), -f2hi(a2)), w2, w2);  // w(1−α)
       const f2_t rinv = f2(rcp_approx(f2lo(om)), rcp_approx(f2hi(om)));
       const f2_t dot = fma2(uR, cR2, fma2(uG, cG2, fma2(uB, cB2, ns)));
-      f2_t d = mul2(fma2(ca, rinv, mul2(w2, dot)), a2);  // dL/dα · α (0 where α = 0)
+      f2_t d = mul2(fma2(ca, rinv, dot), a2);  // dL/dα · α / w (0 where α = 0)
       if (kClamp) d = f2(kl ? 0.0f : f2lo(d), kh ? 0.0f : f2hi(d));
       fma2_acc(U0, a2, uR);
       fma2_acc(U1, a2, uG);
@@ -158,6 +163,7 @@ __device__ __forceinline__ void moments_window(Moments& m, const float* __restri
     m.YY = fmaf(dy * dy, rd, m.YY);
   }
   m.XX += f2lo(Rdxx) + f2hi(Rdxx);
+  m.Od *= wf; m.M1 *= wf; m.M2 *= wf; m.XX *= wf; m.XY *= wf; m.YY *= wf;  // the d-moments back to dL/dα·α
   m.U0 += f2lo(U0) + f2hi(U0);
   m.U1 += f2lo(U1) + f2hi(U1);
   m.U2 += f2lo(U2) + f2hi(U2);
