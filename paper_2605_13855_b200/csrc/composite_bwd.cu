@@ -104,8 +104,11 @@ __device__ __forceinline__ void moments_window(Moments& m, const float* __restri
   const f2_t cR2 = f2s(cR), cG2 = f2s(cG), cB2 = f2s(cB), w2 = f2s(wf);
   f2_t U0 = f2s(0.f), U1 = f2s(0.f), U2 = f2s(0.f), NS = f2s(0.f);  // packed (even, odd pixel) partial sums; NS = −S
   f2_t Rdxx = f2s(0.f);  // Σ d dx² needs no dy: accumulated over the whole window
-  for (int py = py0; py <= py1; py++) {
-    const float dy = __fsub_rn((float)(ty0 + py), my);
+  // row-invariant: the first pair's offsets; the row coordinate as a float counter (exact integers)
+  const f2_t dx2_0 = sub2(f2((float)(tx0 + pxe), (float)(tx0 + pxe + 1)), mx2);
+  float fy = (float)(ty0 + py0);
+  for (int py = py0; py <= py1; py++, fy += 1.0f) {
+    const float dy = __fsub_rn(fy, my);
     const bool ract = valid && fabsf(dy) <= ey;
     if (!__any_sync(FULL, ract)) continue;
     const f2_t by2 = f2s(__fmul_rn(nB, dy));
@@ -114,7 +117,7 @@ __device__ __forceinline__ void moments_window(Moments& m, const float* __restri
     const float lo = ract ? thr_lo : 1.0f;  // folds the row test into the pixel test
     f2_t Rd = f2s(0.f), Rdx = f2s(0.f);
     const float* row = s_u + (py - qy0) * 8 - qx0;
-    f2_t dx2 = sub2(f2((float)(tx0 + pxe), (float)(tx0 + pxe + 1)), mx2);
+    f2_t dx2 = dx2_0;
     const f2_t two2 = f2s(2.0f);
 #pragma unroll 4
     for (int px = pxe; px <= px1; px += 2) {
