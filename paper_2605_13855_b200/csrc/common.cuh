@@ -382,7 +382,7 @@ __device__ __forceinline__ float ramp_fp64(const DevCam& cam, float mux, float m
 // Shared by the forward epilogue and the backward coefficient kernel so C is bit-identical.
 __device__ __forceinline__ void resolve_pixel(float P0, float P1, float P2, float Q, float T, const float* bg,
                                               float& F0, float& F1, float& F2, float& C0, float& C1, float& C2) {
-  float invQ = Q > 0.0f ? __fdiv_rn(1.0f, Q) : 0.0f;
+  float invQ = Q > 0.0f ? __frcp_rn(Q) : 0.0f;  // = 1/Q correctly rounded, without the division sequence
   F0 = P0 * invQ; F1 = P1 * invQ; F2 = P2 * invQ;
   float omT = 1.0f - T;
   C0 = __fmaf_rn(T, bg[0], omT * F0);
@@ -394,7 +394,8 @@ __device__ __forceinline__ void resolve_pixel(float P0, float P1, float P2, floa
 // target value t (both mean over 3HW; inv = 1/(3HW)), then the backward coefficients of Eq. B.2:
 // K = (1−T)/Q (0 if Q = 0), (u, s) = (K g, K g·F), a = T g·(F − c0).
 __device__ __forceinline__ float target_value(const float* t, size_t i) { return t[i]; }
-__device__ __forceinline__ float target_value(const uint8_t* t, size_t i) { return __fdiv_rn((float)t[i], 255.0f); }
+__device__ __forceinline__ float u8_unit(unsigned v) { return __fdiv_rn((float)v, 255.0f); }  // u8/255, rounded once
+__device__ __forceinline__ float target_value(const uint8_t* t, size_t i) { return u8_unit(t[i]); }
 __device__ __forceinline__ float loss_grad_px(float c, float t, int32_t loss, float inv) {
   const float d = c - t;
   return loss == 0 ? (d > 0.f ? inv : (d < 0.f ? -inv : 0.f)) : 2.f * d * inv;
