@@ -62,6 +62,32 @@ def test_status_strings_and_argument_errors_without_gpu():
     assert L.oit_composite_fwd_loss(*args(ctypes.c_void_p(8), 0 | _lib.OIT_TARGET_U8, None)) == 1
 
 
+def test_score_coefficient_reuse_argument_errors_without_gpu():
+    """oit_score_subsample_ex rejects, synchronously and before any launch, a reused coefficient
+    workspace for the D-SSIM loss (the fused forward writes only pixel-local coefficients) and one
+    that is not 16-byte aligned (OIT_EINVAL = 1)."""
+    from paper_2605_13855_b200 import _lib
+    L = _lib.lib()
+    cam = _lib.camera(dict(width=64, height=48, fx=50, fy=50, cx=32, cy=24, R=[1, 0, 0, 0, 1, 0, 0, 0, 1],
+                           t=[0, 0, 0], center=[0, 0, 0]))
+    sc = _lib.Scene(100, ctypes.c_void_p(256), ctypes.c_void_p(256))
+    cams = (_lib.Camera * 1)(cam)
+    tg = (ctypes.c_void_p * 1)(ctypes.c_void_p(256))
+    views = (ctypes.c_int32 * 1)(0)
+    bg = (ctypes.c_float * 3)(0, 0, 0)
+    nbytes = L.oit_score_workspace_bytes(ctypes.byref(cam), 10, 20, 1000)
+    dev = ctypes.c_void_p(256)
+
+    def call(loss, coef):
+        cw = None if coef is None else (ctypes.c_void_p * 1)(coef)
+        return L.oit_score_subsample_ex(ctypes.byref(sc), cams, 1, tg, None, dev, 10, dev, 20, views, 1, loss, bg,
+                                        ctypes.c_float(1.0), dev, dev, 1000, dev, dev, nbytes, cw, None, 1, None)
+
+    assert call(2, ctypes.c_void_p(256)) == 1          # D-SSIM: no reusable coefficients
+    assert call(0, ctypes.c_void_p(256 + 4)) == 1      # misaligned workspace
+    assert call(2, ctypes.c_void_p(256 + 4)) == 1
+
+
 def test_product_package_never_imports_the_oracle():
     pkg = os.path.join(ROOT, "paper_2605_13855_b200")
     for dp, _, files in os.walk(pkg):
